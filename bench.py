@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""CO2 outer-step benchmark (BASELINE.json metric: outer-step params/s,
+% of the HBM roofline, exposed all-reduce %, at 1/2/4/8 B200).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+  python bench.py --impl reference ...                   (reference CPU arm)
+
+A step is one co2_round of the hot path on every rank (the reference's
+co2_round, proj/src/outer_algorithms.cpp:110-211): launch the one-step-stale
+all-reduce of x_{t,tau} (in-place NCCL sum on the engine's comm stream,
+event-fenced), wait on the previous round's reduce, and run the fused
+outer-step kernel over this rank's full parameter buffer.  Inputs are
+synthetic, resident in HBM, and larger than L2 (126 MB), so
+no L2 flush is needed between steps.  `value` is whole-job params/s
+(N * n * K / max-over-ranks device time); `e2e` is the same metric through
+the host-buffer C ABI entry (co2_outer_step_host: pinned H2D, kernel, D2H
+inside the timed region).  The reference arm times the oracle's fp64
+restatement of the reference's unfused per-worker body on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c3": {"workload": "C3: 1.3B-param bf16 params + fp32 anchor/outer momentum, one CO2 "
+                       "worker per B200, tau=12 (BASELINE.json configs[2])",
+           "mode": 2, "n": 1_300_000_000, "tau": 12, "bytes_per_param": 26,
+           "storage": "bf16 params/x_{t-1,1}/xbar + fp32 x_{t,0}/x_{t-1,0}/momentum"},
+    "c2": {"workload": "C2: 125M-param fp32 flat buffer, tau=12 (BASELINE.json configs[1])",
+           "mode": 1, "n": 125_000_000, "tau": 12, "bytes_per_param": 32,
+           "storage": "fp32"},
+    "c4": {"workload": "C4 shard: 7B/8 = 875M-param bf16-mixed outer-state shard per B200",
+           "mode": 2, "n": 875_000_000, "tau": 12, "bytes_per_param": 26,
+           "storage": "bf16 params + fp32 state"},
+}
+HYPER = dict(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and clock-event reasons during the timed
+    region (the recipe's clocks line)."""
+
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+             "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
+
+    def __init__(self, index: int, period: float = 0.01):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period, self._stop = period, threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.NAMES.items():
+                    if r & getattr(nv, attr):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- CPU arms
+def cpu_sample_inputs(cfg, n_sample: int):
+    """fp64 upcast of the same synthetic inputs (first n_sample coordinates)."""
+    from oracle import oracle as O
+    x, p0, p1, xe, m = O.synth(cfg["mode"], n_sample)
+    return [O.to_f64(a) for a in (x, p0, p1, xe, m)]
+
+
+def time_cpu_step(cfg, n_sample: int, threads: int, steps: int, warmup: int):
+    """Times the oracle's fp64 restatement of co2_round's per-worker body
+    (outer_algorithms.cpp:186-202, the reference's unfused passes and fresh
+    temporaries) on n_sample coordinates."""
+    from oracle import oracle as O
+    x, p0, p1, xe, m = cpu_sample_inputs(cfg, n_sample)
+    h = O.hyper(tau=cfg["tau"], **HYPER)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        O.worker_step_f64(x, p0, p1, xe, m, h, threads=threads, want_gap=False)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    return n_sample / statistics.mean(times), statistics.mean(times)
+
+
+def run_reference_arm(args, cfg, rank: int):
+    if rank != 0:
+        return 0
+    cores = host_cores()
+    n_sample = args.ref_sample
+    value, t = time_cpu_step(cfg, n_sample, cores, max(args.steps, 1), max(args.warmup, 0))
+    line = {
+        "impl": "reference", "metric": "CO2 outer-step params/s", "value": value,
+        "unit": "params/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "n_params_per_worker": cfg["n"],
+                   "tau": cfg["tau"], "sample_params": n_sample},
+        "cpu_baseline": {"value": value, "unit": "params/s", "cores": cores, "kind": "port",
+                         "sample": f"{n_sample} coordinates of the {cfg['n']}-param workload, "
+                                   "fp64 upcast, reference unfused passes, coordinate ranges "
+                                   f"split over {cores} threads"},
+        "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "Reference (C++20/Eigen) is not buildable here (Eigen absent); this arm times "
+                "oracle/co2_oracle.c, a bit-exact restatement pinned by the reference's fixtures.",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--ref-sample", type=int, default=1 << 25)
+    ap.add_argument("--max-ctas", type=int, default=0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_16265_b200 import co2
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mode, n, tau, bpp = cfg["mode"], cfg["n"], cfg["tau"], cfg["bytes_per_param"]
+    hyper = co2.Co2Hyper(**HYPER)
+    stream = torch.cuda.current_stream()
+
+    # --- engine: NCCL unique id broadcast over torch.distributed (plumbing)
+    if world > 1:
+        obj = [co2.CollectiveEngine.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    else:
+        uid = bytes(128)
+    eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
+                               max_ctas=args.max_ctas)
+
+    # --- worker state resident in HBM, synthetic inputs
+    init = co2.synth(mode, n, worker=rank)[3]  # x_{0,tau}: the params the reduce sums
+    w = co2.Worker(mode, n, init, keep_gap=False)
+    del init
+    w.snapshot_start()
+    w.snapshot_first()
+    co2.co2_round([w], eng, hyper, tau)  # round 0: snapshots, launches the first reduce
+    from paper_2401_16265_b200 import _lib as L
+    co2.check(co2.lib().co2_synth(mode, 7, rank, 0, n, w.buffer(L.BUF_ANCHOR).data_ptr(),
+                                  w.buffer(L.BUF_PREV_X0).data_ptr(),
+                                  w.buffer(L.BUF_PREV_X1).data_ptr(), None,
+                                  w.buffer(L.BUF_MOMENTUM).data_ptr(), stream.cuda_stream))
+    torch.cuda.synchronize()
+    w.enable_timing(max(args.steps, 1) + max(args.warmup, 0) + 8)
+
+    for _ in range(args.warmup):
+        co2.co2_round([w], eng, hyper, tau, sync=False)
+    torch.cuda.synchronize()
+    w.step_times()  # drop warm-up launches
+    n_events_before = len(eng.events()) if world > 1 else 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            co2.co2_round([w], eng, hyper, tau, sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    kt = w.step_times()
+    r = co2.L.RoundResult()
+    arr = (co2.C.c_void_p * 1)(w.handle.value)
+    co2.check(co2.lib().co2_round_finish(arr, 1, stream.cuda_stream, co2.C.byref(r)))
+
+    # exposed communication (reference definition: 100 * sum(stall) / sum(waited comm))
+    comm = None
+    if world > 1:
+        ev = eng.events()[n_events_before:]
+        launches = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "launch"}
+        completes = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "complete"}
+        waits = [e for e in ev if e["event"] == "wait"]
+        stall = sum(e["stall"] for e in waits)
+        waited = sum(completes[e["handle_id"]] - launches[e["handle_id"]] for e in waits
+                     if e["handle_id"] in launches and e["handle_id"] in completes)
+        comm = {"exposed_pct": 100.0 * stall / waited if waited > 0 else 0.0,
+                "stall_ms_per_step": 1e3 * stall / max(len(waits), 1),
+                "allreduce_ms": 1e3 * waited / max(len(waits), 1),
+                "allreduce_bytes": n * (2 if mode == 2 else 4 if mode == 1 else 8),
+                "note": "no inner-loop compute in this step: the reduce overlaps only the "
+                        "outer step itself (tau*t_comp = 0 worst case); see "
+                        "tools/overlap_sweep.py for the tau sweep"}
+
+    t_tensor = torch.tensor([elapsed, statistics.mean(kt) if kt else 0.0], device="cuda",
+                            dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
+    t_max, k_max = t_tensor.tolist()
+    value = world * n * args.steps / t_max
+    peak, peak_kind = peaks()
+    achieved = bpp * n / k_max / 1e9 if k_max else None
+
+    # --- e2e through the host-buffer entry (pinned H2D + kernel + D2H timed)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist)
+
+    # --- CPU baseline (rank 0, N=1 only): single-core reference restatement
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        v, t = time_cpu_step(cfg, args.cpu_sample, 1, 3, 1)
+        cpu = {"value": v, "unit": "params/s", "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_sample} coordinates of the same synthetic inputs (fp64 "
+                         "upcast), reference unfused passes + fresh temporaries, 1 thread, "
+                         f"{t:.2f} s per step"}
+
+    if rank == 0:
+        line = {
+            "metric": "CO2 outer-step params/s", "value": value, "unit": "params/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if mode != 0 else "f64",
+            "data": "synthetic (counter-SplitMix64 uniforms, SURVEY.md 8d)",
+            "config": {"workload": cfg["workload"], "n_params_per_gpu": n, "tau": tau,
+                       "storage": cfg["storage"], "hyper": HYPER,
+                       "parallelism": f"dp{world} (one CO2 worker per GPU, NCCL all-reduce)",
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "step": "co2_round: AAR launch + stale wait + fused outer step"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None,
+                         "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "fused_step_kernel<ModeBF16>" if mode == 2 else
+                         "fused_step_kernel", "kernel_ms": k_max * 1e3,
+                         "bytes_per_param": bpp},
+            "e2e": e2e, "cpu_baseline": cpu, "comm": comm,
+            "gpu_launches": world * args.steps,
+            "clocks": clk.summary(),
+            "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step,
+                     "n_clipped": r.n_clipped, "n_floored": r.n_floored},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist):
+    """Same metric through co2_outer_step_host: every step copies this step's
+    inputs host->device from pinned memory and reads the results back."""
+    st = co2.STATE_TORCH[mode]
+    lo = co2.LOW_TORCH[mode]
+    x, p0, p1, xe, m = co2.synth(mode, n, worker=rank)
+    hx = torch.empty(n, dtype=st, pin_memory=True)
+    hp0 = torch.empty(n, dtype=st, pin_memory=True)
+    hm = torch.empty(n, dtype=st, pin_memory=True)
+    hp1 = torch.empty(n, dtype=lo, pin_memory=True)
+    hxe = torch.empty(n, dtype=lo, pin_memory=True)
+    hparams = torch.empty(n, dtype=lo, pin_memory=True)
+    for h, d in ((hx, x), (hp0, p0), (hm, m), (hp1, p1), (hxe, xe)):
+        h.copy_(d)
+    del x, p0, p1, xe, m
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    times = []
+    for i in range(args.e2e_steps + 1):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        # anchor_out aliases prev_x0 (the rotation layout), momentum in place
+        co2.outer_step_host(mode, hx, hp0, hp1, hxe, hm, hyper, tau, anchor_out=hp0,
+                            params_out=hparams, chunk=1 << 25, nstreams=3)
+        dt = time.perf_counter() - t0
+        if i > 0:
+            times.append(dt)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sb = 8 if mode == 0 else 4
+    lb = 8 if mode == 0 else (4 if mode == 1 else 2)
+    return {"value": world * n / t.item(), "unit": "params/s",
+            "h2d_bytes_per_step": n * (3 * sb + 2 * lb), "d2h_bytes_per_step": n * (2 * sb + lb),
+            "ms_per_step": 1e3 * t.item(),
+            "api": "co2_outer_step_host (pinned host buffers, 3 streams, 32M-coordinate chunks)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

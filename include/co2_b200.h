@@ -1,0 +1,305 @@
+/*
+ * co2_b200.h -- C ABI of the B200-native CO2 outer-step hot path.
+ *
+ * Drop-in boundary for the reference's C++ operator API (paths relative to
+ * /root/reference/).  Each entry point names the reference interface it
+ * replaces.  No exceptions and no torch/CUDA types cross this boundary: device
+ * buffers are plain pointers, streams are `void*` (a cudaStream_t, NULL = the
+ * legacy default stream), sizes are int64 element counts.
+ *
+ * Error convention (proj/include/co2sim/errors.hpp:8-20):
+ *   CO2_ERR_VALIDATION (2) <-> validation_error   (CLI exit 2)
+ *   CO2_ERR_NUMERIC    (3) <-> numeric_error      (CLI exit 3)
+ * with co2_last_error() returning the reference's exact message text.
+ * Host-checkable validation happens before any launch; numeric checks are
+ * device flags read back by co2_diag_fetch / the synchronous entry points.
+ *
+ * Threading: every launch is asynchronous on the caller's stream.  A
+ * workspace (device scratch for the deterministic block-reduction finish)
+ * must not be used by two streams concurrently.  co2_last_error() is
+ * thread-local.
+ */
+#ifndef CO2_B200_H
+#define CO2_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CO2_ABI_VERSION 1
+
+typedef int32_t co2_status_t;
+enum {
+  CO2_OK = 0,
+  CO2_ERR_VALIDATION = 2, /* validation_error */
+  CO2_ERR_NUMERIC = 3,    /* numeric_error */
+  CO2_ERR_CUDA = 4,
+  CO2_ERR_NCCL = 5
+};
+
+/* Storage/compute modes of the fused step.
+ *   F64        every buffer fp64, fp64 arithmetic: bit-identical to the
+ *              reference's fp64 semantics.
+ *   F32        every buffer fp32, fp32 arithmetic.
+ *   BF16_MIXED x_t0 / prev_x0 / momentum / anchor / gap fp32 ("state"),
+ *              prev_x1 / xbar / params bf16 ("low"), fp32 arithmetic. */
+typedef enum { CO2_MODE_F64 = 0, CO2_MODE_F32 = 1, CO2_MODE_BF16_MIXED = 2 } co2_mode_t;
+typedef enum { CO2_DTYPE_F64 = 0, CO2_DTYPE_F32 = 1, CO2_DTYPE_BF16 = 2 } co2_dtype_t;
+
+/* Device flag bits (OR over coordinates), mapped to the reference's error
+ * precedence by co2_diag_status. */
+enum {
+  CO2_FLAG_GAP_NONFINITE = 1u,   /* outer_algorithms.cpp:62  numeric  */
+  CO2_FLAG_GAP_BELOW_ONE = 2u,   /* outer_algorithms.cpp:81  validation */
+  CO2_FLAG_M_NONFINITE = 4u,     /* outer_algorithms.cpp:88  numeric  */
+  CO2_FLAG_CLIP_NONFINITE = 8u,  /* param_ops.cpp:41         numeric  */
+  CO2_FLAG_X_NONFINITE = 16u,    /* outer_algorithms.cpp:106 numeric  */
+  CO2_FLAG_AVG_NONFINITE = 32u   /* param_ops.cpp:31         numeric  */
+};
+
+/* Co2Hyper (proj/include/co2sim/outer_algorithms.hpp:17-30) plus tau. */
+typedef struct co2_hyper {
+  double alpha, beta, phi, epsilon;
+  int32_t tau;
+  uint8_t penalty, clip, ghost_consistent, pad;
+} co2_hyper_t;
+
+/* Round diagnostics (RoundResult min_gap / max_outer_step,
+ * outer_algorithms.hpp:63-69) plus decision counts and flags. */
+typedef struct co2_diag {
+  double min_gap;        /* +inf when n == 0 */
+  double max_outer_step; /* max_j |x'_j - x_t0_j| */
+  int64_t n_clipped;     /* coordinates with |m'| > phi (clip on) */
+  int64_t n_floored;     /* coordinates with tau*|p1 - p0| < epsilon */
+  uint32_t flags;
+  uint32_t pad;
+} co2_diag_t;
+
+const char* co2_last_error(void);
+int32_t co2_abi_version(void);
+
+/* Co2Hyper::validate (proj/src/outer_algorithms.cpp:37-46). */
+co2_status_t co2_hyper_validate(const co2_hyper_t* hyper);
+
+/* ---- workspace -------------------------------------------------------- */
+size_t co2_workspace_bytes(void);
+/* Zero a caller-allocated device workspace (once, before first use). */
+co2_status_t co2_workspace_init(void* workspace, void* stream);
+/* Async copy of the last launch's diagnostics into host memory (pinned for
+ * true asynchrony); valid after the stream is synchronized. */
+co2_status_t co2_diag_fetch_async(const void* workspace, co2_diag_t* host_out, void* stream);
+/* Synchronous: fetch, synchronize the stream, return co2_diag_status(). */
+co2_status_t co2_diag_fetch(const void* workspace, co2_diag_t* host_out, void* stream);
+/* Map flags to the reference's first error (precedence: staleness_gap
+ * numeric, gap<1 validation, momentum numeric, clip input numeric,
+ * outer_iterate numeric, average numeric). */
+co2_status_t co2_diag_status(const co2_diag_t* diag);
+
+/* ---- the fused outer step ---------------------------------------------- */
+/* Replaces co2_round's per-worker body (proj/src/outer_algorithms.cpp:186-202):
+ *   staleness_gap (outer_algorithms.hpp:37-38) -> delta = prev_x0 - xbar
+ *   (cpp:189) -> penalized_momentum_update (hpp:43-46) -> outer_iterate
+ *   (hpp:49-50) -> min_gap / max_outer_step (cpp:194-196),
+ * in ONE pass over HBM.  xbar is the consumed all-reduce: the average
+ * (xbar_divisor = 1) or the worker sum (xbar_divisor = G; divided once, as
+ * average() does, param_ops.cpp:30).  momentum is updated in place.
+ * anchor_out (state dtype) receives x_{t+1,0} and may alias prev_x0 (the
+ * snapshot rotation then becomes a pointer swap); params_out (low dtype)
+ * receives x_{t+1,0} and may alias xbar.  gap_out (state dtype) receives
+ * Lambda (fixture / debug only).  Any of the three outputs may be NULL.
+ * Asynchronous; diagnostics land in the workspace. */
+co2_status_t co2_outer_step(co2_mode_t mode, int64_t n, const void* x_t0, const void* prev_x0,
+                            const void* prev_x1, const void* xbar, int32_t xbar_divisor,
+                            void* momentum, void* anchor_out, void* params_out, void* gap_out,
+                            const co2_hyper_t* hyper, void* workspace, void* stream);
+
+/* End-to-end form of co2_outer_step over HOST buffers (the reference's own
+ * calling convention: host vectors in, host vectors out).  Streams the
+ * coordinates through the GPU in chunks with H2D / compute / D2H overlapped
+ * on `nstreams` streams (1..4).  Pinned host buffers give full PCIe speed.
+ * Synchronous; returns the diagnostics' status and fills *diag_out. */
+co2_status_t co2_outer_step_host(co2_mode_t mode, int64_t n, const void* x_t0,
+                                 const void* prev_x0, const void* prev_x1, const void* xbar,
+                                 int32_t xbar_divisor, void* momentum, void* anchor_out,
+                                 void* params_out, const co2_hyper_t* hyper, int64_t chunk,
+                                 int32_t nstreams, co2_diag_t* diag_out);
+
+/* ---- unfused reference operators (per-op parity) ------------------------ */
+/* All buffers of dtype dt; asynchronous; flags in the workspace.  Scalar
+ * validation (tau, epsilon, beta, alpha, phi) happens here, before launch. */
+/* staleness_gap: proj/include/co2sim/outer_algorithms.hpp:37-38 */
+co2_status_t co2_staleness_gap(co2_dtype_t dt, int64_t n, const void* x_t0, const void* prev_x0,
+                               const void* prev_x1, int32_t tau, double epsilon, void* gap_out,
+                               void* workspace, void* stream);
+/* penalized_momentum_update: outer_algorithms.hpp:43-46 */
+co2_status_t co2_penalized_momentum(co2_dtype_t dt, int64_t n, const void* m_prev, double beta,
+                                    const void* gap, const void* delta, int32_t penalty,
+                                    void* m_out, void* workspace, void* stream);
+/* outer_iterate: outer_algorithms.hpp:49-50 */
+co2_status_t co2_outer_iterate(co2_dtype_t dt, int64_t n, const void* x_t0, double alpha,
+                               const void* m, double phi, int32_t clip, void* x_out,
+                               void* workspace, void* stream);
+/* clip_elementwise: proj/include/co2sim/param_ops.hpp:23-24 */
+co2_status_t co2_clip_elementwise(co2_dtype_t dt, int64_t n, const void* v, double phi,
+                                  void* out, void* workspace, void* stream);
+/* average: proj/include/co2sim/param_ops.hpp:16-21.  contributions is a
+ * HOST array of g device pointers (g <= 64), summed in ascending index
+ * order and divided by g once.  F64: fp64; F32: fp32; BF16: fp32
+ * accumulation, one rounding to bf16. */
+co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const* contributions, int64_t n,
+                         void* out, void* workspace, void* stream);
+/* a - b elementwise (the delta of outer_algorithms.cpp:189) */
+co2_status_t co2_sub(co2_dtype_t dt, int64_t n, const void* a, const void* b, void* out,
+                     void* stream);
+/* dst[j] = convert(src[j]) (snapshot copies, InnerTrace contract
+ * proj/src/inner_loop.cpp:73,96-100) */
+co2_status_t co2_convert(co2_dtype_t dst_dt, void* dst, co2_dtype_t src_dt, const void* src,
+                         int64_t n, void* stream);
+
+/* ---- synthetic inputs ------------------------------------ */
+/* Counter-SplitMix64 generator of RngStream (proj/include/co2sim/rng.hpp:
+ * 12-54) in random-access form; fills coordinates [j0, j0+count) of one
+ * worker's buffers in the mode's storage dtypes.  Any pointer may be NULL. */
+co2_status_t co2_synth(co2_mode_t mode, uint64_t seed, int32_t worker, int64_t j0, int64_t count,
+                       void* x_t0, void* prev_x0, void* prev_x1, void* x_end, void* momentum,
+                       void* stream);
+/* Inner-step stand-in x <- x - lr * g with g = scale*(2U-1) drawn from the
+ * counter stream (seed, (5<<32)|worker, draw offset j + step*n).  Used by
+ * the schedule benchmarks as the local compute the all-reduce overlaps. */
+co2_status_t co2_synthetic_inner_step(co2_dtype_t dt, int64_t n, void* params, double lr,
+                                      double scale, uint64_t seed, int32_t worker, int64_t step,
+                                      int32_t repeat, void* stream);
+/* Fill a buffer with a constant (L2 flush helper for benchmarks). */
+co2_status_t co2_fill_u32(void* dst, uint32_t value, int64_t count, void* stream);
+
+/* ---- timing model (proj/src/timing_model.cpp:27-43,107-123) ------------- */
+/* ClusterSpec (proj/include/co2sim/timing_model.hpp:14-25). */
+typedef struct co2_cluster {
+  int32_t workers, gpus_per_node;
+  double t_comp, t_outer, param_bytes, inter_bandwidth, latency;
+  int32_t has_measured_override;
+  double measured_override;
+} co2_cluster_t;
+typedef struct co2_round_timing {
+  int32_t t;
+  double start, stall, end;
+} co2_round_timing_t;
+typedef struct co2_timeline {
+  int32_t workers, tau, rounds, batch_size;
+  double comm_time, wall_time, total_stall, overlap_ratio_achieved, throughput;
+} co2_timeline_t;
+co2_status_t co2_cluster_validate(const co2_cluster_t* spec);
+co2_status_t co2_allreduce_time(const co2_cluster_t* spec, double* out);
+co2_status_t co2_overlap_ratio(int32_t tau, double t_comp, double t_comm, double* out);
+/* simulate_timeline(AlgorithmKind::co2, ...); per_round (nullable) must hold
+ * `rounds` entries. */
+co2_status_t co2_simulate_timeline_co2(const co2_cluster_t* spec, int32_t tau, int32_t rounds,
+                                       int32_t batch_size, co2_timeline_t* out,
+                                       co2_round_timing_t* per_round);
+
+/* ---- one-step-stale all-reduce engine (CollectiveEngine,
+ *      proj/include/co2sim/collective.hpp:54-93) ----------------------------
+ * A handle is launched after the compute stream's current work (event
+ * fence), runs on the engine's own high-priority comm stream, and is
+ * consumed exactly once by co2_aar_wait, which makes the consumer stream
+ * wait on its completion event.  At most two handles are live (the
+ * reference's overlap window, collective.cpp:39-42).
+ * Transports:
+ *   NCCL  one rank per GPU; in-place ncclAllReduce(sum) of the buffer; the
+ *         consumer divides by world size (co2_outer_step xbar_divisor).
+ *   LOCAL G simulated workers on one GPU; fixed-order average kernel of the
+ *         G contribution buffers into `out` (bitwise the reference average).
+ */
+typedef struct co2_aar co2_aar_t;
+#define CO2_NCCL_ID_BYTES 128
+co2_status_t co2_nccl_unique_id(uint8_t id_out[CO2_NCCL_ID_BYTES]);
+co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO2_NCCL_ID_BYTES],
+                                 int32_t rank, int32_t world, int32_t max_ctas);
+co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers);
+co2_status_t co2_aar_destroy(co2_aar_t* engine);
+int32_t co2_aar_world(const co2_aar_t* engine);
+/* launch_all_reduce (collective.cpp:31-58).  NCCL: bufs[0] is reduced in
+ * place (sum) and out must equal bufs[0] or be NULL.  LOCAL: bufs holds
+ * `workers` device pointers, out receives the average. */
+co2_status_t co2_aar_launch(co2_aar_t* engine, co2_dtype_t dt, const void* const* bufs,
+                            void* out, int64_t n, void* producer_stream, uint64_t* handle_out);
+/* is_completed (collective.cpp:74-86): non-blocking cudaEventQuery. */
+co2_status_t co2_aar_poll(co2_aar_t* engine, uint64_t handle, int32_t* done);
+/* wait (collective.cpp:88-105): consumer stream waits on completion;
+ * consume-once.  Stall is measured on the device (events straddling the
+ * wait) and is readable with co2_aar_stall once the consumer passed it. */
+co2_status_t co2_aar_wait(co2_aar_t* engine, uint64_t handle, void* consumer_stream);
+co2_status_t co2_aar_stall(co2_aar_t* engine, uint64_t handle, double* stall_seconds,
+                           double* comm_seconds);
+co2_status_t co2_aar_live(const co2_aar_t* engine, int32_t* live);
+/* Blocking all-reduce (sum) on the given stream; used by ghost-consistent
+ * mode for the averaged snapshots (outer_algorithms.cpp:163-169). */
+co2_status_t co2_aar_allreduce_blocking(co2_aar_t* engine, co2_dtype_t dt, void* buf, int64_t n,
+                                        void* stream);
+/* Event log (collective.hpp:24-29): kind 0 launch, 1 complete, 2 wait;
+ * t is seconds since engine creation on the device clock. */
+typedef struct co2_event {
+  int32_t kind;
+  int32_t pad;
+  uint64_t handle;
+  double t, stall;
+} co2_event_t;
+co2_status_t co2_aar_events(co2_aar_t* engine, co2_event_t* out, int64_t cap, int64_t* count);
+
+/* ---- worker state + co2_round (outer_algorithms.cpp:110-211) ------------- */
+/* Device-resident worker: ping-pong params, anchor x_{t,0}, x_{t,1}
+ * snapshot, prev_x0, prev_x1, momentum, gap.  The inner loop mutates the
+ * buffer returned by co2_worker_params(); the snapshot hooks capture the
+ * InnerTrace contract (proj/include/co2sim/inner_loop.hpp:51-61). */
+typedef struct co2_worker co2_worker_t;
+enum {
+  CO2_BUF_PARAMS = 0,  /* current working params (low dtype) */
+  CO2_BUF_ANCHOR = 1,  /* x_{t,0} (state dtype) */
+  CO2_BUF_XFIRST = 2,  /* x_{t,1} (low dtype) */
+  CO2_BUF_PREV_X0 = 3, /* state dtype */
+  CO2_BUF_PREV_X1 = 4, /* low dtype */
+  CO2_BUF_MOMENTUM = 5,/* state dtype */
+  CO2_BUF_GAP = 6,     /* state dtype */
+  CO2_BUF_XBAR = 7     /* last consumed all-reduce result (low dtype; NCCL: the sum) */
+};
+/* init_params: device buffer in the low dtype (or NULL for zeros). */
+co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, int64_t n,
+                               const void* init_params, int32_t keep_gap, void* stream);
+co2_status_t co2_worker_destroy(co2_worker_t* w);
+void* co2_worker_buffer(co2_worker_t* w, int32_t which);
+int32_t co2_worker_round(const co2_worker_t* w);
+/* Snapshot hooks: x_{t,0} <- params (call before the first inner step;
+ * a no-op for t >= 1 where the outer step already wrote the anchor), and
+ * x_{t,1} <- params (call after the first inner step). */
+co2_status_t co2_worker_snapshot_start(co2_worker_t* w, void* stream);
+co2_status_t co2_worker_snapshot_first(co2_worker_t* w, void* stream);
+typedef struct co2_round_result {
+  double stall_seconds; /* device-measured, 0 when not yet available */
+  int32_t outer_applied;
+  int32_t pad;
+  double min_gap, max_outer_step;
+  int64_t n_clipped, n_floored;
+} co2_round_result_t;
+/* co2_round over the `g` workers this process owns (g == engine workers
+ * for LOCAL, g == 1 for NCCL).  Synchronous only when `sync` != 0 (then
+ * diagnostics and errors are reported); otherwise the diagnostics are read
+ * by co2_round_finish. */
+co2_status_t co2_round(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,
+                       const co2_hyper_t* hyper, void* stream, int32_t sync,
+                       co2_round_result_t* result);
+co2_status_t co2_round_finish(co2_worker_t* const* workers, int32_t g, void* stream,
+                              co2_round_result_t* result);
+/* Device timing of the fused outer-step launch inside co2_round: events
+ * bracket the kernel on the round's stream (a ring of `cap` pairs).
+ * co2_worker_step_times synchronizes on the recorded events and returns the
+ * durations (seconds) since the previous call, oldest first. */
+co2_status_t co2_worker_enable_timing(co2_worker_t* w, int32_t cap);
+co2_status_t co2_worker_step_times(co2_worker_t* w, double* out, int32_t cap, int32_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CO2_B200_H */

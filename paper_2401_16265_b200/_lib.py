@@ -1,0 +1,166 @@
+"""ctypes binding of the C ABI declared in include/co2_b200.h.
+
+The shared library is built in-tree (``make`` at the repo root, or
+``__graft_entry__.build()``).  There is no fallback: if the library is
+missing or stale every entry point raises, loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libco2b200.so")
+
+OK, ERR_VALIDATION, ERR_NUMERIC, ERR_CUDA, ERR_NCCL = 0, 2, 3, 4, 5
+MODE_F64, MODE_F32, MODE_BF16_MIXED = 0, 1, 2
+DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
+FLAG_GAP_NONFINITE, FLAG_GAP_BELOW_ONE, FLAG_M_NONFINITE = 1, 2, 4
+FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
+BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
+BUF_MOMENTUM, BUF_GAP, BUF_XBAR = 5, 6, 7
+NCCL_ID_BYTES = 128
+
+
+class Hyper(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("beta", C.c_double), ("phi", C.c_double),
+                ("epsilon", C.c_double), ("tau", C.c_int32), ("penalty", C.c_uint8),
+                ("clip", C.c_uint8), ("ghost_consistent", C.c_uint8), ("pad", C.c_uint8)]
+
+
+class Diag(C.Structure):
+    _fields_ = [("min_gap", C.c_double), ("max_outer_step", C.c_double),
+                ("n_clipped", C.c_int64), ("n_floored", C.c_int64),
+                ("flags", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class Cluster(C.Structure):
+    _fields_ = [("workers", C.c_int32), ("gpus_per_node", C.c_int32), ("t_comp", C.c_double),
+                ("t_outer", C.c_double), ("param_bytes", C.c_double),
+                ("inter_bandwidth", C.c_double), ("latency", C.c_double),
+                ("has_measured_override", C.c_int32), ("measured_override", C.c_double)]
+
+
+class RoundTiming(C.Structure):
+    _fields_ = [("t", C.c_int32), ("start", C.c_double), ("stall", C.c_double),
+                ("end", C.c_double)]
+
+
+class Timeline(C.Structure):
+    _fields_ = [("workers", C.c_int32), ("tau", C.c_int32), ("rounds", C.c_int32),
+                ("batch_size", C.c_int32), ("comm_time", C.c_double), ("wall_time", C.c_double),
+                ("total_stall", C.c_double), ("overlap_ratio_achieved", C.c_double),
+                ("throughput", C.c_double)]
+
+
+class Event(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("handle", C.c_uint64),
+                ("t", C.c_double), ("stall", C.c_double)]
+
+
+class RoundResult(C.Structure):
+    _fields_ = [("stall_seconds", C.c_double), ("outer_applied", C.c_int32), ("pad", C.c_int32),
+                ("min_gap", C.c_double), ("max_outer_step", C.c_double),
+                ("n_clipped", C.c_int64), ("n_floored", C.c_int64)]
+
+
+P, I32, I64, U64, D, U8P = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_char_p
+ST = C.c_int32
+
+# name -> (restype, argtypes); exactly the symbols of include/co2_b200.h
+SIGNATURES = {
+    "co2_last_error": (C.c_char_p, []),
+    "co2_abi_version": (I32, []),
+    "co2_hyper_validate": (ST, [C.POINTER(Hyper)]),
+    "co2_workspace_bytes": (C.c_size_t, []),
+    "co2_workspace_init": (ST, [P, P]),
+    "co2_diag_fetch_async": (ST, [P, C.POINTER(Diag), P]),
+    "co2_diag_fetch": (ST, [P, C.POINTER(Diag), P]),
+    "co2_diag_status": (ST, [C.POINTER(Diag)]),
+    "co2_outer_step": (ST, [I32, I64, P, P, P, P, I32, P, P, P, P, C.POINTER(Hyper), P, P]),
+    "co2_outer_step_host": (ST, [I32, I64, P, P, P, P, I32, P, P, P, C.POINTER(Hyper), I64, I32,
+                                 C.POINTER(Diag)]),
+    "co2_staleness_gap": (ST, [I32, I64, P, P, P, I32, D, P, P, P]),
+    "co2_penalized_momentum": (ST, [I32, I64, P, D, P, P, I32, P, P, P]),
+    "co2_outer_iterate": (ST, [I32, I64, P, D, P, D, I32, P, P, P]),
+    "co2_clip_elementwise": (ST, [I32, I64, P, D, P, P, P]),
+    "co2_average": (ST, [I32, I32, C.POINTER(P), I64, P, P, P]),
+    "co2_sub": (ST, [I32, I64, P, P, P, P]),
+    "co2_convert": (ST, [I32, P, I32, P, I64, P]),
+    "co2_synth": (ST, [I32, U64, I32, I64, I64, P, P, P, P, P, P]),
+    "co2_synthetic_inner_step": (ST, [I32, I64, P, D, D, U64, I32, I64, I32, P]),
+    "co2_fill_u32": (ST, [P, C.c_uint32, I64, P]),
+    "co2_cluster_validate": (ST, [C.POINTER(Cluster)]),
+    "co2_allreduce_time": (ST, [C.POINTER(Cluster), C.POINTER(D)]),
+    "co2_overlap_ratio": (ST, [I32, D, D, C.POINTER(D)]),
+    "co2_simulate_timeline_co2": (ST, [C.POINTER(Cluster), I32, I32, I32, C.POINTER(Timeline),
+                                       C.POINTER(RoundTiming)]),
+    "co2_nccl_unique_id": (ST, [C.POINTER(C.c_uint8)]),
+    "co2_aar_create_nccl": (ST, [C.POINTER(P), C.POINTER(C.c_uint8), I32, I32, I32]),
+    "co2_aar_create_local": (ST, [C.POINTER(P), I32]),
+    "co2_aar_destroy": (ST, [P]),
+    "co2_aar_world": (I32, [P]),
+    "co2_aar_launch": (ST, [P, I32, C.POINTER(P), P, I64, P, C.POINTER(U64)]),
+    "co2_aar_poll": (ST, [P, U64, C.POINTER(I32)]),
+    "co2_aar_wait": (ST, [P, U64, P]),
+    "co2_aar_stall": (ST, [P, U64, C.POINTER(D), C.POINTER(D)]),
+    "co2_aar_live": (ST, [P, C.POINTER(I32)]),
+    "co2_aar_allreduce_blocking": (ST, [P, I32, P, I64, P]),
+    "co2_aar_events": (ST, [P, C.POINTER(Event), I64, C.POINTER(I64)]),
+    "co2_worker_create": (ST, [C.POINTER(P), I32, I64, P, I32, P]),
+    "co2_worker_destroy": (ST, [P]),
+    "co2_worker_buffer": (P, [P, I32]),
+    "co2_worker_round": (I32, [P]),
+    "co2_worker_snapshot_start": (ST, [P, P]),
+    "co2_worker_snapshot_first": (ST, [P, P]),
+    "co2_round": (ST, [C.POINTER(P), I32, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),
+    "co2_round_finish": (ST, [C.POINTER(P), I32, P, C.POINTER(RoundResult)]),
+    "co2_worker_enable_timing": (ST, [P, I32]),
+    "co2_worker_step_times": (ST, [P, C.POINTER(D), I32, C.POINTER(I32)]),
+}
+
+
+class ValidationError(RuntimeError):
+    """co2sim::validation_error (proj/include/co2sim/errors.hpp:8-13)."""
+
+
+class NumericError(RuntimeError):
+    """co2sim::numeric_error (proj/include/co2sim/errors.hpp:15-20)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libco2b200.so (no fallback: raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+                "the CO2 outer step has no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.co2_abi_version() != 1:
+            raise ImportError("libco2b200.so ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def check(code: int) -> None:
+    """Map a co2_status_t to the reference's exception types."""
+    if code == OK:
+        return
+    msg = lib().co2_last_error().decode()
+    if code == ERR_VALIDATION:
+        raise ValidationError(msg)
+    if code == ERR_NUMERIC:
+        raise NumericError(msg)
+    raise CudaError(f"status {code}: {msg}")

@@ -1,0 +1,474 @@
+"""Python mirror of the reference's CO2 operator API over device buffers.
+
+Same names, argument meaning and error behaviour as the reference
+(paths relative to /root/reference/):
+
+  staleness_gap              proj/include/co2sim/outer_algorithms.hpp:37-38
+  penalized_momentum_update  proj/include/co2sim/outer_algorithms.hpp:43-46
+  outer_iterate              proj/include/co2sim/outer_algorithms.hpp:49-50
+  clip_elementwise, average  proj/include/co2sim/param_ops.hpp:16-24
+  Co2Hyper                   proj/include/co2sim/outer_algorithms.hpp:17-30
+  CollectiveEngine           proj/include/co2sim/collective.hpp:54-93
+  co2_round                  proj/include/co2sim/outer_algorithms.hpp:77-81
+  allreduce_time, overlap_ratio, simulate_timeline (co2)
+                             proj/include/co2sim/timing_model.hpp:27-72
+
+Everything runs through the C ABI (include/co2_b200.h) into the sm_100a
+kernels of libco2b200.so; torch supplies device memory and streams only.
+ParamVector becomes a 1-D CUDA tensor (float64 / float32 / bfloat16).  The
+per-op functions are synchronous like the reference (they return after the
+device flags were read so they can raise); the fused `outer_step` is
+asynchronous unless `check=True`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib as L
+from ._lib import NumericError, ValidationError, check, lib  # noqa: F401
+
+MODE_F64, MODE_F32, MODE_BF16_MIXED = L.MODE_F64, L.MODE_F32, L.MODE_BF16_MIXED
+
+_DT = {torch.float64: L.DTYPE_F64, torch.float32: L.DTYPE_F32, torch.bfloat16: L.DTYPE_BF16}
+STATE_TORCH = {MODE_F64: torch.float64, MODE_F32: torch.float32, MODE_BF16_MIXED: torch.float32}
+LOW_TORCH = {MODE_F64: torch.float64, MODE_F32: torch.float32, MODE_BF16_MIXED: torch.bfloat16}
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValidationError("buffers must be contiguous CUDA tensors")
+    return t.data_ptr()
+
+
+def _dtype(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ValidationError(f"unsupported dtype {t.dtype}") from None
+
+
+class Workspace:
+    """Device scratch for the deterministic block-reduction finish plus a
+    pinned diagnostics mirror.  One per stream."""
+
+    def __init__(self, device=None):
+        nbytes = lib().co2_workspace_bytes()
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device or "cuda")
+        self.diag = L.Diag()
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def fetch(self, stream=None) -> L.Diag:
+        """Synchronize and return the last launch's diagnostics (raises
+        with the reference's message on flags)."""
+        check(lib().co2_diag_fetch(self.ptr, C.byref(self.diag), _stream(stream)))
+        return self.diag
+
+
+_ws_cache: dict = {}
+
+
+def _ws(device=None) -> Workspace:
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    if dev not in _ws_cache:
+        _ws_cache[dev] = Workspace(device=f"cuda:{dev}")
+    return _ws_cache[dev]
+
+
+# ------------------------------------------------------------------ hyper
+@dataclass
+class Co2Hyper:
+    """Co2Hyper (proj/include/co2sim/outer_algorithms.hpp:17-30)."""
+
+    alpha: float = 1.0
+    beta: float = 0.7
+    phi: float = 1.0
+    epsilon: float = 1e-12
+    penalty: bool = True
+    clip: bool = True
+    ghost_consistent: bool = False
+
+    def c(self, tau: int = 1) -> L.Hyper:
+        return L.Hyper(self.alpha, self.beta, self.phi, self.epsilon, int(tau), int(self.penalty),
+                       int(self.clip), int(self.ghost_consistent), 0)
+
+    def validate(self) -> None:
+        """Co2Hyper::validate (proj/src/outer_algorithms.cpp:37-46)."""
+        h = self.c()
+        check(lib().co2_hyper_validate(C.byref(h)))
+
+
+# ------------------------------------------------------------- unfused ops
+def _same_len(*ts, msg: str):
+    n = ts[0].numel()
+    for t in ts[1:]:
+        if t.numel() != n:
+            raise ValidationError(msg)
+    return n
+
+
+def staleness_gap(x_t0, prev_x0, prev_x1, tau: int, epsilon: float, *, stream=None):
+    """staleness_gap (proj/src/outer_algorithms.cpp:48-64)."""
+    if tau < 1:
+        raise ValidationError("staleness_gap: tau must be >= 1")
+    if not epsilon > 0.0:
+        raise ValidationError("staleness_gap: epsilon must be positive")
+    n = _same_len(x_t0, prev_x0, prev_x1, msg="staleness_gap: dimensions differ")
+    out = torch.empty_like(x_t0)
+    ws = _ws(x_t0.device)
+    check(lib().co2_staleness_gap(_dtype(x_t0), n, _ptr(x_t0), _ptr(prev_x0), _ptr(prev_x1), tau,
+                                  epsilon, _ptr(out), ws.ptr, _stream(stream)))
+    ws.fetch(stream)
+    return out
+
+
+def penalized_momentum_update(m_prev, beta: float, gap, delta, penalty_enabled: bool, *,
+                              stream=None):
+    """penalized_momentum_update (proj/src/outer_algorithms.cpp:66-90)."""
+    if beta < 0.0 or beta >= 1.0:
+        raise ValidationError("momentum update: beta must lie in [0, 1)")
+    n = _same_len(m_prev, delta, msg="momentum update: dimensions differ")
+    if penalty_enabled and gap.numel() != n:
+        raise ValidationError("momentum update: gap dimension differs")
+    out = torch.empty_like(m_prev)
+    ws = _ws(m_prev.device)
+    check(lib().co2_penalized_momentum(_dtype(m_prev), n, _ptr(m_prev), beta,
+                                       _ptr(gap if penalty_enabled else delta), _ptr(delta),
+                                       int(penalty_enabled), _ptr(out), ws.ptr, _stream(stream)))
+    ws.fetch(stream)
+    return out
+
+
+def outer_iterate(x_t0, alpha: float, m, phi: float, clip_enabled: bool, *, stream=None):
+    """outer_iterate (proj/src/outer_algorithms.cpp:92-108)."""
+    if not alpha > 0.0:
+        raise ValidationError("outer_iterate: alpha must be positive")
+    n = _same_len(x_t0, m, msg="outer_iterate: dimensions differ")
+    out = torch.empty_like(x_t0)
+    ws = _ws(x_t0.device)
+    check(lib().co2_outer_iterate(_dtype(x_t0), n, _ptr(x_t0), alpha, _ptr(m), phi,
+                                  int(clip_enabled), _ptr(out), ws.ptr, _stream(stream)))
+    ws.fetch(stream)
+    return out
+
+
+def clip_elementwise(v, phi: float, *, stream=None):
+    """clip_elementwise (proj/src/param_ops.cpp:35-43)."""
+    out = torch.empty_like(v)
+    ws = _ws(v.device)
+    check(lib().co2_clip_elementwise(_dtype(v), v.numel(), _ptr(v), phi, _ptr(out), ws.ptr,
+                                     _stream(stream)))
+    ws.fetch(stream)
+    return out
+
+
+def average(contributions, *, stream=None):
+    """average (proj/src/param_ops.cpp:16-33): ascending-order sum, one
+    division by G."""
+    if len(contributions) == 0:
+        raise ValidationError("average: empty contribution list")
+    n = _same_len(*contributions, msg="average: contribution dimensions differ")
+    out = torch.empty_like(contributions[0])
+    ptrs = (C.c_void_p * len(contributions))(*[_ptr(c) for c in contributions])
+    ws = _ws(out.device)
+    check(lib().co2_average(_dtype(out), len(contributions), ptrs, n, _ptr(out), ws.ptr,
+                            _stream(stream)))
+    ws.fetch(stream)
+    return out
+
+
+# ------------------------------------------------------------- fused step
+def outer_step(mode: int, x_t0, prev_x0, prev_x1, xbar, momentum, hyper: Co2Hyper, tau: int, *,
+               divisor: int = 1, anchor_out=None, params_out=None, gap_out=None,
+               workspace: Workspace | None = None, stream=None, check_flags: bool = True):
+    """Fused co2_round per-worker body (proj/src/outer_algorithms.cpp:186-196).
+    Updates `momentum` in place; returns the Diag when check_flags (after a
+    stream sync), else None (asynchronous)."""
+    n = _same_len(x_t0, prev_x0, prev_x1, xbar, momentum, msg="staleness_gap: dimensions differ")
+    for t in (anchor_out, params_out, gap_out):
+        if t is not None and t.numel() != n:
+            raise ValidationError("outer step: output dimension differs")
+    ws = workspace or _ws(x_t0.device)
+    h = hyper.c(tau)
+    check(lib().co2_outer_step(mode, n, _ptr(x_t0), _ptr(prev_x0), _ptr(prev_x1), _ptr(xbar),
+                               divisor, _ptr(momentum), _ptr(anchor_out), _ptr(params_out),
+                               _ptr(gap_out), C.byref(h), ws.ptr, _stream(stream)))
+    if check_flags:
+        return ws.fetch(stream)
+    return None
+
+
+def outer_step_host(mode: int, x_t0, prev_x0, prev_x1, xbar, momentum, hyper: Co2Hyper, tau: int,
+                    *, divisor: int = 1, anchor_out=None, params_out=None, chunk: int = 1 << 24,
+                    nstreams: int = 3) -> L.Diag:
+    """End-to-end fused step over HOST tensors (pinned for full PCIe rate):
+    the reference's own calling convention (host vectors in and out)."""
+    n = x_t0.numel()
+    d = L.Diag()
+    h = hyper.c(tau)
+
+    def hp(t):
+        return None if t is None else t.data_ptr()
+
+    check(lib().co2_outer_step_host(mode, n, hp(x_t0), hp(prev_x0), hp(prev_x1), hp(xbar), divisor,
+                                    hp(momentum), hp(anchor_out), hp(params_out), C.byref(h),
+                                    chunk, nstreams, C.byref(d)))
+    return d
+
+
+def synth(mode: int, n: int, *, seed: int = 7, worker: int = 0, j0: int = 0, device="cuda",
+          stream=None):
+    """Synthetic inputs generated on the device: returns
+    (x_t0, prev_x0, prev_x1, x_end, momentum)."""
+    st, lo = STATE_TORCH[mode], LOW_TORCH[mode]
+    x = torch.empty(n, dtype=st, device=device)
+    p0 = torch.empty(n, dtype=st, device=device)
+    m = torch.empty(n, dtype=st, device=device)
+    p1 = torch.empty(n, dtype=lo, device=device)
+    xe = torch.empty(n, dtype=lo, device=device)
+    check(lib().co2_synth(mode, seed, worker, j0, n, _ptr(x), _ptr(p0), _ptr(p1), _ptr(xe), _ptr(m),
+                          _stream(stream)))
+    return x, p0, p1, xe, m
+
+
+def synthetic_inner_step(params, *, lr: float, scale: float = 1.0, seed: int = 7, worker: int = 0,
+                         step: int = 0, repeat: int = 1, stream=None):
+    check(lib().co2_synthetic_inner_step(_dtype(params), params.numel(), _ptr(params), lr, scale,
+                                         seed, worker, step, repeat, _stream(stream)))
+
+
+# ------------------------------------------------------------ timing model
+@dataclass
+class ClusterSpec:
+    """ClusterSpec (proj/include/co2sim/timing_model.hpp:14-25)."""
+
+    workers: int = 1
+    gpus_per_node: int = 8
+    t_comp: float = 0.0
+    t_outer: float = 0.0
+    param_bytes: float = 0.0
+    inter_bandwidth: float = 1.0
+    latency: float = 0.0
+    measured_override: float | None = None
+
+    def c(self) -> L.Cluster:
+        mo = self.measured_override
+        return L.Cluster(self.workers, self.gpus_per_node, self.t_comp, self.t_outer,
+                         self.param_bytes, self.inter_bandwidth, self.latency,
+                         0 if mo is None else 1, 0.0 if mo is None else mo)
+
+    def validate(self) -> None:
+        s = self.c()
+        check(lib().co2_cluster_validate(C.byref(s)))
+
+
+def allreduce_time(spec: ClusterSpec) -> float:
+    s, out = spec.c(), C.c_double()
+    check(lib().co2_allreduce_time(C.byref(s), C.byref(out)))
+    return out.value
+
+
+def overlap_ratio(tau: int, t_comp: float, t_comm: float) -> float:
+    out = C.c_double()
+    check(lib().co2_overlap_ratio(tau, t_comp, t_comm, C.byref(out)))
+    return out.value
+
+
+@dataclass
+class TimelineReport:
+    workers: int
+    tau: int
+    rounds: int
+    batch_size: int
+    comm_time: float
+    wall_time: float
+    total_stall: float
+    overlap_ratio_achieved: float
+    throughput: float
+    per_round: list = field(default_factory=list)
+
+
+def simulate_timeline_co2(spec: ClusterSpec, tau: int, rounds: int,
+                          batch_size: int = 1) -> TimelineReport:
+    """simulate_timeline(AlgorithmKind::co2, ...) (proj/src/timing_model.cpp:76-123)."""
+    s, out = spec.c(), L.Timeline()
+    per = (L.RoundTiming * max(rounds, 1))()
+    check(lib().co2_simulate_timeline_co2(C.byref(s), tau, rounds, batch_size, C.byref(out), per))
+    return TimelineReport(out.workers, out.tau, out.rounds, out.batch_size, out.comm_time,
+                          out.wall_time, out.total_stall, out.overlap_ratio_achieved,
+                          out.throughput,
+                          [(per[i].t, per[i].start, per[i].stall, per[i].end)
+                           for i in range(rounds)])
+
+
+# ------------------------------------------------------- collective engine
+class CollectiveEngine:
+    """One-step-stale all-reduce (proj/include/co2sim/collective.hpp:54-93).
+
+    transport "local": G simulated workers on this GPU, fixed-order average.
+    transport "nccl":  one rank per GPU; in-place ncclAllReduce(sum)."""
+
+    def __init__(self, workers: int = 1, *, transport: str = "local", rank: int = 0,
+                 nccl_id: bytes | None = None, max_ctas: int = 0):
+        self.handle = C.c_void_p()
+        self.transport = transport
+        if transport == "local":
+            check(lib().co2_aar_create_local(C.byref(self.handle), workers))
+        elif transport == "nccl":
+            if nccl_id is None:
+                raise ValidationError("nccl transport needs the rank-0 unique id")
+            uid = (C.c_uint8 * L.NCCL_ID_BYTES)(*nccl_id)
+            check(lib().co2_aar_create_nccl(C.byref(self.handle), uid, rank, workers, max_ctas))
+        else:
+            raise ValidationError(f"unknown transport {transport}")
+        self.workers = workers
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * L.NCCL_ID_BYTES)()
+        check(lib().co2_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def close(self):
+        if self.handle:
+            lib().co2_aar_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launch_all_reduce(self, contributions, out=None, *, stream=None) -> int:
+        if self.transport == "local" and len(contributions) != self.workers:
+            raise ValidationError(
+                f"launch_all_reduce: contribution count {len(contributions)} does not match "
+                f"worker count {self.workers}")
+        ptrs = (C.c_void_p * len(contributions))(*[_ptr(c) for c in contributions])
+        h = C.c_uint64()
+        check(lib().co2_aar_launch(self.handle, _dtype(contributions[0]), ptrs, _ptr(out),
+                                   contributions[0].numel(), _stream(stream), C.byref(h)))
+        return h.value
+
+    def is_completed(self, handle: int) -> bool:
+        d = C.c_int32()
+        check(lib().co2_aar_poll(self.handle, handle, C.byref(d)))
+        return bool(d.value)
+
+    def wait(self, handle: int, *, stream=None) -> None:
+        check(lib().co2_aar_wait(self.handle, handle, _stream(stream)))
+
+    def stall(self, handle: int) -> tuple[float, float]:
+        s, c = C.c_double(), C.c_double()
+        check(lib().co2_aar_stall(self.handle, handle, C.byref(s), C.byref(c)))
+        return s.value, c.value
+
+    def live_handles(self) -> int:
+        v = C.c_int32()
+        check(lib().co2_aar_live(self.handle, C.byref(v)))
+        return v.value
+
+    def events(self) -> list[dict]:
+        cnt = C.c_int64()
+        check(lib().co2_aar_events(self.handle, None, 0, C.byref(cnt)))
+        arr = (L.Event * max(cnt.value, 1))()
+        check(lib().co2_aar_events(self.handle, arr, cnt.value, C.byref(cnt)))
+        kinds = ["launch", "complete", "wait"]
+        return [{"event": kinds[arr[i].kind], "handle_id": arr[i].handle, "t_sim": arr[i].t,
+                 "stall": arr[i].stall} for i in range(cnt.value)]
+
+
+# ---------------------------------------------------------- worker + round
+class Worker:
+    """Device-resident WorkerState + OuterState (outer_algorithms.hpp:52-61)."""
+
+    def __init__(self, mode: int, n: int, init=None, *, keep_gap: bool = True, stream=None):
+        self.handle = C.c_void_p()
+        self.mode, self.n = mode, n
+        check(lib().co2_worker_create(C.byref(self.handle), mode, n, _ptr(init), int(keep_gap),
+                                      _stream(stream)))
+
+    def close(self):
+        if self.handle:
+            lib().co2_worker_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def buffer(self, which: int) -> torch.Tensor | None:
+        """A zero-copy tensor view of one device buffer."""
+        ptr = lib().co2_worker_buffer(self.handle, which)
+        if not ptr:
+            return None
+        state = which in (L.BUF_ANCHOR, L.BUF_PREV_X0, L.BUF_MOMENTUM, L.BUF_GAP)
+        dt = STATE_TORCH[self.mode] if state else LOW_TORCH[self.mode]
+        return _view(ptr, self.n, dt)
+
+    @property
+    def params(self):
+        return self.buffer(L.BUF_PARAMS)
+
+    @property
+    def t(self) -> int:
+        return lib().co2_worker_round(self.handle)
+
+    def enable_timing(self, cap: int = 4096):
+        check(lib().co2_worker_enable_timing(self.handle, cap))
+
+    def step_times(self, cap: int = 4096) -> list[float]:
+        """Device durations (s) of the fused launches since the last call."""
+        out = (C.c_double * cap)()
+        cnt = C.c_int32()
+        check(lib().co2_worker_step_times(self.handle, out, cap, C.byref(cnt)))
+        return [out[i] for i in range(cnt.value)]
+
+    def snapshot_start(self, stream=None):
+        check(lib().co2_worker_snapshot_start(self.handle, _stream(stream)))
+
+    def snapshot_first(self, stream=None):
+        check(lib().co2_worker_snapshot_first(self.handle, _stream(stream)))
+
+
+def _view(ptr: int, n: int, dtype) -> torch.Tensor:
+    """Wrap a raw device pointer owned by the library as a tensor (no copy)."""
+    esz = torch.tensor([], dtype=dtype).element_size()
+
+    class _Cuda:
+        __cuda_array_interface__ = {
+            "shape": (n,), "typestr": {torch.float64: "<f8", torch.float32: "<f4",
+                                       torch.bfloat16: "<u2"}[dtype],
+            "data": (ptr, False), "version": 3, "strides": None}
+
+    t = torch.as_tensor(_Cuda(), device="cuda")
+    if dtype == torch.bfloat16:
+        t = t.view(torch.bfloat16)
+    assert t.element_size() == esz
+    return t
+
+
+def co2_round(workers: list[Worker], engine: CollectiveEngine, hyper: Co2Hyper, tau: int, *,
+              stream=None, sync: bool = True) -> L.RoundResult:
+    """co2_round (proj/src/outer_algorithms.cpp:110-211) over device workers."""
+    arr = (C.c_void_p * len(workers))(*[w.handle.value for w in workers])
+    h = hyper.c(tau)
+    r = L.RoundResult()
+    check(lib().co2_round(arr, len(workers), engine.handle, C.byref(h), _stream(stream), int(sync),
+                          C.byref(r)))
+    return r

@@ -1,0 +1,665 @@
+// One-step-stale all-reduce engine (CollectiveEngine) and the co2_round
+// driver over device-resident worker state.
+//
+// Reference: proj/include/co2sim/collective.hpp:54-93, proj/src/collective.cpp
+// (simulated clock + std::async average) and proj/src/outer_algorithms.cpp:
+// 110-211 (co2_round).  Here the "launch" is a real collective on a
+// dedicated high-priority comm stream fenced by an event after the producer's
+// work, "poll" is cudaEventQuery, and "wait" makes the consumer stream wait on
+// the completion event -- the host never blocks on the reduce.  Stall is the
+// device time between the consumer reaching the wait and the reduce finishing
+// (events straddling cudaStreamWaitEvent), the measured counterpart of the
+// reference's `stall = max(0, completion - now)` (collective.cpp:93).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace co2;
+
+#define CO2_NCCL(call)                                                                    \
+  do {                                                                                    \
+    ncclResult_t _r = (call);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      return ::co2::fail(CO2_ERR_NCCL, "NCCL error %s in %s", ncclGetErrorString(_r), #call); \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+namespace {
+
+enum { T_NCCL = 0, T_LOCAL = 1 };
+
+struct Handle {
+  cudaEvent_t start = nullptr, done = nullptr, wait_begin = nullptr, wait_end = nullptr;
+  bool consumed = false, polled = false, last_poll = false, completion_logged = false;
+  bool waited = false;
+  co2_diag_t* diag = nullptr;  // LOCAL: pinned copy of the average's flags
+};
+
+ncclDataType_t nccl_dtype(co2_dtype_t d) {
+  return d == CO2_DTYPE_F64 ? ncclFloat64 : (d == CO2_DTYPE_F32 ? ncclFloat32 : ncclBfloat16);
+}
+
+}  // namespace
+
+struct co2_aar {
+  int transport = T_LOCAL;
+  int rank = 0, world = 1, workers = 1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t epoch = nullptr;
+  void* ws = nullptr;
+  int live = 0;
+  std::vector<Handle> handles;
+};
+
+static co2_status_t engine_common_init(co2_aar* e) {
+  int lo = 0, hi = 0;
+  CO2_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CO2_CUDA(cudaStreamCreateWithPriority(&e->comm_stream, cudaStreamNonBlocking, hi));
+  CO2_CUDA(cudaEventCreate(&e->epoch));
+  CO2_CUDA(cudaEventRecord(e->epoch, e->comm_stream));
+  CO2_CUDA(cudaMalloc(&e->ws, co2_workspace_bytes()));
+  CO2_CUDA(cudaMemsetAsync(e->ws, 0, co2_workspace_bytes(), e->comm_stream));
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_nccl_unique_id(uint8_t id_out[CO2_NCCL_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == CO2_NCCL_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  CO2_NCCL(ncclGetUniqueId(&id));
+  memcpy(id_out, &id, sizeof id);
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO2_NCCL_ID_BYTES],
+                                            int32_t rank, int32_t world, int32_t max_ctas) {
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(CO2_ERR_VALIDATION, "aar: bad rank %d / world %d", rank, world);
+  co2_aar* e = new co2_aar();
+  e->transport = T_NCCL;
+  e->rank = rank;
+  e->world = world;
+  e->workers = world;
+  co2_status_t s = engine_common_init(e);
+  if (s != CO2_OK) {
+    delete e;
+    return s;
+  }
+  if (world > 1) {
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof uid);
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (max_ctas > 0) cfg.maxCTAs = max_ctas;
+    ncclResult_t r = ncclCommInitRankConfig(&e->comm, world, uid, rank, &cfg);
+    if (r != ncclSuccess) {
+      delete e;
+      return fail(CO2_ERR_NCCL, "NCCL error %s in ncclCommInitRankConfig", ncclGetErrorString(r));
+    }
+  }
+  *out = e;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers) {
+  if (workers < 1 || workers > 64)
+    return fail(CO2_ERR_VALIDATION, "aar: local workers must lie in [1, 64]");
+  co2_aar* e = new co2_aar();
+  e->transport = T_LOCAL;
+  e->workers = workers;
+  co2_status_t s = engine_common_init(e);
+  if (s != CO2_OK) {
+    delete e;
+    return s;
+  }
+  *out = e;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
+  if (!e) return CO2_OK;
+  cudaStreamSynchronize(e->comm_stream);
+  for (Handle& h : e->handles) {
+    for (cudaEvent_t ev : {h.start, h.done, h.wait_begin, h.wait_end})
+      if (ev) cudaEventDestroy(ev);
+    if (h.diag) cudaFreeHost(h.diag);
+  }
+  if (e->comm) ncclCommDestroy(e->comm);
+  if (e->ws) cudaFree(e->ws);
+  if (e->epoch) cudaEventDestroy(e->epoch);
+  if (e->comm_stream) cudaStreamDestroy(e->comm_stream);
+  delete e;
+  return CO2_OK;
+}
+
+extern "C" int32_t co2_aar_world(const co2_aar_t* e) { return e ? e->workers : 0; }
+
+static co2_status_t record_for(co2_aar* e, uint64_t h, Handle** out) {
+  if (!e || h >= e->handles.size()) return fail(CO2_ERR_VALIDATION, "unknown reduce handle");
+  *out = &e->handles[h];
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_launch(co2_aar_t* e, co2_dtype_t dt, const void* const* bufs,
+                                       void* out, int64_t n, void* producer, uint64_t* handle_out) {
+  // launch_all_reduce, collective.cpp:31-58
+  if (!e) return fail(CO2_ERR_VALIDATION, "aar: null engine");
+  if (e->live >= 2)
+    return fail(CO2_ERR_VALIDATION,
+                "launch_all_reduce: overlap window exceeded, two reduces already live");
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "launch_all_reduce: negative size");
+  Handle h;
+  CO2_CUDA(cudaEventCreateWithFlags(&h.start, cudaEventDefault));
+  CO2_CUDA(cudaEventCreateWithFlags(&h.done, cudaEventDefault));
+  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_begin, cudaEventDefault));
+  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_end, cudaEventDefault));
+  // Fence: the reduce reads x_{t,tau} only after the producer wrote it.
+  cudaEvent_t fence;
+  CO2_CUDA(cudaEventCreateWithFlags(&fence, cudaEventDisableTiming));
+  CO2_CUDA(cudaEventRecord(fence, S(producer)));
+  CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, fence, 0));
+  CO2_CUDA(cudaEventDestroy(fence));
+  CO2_CUDA(cudaEventRecord(h.start, e->comm_stream));
+  if (e->transport == T_NCCL) {
+    if (out && out != bufs[0])
+      return fail(CO2_ERR_VALIDATION, "launch_all_reduce: NCCL transport reduces in place");
+    if (e->world > 1 && n > 0)
+      CO2_NCCL(ncclAllReduce(bufs[0], const_cast<void*>(bufs[0]), (size_t)n, nccl_dtype(dt), ncclSum,
+                             e->comm, e->comm_stream));
+  } else {
+    CO2_TRY(co2_average(dt, e->workers, bufs, n, out, e->ws, e->comm_stream));
+    CO2_CUDA(cudaMallocHost(&h.diag, sizeof(co2_diag_t)));
+    h.diag->flags = 0;
+    CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
+  }
+  CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
+  e->handles.push_back(h);
+  e->live += 1;
+  *handle_out = e->handles.size() - 1;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_poll(co2_aar_t* e, uint64_t handle, int32_t* done) {
+  // is_completed, collective.cpp:74-86 (never blocks)
+  Handle* h = nullptr;
+  CO2_TRY(record_for(e, handle, &h));
+  if (h->consumed) return fail(CO2_ERR_VALIDATION, "is_completed: handle already consumed");
+  cudaError_t q = cudaEventQuery(h->done);
+  if (q != cudaSuccess && q != cudaErrorNotReady) return cuda_fail(q, "cudaEventQuery");
+  bool d = q == cudaSuccess;
+  h->polled = true;
+  h->last_poll = d;
+  if (d) h->completion_logged = true;
+  *done = d ? 1 : 0;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_wait(co2_aar_t* e, uint64_t handle, void* consumer) {
+  // wait, collective.cpp:88-105: consume once; the consumer stream (not the
+  // host) waits for completion.
+  Handle* h = nullptr;
+  CO2_TRY(record_for(e, handle, &h));
+  if (h->consumed) return fail(CO2_ERR_VALIDATION, "wait: handle already consumed");
+  CO2_CUDA(cudaEventRecord(h->wait_begin, S(consumer)));
+  CO2_CUDA(cudaStreamWaitEvent(S(consumer), h->done, 0));
+  CO2_CUDA(cudaEventRecord(h->wait_end, S(consumer)));
+  h->consumed = true;
+  h->waited = true;
+  e->live -= 1;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_stall(co2_aar_t* e, uint64_t handle, double* stall,
+                                      double* comm) {
+  Handle* h = nullptr;
+  CO2_TRY(record_for(e, handle, &h));
+  if (!h->waited) return fail(CO2_ERR_VALIDATION, "stall: handle not waited yet");
+  CO2_CUDA(cudaEventSynchronize(h->wait_end));
+  float ms = 0.f;
+  if (stall) {
+    CO2_CUDA(cudaEventElapsedTime(&ms, h->wait_begin, h->wait_end));
+    *stall = ms * 1e-3;
+  }
+  if (comm) {
+    CO2_CUDA(cudaEventElapsedTime(&ms, h->start, h->done));
+    *comm = ms * 1e-3;
+  }
+  if (h->diag && h->diag->flags) return co2_diag_status(h->diag);
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_live(const co2_aar_t* e, int32_t* live) {
+  if (!e) return fail(CO2_ERR_VALIDATION, "aar: null engine");
+  *live = e->live;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_allreduce_blocking(co2_aar_t* e, co2_dtype_t dt, void* buf,
+                                                   int64_t n, void* stream) {
+  if (!e) return fail(CO2_ERR_VALIDATION, "aar: null engine");
+  if (e->transport != T_NCCL)
+    return fail(CO2_ERR_VALIDATION, "allreduce_blocking: NCCL transport only");
+  if (e->world > 1 && n > 0)
+    CO2_NCCL(ncclAllReduce(buf, buf, (size_t)n, nccl_dtype(dt), ncclSum, e->comm, S(stream)));
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_events(co2_aar_t* e, co2_event_t* out, int64_t cap,
+                                       int64_t* count) {
+  // Event log of collective.hpp:24-29 from device timestamps.
+  if (!e) return fail(CO2_ERR_VALIDATION, "aar: null engine");
+  int64_t k = 0;
+  auto push = [&](int kind, uint64_t id, double t, double stall) {
+    if (k < cap && out) out[k] = co2_event_t{kind, 0, id, t, stall};
+    ++k;
+  };
+  for (uint64_t i = 0; i < e->handles.size(); ++i) {
+    Handle& h = e->handles[i];
+    CO2_CUDA(cudaEventSynchronize(h.done));
+    float ms = 0.f;
+    CO2_CUDA(cudaEventElapsedTime(&ms, e->epoch, h.start));
+    push(0, i, ms * 1e-3, 0.0);
+    CO2_CUDA(cudaEventElapsedTime(&ms, e->epoch, h.done));
+    push(1, i, ms * 1e-3, 0.0);
+    if (h.waited) {
+      CO2_CUDA(cudaEventSynchronize(h.wait_end));
+      float st = 0.f, te = 0.f;
+      CO2_CUDA(cudaEventElapsedTime(&st, h.wait_begin, h.wait_end));
+      CO2_CUDA(cudaEventElapsedTime(&te, e->epoch, h.wait_end));
+      push(2, i, te * 1e-3, st * 1e-3);
+    }
+  }
+  *count = k;
+  return CO2_OK;
+}
+
+// ===================================================================== worker
+struct co2_worker {
+  co2_mode_t mode = CO2_MODE_F32;
+  int64_t n = 0;
+  int t = 0;
+  int cur = 0;
+  void* params[2] = {nullptr, nullptr};
+  void* anchor = nullptr;
+  void* xfirst = nullptr;
+  void* prev_x0 = nullptr;
+  void* prev_x1 = nullptr;
+  void* m = nullptr;
+  void* gap = nullptr;
+  void* avg[2] = {nullptr, nullptr};  // LOCAL transport consumed averages
+  void* tmp_state = nullptr;          // ghost: bar0
+  void* tmp_low = nullptr;            // ghost: bar1
+  void* xbar = nullptr;               // last consumed reduce (for CO2_BUF_XBAR)
+  void* ws = nullptr;
+  co2_diag_t* host_diag = nullptr;  // pinned
+  bool has_pending = false;
+  uint64_t pending = 0;
+  uint64_t consumed = 0;
+  bool has_consumed = false;
+  // optional device timing of the fused launch (ring of event pairs)
+  std::vector<cudaEvent_t> tev;  // 2 * cap
+  int64_t tev_recorded = 0, tev_read = 0;
+};
+
+static co2_status_t step_launch(co2_worker* w, co2_mode_t mode, int64_t n, const void* x_t0,
+                                const void* p0, const void* p1, const void* xbar,
+                                int32_t divisor, void* m, void* anchor, void* params, void* gap,
+                                const co2_hyper_t* h, cudaStream_t st) {
+  const int64_t cap = (int64_t)w->tev.size() / 2;
+  const int64_t slot = cap ? w->tev_recorded % cap : 0;
+  if (cap) CO2_CUDA(cudaEventRecord(w->tev[2 * slot], st));
+  CO2_TRY(outer_step_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params, gap, h, w->ws,
+                          st));
+  if (cap) {
+    CO2_CUDA(cudaEventRecord(w->tev[2 * slot + 1], st));
+    w->tev_recorded += 1;
+  }
+  return CO2_OK;
+}
+
+static co2_status_t walloc(void** p, size_t bytes) {
+  CO2_CUDA(cudaMalloc(p, bytes ? bytes : 16));
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, int64_t n,
+                                          const void* init, int32_t keep_gap, void* stream) {
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "worker: negative dimension");
+  if (mode != CO2_MODE_F64 && mode != CO2_MODE_F32 && mode != CO2_MODE_BF16_MIXED)
+    return fail(CO2_ERR_VALIDATION, "worker: unknown mode %d", (int)mode);
+  co2_worker* w = new co2_worker();
+  w->mode = mode;
+  w->n = n;
+  const size_t sb = state_bytes(mode) * n, lb = low_bytes(mode) * n;
+  co2_status_t s = CO2_OK;
+  auto A = [&](void** p, size_t b) {
+    if (s == CO2_OK) s = walloc(p, b);
+  };
+  A(&w->params[0], lb);
+  A(&w->params[1], lb);
+  A(&w->anchor, sb);
+  A(&w->xfirst, lb);
+  A(&w->prev_x0, sb);
+  A(&w->prev_x1, lb);
+  A(&w->m, sb);
+  if (keep_gap) A(&w->gap, sb);
+  A(&w->ws, co2_workspace_bytes());
+  if (s != CO2_OK) {
+    co2_worker_destroy(w);
+    return s;
+  }
+  cudaStream_t st = S(stream);
+  CO2_CUDA(cudaMallocHost(&w->host_diag, sizeof(co2_diag_t)));
+  CO2_CUDA(cudaMemsetAsync(w->ws, 0, co2_workspace_bytes(), st));
+  // OuterState init, outer_algorithms.cpp:416-418: momentum zeros, gap ones.
+  CO2_CUDA(cudaMemsetAsync(w->m, 0, sb ? sb : 1, st));
+  if (init) {
+    CO2_CUDA(cudaMemcpyAsync(w->params[0], init, lb, cudaMemcpyDeviceToDevice, st));
+  } else {
+    CO2_CUDA(cudaMemsetAsync(w->params[0], 0, lb ? lb : 1, st));
+  }
+  if (w->gap && n > 0) {
+    if (mode == CO2_MODE_F64) {
+      std::vector<double> ones(n, 1.0);
+      CO2_CUDA(cudaMemcpy(w->gap, ones.data(), sb, cudaMemcpyHostToDevice));
+    } else {
+      CO2_TRY(co2_fill_u32(w->gap, 0x3f800000u, n, stream));
+    }
+  }
+  *out = w;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_worker_destroy(co2_worker_t* w) {
+  if (!w) return CO2_OK;
+  for (void* p : {w->params[0], w->params[1], w->anchor, w->xfirst, w->prev_x0, w->prev_x1, w->m,
+                  w->gap, w->avg[0], w->avg[1], w->tmp_state, w->tmp_low, w->ws})
+    if (p) cudaFree(p);
+  if (w->host_diag) cudaFreeHost(w->host_diag);
+  for (cudaEvent_t ev : w->tev) cudaEventDestroy(ev);
+  delete w;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_worker_enable_timing(co2_worker_t* w, int32_t cap) {
+  if (!w || cap < 1) return fail(CO2_ERR_VALIDATION, "timing: bad arguments");
+  for (cudaEvent_t ev : w->tev) cudaEventDestroy(ev);
+  w->tev.assign(2 * (size_t)cap, nullptr);
+  for (cudaEvent_t& ev : w->tev) CO2_CUDA(cudaEventCreate(&ev));
+  w->tev_recorded = w->tev_read = 0;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_worker_step_times(co2_worker_t* w, double* out, int32_t cap,
+                                              int32_t* count) {
+  if (!w) return fail(CO2_ERR_VALIDATION, "timing: null worker");
+  const int64_t ring = (int64_t)w->tev.size() / 2;
+  int64_t first = w->tev_read;
+  if (ring && w->tev_recorded - first > ring) first = w->tev_recorded - ring;  // overwritten
+  int32_t k = 0;
+  for (int64_t i = first; ring && i < w->tev_recorded && k < cap; ++i) {
+    const int64_t s = i % ring;
+    CO2_CUDA(cudaEventSynchronize(w->tev[2 * s + 1]));
+    float ms = 0.f;
+    CO2_CUDA(cudaEventElapsedTime(&ms, w->tev[2 * s], w->tev[2 * s + 1]));
+    if (out) out[k] = ms * 1e-3;
+    ++k;
+  }
+  w->tev_read = w->tev_recorded;
+  *count = k;
+  return CO2_OK;
+}
+
+extern "C" void* co2_worker_buffer(co2_worker_t* w, int32_t which) {
+  if (!w) return nullptr;
+  switch (which) {
+    case CO2_BUF_PARAMS: return w->params[w->cur];
+    case CO2_BUF_ANCHOR: return w->anchor;
+    case CO2_BUF_XFIRST: return w->xfirst;
+    case CO2_BUF_PREV_X0: return w->prev_x0;
+    case CO2_BUF_PREV_X1: return w->prev_x1;
+    case CO2_BUF_MOMENTUM: return w->m;
+    case CO2_BUF_GAP: return w->gap;
+    case CO2_BUF_XBAR: return w->xbar;
+  }
+  return nullptr;
+}
+
+extern "C" int32_t co2_worker_round(const co2_worker_t* w) { return w ? w->t : -1; }
+
+extern "C" co2_status_t co2_worker_snapshot_start(co2_worker_t* w, void* stream) {
+  // InnerTrace::x_start = params (inner_loop.cpp:73).  For t >= 1 the outer
+  // step already wrote x_{t,0} into the anchor (fused snapshot capture).
+  if (!w) return fail(CO2_ERR_VALIDATION, "worker: null");
+  if (w->t > 0) return CO2_OK;
+  return co2_convert(state_dtype(w->mode), w->anchor, low_dtype(w->mode), w->params[w->cur], w->n,
+                     stream);
+}
+
+extern "C" co2_status_t co2_worker_snapshot_first(co2_worker_t* w, void* stream) {
+  // InnerTrace::x_first = params after inner step 0 (inner_loop.cpp:96-98).
+  if (!w) return fail(CO2_ERR_VALIDATION, "worker: null");
+  return co2_convert(low_dtype(w->mode), w->xfirst, low_dtype(w->mode), w->params[w->cur], w->n,
+                     stream);
+}
+
+static co2_status_t copy_dev(void* d, const void* s, size_t bytes, cudaStream_t st) {
+  if (bytes) CO2_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, st));
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_round_finish(co2_worker_t* const* ws, int32_t g, void* stream,
+                                         co2_round_result_t* res) {
+  CO2_CUDA(cudaStreamSynchronize(S(stream)));
+  co2_round_result_t r = *res;
+  r.min_gap = INFINITY;
+  r.max_outer_step = 0.0;
+  r.n_clipped = 0;
+  r.n_floored = 0;
+  co2_status_t first = CO2_OK;
+  char msg[512] = {0};
+  for (int i = 0; i < g; ++i) {  // worker order = the reference's error order (cpp:186)
+    const co2_diag_t& d = *ws[i]->host_diag;
+    r.min_gap = d.min_gap < r.min_gap ? d.min_gap : r.min_gap;
+    r.max_outer_step = d.max_outer_step > r.max_outer_step ? d.max_outer_step : r.max_outer_step;
+    r.n_clipped += d.n_clipped;
+    r.n_floored += d.n_floored;
+    if (first == CO2_OK && d.flags) {
+      first = co2_diag_status(&d);
+      snprintf(msg, sizeof msg, "%s", co2_last_error());
+    }
+  }
+  *res = r;
+  if (first != CO2_OK) return fail(first, "%s", msg);
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
+                                  const co2_hyper_t* hyper, void* stream, int32_t sync,
+                                  co2_round_result_t* res) {
+  // co2_round, proj/src/outer_algorithms.cpp:110-211
+  CO2_TRY(co2_hyper_validate(hyper));  // :115
+  if (!e || !ws || g < 1) return fail(CO2_ERR_VALIDATION, "co2_round: bad arguments");
+  if (hyper->tau < 1) return fail(CO2_ERR_VALIDATION, "staleness_gap: tau must be >= 1");
+  if (g != (e->transport == T_LOCAL ? e->workers : 1))
+    return fail(CO2_ERR_VALIDATION,
+                "launch_all_reduce: contribution count %d does not match worker count %d", g,
+                e->transport == T_LOCAL ? e->workers : 1);
+  co2_worker* w0 = ws[0];
+  const co2_mode_t mode = w0->mode;
+  const int64_t n = w0->n;
+  for (int i = 0; i < g; ++i) {
+    if (ws[i]->mode != mode || ws[i]->n != n)
+      return fail(CO2_ERR_VALIDATION, "staleness_gap: dimensions differ");
+    if (ws[i]->t != w0->t || ws[i]->has_pending != w0->has_pending ||
+        (w0->has_pending && ws[i]->pending != w0->pending))
+      return fail(CO2_ERR_VALIDATION, "outer round: pending handles diverged");
+  }
+  if (hyper->ghost_consistent && e->transport != T_LOCAL && e->world > 1)
+    return fail(CO2_ERR_VALIDATION,
+                "co2_round: ghost-consistent mode over NCCL runs in the sharded driver");
+  cudaStream_t st = S(stream);
+  const co2_dtype_t sdt = state_dtype(mode), ldt = low_dtype(mode);
+  const size_t sb = state_bytes(mode) * n, lb = low_bytes(mode) * n;
+  const bool local = e->transport == T_LOCAL;
+  co2_round_result_t r{};
+  r.min_gap = INFINITY;
+
+  // 1. Launch the reduce of x_{t,tau} (:120).
+  if (local && !w0->avg[0]) {
+    CO2_TRY(walloc(&w0->avg[0], lb));
+    CO2_TRY(walloc(&w0->avg[1], lb));
+  }
+  const void* bufs[64];
+  for (int i = 0; i < g; ++i) bufs[i] = ws[i]->params[ws[i]->cur];
+  void* avg_out = local ? w0->avg[w0->t % 2] : const_cast<void*>(bufs[0]);
+  uint64_t launched = 0;
+  CO2_TRY(co2_aar_launch(e, ldt, bufs, avg_out, n, stream, &launched));
+
+  if (w0->t == 0) {
+    // 2. Round 0 (:122-151): snapshots only; x_{1,0} = x_{0,tau} stays
+    // worker-local.  The in-flight reduce owns params[cur]; continue on the
+    // other buffer and seed the anchor x_{1,0}.
+    for (int i = 0; i < g; ++i) {
+      co2_worker* w = ws[i];
+      void* src = w->params[w->cur];
+      void* dst = w->params[1 - w->cur];
+      CO2_TRY(copy_dev(dst, src, lb, st));
+      std::swap(w->prev_x0, w->anchor);  // prev_x0 <- x_{0,0}
+      std::swap(w->prev_x1, w->xfirst);  // prev_x1 <- x_{0,1}
+      w->cur = 1 - w->cur;
+    }
+    if (hyper->ghost_consistent && g > 1) {  // :133-145 averaged snapshots
+      std::vector<const void*> s0(g), s1(g);
+      for (int i = 0; i < g; ++i) {
+        s0[i] = ws[i]->prev_x0;
+        s1[i] = ws[i]->prev_x1;
+      }
+      if (!w0->tmp_state) CO2_TRY(walloc(&w0->tmp_state, sb));
+      if (!w0->tmp_low) CO2_TRY(walloc(&w0->tmp_low, lb));
+      CO2_TRY(co2_average(sdt, g, s0.data(), n, w0->tmp_state, w0->ws, stream));
+      CO2_TRY(co2_diag_fetch_async(w0->ws, w0->host_diag, stream));
+      CO2_TRY(co2_average(ldt, g, s1.data(), n, w0->tmp_low, w0->ws, stream));
+      CO2_TRY(co2_diag_fetch_async(w0->ws, ws[g - 1]->host_diag, stream));
+      for (int i = 0; i < g; ++i) {
+        CO2_TRY(copy_dev(ws[i]->prev_x0, w0->tmp_state, sb, st));
+        CO2_TRY(copy_dev(ws[i]->prev_x1, w0->tmp_low, lb, st));
+      }
+    } else {
+      for (int i = 0; i < g; ++i) {
+        ws[i]->host_diag->flags = 0;
+        ws[i]->host_diag->min_gap = INFINITY;
+        ws[i]->host_diag->max_outer_step = 0.0;
+        ws[i]->host_diag->n_clipped = ws[i]->host_diag->n_floored = 0;
+      }
+    }
+    for (int i = 0; i < g; ++i) {
+      co2_worker* w = ws[i];
+      CO2_TRY(co2_convert(sdt, w->anchor, ldt, w->params[w->cur], n, stream));  // x_{1,0}
+      w->pending = launched;
+      w->has_pending = true;
+      w->t = 1;
+    }
+    r.outer_applied = 0;
+    if (sync) {
+      CO2_CUDA(cudaStreamSynchronize(st));
+      if (hyper->ghost_consistent && g > 1) {
+        for (co2_diag_t* d : {w0->host_diag, ws[g - 1]->host_diag})
+          if (d->flags) return co2_diag_status(d);
+      }
+    }
+    if (res) *res = r;
+    return CO2_OK;
+  }
+
+  // 3. Rounds t >= 1: poll, then wait on the previous reduce (:153-159).
+  const uint64_t prev = w0->pending;
+  int32_t done = 0;
+  CO2_TRY(co2_aar_poll(e, prev, &done));
+  CO2_TRY(co2_aar_wait(e, prev, stream));
+  const int t = w0->t;
+  void* xbar = local ? w0->avg[(t - 1) % 2] : ws[0]->params[1 - ws[0]->cur];
+  const int32_t divisor = local ? 1 : e->world;
+
+  if (hyper->ghost_consistent && g > 1) {
+    // :161-184 -- one shared state driven by the averaged snapshots.
+    std::vector<const void*> s0(g), s1(g);
+    for (int i = 0; i < g; ++i) {
+      s0[i] = ws[i]->anchor;
+      s1[i] = ws[i]->xfirst;
+    }
+    if (!w0->tmp_state) CO2_TRY(walloc(&w0->tmp_state, sb));
+    if (!w0->tmp_low) CO2_TRY(walloc(&w0->tmp_low, lb));
+    CO2_TRY(co2_average(sdt, g, s0.data(), n, w0->tmp_state, w0->ws, stream));  // bar0
+    CO2_TRY(co2_average(ldt, g, s1.data(), n, w0->tmp_low, ws[g - 1]->ws, stream));  // bar1
+    co2_worker* w = w0;
+    void* out_params = w->params[1 - w->cur];
+    CO2_TRY(step_launch(w, mode, n, w0->tmp_state, w->prev_x0, w->prev_x1, xbar, divisor, w->m,
+                        w->prev_x0, out_params, w->gap, hyper, st));
+    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    // Rotation: anchor <- x_{t+1,0} (written over prev_x0), prev_x0 <- bar0,
+    // prev_x1 <- bar1.
+    void* old_anchor = w->anchor;
+    w->anchor = w->prev_x0;
+    w->prev_x0 = w0->tmp_state;
+    w0->tmp_state = old_anchor;
+    void* old_p1 = w->prev_x1;
+    w->prev_x1 = w0->tmp_low;
+    w0->tmp_low = old_p1;
+    w->cur = 1 - w->cur;
+    for (int i = 1; i < g; ++i) {
+      co2_worker* v = ws[i];
+      CO2_TRY(copy_dev(v->m, w->m, sb, st));
+      if (v->gap && w->gap) CO2_TRY(copy_dev(v->gap, w->gap, sb, st));
+      CO2_TRY(copy_dev(v->prev_x0, w->prev_x0, sb, st));
+      CO2_TRY(copy_dev(v->prev_x1, w->prev_x1, lb, st));
+      CO2_TRY(copy_dev(v->anchor, w->anchor, sb, st));
+      v->cur = 1 - v->cur;
+      CO2_TRY(copy_dev(v->params[v->cur], w->params[w->cur], lb, st));
+      v->host_diag->flags = 0;
+      v->host_diag->min_gap = INFINITY;
+      v->host_diag->max_outer_step = 0.0;
+      v->host_diag->n_clipped = v->host_diag->n_floored = 0;
+    }
+  } else {
+    // :185-203 -- per-worker fused step; rotation is a pointer swap.
+    for (int i = 0; i < g; ++i) {
+      co2_worker* w = ws[i];
+      void* out_params = w->params[1 - w->cur];
+      void* xb = local ? xbar : out_params;  // NCCL: the sum lives in the other buffer
+      CO2_TRY(step_launch(w, mode, n, w->anchor, w->prev_x0, w->prev_x1, xb, divisor, w->m,
+                          w->prev_x0, out_params, w->gap, hyper, st));
+      CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+      std::swap(w->anchor, w->prev_x0);  // anchor <- x_{t+1,0}; prev_x0 <- x_{t,0}
+      std::swap(w->prev_x1, w->xfirst);  // prev_x1 <- x_{t,1}
+      w->cur = 1 - w->cur;
+    }
+  }
+  for (int i = 0; i < g; ++i) {
+    ws[i]->xbar = local ? xbar : nullptr;  // NCCL consumed its sum in place
+    ws[i]->consumed = prev;
+    ws[i]->has_consumed = true;
+    ws[i]->pending = launched;
+    ws[i]->t += 1;
+  }
+  r.outer_applied = 1;
+  if (sync) {
+    co2_status_t s = co2_round_finish(ws, g, stream, &r);
+    double stall = 0.0;
+    co2_status_t s2 = co2_aar_stall(e, prev, &stall, nullptr);
+    r.stall_seconds = stall;
+    if (res) *res = r;
+    if (s != CO2_OK) return s;
+    return s2;
+  }
+  if (res) *res = r;
+  return CO2_OK;
+}

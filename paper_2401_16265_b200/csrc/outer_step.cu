@@ -1,0 +1,829 @@
+// Fused CO2 outer step and the unfused reference operators for sm_100a.
+//
+// The path is HBM-bandwidth bound (~0.5 FLOP/B): no tensor
+// cores.  The fused kernel reads x_t0, prev_x0, prev_x1, xbar and m once and
+// writes m', the new anchor and the params once: 32 B/param in fp32, 26 B in
+// bf16-mixed, 64 B in fp64 (versus ~264 B/param in the reference's unfused
+// fp64 passes, outer_algorithms.cpp:48-108).  Streams are 128-bit
+// coalesced with evict-first cache hints, U independent vectors per thread
+// are in flight before any arithmetic, and the grid is sized to the resident
+// CTA count of the 148 SMs (grid-stride persistent loop).
+//
+// Bit-exactness: built with --fmad=false and IEEE division, every element op
+// below is exactly one IEEE op in the reference's order, so the F64 mode is
+// bitwise the reference (built -ffp-contract=off, proj/CMakeLists.txt:12-13)
+// and the F32 / BF16-mixed modes are bitwise the same-op-order oracle.
+//
+// Diagnostics (min Lambda, max |x' - x_t0|, clip / floor counts, error
+// flags) are reduced warp-shuffle -> shared memory -> per-block partials,
+// and the last block to arrive (atomic ticket) folds the partials in fixed
+// index order, so results are deterministic without a second launch.
+#include <cuda_bf16.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace co2 {
+namespace {
+
+// ------------------------------------------------------------ storage types
+struct bf16s {  // bf16 storage as raw bits
+  uint16_t b;
+};
+
+__device__ __forceinline__ float to_c(float v) { return v; }
+__device__ __forceinline__ double to_c(double v) { return v; }
+__device__ __forceinline__ float to_c(bf16s v) { return __uint_as_float(((uint32_t)v.b) << 16); }
+
+template <typename T>
+struct Store;
+template <>
+struct Store<double> {
+  __device__ static __forceinline__ double from(double v) { return v; }
+};
+template <>
+struct Store<float> {
+  __device__ static __forceinline__ float from(float v) { return v; }
+};
+template <>
+struct Store<bf16s> {
+  __device__ static __forceinline__ bf16s from(float v) {
+    // cvt.rn.bf16.f32: round-to-nearest-even, canonical NaN 0x7fff.
+    __nv_bfloat16 h = __float2bfloat16_rn(v);
+    return bf16s{__bfloat16_as_ushort(h)};
+  }
+};
+
+// Modes: storage of state (x_t0, prev_x0, m, anchor, gap), storage of low
+// (prev_x1, xbar, params), compute type, elements per vector.
+struct ModeF64 {
+  using TS = double;
+  using TL = double;
+  using TC = double;
+  static constexpr int VEC = 2;
+  static constexpr int U = 4;
+};
+struct ModeF32 {
+  using TS = float;
+  using TL = float;
+  using TC = float;
+  static constexpr int VEC = 4;
+  static constexpr int U = 2;
+};
+struct ModeBF16 {
+  using TS = float;
+  using TL = bf16s;
+  using TC = float;
+  static constexpr int VEC = 8;
+  static constexpr int U = 2;
+};
+
+// ------------------------------------------------------- vector load/store
+template <typename T, int N>
+__device__ __forceinline__ void ld_vec(const T* __restrict__ p, T (&out)[N]) {
+  constexpr int BYTES = N * (int)sizeof(T);
+  if constexpr (BYTES % 16 == 0) {
+    uint4 r[BYTES / 16];
+#pragma unroll
+    for (int k = 0; k < BYTES / 16; ++k) r[k] = __ldcs(reinterpret_cast<const uint4*>(p) + k);
+    memcpy(out, r, BYTES);
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = p[k];
+  }
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void st_vec(T* __restrict__ p, const T (&in)[N]) {
+  constexpr int BYTES = N * (int)sizeof(T);
+  if constexpr (BYTES % 16 == 0) {
+    uint4 r[BYTES / 16];
+    memcpy(r, in, BYTES);
+#pragma unroll
+    for (int k = 0; k < BYTES / 16; ++k) __stcs(reinterpret_cast<uint4*>(p) + k, r[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k) p[k] = in[k];
+  }
+}
+
+// --------------------------------------------------------- diag reduction
+struct Acc {
+  double min_gap = INFINITY;
+  double max_step = 0.0;
+  unsigned int clipped = 0, floored = 0, flags = 0;
+};
+
+template <int NT>
+__device__ void block_finish(const Acc& a, void* ws) {
+  // Warp level.
+  double mg = a.min_gap, ms = a.max_step;
+  unsigned long long cl = a.clipped, fl = a.floored;
+  unsigned int fg = a.flags;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double omg = __shfl_xor_sync(0xffffffffu, mg, o);
+    double oms = __shfl_xor_sync(0xffffffffu, ms, o);
+    mg = omg < mg ? omg : mg;
+    ms = oms > ms ? oms : ms;
+    cl += __shfl_xor_sync(0xffffffffu, cl, o);
+    fl += __shfl_xor_sync(0xffffffffu, fl, o);
+    fg |= __shfl_xor_sync(0xffffffffu, fg, o);
+  }
+  constexpr int NW = NT / 32;
+  __shared__ Partial sh[NW];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = Partial{mg, ms, cl, fl, fg, 0u};
+  __syncthreads();
+  WsHeader* hdr = ws_header(ws);
+  Partial* parts = ws_partials(ws);
+  if (threadIdx.x == 0) {
+    Partial b = sh[0];
+    for (int w = 1; w < NW; ++w) {  // fixed order
+      b.min_gap = sh[w].min_gap < b.min_gap ? sh[w].min_gap : b.min_gap;
+      b.max_step = sh[w].max_step > b.max_step ? sh[w].max_step : b.max_step;
+      b.clipped += sh[w].clipped;
+      b.floored += sh[w].floored;
+      b.flags |= sh[w].flags;
+    }
+    parts[blockIdx.x] = b;
+    __threadfence();
+    unsigned int t = atomicAdd(&hdr->ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // Last block: fold all partials in fixed index order (thread-strided, then
+  // a fixed warp tree and fixed warp order), deterministic for a given grid.
+  __threadfence();
+  Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+    const Partial* q = parts + i;
+    double qmg = __ldcg(&q->min_gap), qms = __ldcg(&q->max_step);
+    b.min_gap = qmg < b.min_gap ? qmg : b.min_gap;
+    b.max_step = qms > b.max_step ? qms : b.max_step;
+    b.clipped += __ldcg(&q->clipped);
+    b.floored += __ldcg(&q->floored);
+    b.flags |= __ldcg(&q->flags);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double omg = __shfl_xor_sync(0xffffffffu, b.min_gap, o);
+    double oms = __shfl_xor_sync(0xffffffffu, b.max_step, o);
+    b.min_gap = omg < b.min_gap ? omg : b.min_gap;
+    b.max_step = oms > b.max_step ? oms : b.max_step;
+    b.clipped += __shfl_xor_sync(0xffffffffu, b.clipped, o);
+    b.floored += __shfl_xor_sync(0xffffffffu, b.floored, o);
+    b.flags |= __shfl_xor_sync(0xffffffffu, b.flags, o);
+  }
+  __syncthreads();
+  if (lane == 0) sh[wid] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Partial r = sh[0];
+    for (int w = 1; w < NW; ++w) {
+      r.min_gap = sh[w].min_gap < r.min_gap ? sh[w].min_gap : r.min_gap;
+      r.max_step = sh[w].max_step > r.max_step ? sh[w].max_step : r.max_step;
+      r.clipped += sh[w].clipped;
+      r.floored += sh[w].floored;
+      r.flags |= sh[w].flags;
+    }
+    hdr->diag.min_gap = r.min_gap;
+    hdr->diag.max_outer_step = r.max_step;
+    hdr->diag.n_clipped = (int64_t)r.clipped;
+    hdr->diag.n_floored = (int64_t)r.floored;
+    hdr->diag.flags = r.flags;
+    hdr->diag.pad = 0;
+    hdr->ticket = 0;  // self-reset for the next launch on this workspace
+    __threadfence();
+  }
+}
+
+// ---------------------------------------------------------- fused element
+template <typename TC>
+struct Hyp {
+  TC tau, eps, beta, phi, alpha, divisor;
+  int penalty, clip, divide;
+};
+
+// One coordinate of SURVEY.md 8(a) "Fused per-element semantics":
+//   n0 = |x_t0 - p0|                       outer_algorithms.cpp:57
+//   d  = max(|tau*(p1 - p0)|, eps)          :58-60 (std::max NaN semantics)
+//   L  = n0/d + 1                           :61
+//   D  = p0 - xbar                          :189
+//   m' = beta*m + D/L   (or beta*m + D)     :84 / :86
+//   c  = min(max(m', -phi), phi)  (or m')   param_ops.cpp:42
+//   x' = x_t0 - alpha*c                     outer_algorithms.cpp:102 / :104
+template <typename TC>
+__device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& xn, TC& lam,
+                                         const Hyp<TC>& h, Acc& acc) {
+  if (h.divide) xb = xb / h.divisor;  // average(): sum / G, param_ops.cpp:30
+  TC n0 = fabs(x - q0);
+  TC av = fabs(h.tau * (q1 - q0));
+  bool floored = av < h.eps;
+  TC d = floored ? h.eps : av;
+  lam = n0 / d + (TC)1;
+  TC dl = q0 - xb;
+  TC mn;
+  if (h.penalty) {
+    TC bm = h.beta * m;
+    TC q = dl / lam;
+    mn = bm + q;
+  } else {
+    TC bm = h.beta * m;
+    mn = bm + dl;
+  }
+  TC c = mn;
+  bool clipped = false;
+  if (h.clip) {
+    clipped = (mn < -h.phi) || (h.phi < mn);
+    TC lo = (mn < -h.phi) ? -h.phi : mn;  // std::max(mn, -phi)
+    c = (h.phi < lo) ? h.phi : lo;         // std::min(lo, phi)
+  }
+  TC ac = h.alpha * c;
+  xn = x - ac;
+  m = mn;
+  unsigned int f = 0;
+  if (!isfinite(lam)) f |= CO2_FLAG_GAP_NONFINITE;
+  if (h.penalty && lam < (TC)1) f |= CO2_FLAG_GAP_BELOW_ONE;
+  if (!isfinite(mn)) f |= CO2_FLAG_M_NONFINITE;
+  if (!isfinite(xn)) f |= CO2_FLAG_X_NONFINITE;
+  acc.flags |= f;
+  acc.floored += floored;
+  acc.clipped += clipped;
+  double dlam = (double)lam;
+  acc.min_gap = dlam < acc.min_gap ? dlam : acc.min_gap;
+  double st = (double)fabs(xn - x);
+  acc.max_step = st > acc.max_step ? st : acc.max_step;
+}
+
+struct StepArgs {
+  const void* x_t0;
+  const void* p0;
+  const void* p1;
+  const void* xbar;
+  void* m;
+  void* anchor;
+  void* params;
+  void* gap;
+  int64_t n;
+  double alpha, beta, phi, eps;
+  int tau, divisor, penalty, clip;
+  void* ws;
+};
+
+template <class M, int V, int U, int NT>
+__global__ void __launch_bounds__(NT) fused_step_kernel(const StepArgs a) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  Hyp<TC> h;
+  h.tau = (TC)a.tau;
+  h.eps = (TC)a.eps;
+  h.beta = (TC)a.beta;
+  h.phi = (TC)a.phi;
+  h.alpha = (TC)a.alpha;
+  h.divisor = (TC)a.divisor;
+  h.penalty = a.penalty;
+  h.clip = a.clip;
+  h.divide = a.divisor > 1;
+
+  const TS* __restrict__ X = static_cast<const TS*>(a.x_t0);
+  const TS* __restrict__ P0 = static_cast<const TS*>(a.p0);
+  const TL* __restrict__ P1 = static_cast<const TL*>(a.p1);
+  const TL* XB = static_cast<const TL*>(a.xbar);  // may alias params
+  TS* Mm = static_cast<TS*>(a.m);
+  TS* A = static_cast<TS*>(a.anchor);  // may alias prev_x0
+  TL* PR = static_cast<TL*>(a.params);  // may alias xbar
+  TS* G = static_cast<TS*>(a.gap);
+
+  Acc acc;
+  const int64_t nv = a.n / V;
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+
+  auto process = [&](const int64_t (&idx)[U], int cnt) {
+    TS x[U][V], q0[U][V], mo[U][V];
+    TL q1[U][V], xb[U][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u < cnt) {
+        const int64_t e = idx[u] * V;
+        ld_vec<TS, V>(X + e, x[u]);
+        ld_vec<TS, V>(P0 + e, q0[u]);
+        ld_vec<TL, V>(P1 + e, q1[u]);
+        ld_vec<TL, V>(XB + e, xb[u]);
+        ld_vec<TS, V>(Mm + e, mo[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u < cnt) {
+        const int64_t e = idx[u] * V;
+        TS mn[V], xs[V], gs[V];
+        TL xl[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          TC m = to_c(mo[u][v]), xn, lam;
+          co2_elem<TC>(to_c(x[u][v]), to_c(q0[u][v]), to_c(q1[u][v]), to_c(xb[u][v]), m, xn,
+                       lam, h, acc);
+          mn[v] = (TS)m;
+          xs[v] = (TS)xn;
+          gs[v] = (TS)lam;
+          xl[v] = Store<TL>::from(xn);
+        }
+        st_vec<TS, V>(Mm + e, mn);
+        if (A) st_vec<TS, V>(A + e, xs);
+        if (PR) st_vec<TL, V>(PR + e, xl);
+        if (G) st_vec<TS, V>(G + e, gs);
+      }
+    }
+  };
+
+  for (; i + (int64_t)(U - 1) * stride < nv; i += (int64_t)U * stride) {
+    int64_t idx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) idx[u] = i + (int64_t)u * stride;
+    process(idx, U);
+  }
+  for (; i < nv; i += stride) {
+    int64_t idx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) idx[u] = i;
+    process(idx, 1);
+  }
+  // Scalar tail (n % V coordinates).
+  const int64_t t = nv * V + (int64_t)blockIdx.x * NT + threadIdx.x;
+  if (V > 1 && t < a.n) {
+    TC m = to_c(Mm[t]), xn, lam;
+    co2_elem<TC>(to_c(X[t]), to_c(P0[t]), to_c(P1[t]), to_c(XB[t]), m, xn, lam, h, acc);
+    Mm[t] = (TS)m;
+    if (A) A[t] = (TS)xn;
+    if (PR) PR[t] = Store<TL>::from(xn);
+    if (G) G[t] = (TS)lam;
+  }
+  block_finish<NT>(acc, a.ws);
+}
+
+constexpr int kThreads = 256;
+
+template <typename K>
+int grid_for(K kernel, int64_t work_items, int threads) {
+  static int cached_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  (void)cached_dev;
+  if (per_sm < 1) per_sm = 1;
+  int64_t cap = (int64_t)per_sm * sm_count();
+  if (cap > kMaxBlocks) cap = kMaxBlocks;
+  int64_t need = (work_items + threads - 1) / threads;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+template <class M>
+co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
+  bool vec_ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
+                aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap);
+  if (vec_ok) {
+    auto k = fused_step_kernel<M, M::VEC, M::U, kThreads>;
+    int grid = grid_for(k, (a.n / M::VEC + M::U - 1) / M::U, kThreads);
+    k<<<grid, kThreads, 0, s>>>(a);
+  } else {
+    auto k = fused_step_kernel<M, 1, 4, kThreads>;
+    int grid = grid_for(k, (a.n + 3) / 4, kThreads);
+    k<<<grid, kThreads, 0, s>>>(a);
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+// ------------------------------------------------------ unfused operators
+template <typename T>
+struct Ptrs64 {
+  const T* p[64];
+};
+
+enum OpKind { OP_GAP = 0, OP_MOMENTUM = 1, OP_ITERATE = 2, OP_CLIP = 3 };
+
+struct OpArgs {
+  const void* a;
+  const void* b;
+  const void* c;
+  void* out;
+  int64_t n;
+  double s0, s1;  // scalars (tau/eps, beta/-, alpha/phi, phi/-)
+  int i0;         // penalty / clip flag
+  void* ws;
+};
+
+// T storage, TC compute.
+template <typename T, typename TC, int OP>
+__global__ void __launch_bounds__(kThreads) op_kernel(const OpArgs a) {
+  const T* A = static_cast<const T*>(a.a);
+  const T* B = static_cast<const T*>(a.b);
+  const T* Cc = static_cast<const T*>(a.c);
+  T* O = static_cast<T*>(a.out);
+  Acc acc;
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < a.n;
+       j += (int64_t)gridDim.x * kThreads) {
+    if (OP == OP_GAP) {  // outer_algorithms.cpp:57-62
+      TC tau = (TC)a.s0, eps = (TC)a.s1;
+      TC x = to_c(A[j]), q0 = to_c(B[j]), q1 = to_c(Cc[j]);
+      TC n0 = fabs(x - q0);
+      TC av = fabs(tau * (q1 - q0));
+      bool fl = av < eps;
+      TC d = fl ? eps : av;
+      TC lam = n0 / d + (TC)1;
+      if (!isfinite(lam)) acc.flags |= CO2_FLAG_GAP_NONFINITE;
+      acc.floored += fl;
+      double dl = (double)lam;
+      acc.min_gap = dl < acc.min_gap ? dl : acc.min_gap;
+      O[j] = Store<T>::from(lam);
+    } else if (OP == OP_MOMENTUM) {  // outer_algorithms.cpp:78-88
+      TC beta = (TC)a.s0;
+      TC mp = to_c(A[j]), g = to_c(B[j]), dl = to_c(Cc[j]);
+      TC m;
+      if (a.i0) {
+        if (g < (TC)1) acc.flags |= CO2_FLAG_GAP_BELOW_ONE;
+        TC bm = beta * mp;
+        TC q = dl / g;
+        m = bm + q;
+      } else {
+        TC bm = beta * mp;
+        m = bm + dl;
+      }
+      if (!isfinite(m)) acc.flags |= CO2_FLAG_M_NONFINITE;
+      O[j] = Store<T>::from(m);
+    } else if (OP == OP_ITERATE) {  // outer_algorithms.cpp:100-106
+      TC alpha = (TC)a.s0, phi = (TC)a.s1;
+      TC x = to_c(A[j]), m = to_c(B[j]);
+      TC c = m;
+      if (a.i0) {
+        if (!isfinite(m)) acc.flags |= CO2_FLAG_CLIP_NONFINITE;
+        acc.clipped += (m < -phi) || (phi < m);
+        TC lo = (m < -phi) ? -phi : m;
+        c = (phi < lo) ? phi : lo;
+      }
+      TC ac = alpha * c;
+      TC xn = x - ac;
+      if (!isfinite(xn)) acc.flags |= CO2_FLAG_X_NONFINITE;
+      double st = (double)fabs(xn - x);
+      acc.max_step = st > acc.max_step ? st : acc.max_step;
+      O[j] = Store<T>::from(xn);
+    } else {  // OP_CLIP, param_ops.cpp:35-43
+      TC phi = (TC)a.s0;
+      TC v = to_c(A[j]);
+      if (!isfinite(v)) acc.flags |= CO2_FLAG_CLIP_NONFINITE;
+      acc.clipped += (v < -phi) || (phi < v);
+      TC lo = (v < -phi) ? -phi : v;
+      O[j] = Store<T>::from((phi < lo) ? phi : lo);
+    }
+  }
+  block_finish<kThreads>(acc, a.ws);
+}
+
+template <typename T, typename TC>
+__global__ void __launch_bounds__(kThreads)
+    average_kernel(const Ptrs64<T> c, int g, T* out, int64_t n, void* ws) {
+  // param_ops.cpp:16-33: ascending-worker sum, one division by G.
+  Acc acc;
+  const TC gd = (TC)g;
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * kThreads) {
+    TC s = to_c(c.p[0][j]);
+    for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
+    TC r = s / gd;
+    if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
+    out[j] = Store<T>::from(r);
+  }
+  block_finish<kThreads>(acc, ws);
+}
+
+template <typename T, typename TC>
+__global__ void sub_kernel(const T* a, const T* b, T* o, int64_t n) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    TC r = to_c(a[j]) - to_c(b[j]);
+    o[j] = Store<T>::from(r);
+  }
+}
+
+template <typename TD, typename TSRC>
+__global__ void convert_kernel(TD* d, const TSRC* s, int64_t n) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(TD) == 8 || sizeof(TSRC) == 8) {
+      d[j] = Store<TD>::from((decltype(to_c(TD{})))to_c(s[j]));
+    } else {
+      d[j] = Store<TD>::from((float)to_c(s[j]));
+    }
+  }
+}
+
+// ------------------------------------------------------- synthetic inputs
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.hpp:45-49
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+__device__ __forceinline__ double sym_at(uint64_t key, int64_t j) {
+  // rng.hpp:17-25 in random-access form: draw j uses counter j+1.
+  uint64_t u = mix64(key + (uint64_t)(j + 1) * kGolden);
+  double U = (double)(u >> 11) * 0x1.0p-53;
+  return 2.0 * U - 1.0;
+}
+
+template <class M>
+__global__ void synth_kernel(uint64_t kp0, uint64_t kp1, uint64_t kx, uint64_t ke, uint64_t km,
+                             int64_t j0, int64_t count, typename M::TS* x_t0,
+                             typename M::TS* p0, typename M::TL* p1, typename M::TL* x_end,
+                             typename M::TS* m) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = j0 + i;
+    // round_state: double -> state dtype -> back to double.
+    double p0v = (double)(TS)(0.02 * sym_at(kp0, j));
+    const bool stalled = (j % 61) == 0;
+    if (stalled) p0v = (double)to_c(Store<TL>::from((TC)p0v));
+    if (p0) p0[i] = (TS)p0v;
+    if (p1) {
+      double v = stalled ? p0v : p0v - 1e-3 * sym_at(kp1, j);
+      p1[i] = Store<TL>::from((TC)v);
+    }
+    if (x_t0) x_t0[i] = (TS)(p0v + 4e-3 * sym_at(kx, j));
+    if (x_end) x_end[i] = Store<TL>::from((TC)(p0v - 4e-3 * sym_at(ke, j)));
+    if (m) m[i] = (TS)(1e-2 * sym_at(km, j));
+  }
+}
+
+template <typename T, typename TC>
+__global__ void inner_step_kernel(T* x, int64_t n, double lr, double scale, uint64_t key,
+                                  int64_t offset, int repeat) {
+  const TC lrc = (TC)lr, sc = (TC)scale;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    TC g = 0;
+    for (int r = 0; r < repeat; ++r) g += sc * (TC)sym_at(key, offset + j + (int64_t)r * n);
+    TC v = to_c(x[j]);
+    TC step = lrc * g;
+    x[j] = Store<T>::from(v - step);
+  }
+}
+
+__global__ void fill_u32_kernel(uint32_t* d, uint32_t v, int64_t n) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    d[j] = v;
+}
+
+uint64_t host_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t host_key(uint64_t seed, uint64_t stream) {  // rng.hpp:14-15
+  return host_mix(host_mix(seed + kGolden) ^ stream);
+}
+
+int simple_grid(int64_t n, int threads) {
+  int64_t need = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * 8;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+co2_status_t check_dtype(co2_dtype_t dt) {
+  if (dt != CO2_DTYPE_F64 && dt != CO2_DTYPE_F32 && dt != CO2_DTYPE_BF16)
+    return fail(CO2_ERR_VALIDATION, "unknown dtype %d", (int)dt);
+  return CO2_OK;
+}
+
+template <int OP>
+co2_status_t launch_op(co2_dtype_t dt, const OpArgs& a, cudaStream_t s) {
+  CO2_TRY(check_dtype(dt));
+  if (!a.ws) return fail(CO2_ERR_VALIDATION, "null workspace");
+  int grid = simple_grid(a.n, kThreads);
+  if (grid > kMaxBlocks) grid = kMaxBlocks;
+  if (dt == CO2_DTYPE_F64)
+    op_kernel<double, double, OP><<<grid, kThreads, 0, s>>>(a);
+  else if (dt == CO2_DTYPE_F32)
+    op_kernel<float, float, OP><<<grid, kThreads, 0, s>>>(a);
+  else
+    op_kernel<bf16s, float, OP><<<grid, kThreads, 0, s>>>(a);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+co2_status_t outer_step_impl(co2_mode_t mode, int64_t n, const void* x_t0, const void* p0,
+                             const void* p1, const void* xbar, int32_t divisor, void* m,
+                             void* anchor, void* params, void* gap, const co2_hyper_t* h,
+                             void* ws, cudaStream_t s) {
+  StepArgs a{x_t0, p0, p1, xbar, m, anchor, params, gap, n, h->alpha, h->beta, h->phi,
+             h->epsilon, h->tau, divisor, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws};
+  switch (mode) {
+    case CO2_MODE_F64: return launch_fused<ModeF64>(a, s);
+    case CO2_MODE_F32: return launch_fused<ModeF32>(a, s);
+    case CO2_MODE_BF16_MIXED: return launch_fused<ModeBF16>(a, s);
+  }
+  return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
+}
+
+}  // namespace co2
+
+using namespace co2;
+
+extern "C" co2_status_t co2_staleness_gap(co2_dtype_t dt, int64_t n, const void* x_t0,
+                                          const void* prev_x0, const void* prev_x1, int32_t tau,
+                                          double epsilon, void* gap_out, void* ws, void* stream) {
+  // outer_algorithms.cpp:50-56 (scalar validation first)
+  if (tau < 1) return fail(CO2_ERR_VALIDATION, "staleness_gap: tau must be >= 1");
+  if (!(epsilon > 0.0)) return fail(CO2_ERR_VALIDATION, "staleness_gap: epsilon must be positive");
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "staleness_gap: dimensions differ");
+  OpArgs a{x_t0, prev_x0, prev_x1, gap_out, n, (double)tau, epsilon, 0, ws};
+  return launch_op<OP_GAP>(dt, a, S(stream));
+}
+
+extern "C" co2_status_t co2_penalized_momentum(co2_dtype_t dt, int64_t n, const void* m_prev,
+                                               double beta, const void* gap, const void* delta,
+                                               int32_t penalty, void* m_out, void* ws,
+                                               void* stream) {
+  // outer_algorithms.cpp:70-72
+  if (beta < 0.0 || beta >= 1.0)
+    return fail(CO2_ERR_VALIDATION, "momentum update: beta must lie in [0, 1)");
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "momentum update: dimensions differ");
+  OpArgs a{m_prev, gap, delta, m_out, n, beta, 0.0, penalty ? 1 : 0, ws};
+  return launch_op<OP_MOMENTUM>(dt, a, S(stream));
+}
+
+extern "C" co2_status_t co2_outer_iterate(co2_dtype_t dt, int64_t n, const void* x_t0,
+                                          double alpha, const void* m, double phi, int32_t clip,
+                                          void* x_out, void* ws, void* stream) {
+  // outer_algorithms.cpp:94-96; clip_elementwise's phi check param_ops.cpp:36-38
+  if (!(alpha > 0.0)) return fail(CO2_ERR_VALIDATION, "outer_iterate: alpha must be positive");
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "outer_iterate: dimensions differ");
+  if (clip && !(phi > 0.0))
+    return fail(CO2_ERR_VALIDATION, "clip_elementwise: phi must be positive");
+  OpArgs a{x_t0, m, nullptr, x_out, n, alpha, phi, clip ? 1 : 0, ws};
+  return launch_op<OP_ITERATE>(dt, a, S(stream));
+}
+
+extern "C" co2_status_t co2_clip_elementwise(co2_dtype_t dt, int64_t n, const void* v, double phi,
+                                             void* out, void* ws, void* stream) {
+  if (!(phi > 0.0)) return fail(CO2_ERR_VALIDATION, "clip_elementwise: phi must be positive");
+  OpArgs a{v, nullptr, nullptr, out, n, phi, 0.0, 0, ws};
+  return launch_op<OP_CLIP>(dt, a, S(stream));
+}
+
+extern "C" co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const* contributions,
+                                    int64_t n, void* out, void* ws, void* stream) {
+  if (g <= 0) return fail(CO2_ERR_VALIDATION, "average: empty contribution list");
+  if (g > 64) return fail(CO2_ERR_VALIDATION, "average: at most 64 contributions");
+  CO2_TRY(check_dtype(dt));
+  if (!ws) return fail(CO2_ERR_VALIDATION, "null workspace");
+  int grid = simple_grid(n, kThreads);
+  if (grid > kMaxBlocks) grid = kMaxBlocks;
+  cudaStream_t s = S(stream);
+  if (dt == CO2_DTYPE_F64) {
+    Ptrs64<double> p{};
+    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const double*>(contributions[i]);
+    average_kernel<double, double><<<grid, kThreads, 0, s>>>(p, g, static_cast<double*>(out), n, ws);
+  } else if (dt == CO2_DTYPE_F32) {
+    Ptrs64<float> p{};
+    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const float*>(contributions[i]);
+    average_kernel<float, float><<<grid, kThreads, 0, s>>>(p, g, static_cast<float*>(out), n, ws);
+  } else {
+    Ptrs64<bf16s> p{};
+    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const bf16s*>(contributions[i]);
+    average_kernel<bf16s, float><<<grid, kThreads, 0, s>>>(p, g, static_cast<bf16s*>(out), n, ws);
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_sub(co2_dtype_t dt, int64_t n, const void* a, const void* b, void* out,
+                                void* stream) {
+  CO2_TRY(check_dtype(dt));
+  int grid = simple_grid(n, kThreads);
+  cudaStream_t s = S(stream);
+  if (dt == CO2_DTYPE_F64)
+    sub_kernel<double, double><<<grid, kThreads, 0, s>>>(
+        static_cast<const double*>(a), static_cast<const double*>(b), static_cast<double*>(out), n);
+  else if (dt == CO2_DTYPE_F32)
+    sub_kernel<float, float><<<grid, kThreads, 0, s>>>(
+        static_cast<const float*>(a), static_cast<const float*>(b), static_cast<float*>(out), n);
+  else
+    sub_kernel<bf16s, float><<<grid, kThreads, 0, s>>>(
+        static_cast<const bf16s*>(a), static_cast<const bf16s*>(b), static_cast<bf16s*>(out), n);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+namespace {
+template <typename TD>
+co2_status_t convert_from(TD* d, co2_dtype_t sdt, const void* s, int64_t n, cudaStream_t st) {
+  int grid = simple_grid(n, kThreads);
+  if (sdt == CO2_DTYPE_F64)
+    convert_kernel<TD, double><<<grid, kThreads, 0, st>>>(d, static_cast<const double*>(s), n);
+  else if (sdt == CO2_DTYPE_F32)
+    convert_kernel<TD, float><<<grid, kThreads, 0, st>>>(d, static_cast<const float*>(s), n);
+  else
+    convert_kernel<TD, bf16s><<<grid, kThreads, 0, st>>>(d, static_cast<const bf16s*>(s), n);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+}  // namespace
+
+extern "C" co2_status_t co2_convert(co2_dtype_t ddt, void* dst, co2_dtype_t sdt, const void* src,
+                                    int64_t n, void* stream) {
+  CO2_TRY(check_dtype(ddt));
+  CO2_TRY(check_dtype(sdt));
+  if (n == 0) return CO2_OK;
+  if (ddt == sdt) {
+    size_t es = ddt == CO2_DTYPE_F64 ? 8 : (ddt == CO2_DTYPE_F32 ? 4 : 2);
+    CO2_CUDA(cudaMemcpyAsync(dst, src, es * (size_t)n, cudaMemcpyDeviceToDevice, S(stream)));
+    return CO2_OK;
+  }
+  if (ddt == CO2_DTYPE_F64) return convert_from(static_cast<double*>(dst), sdt, src, n, S(stream));
+  if (ddt == CO2_DTYPE_F32) return convert_from(static_cast<float*>(dst), sdt, src, n, S(stream));
+  return convert_from(static_cast<bf16s*>(dst), sdt, src, n, S(stream));
+}
+
+extern "C" co2_status_t co2_synth(co2_mode_t mode, uint64_t seed, int32_t worker, int64_t j0,
+                                  int64_t count, void* x_t0, void* p0, void* p1, void* x_end,
+                                  void* m, void* stream) {
+  if (count < 0 || j0 < 0) return fail(CO2_ERR_VALIDATION, "synth: negative range");
+  if (count == 0) return CO2_OK;
+  uint64_t w = (uint64_t)(uint32_t)worker;
+  // stream key = (buffer_id << 32) | worker; p0 worker-independent.
+  uint64_t kp0 = host_key(seed, (0ull << 32) | 0ull), kp1 = host_key(seed, (1ull << 32) | w),
+           kx = host_key(seed, (2ull << 32) | w), ke = host_key(seed, (3ull << 32) | w),
+           km = host_key(seed, (4ull << 32) | w);
+  int grid = simple_grid(count, kThreads);
+  cudaStream_t s = S(stream);
+  switch (mode) {
+    case CO2_MODE_F64:
+      synth_kernel<ModeF64><<<grid, kThreads, 0, s>>>(
+          kp0, kp1, kx, ke, km, j0, count, (double*)x_t0, (double*)p0, (double*)p1,
+          (double*)x_end, (double*)m);
+      break;
+    case CO2_MODE_F32:
+      synth_kernel<ModeF32><<<grid, kThreads, 0, s>>>(kp0, kp1, kx, ke, km, j0, count,
+                                                       (float*)x_t0, (float*)p0, (float*)p1,
+                                                       (float*)x_end, (float*)m);
+      break;
+    case CO2_MODE_BF16_MIXED:
+      synth_kernel<ModeBF16><<<grid, kThreads, 0, s>>>(kp0, kp1, kx, ke, km, j0, count,
+                                                        (float*)x_t0, (float*)p0, (bf16s*)p1,
+                                                        (bf16s*)x_end, (float*)m);
+      break;
+    default:
+      return fail(CO2_ERR_VALIDATION, "synth: unknown mode %d", (int)mode);
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_synthetic_inner_step(co2_dtype_t dt, int64_t n, void* params,
+                                                 double lr, double scale, uint64_t seed,
+                                                 int32_t worker, int64_t step, int32_t repeat,
+                                                 void* stream) {
+  CO2_TRY(check_dtype(dt));
+  if (repeat < 1) repeat = 1;
+  uint64_t key = host_key(seed, (5ull << 32) | (uint64_t)(uint32_t)worker);
+  int64_t offset = step * n * (int64_t)repeat;
+  int grid = simple_grid(n, kThreads);
+  cudaStream_t s = S(stream);
+  if (dt == CO2_DTYPE_F64)
+    inner_step_kernel<double, double><<<grid, kThreads, 0, s>>>((double*)params, n, lr, scale, key,
+                                                                offset, repeat);
+  else if (dt == CO2_DTYPE_F32)
+    inner_step_kernel<float, float><<<grid, kThreads, 0, s>>>((float*)params, n, lr, scale, key,
+                                                              offset, repeat);
+  else
+    inner_step_kernel<bf16s, float><<<grid, kThreads, 0, s>>>((bf16s*)params, n, lr, scale, key,
+                                                              offset, repeat);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_fill_u32(void* dst, uint32_t value, int64_t count, void* stream) {
+  if (count <= 0) return CO2_OK;
+  fill_u32_kernel<<<simple_grid(count, kThreads), kThreads, 0, S(stream)>>>((uint32_t*)dst, value,
+                                                                             count);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}

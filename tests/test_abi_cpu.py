@@ -1,0 +1,163 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol
+include/co2_b200.h declares, validates like the reference, and its host-side
+timing model reproduces the reference's KATs."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+from paper_2401_16265_b200 import _lib as L
+from paper_2401_16265_b200 import co2
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "co2_b200.h")) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(co2_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 40
+    out = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (co2_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert set(syms) == set(L.SIGNATURES), set(syms) ^ set(L.SIGNATURES)
+    lib = L.lib()
+    for s in syms:
+        assert hasattr(lib, s)
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True, text=True,
+                         check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_hyper_validation_messages():
+    """Co2Hyper::validate messages (proj/src/outer_algorithms.cpp:37-46)."""
+    co2.Co2Hyper().validate()
+    for kw, msg in [({"alpha": 0.0}, "hyper: alpha must be positive"),
+                    ({"beta": 1.0}, "hyper: beta must lie in [0, 1)"),
+                    ({"beta": -0.1}, "hyper: beta must lie in [0, 1)"),
+                    ({"phi": 0.0}, "hyper: phi must be positive"),
+                    ({"epsilon": 0.0}, "hyper: epsilon must be positive")]:
+        with pytest.raises(co2.ValidationError) as e:
+            co2.Co2Hyper(**kw).validate()
+        assert str(e.value) == msg
+
+
+def test_outer_step_validates_before_launch():
+    """Host-checkable validation happens before any device work."""
+    import ctypes as C
+    h = co2.Co2Hyper(alpha=-1.0).c(4)
+    st = L.lib().co2_outer_step(L.MODE_F32, 0, None, None, None, None, 1, None, None, None, None,
+                                C.byref(h), None, None)
+    assert st == L.ERR_VALIDATION
+    assert L.lib().co2_last_error().decode() == "hyper: alpha must be positive"
+    h = co2.Co2Hyper().c(0)
+    st = L.lib().co2_outer_step(L.MODE_F32, 0, None, None, None, None, 1, None, None, None, None,
+                                C.byref(h), None, None)
+    assert st == L.ERR_VALIDATION
+    assert L.lib().co2_last_error().decode() == "staleness_gap: tau must be >= 1"
+
+
+def test_allreduce_time_ring_formula(golden):
+    """proj/tests/test_timing_model.cpp:23-47"""
+    k = golden["allreduce_time"]
+    s = co2.ClusterSpec(workers=k["workers"], latency=k["latency"], param_bytes=k["param_bytes"],
+                        inter_bandwidth=k["bandwidth"])
+    assert co2.allreduce_time(s) == pytest.approx(k["expected"], rel=1e-15)
+    s.workers = 2
+    assert co2.allreduce_time(s) == pytest.approx(k["expected_w2"], rel=1e-15)
+    s = co2.ClusterSpec(workers=8, latency=1.0, param_bytes=1e12, measured_override=0.25)
+    assert co2.allreduce_time(s) == 0.25
+    s.workers = 1
+    assert co2.allreduce_time(s) == 0.0
+
+
+def test_cluster_validation():
+    """proj/tests/test_timing_model.cpp:49-62"""
+    for kw in [{"workers": 0}, {"latency": -1.0}, {"inter_bandwidth": 0.0},
+               {"measured_override": -0.5}]:
+        with pytest.raises(co2.ValidationError):
+            co2.ClusterSpec(**({"workers": 2} | kw)).validate()
+
+
+def test_overlap_ratio():
+    """proj/tests/test_timing_model.cpp:64-71"""
+    assert co2.overlap_ratio(2, 0.25, 1.0) == 0.5
+    assert co2.overlap_ratio(8, 0.25, 1.0) == 1.0
+    assert co2.overlap_ratio(1, 0.0, 1.0) == 0.0
+    assert co2.overlap_ratio(1, 0.5, 0.0) == 1.0
+    with pytest.raises(co2.ValidationError):
+        co2.overlap_ratio(0, 0.1, 1.0)
+    with pytest.raises(co2.ValidationError):
+        co2.overlap_ratio(1, -0.1, 1.0)
+
+
+def test_overlap_table_acceptance(golden):
+    """proj/tests/acceptance.cpp:60-75: paper's overlap table within 0.5pp."""
+    k = golden["overlap_table"]
+    for tau, exp in zip(k["taus"], k["expected_pct"]):
+        assert abs(100.0 * co2.overlap_ratio(tau, k["t_comp"], k["t_comm"]) - exp) <= k["tol_pp"]
+
+
+def test_co2_timeline_hand_traces(golden):
+    """proj/tests/test_timing_model.cpp:79-116"""
+    for k in golden["timeline"]:
+        spec = co2.ClusterSpec(workers=k["workers"], t_comp=k["t_comp"], t_outer=k["t_outer"],
+                               measured_override=k["comm"])
+        r = co2.simulate_timeline_co2(spec, k["tau"], k["rounds"])
+        assert r.wall_time == k["wall_time"]
+        if "total_stall" in k:
+            assert r.total_stall == k["total_stall"]
+        if "overlap" in k:
+            assert r.overlap_ratio_achieved == pytest.approx(k["overlap"])
+        if "per_round" in k:
+            assert [list(p[1:]) for p in r.per_round] == k["per_round"]
+        if "throughput" in k:
+            assert r.throughput == k["throughput"]
+    with pytest.raises(co2.ValidationError):
+        co2.simulate_timeline_co2(co2.ClusterSpec(workers=2, measured_override=1.0), 0, 3)
+    with pytest.raises(co2.ValidationError):
+        co2.simulate_timeline_co2(co2.ClusterSpec(workers=2, measured_override=1.0), 2, 0)
+
+
+def test_overlap_flatness_acceptance():
+    """proj/tests/acceptance.cpp:88-116 (co2 half): with tau*t_comp >= t_comm
+    the one-round-stale pattern has zero stall and flat throughput."""
+    fast = co2.simulate_timeline_co2(co2.ClusterSpec(workers=16, t_comp=0.109,
+                                                     measured_override=0.109), 12, 50)
+    slow = co2.simulate_timeline_co2(co2.ClusterSpec(workers=16, t_comp=0.109,
+                                                     measured_override=1.09), 12, 50)
+    assert fast.total_stall == 0.0 and slow.total_stall == 0.0
+    assert abs(fast.throughput - slow.throughput) / fast.throughput < 1e-3
+
+
+def test_facade_header_compiles():
+    r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"),
+                        "-I/usr/local/cuda/include",
+                        os.path.join(ROOT, "tests", "cpp", "facade_test.cpp")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_product_does_not_reference_oracle():
+    """The product path never links or imports the oracle (test infra only)."""
+    pkg = os.path.join(ROOT, "paper_2401_16265_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cpp", ".cuh", ".h")):
+                with open(os.path.join(dirpath, fn)) as f:
+                    src = f.read()
+                for needle in ("import oracle", "from oracle", "co2_oracle.h", "libco2oracle",
+                               "orc_"):
+                    assert needle not in src, (fn, needle)
+    out = subprocess.run(["ldd", L.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle" not in out

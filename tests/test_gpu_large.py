@@ -1,0 +1,52 @@
+"""Full-size configurations (BASELINE.json configs C2, C3, C4-shard): the
+fused step at production sizes, checked bitwise against the oracle on
+sampled coordinate windows (the step is per-coordinate, so any window is an
+exact sub-problem) plus size-independent properties."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2401_16265_b200 import co2
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = [
+    ("C2_125M_f32", co2.MODE_F32, 125_000_000, 12),
+    ("C3_1.3B_bf16_mixed", co2.MODE_BF16_MIXED, 1_300_000_000, 12),
+    ("C4_7B_shard_of_8_bf16_mixed", co2.MODE_BF16_MIXED, 875_000_000, 12),
+]
+
+
+def to_np(t):
+    t = t.detach().cpu()
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16).copy()
+    return t.numpy().copy()
+
+
+@pytest.mark.parametrize("name,mode,n,tau", CONFIGS)
+def test_full_size_windows_bitwise(name, mode, n, tau):
+    torch.cuda.empty_cache()
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    h = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    # in-place layout of the round driver: anchor over prev_x0, params over xbar
+    d = co2.outer_step(mode, x, p0, p1, xe, m, h, tau, anchor_out=p0, params_out=xe)
+    oh = O.hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12, tau=tau)
+    rng = np.random.default_rng(1234)
+    starts = sorted(set(rng.integers(0, n - 4096, size=24).tolist()) | {0, n - 4096})
+    for j0 in starts:
+        ox, op0, op1, oxe, om = O.synth(mode, 4096, j0=j0)
+        ref = O.outer_step(mode, ox, op0, op1, oxe, om, oh)
+        sl = slice(j0, j0 + 4096)
+        assert to_np(m[sl]).tobytes() == ref.m.tobytes(), (name, j0)
+        assert to_np(p0[sl]).tobytes() == ref.anchor.tobytes(), (name, j0)
+        assert to_np(xe[sl]).tobytes() == ref.params.tobytes(), (name, j0)
+    # size-independent properties (outer_algorithms tests :105-120, :329-350)
+    assert d.flags == 0
+    assert d.min_gap >= 1.0
+    assert d.max_outer_step <= np.float32(5e-3) * (1 + 2.0 ** -16)
+    assert d.n_floored == (n + 60) // 61  # stalled coordinates j % 61 == 0
+    assert 0 < d.n_clipped < n
+    del x, p0, p1, xe, m
+    torch.cuda.empty_cache()

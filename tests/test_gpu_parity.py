@@ -1,0 +1,275 @@
+"""GPU parity of the sm_100a kernels against the CPU oracle (bitwise).
+
+All calls go through the C ABI (libco2b200.so).  The oracle (oracle/) is the
+checker only.
+"""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT
+from oracle import oracle as O
+from paper_2401_16265_b200 import _lib as L
+from paper_2401_16265_b200 import co2
+
+pytestmark = pytest.mark.gpu
+
+MODES = [co2.MODE_F64, co2.MODE_F32, co2.MODE_BF16_MIXED]
+COMBOS = [(True, True), (True, False), (False, True), (False, False)]
+
+
+def to_np(t: torch.Tensor) -> np.ndarray:
+    t = t.detach().cpu()
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16).copy()
+    return t.numpy().copy()
+
+
+def to_dev(a: np.ndarray, dtype=None) -> torch.Tensor:
+    if a.dtype == np.uint16:
+        return torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).cuda()
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def same(a: np.ndarray, b: np.ndarray) -> bool:
+    return a.dtype == b.dtype and a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+def hyper(tau=4, penalty=True, clip=True, phi=5e-3):
+    return co2.Co2Hyper(alpha=1.0, beta=0.7, phi=phi, epsilon=1e-12, penalty=penalty, clip=clip)
+
+
+def ohyper(tau=4, penalty=True, clip=True, phi=5e-3):
+    return O.hyper(alpha=1.0, beta=0.7, phi=phi, epsilon=1e-12, tau=tau, penalty=penalty,
+                   clip=clip)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("j0", [0, 12345])
+def test_synth_generator_bitwise(mode, j0):
+    n = 100003
+    for worker in (0, 3):
+        gpu = co2.synth(mode, n, worker=worker, j0=j0)
+        torch.cuda.synchronize()
+        cpu = O.synth(mode, n, worker=worker, j0=j0)
+        for g, c in zip(gpu, cpu):
+            assert same(to_np(g), c)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("penalty,clip", COMBOS)
+@pytest.mark.parametrize("n", [1, 7, 1000003])
+def test_fused_step_bitwise(mode, penalty, clip, n):
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    ox, op0, op1, oxe, om = O.synth(mode, n)
+    ref = O.outer_step(mode, ox, op0, op1, oxe, om, ohyper(4, penalty, clip))
+    assert ref.status == 0
+    anchor = torch.empty_like(x)
+    params = torch.empty_like(xe)
+    gap = torch.empty_like(x)
+    d = co2.outer_step(mode, x, p0, p1, xe, m, hyper(4, penalty, clip), 4, anchor_out=anchor,
+                       params_out=params, gap_out=gap)
+    assert same(to_np(m), ref.m)
+    assert same(to_np(anchor), ref.anchor)
+    assert same(to_np(params), ref.params)
+    assert same(to_np(gap), ref.gap)
+    assert d.min_gap == ref.diag.min_gap
+    assert d.max_outer_step == ref.diag.max_outer_step
+    assert d.n_clipped == ref.diag.n_clipped and d.n_floored == ref.diag.n_floored
+    assert d.flags == 0
+    if mode == co2.MODE_F64:  # and bit-for-bit the reference's unfused fp64 passes
+        r64 = O.worker_step_f64(ox, op0, op1, oxe, om, ohyper(4, penalty, clip))
+        assert same(to_np(m), r64.m) and same(to_np(params), r64.next)
+        assert d.min_gap == r64.min_gap and d.max_outer_step == r64.max_outer_step
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_fused_divisor_sum(mode):
+    """xbar as a G-worker sum divided once in the kernel (average(), param_ops.cpp:30)."""
+    n, G = 65537, 3
+    x, p0, p1, _, m = co2.synth(mode, n)
+    ox, op0, op1, _, om = O.synth(mode, n)
+    s = O.synth(mode, n, worker=0)[3]
+    for w in (1, 2):
+        e = O.synth(mode, n, worker=w)[3]
+        if mode == O.MODE_BF16_MIXED:
+            s = O.f32_to_bf16_bits(O.bf16_bits_to_f32(s) + O.bf16_bits_to_f32(e))
+        else:
+            s = s + e
+    ref = O.outer_step(mode, ox, op0, op1, s, om, ohyper(), divisor=G)
+    params = torch.empty(n, dtype=co2.LOW_TORCH[mode], device="cuda")
+    co2.outer_step(mode, x, p0, p1, to_dev(s), m, hyper(), 4, divisor=G, params_out=params)
+    assert same(to_np(m), ref.m) and same(to_np(params), ref.params)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_fused_in_place_aliasing(mode):
+    """anchor_out aliasing prev_x0 and params_out aliasing xbar (the round
+    driver's layout) give the same bits as separate outputs."""
+    n = 333333
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    a2, b2 = torch.empty_like(p0), torch.empty_like(xe)
+    m2 = m.clone()
+    co2.outer_step(mode, x, p0, p1, xe, m2, hyper(), 4, anchor_out=a2, params_out=b2)
+    co2.outer_step(mode, x, p0, p1, xe, m, hyper(), 4, anchor_out=p0, params_out=xe)
+    assert same(to_np(m), to_np(m2)) and same(to_np(p0), to_np(a2))
+    assert same(to_np(xe), to_np(b2))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_fused_unaligned_views(mode):
+    """Sub-views that break 16-byte alignment take the scalar-vector path
+    and still match bit for bit."""
+    n = 10001
+    x, p0, p1, xe, m = co2.synth(mode, n + 1)
+    ox, op0, op1, oxe, om = O.synth(mode, n + 1)
+    ref = O.outer_step(mode, ox[1:], op0[1:], op1[1:], oxe[1:], om[1:], ohyper())
+    mv = m[1:]
+    params = torch.empty(n + 1, dtype=xe.dtype, device="cuda")[1:]
+    d = co2.outer_step(mode, x[1:], p0[1:], p1[1:], xe[1:], mv, hyper(), 4, params_out=params)
+    assert same(to_np(mv), ref.m) and same(to_np(params), ref.params)
+    assert d.n_clipped == ref.diag.n_clipped
+
+
+def test_fused_errors_follow_reference_precedence():
+    n = 4096
+    mode = co2.MODE_F32
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    bad = x.clone()
+    bad[1000] = float("nan")
+    with pytest.raises(co2.NumericError, match="non-finite value in staleness_gap"):
+        co2.outer_step(mode, bad, p0, p1, xe, m.clone(), hyper(), 4)
+    mm = m.clone()
+    mm[7] = float("inf")
+    with pytest.raises(co2.NumericError, match="non-finite value in momentum update"):
+        co2.outer_step(mode, x, p0, p1, xe, mm, hyper(), 4)
+    # both: staleness_gap wins (it is checked first in the reference)
+    with pytest.raises(co2.NumericError, match="staleness_gap"):
+        co2.outer_step(mode, bad, p0, p1, xe, mm.clone(), hyper(), 4)
+    # p1 = +inf: Lambda = finite/inf + 1 = 1, no error (reference std::max semantics)
+    pp = p1.clone()
+    pp[3] = float("inf")
+    gap = torch.empty_like(x)
+    co2.outer_step(mode, x, p0, pp, xe, m.clone(), hyper(), 4, gap_out=gap)
+    assert gap[3].item() == 1.0
+    pp[3] = float("nan")
+    with pytest.raises(co2.NumericError, match="staleness_gap"):
+        co2.outer_step(mode, x, p0, pp, xe, m.clone(), hyper(), 4)
+    with pytest.raises(co2.ValidationError, match="hyper: phi must be positive"):
+        co2.outer_step(mode, x, p0, p1, xe, m.clone(), co2.Co2Hyper(phi=0.0), 4)
+
+
+def test_fused_empty_and_determinism():
+    mode = co2.MODE_F32
+    e = torch.empty(0, device="cuda")
+    d = co2.outer_step(mode, e, e, e, e, e.clone(), hyper(), 4)
+    assert d.min_gap == float("inf") and d.max_outer_step == 0.0 and d.n_clipped == 0
+    x, p0, p1, xe, m = co2.synth(mode, 2_000_000)
+    outs = []
+    for _ in range(3):
+        mm = m.clone()
+        d = co2.outer_step(mode, x, p0, p1, xe, mm, hyper(), 4)
+        outs.append((mm.clone(), d.min_gap, d.max_outer_step, d.n_clipped, d.n_floored))
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and o[1:] == outs[0][1:]
+
+
+# ---------------------------------------------------------- unfused ops
+@pytest.mark.parametrize("dt", [torch.float64])
+def test_unfused_ops_vs_oracle(dt):
+    n = 50021
+    ox, op0, op1, oxe, om = O.synth(O.MODE_F64, n)
+    x, p0, p1, xe, m = (to_dev(a) for a in (ox, op0, op1, oxe, om))
+    gap = co2.staleness_gap(x, p0, p1, 4, 1e-12)
+    assert same(to_np(gap), O.staleness_gap(ox, op0, op1, 4, 1e-12))
+    delta_np = op0 - oxe
+    delta = to_dev(delta_np)
+    mm = co2.penalized_momentum_update(m, 0.7, gap, delta, True)
+    ref_m = O.penalized_momentum_update(om, 0.7, to_np(gap), delta_np, True)
+    assert same(to_np(mm), ref_m)
+    xn = co2.outer_iterate(x, 1.0, mm, 5e-3, True)
+    assert same(to_np(xn), O.outer_iterate(ox, 1.0, ref_m, 5e-3, True))
+    xr = co2.outer_iterate(x, 1.0, mm, 5e-3, False)
+    assert same(to_np(xr), O.outer_iterate(ox, 1.0, ref_m, 5e-3, False))
+    c = co2.clip_elementwise(mm, 5e-3)
+    assert same(to_np(c), O.clip_elementwise(ref_m, 5e-3))
+
+
+def test_unfused_kats_and_errors(golden):
+    k = golden["momentum"]
+    t = lambda v: torch.tensor(v, dtype=torch.float64, device="cuda")  # noqa: E731
+    assert co2.penalized_momentum_update(t(k["m_prev"]), k["beta"], t(k["gap"]), t(k["delta"]),
+                                         True).tolist() == k["expected_penalty"]
+    with pytest.raises(co2.ValidationError, match="gap coordinate below 1"):
+        co2.penalized_momentum_update(t(k["m_prev"]), k["beta"], t(k["bad_gap"]), t(k["delta"]),
+                                      True)
+    for g in golden["staleness_gap"]:
+        got = co2.staleness_gap(t(g["x_t0"]), t(g["prev_x0"]), t(g["prev_x1"]), g["tau"],
+                                g["epsilon"]).cpu().numpy()
+        ref = O.staleness_gap(np.array(g["x_t0"]), np.array(g["prev_x0"]), np.array(g["prev_x1"]),
+                              g["tau"], g["epsilon"])
+        assert same(got, ref)
+    oi = golden["outer_iterate"]
+    assert co2.outer_iterate(t(oi["x"]), oi["alpha"], t(oi["m"]), oi["phi"],
+                             True).tolist() == oi["expected_clip"]
+    with pytest.raises(co2.NumericError, match="clip_elementwise input"):
+        co2.clip_elementwise(t([float("nan")]), 1.0)
+    with pytest.raises(co2.NumericError, match="clip_elementwise input"):
+        co2.outer_iterate(t([1.0]), 1.0, t([float("inf")]), 1.0, True)
+    with pytest.raises(co2.NumericError, match="outer_iterate"):
+        co2.outer_iterate(t([1.0]), 1.0, t([float("inf")]), 1.0, False)
+
+
+def test_average_golden_and_fixed_order(golden):
+    ins = [torch.tensor(v, dtype=torch.float64, device="cuda") for v in golden["average"]["inputs"]]
+    assert co2.average(ins).tolist() == golden["average"]["expected"]
+    with pytest.raises(co2.NumericError, match="non-finite value in average"):
+        co2.average([torch.tensor([1.0, float("inf")], dtype=torch.float64, device="cuda"),
+                     torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda")])
+    n = 100001
+    for mode in (O.MODE_F32, O.MODE_BF16_MIXED):
+        ends = [O.synth(mode, n, worker=w)[3] for w in range(5)]
+        got = co2.average([to_dev(e) for e in ends])
+        assert same(to_np(got), O.average_lp(ends, mode == O.MODE_BF16_MIXED))
+
+
+def test_host_e2e_entry_equals_device_path():
+    """co2_outer_step_host (pinned host buffers, chunked multi-stream
+    pipeline) returns the same bits and diagnostics as the device entry."""
+    for mode in MODES:
+        n = 1_000_003
+        ox, op0, op1, oxe, om = O.synth(mode, n)
+        ref = O.outer_step(mode, ox, op0, op1, oxe, om, ohyper())
+
+        def pin(a):
+            t = torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a.copy())
+            return t.pin_memory()
+
+        hx, hp0, hp1, hxe, hm = (pin(a) for a in (ox, op0, op1, oxe, om))
+        anchor = torch.empty_like(hx).pin_memory()
+        params = torch.empty_like(hxe).pin_memory()
+        d = co2.outer_step_host(mode, hx, hp0, hp1, hxe, hm, hyper(), 4, anchor_out=anchor,
+                                params_out=params, chunk=100_000, nstreams=3)
+
+        def back(t, like):
+            a = t.numpy()
+            return a.view(np.uint16) if like.dtype == np.uint16 else a
+
+        assert same(back(hm, om), ref.m)
+        assert same(back(anchor, ox), ref.anchor)
+        assert same(back(params, oxe), ref.params)
+        assert d.n_clipped == ref.diag.n_clipped and d.min_gap == ref.diag.min_gap
+        assert d.max_outer_step == ref.diag.max_outer_step
+
+
+def test_cpp_facade_binary():
+    exe = os.path.join(ROOT, "build", "facade_test")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", ROOT, "facade_test"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FACADE OK" in r.stdout

@@ -1,0 +1,241 @@
+"""co2_round + CollectiveEngine on the GPU against the reference's fixtures and
+the oracle (bitwise).  Inner loops run on the host (fixtures) or as the
+synthetic inner-step kernel; the outer rounds run through the C ABI."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2401_16265_b200 import _lib as L
+from paper_2401_16265_b200 import co2
+from simdrive import OracleRound, inner_loop, shard_gradient
+
+pytestmark = pytest.mark.gpu
+
+
+def to_np(t):
+    t = t.detach().cpu()
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16).copy()
+    return t.numpy().copy()
+
+
+def run_fixture_rounds(fx, ghost=False, check_expect=True):
+    feats = np.array(fx["features"], dtype=np.float64)
+    targs = np.array(fx["targets"], dtype=np.float64)
+    shards, hd, tau = fx["shards"], fx["hyper"], fx["tau"]
+    lr = fx["schedule"]["base_lr"]
+    g, n = len(shards), len(fx["init"])
+    hyper = co2.Co2Hyper(alpha=hd["alpha"], beta=hd["beta"], phi=hd["phi"],
+                         epsilon=hd["epsilon"], penalty=hd["penalty"], clip=hd["clip"],
+                         ghost_consistent=ghost)
+    eng = co2.CollectiveEngine(g, transport="local")
+    init = torch.tensor(fx["init"], dtype=torch.float64, device="cuda")
+    ws = [co2.Worker(co2.MODE_F64, n, init) for _ in range(g)]
+    rounds = []
+    for t in range(fx["rounds"]):
+        traces = []
+        for w in ws:
+            w.snapshot_start()
+            x = w.params.cpu().numpy()
+            xs, xf, xe = inner_loop(feats, targs, shards[len(traces)], x, lr, tau)
+            w.params.copy_(torch.from_numpy(xf))
+            w.snapshot_first()
+            w.params.copy_(torch.from_numpy(xe))
+            traces.append((xs, xf, xe))
+        r = co2.co2_round(ws, eng, hyper, tau)
+        rounds.append({
+            "traces": traces,
+            "result": (r.outer_applied, r.min_gap, r.max_outer_step),
+            "xbar": None if t == 0 else ws[0].buffer(L.BUF_XBAR).cpu().numpy(),
+            "params": [w.params.cpu().numpy() for w in ws],
+            "m": [w.buffer(L.BUF_MOMENTUM).cpu().numpy() for w in ws],
+            "gap": [w.buffer(L.BUF_GAP).cpu().numpy() for w in ws],
+        })
+    return rounds, ws, eng
+
+
+def test_fixture_co2_dim1_on_gpu(fixture_co2_dim1):
+    """proj/fixtures/co2_dim1.json at tolerance 0 through the product path."""
+    fx = fixture_co2_dim1
+    rounds, _, _ = run_fixture_rounds(fx)
+    for t, er in enumerate(fx["expect"]["rounds"]):
+        got = rounds[t]
+        if "consumed_average" in er:
+            assert got["xbar"].tolist() == er["consumed_average"]
+        for i, ew in enumerate(er["workers"]):
+            assert got["traces"][i][1].tolist() == ew["x_first"]
+            assert got["traces"][i][2].tolist() == ew["x_end"]
+            assert got["params"][i].tolist() == ew["params_after"]
+            if "momentum_after" in ew:
+                assert got["m"][i].tolist() == ew["momentum_after"]
+                assert got["gap"][i].tolist() == ew["gap_after"]
+    fin = fx["expect"]
+    assert [p.tolist() for p in rounds[-1]["params"]] == fin["final_params"]
+    assert [m.tolist() for m in rounds[-1]["m"]] == fin["final_momentum"]
+    assert rounds[0]["result"][0] == 0 and rounds[1]["result"][0] == 1
+    assert rounds[1]["result"][1] == 1.875  # min_gap (RoundResult)
+
+
+def test_delayed_momentum_recurrence_on_gpu(golden):
+    """proj/tests/acceptance.cpp:178-243 through co2_round (penalty/clip off):
+    bitwise against an independently coded delayed-momentum recurrence."""
+    k = golden["delayed_momentum"]
+    fx = {"features": k["features"], "targets": k["targets"], "shards": k["shards"],
+          "hyper": {"alpha": k["alpha"], "beta": k["beta"], "phi": 1.0, "epsilon": 1e-12,
+                    "penalty": False, "clip": False},
+          "tau": k["tau"], "schedule": {"base_lr": k["lr"]}, "init": k["init"],
+          "rounds": k["rounds"]}
+    rounds, _, _ = run_fixture_rounds(fx)
+    feats, targs = np.array(k["features"], float), np.array(k["targets"], float)
+    x = [np.array(k["init"], float) for _ in range(2)]
+    m = [np.zeros(2), np.zeros(2)]
+    prev0 = avg_prev = None
+    for t in range(k["rounds"]):
+        starts = [xi.copy() for xi in x]
+        for i in range(2):
+            for _ in range(k["tau"]):
+                x[i] = x[i] - k["lr"] * shard_gradient(feats, targs, k["shards"][i], x[i])
+        avg_t = O.average(x)
+        if t == 0:
+            prev0, avg_prev = starts, avg_t
+        else:
+            for i in range(2):
+                m[i] = k["beta"] * m[i] + (prev0[i] - avg_prev)
+                x[i] = starts[i] - k["alpha"] * m[i]
+                prev0[i] = starts[i]
+            avg_prev = avg_t
+        for i in range(2):
+            assert rounds[t]["params"][i].tobytes() == x[i].tobytes(), (t, i)
+
+
+def test_ghost_consistent_rounds_match_oracle(fixture_co2_dim1):
+    """Ghost-consistent branch (outer_algorithms.cpp:161-184): identical
+    workers, bitwise equal to the oracle's ghost round."""
+    fx = dict(fixture_co2_dim1)
+    fx["rounds"] = 6
+    rounds, _, _ = run_fixture_rounds(fx, ghost=True)
+
+    class H:
+        pass
+
+    h = H()
+    hd = fx["hyper"]
+    h.alpha, h.beta, h.phi, h.epsilon = hd["alpha"], hd["beta"], hd["phi"], hd["epsilon"]
+    h.penalty, h.clip, h.ghost_consistent = hd["penalty"], hd["clip"], True
+    orr = OracleRound(2, 1, h, fx["tau"])
+    for t, rd in enumerate(rounds):
+        traces = rd["traces"]
+        params, _, _, _ = orr.round([tr[2] for tr in traces], traces)
+        for i in range(2):
+            assert rd["params"][i].tobytes() == params[i].tobytes()
+            assert rd["m"][i].tobytes() == orr.m[i].tobytes()
+        if t >= 1:
+            assert rd["params"][0].tobytes() == rd["params"][1].tobytes()
+
+
+class OracleRoundLP:
+    """co2_round in the fp32 / bf16-mixed storage layout on the oracle."""
+
+    def __init__(self, mode, g, hyper):
+        self.mode, self.g, self.h = mode, g, hyper
+        self.t, self.m, self.p0, self.p1, self.pending = 0, None, None, None, None
+
+    def round(self, params, traces, m0):
+        launched = O.average_lp(params, self.mode == O.MODE_BF16_MIXED)
+        if self.t == 0:
+            self.p0 = [tr[0] for tr in traces]
+            self.p1 = [tr[1] for tr in traces]
+            self.m = [m0.copy() for _ in range(self.g)]
+            self.pending, self.t = launched, 1
+            return [p.copy() for p in params]
+        out = []
+        for i in range(self.g):
+            r = O.outer_step(self.mode, traces[i][0], self.p0[i], self.p1[i], self.pending,
+                             self.m[i], self.h)
+            assert r.status == 0
+            self.m[i] = r.m
+            self.p0[i], self.p1[i] = traces[i][0], traces[i][1]
+            out.append(r.params)
+        self.pending, self.t = launched, self.t + 1
+        return out
+
+
+@pytest.mark.parametrize("mode", [co2.MODE_F32, co2.MODE_BF16_MIXED])
+def test_c1_simulated_workers_bitwise(mode):
+    """Config C1: 1M params, 4 simulated workers, tau=4, synthetic deltas;
+    4 rounds of the product co2_round vs the oracle, bitwise every round."""
+    n, G, tau = 1 << 20, 4, 4
+    hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    oh = O.hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12, tau=tau)
+    eng = co2.CollectiveEngine(G, transport="local")
+    ws = []
+    for w in range(G):
+        init = co2.synth(mode, n, worker=w)[3]  # x_end-style draws as x_{0,0}
+        ws.append(co2.Worker(mode, n, init))
+    orr = OracleRoundLP(mode, G, oh)
+    m0 = np.zeros(n, np.float32)
+    for t in range(4):
+        traces = []
+        for i, w in enumerate(ws):
+            w.snapshot_start()
+            for k in range(tau):
+                co2.synthetic_inner_step(w.params, lr=1e-3, scale=1.0, worker=i,
+                                         step=t * tau + k)
+                if k == 0:
+                    w.snapshot_first()
+            traces.append((to_np(w.buffer(L.BUF_ANCHOR)), to_np(w.buffer(L.BUF_XFIRST)),
+                           to_np(w.params)))
+        params_before = [tr[2] for tr in traces]
+        r = co2.co2_round(ws, eng, hyper, tau)
+        ref = orr.round(params_before, traces, m0)
+        for i, w in enumerate(ws):
+            assert to_np(w.params).tobytes() == ref[i].tobytes(), (t, i)
+            if t >= 1:
+                assert to_np(w.buffer(L.BUF_MOMENTUM)).tobytes() == orr.m[i].tobytes()
+        if t >= 1:
+            assert r.outer_applied == 1 and r.min_gap >= 1.0
+            assert r.max_outer_step <= np.float32(5e-3) * (1 + 1e-6)
+
+
+def test_engine_semantics():
+    """CollectiveEngine contract (proj/tests/test_collective.cpp:43-207)."""
+    eng = co2.CollectiveEngine(2, transport="local")
+    a = torch.tensor([1.0, -2.0], dtype=torch.float64, device="cuda")
+    b = torch.tensor([3.0, 6.0], dtype=torch.float64, device="cuda")
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    h0 = eng.launch_all_reduce([a, b], out)
+    h1 = eng.launch_all_reduce([a, b], out)
+    assert eng.live_handles() == 2
+    with pytest.raises(co2.ValidationError, match="overlap window exceeded"):
+        eng.launch_all_reduce([a, b], out)
+    torch.cuda.synchronize()
+    assert eng.is_completed(h0)
+    eng.wait(h0)
+    assert eng.live_handles() == 1
+    with pytest.raises(co2.ValidationError, match="wait: handle already consumed"):
+        eng.wait(h0)
+    with pytest.raises(co2.ValidationError, match="is_completed: handle already consumed"):
+        eng.is_completed(h0)
+    with pytest.raises(co2.ValidationError, match="unknown reduce handle"):
+        eng.is_completed(99)
+    with pytest.raises(co2.ValidationError, match="contribution count 3"):
+        eng.launch_all_reduce([a, b, a], out)
+    eng.wait(h1)
+    torch.cuda.synchronize()
+    assert out.tolist() == O.average([np.array([1.0, -2.0]), np.array([3.0, 6.0])]).tolist()
+    stall, comm = eng.stall(h1)
+    assert stall >= 0.0 and comm >= 0.0
+    ev = eng.events()
+    kinds = [e["event"] for e in ev if e["handle_id"] == 0]
+    assert kinds == ["launch", "complete", "wait"]
+    assert ev[0]["t_sim"] <= ev[1]["t_sim"] <= ev[2]["t_sim"]
+
+
+def test_round_rejects_bad_hyper_and_counts():
+    eng = co2.CollectiveEngine(2, transport="local")
+    ws = [co2.Worker(co2.MODE_F32, 16) for _ in range(2)]
+    with pytest.raises(co2.ValidationError, match="hyper: beta"):
+        co2.co2_round(ws, eng, co2.Co2Hyper(beta=1.5), 2)
+    with pytest.raises(co2.ValidationError, match="contribution count"):
+        co2.co2_round(ws[:1], eng, co2.Co2Hyper(), 2)
