@@ -46,7 +46,10 @@ def test_full_size_windows_bitwise(name, mode, n, tau):
     assert d.flags == 0
     assert d.min_gap >= 1.0
     assert d.max_outer_step <= np.float32(5e-3) * (1 + 2.0 ** -16)
-    assert d.n_floored == (n + 60) // 61  # stalled coordinates j % 61 == 0
+    # stalled coordinates j % 61 == 0, plus the rare draws where p1 rounds back
+    # onto p0 (|1e-3 * (2U-1)| below half an ulp of p0)
+    stalled = (n + 60) // 61
+    assert stalled <= d.n_floored <= stalled + n // 100000
     assert 0 < d.n_clipped < n
     del x, p0, p1, xe, m
     torch.cuda.empty_cache()
