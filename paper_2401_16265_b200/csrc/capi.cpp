@@ -191,9 +191,9 @@ extern "C" co2_status_t co2_outer_step_host(co2_mode_t mode, int64_t n, const vo
       if (s.buf) CO2_CUDA(cudaFree(s.buf));
       CO2_CUDA(cudaMalloc(&s.buf, need));
       s.bytes = need;
-      char* base = static_cast<char*>(s.buf);
-      void* ws = base + align(3 * sb * chunk) + align(3 * lb * chunk);
-      CO2_CUDA(cudaMemsetAsync(ws, 0, kWsBytes, s.stream));
+      // The workspace sits at offset 0 so its self-resetting ticket survives
+      // calls with other modes / chunk sizes that reuse this buffer.
+      CO2_CUDA(cudaMemsetAsync(s.buf, 0, kWsBytes, s.stream));
     }
   }
   const int64_t nchunks = n == 0 ? 0 : (n + chunk - 1) / chunk;
@@ -209,14 +209,14 @@ extern "C" co2_status_t co2_outer_step_host(co2_mode_t mode, int64_t n, const vo
     StageSlot& s = P.slots[c % nstreams];
     const int64_t j0 = c * chunk;
     const int64_t len = std::min<int64_t>(chunk, n - j0);
-    char* base = static_cast<char*>(s.buf);
+    void* ws = s.buf;
+    char* base = static_cast<char*>(s.buf) + align(kWsBytes);
     char* dx = base;
     char* dp0 = dx + sb * chunk;
     char* dm = dp0 + sb * chunk;
     char* dp1 = base + align(3 * sb * chunk);
     char* dxb = dp1 + lb * chunk;
     char* dpr = dxb + lb * chunk;
-    void* ws = base + align(3 * sb * chunk) + align(3 * lb * chunk);
     const size_t so = sb * j0, lo = lb * j0, sl = sb * len, ll = lb * len;
     CO2_CUDA(cudaMemcpyAsync(dx, H(x_t0, so), sl, cudaMemcpyHostToDevice, s.stream));
     CO2_CUDA(cudaMemcpyAsync(dp0, H(p0, so), sl, cudaMemcpyHostToDevice, s.stream));

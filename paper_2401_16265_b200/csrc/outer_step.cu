@@ -21,6 +21,9 @@
 #include <cuda_bf16.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -56,27 +59,21 @@ struct Store<bf16s> {
 };
 
 // Modes: storage of state (x_t0, prev_x0, m, anchor, gap), storage of low
-// (prev_x1, xbar, params), compute type, elements per vector.
+// (prev_x1, xbar, params) and compute type.
 struct ModeF64 {
   using TS = double;
   using TL = double;
   using TC = double;
-  static constexpr int VEC = 2;
-  static constexpr int U = 4;
 };
 struct ModeF32 {
   using TS = float;
   using TL = float;
   using TC = float;
-  static constexpr int VEC = 4;
-  static constexpr int U = 2;
 };
 struct ModeBF16 {
   using TS = float;
   using TL = bf16s;
   using TC = float;
-  static constexpr int VEC = 8;
-  static constexpr int U = 2;
 };
 
 // ------------------------------------------------------- vector load/store
@@ -88,6 +85,12 @@ __device__ __forceinline__ void ld_vec(const T* __restrict__ p, T (&out)[N]) {
 #pragma unroll
     for (int k = 0; k < BYTES / 16; ++k) r[k] = __ldcs(reinterpret_cast<const uint4*>(p) + k);
     memcpy(out, r, BYTES);
+  } else if constexpr (BYTES == 8) {
+    uint2 r = __ldcs(reinterpret_cast<const uint2*>(p));
+    memcpy(out, &r, 8);
+  } else if constexpr (BYTES == 4) {
+    unsigned int r = __ldcs(reinterpret_cast<const unsigned int*>(p));
+    memcpy(out, &r, 4);
   } else {
 #pragma unroll
     for (int k = 0; k < N; ++k) out[k] = p[k];
@@ -102,6 +105,14 @@ __device__ __forceinline__ void st_vec(T* __restrict__ p, const T (&in)[N]) {
     memcpy(r, in, BYTES);
 #pragma unroll
     for (int k = 0; k < BYTES / 16; ++k) __stcs(reinterpret_cast<uint4*>(p) + k, r[k]);
+  } else if constexpr (BYTES == 8) {
+    uint2 r;
+    memcpy(&r, in, 8);
+    __stcs(reinterpret_cast<uint2*>(p), r);
+  } else if constexpr (BYTES == 4) {
+    unsigned int r;
+    memcpy(&r, in, 4);
+    __stcs(reinterpret_cast<unsigned int*>(p), r);
   } else {
 #pragma unroll
     for (int k = 0; k < N; ++k) p[k] = in[k];
@@ -113,6 +124,24 @@ struct Acc {
   double min_gap = INFINITY;
   double max_step = 0.0;
   unsigned int clipped = 0, floored = 0, flags = 0;
+};
+
+// Per-thread accumulator in the compute type: min / max in fp32 are exact
+// and convert to double once per thread, not once per element.
+template <typename TC>
+struct AccT {
+  TC min_gap = (TC)INFINITY;
+  TC max_step = (TC)0;
+  unsigned int clipped = 0, floored = 0, flags = 0;
+  __device__ Acc widen() const {
+    Acc a;
+    a.min_gap = (double)min_gap;
+    a.max_step = (double)max_step;
+    a.clipped = clipped;
+    a.floored = floored;
+    a.flags = flags;
+    return a;
+  }
 };
 
 template <int NT>
@@ -218,7 +247,7 @@ struct Hyp {
 //   x' = x_t0 - alpha*c                     outer_algorithms.cpp:102 / :104
 template <typename TC>
 __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& xn, TC& lam,
-                                         const Hyp<TC>& h, Acc& acc) {
+                                         const Hyp<TC>& h, AccT<TC>& acc) {
   if (h.divide) xb = xb / h.divisor;  // average(): sum / G, param_ops.cpp:30
   TC n0 = fabs(x - q0);
   TC av = fabs(h.tau * (q1 - q0));
@@ -253,9 +282,8 @@ __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& x
   acc.flags |= f;
   acc.floored += floored;
   acc.clipped += clipped;
-  double dlam = (double)lam;
-  acc.min_gap = dlam < acc.min_gap ? dlam : acc.min_gap;
-  double st = (double)fabs(xn - x);
+  acc.min_gap = lam < acc.min_gap ? lam : acc.min_gap;
+  TC st = fabs(xn - x);
   acc.max_step = st > acc.max_step ? st : acc.max_step;
 }
 
@@ -299,7 +327,7 @@ __global__ void __launch_bounds__(NT) fused_step_kernel(const StepArgs a) {
   TL* PR = static_cast<TL*>(a.params);  // may alias xbar
   TS* G = static_cast<TS*>(a.gap);
 
-  Acc acc;
+  AccT<TC> acc;
   const int64_t nv = a.n / V;
   const int64_t stride = (int64_t)gridDim.x * NT;
   int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
@@ -364,7 +392,7 @@ __global__ void __launch_bounds__(NT) fused_step_kernel(const StepArgs a) {
     if (PR) PR[t] = Store<TL>::from(xn);
     if (G) G[t] = (TS)lam;
   }
-  block_finish<NT>(acc, a.ws);
+  block_finish<NT>(acc.widen(), a.ws);
 }
 
 constexpr int kThreads = 256;
@@ -385,18 +413,52 @@ int grid_for(K kernel, int64_t work_items, int threads) {
   return (int)(need < cap ? need : cap);
 }
 
+template <class M, int V, int U>
+void launch_variant(const StepArgs& a, cudaStream_t s) {
+  auto k = fused_step_kernel<M, V, U, kThreads>;
+  int grid = grid_for(k, (a.n / V + U - 1) / U, kThreads);
+  k<<<grid, kThreads, 0, s>>>(a);
+}
+
+// Tuning knob: CO2_FUSED_VARIANT selects the (elements per vector, vectors
+// in flight per thread) instantiation; 0 is the measured default.
+int fused_variant() {
+  static int v = [] {
+    const char* e = getenv("CO2_FUSED_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <class M>
 co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
   bool vec_ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
                 aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap);
-  if (vec_ok) {
-    auto k = fused_step_kernel<M, M::VEC, M::U, kThreads>;
-    int grid = grid_for(k, (a.n / M::VEC + M::U - 1) / M::U, kThreads);
-    k<<<grid, kThreads, 0, s>>>(a);
+  if (!vec_ok) {
+    launch_variant<M, 1, 4>(a, s);
+  } else if constexpr (std::is_same<M, ModeBF16>::value) {
+    // 4 elements/thread/vector keeps the fp32 streams at 16 B and the bf16
+    // streams at 8 B per lane: every load instruction is warp-contiguous.
+    switch (fused_variant()) {
+      case 1: launch_variant<M, 8, 2>(a, s); break;
+      case 2: launch_variant<M, 4, 2>(a, s); break;
+      case 3: launch_variant<M, 4, 8>(a, s); break;
+      case 4: launch_variant<M, 8, 1>(a, s); break;
+      default: launch_variant<M, 4, 4>(a, s); break;
+    }
+  } else if constexpr (std::is_same<M, ModeF32>::value) {
+    switch (fused_variant()) {
+      case 1: launch_variant<M, 4, 4>(a, s); break;
+      case 2: launch_variant<M, 4, 1>(a, s); break;
+      case 3: launch_variant<M, 8, 2>(a, s); break;
+      default: launch_variant<M, 4, 2>(a, s); break;
+    }
   } else {
-    auto k = fused_step_kernel<M, 1, 4, kThreads>;
-    int grid = grid_for(k, (a.n + 3) / 4, kThreads);
-    k<<<grid, kThreads, 0, s>>>(a);
+    switch (fused_variant()) {
+      case 1: launch_variant<M, 2, 2>(a, s); break;
+      case 2: launch_variant<M, 2, 8>(a, s); break;
+      default: launch_variant<M, 2, 4>(a, s); break;
+    }
   }
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
