@@ -518,6 +518,14 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     CO2_TRY(walloc(&w0->avg[0], lb));
     CO2_TRY(walloc(&w0->avg[1], lb));
   }
+  if (w0->t == 0) {
+    // Round 0 keeps x_{1,0} = x_{0,tau} worker-local, but the reduce about
+    // to be launched owns params[cur] (NCCL reduces it in place): copy the
+    // params to the other buffer first, so the launch fence orders the copy
+    // before the collective touches the buffer.
+    for (int i = 0; i < g; ++i)
+      CO2_TRY(copy_dev(ws[i]->params[1 - ws[i]->cur], ws[i]->params[ws[i]->cur], lb, st));
+  }
   const void* bufs[64];
   for (int i = 0; i < g; ++i) bufs[i] = ws[i]->params[ws[i]->cur];
   void* avg_out = local ? w0->avg[w0->t % 2] : const_cast<void*>(bufs[0]);
@@ -525,14 +533,10 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
   CO2_TRY(co2_aar_launch(e, ldt, bufs, avg_out, n, stream, &launched));
 
   if (w0->t == 0) {
-    // 2. Round 0 (:122-151): snapshots only; x_{1,0} = x_{0,tau} stays
-    // worker-local.  The in-flight reduce owns params[cur]; continue on the
-    // other buffer and seed the anchor x_{1,0}.
+    // 2. Round 0 (:122-151): snapshots only; continue on the copied buffer
+    // and seed the anchor x_{1,0}.
     for (int i = 0; i < g; ++i) {
       co2_worker* w = ws[i];
-      void* src = w->params[w->cur];
-      void* dst = w->params[1 - w->cur];
-      CO2_TRY(copy_dev(dst, src, lb, st));
       std::swap(w->prev_x0, w->anchor);  // prev_x0 <- x_{0,0}
       std::swap(w->prev_x1, w->xfirst);  // prev_x1 <- x_{0,1}
       w->cur = 1 - w->cur;

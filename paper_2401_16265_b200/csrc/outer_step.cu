@@ -302,8 +302,8 @@ struct StepArgs {
   void* ws;
 };
 
-template <class M, int V, int U, int NT>
-__global__ void __launch_bounds__(NT) fused_step_kernel(const StepArgs a) {
+template <class M, int V, int U, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
   using TC = typename M::TC;
@@ -413,9 +413,9 @@ int grid_for(K kernel, int64_t work_items, int threads) {
   return (int)(need < cap ? need : cap);
 }
 
-template <class M, int V, int U>
+template <class M, int V, int U, int MINB = 1>
 void launch_variant(const StepArgs& a, cudaStream_t s) {
-  auto k = fused_step_kernel<M, V, U, kThreads>;
+  auto k = fused_step_kernel<M, V, U, kThreads, MINB>;
   int grid = grid_for(k, (a.n / V + U - 1) / U, kThreads);
   k<<<grid, kThreads, 0, s>>>(a);
 }
@@ -437,27 +437,32 @@ co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
   if (!vec_ok) {
     launch_variant<M, 1, 4>(a, s);
   } else if constexpr (std::is_same<M, ModeBF16>::value) {
-    // 4 elements/thread/vector keeps the fp32 streams at 16 B and the bf16
-    // streams at 8 B per lane: every load instruction is warp-contiguous.
+    // Measured on B200 (tools/tune_fused.py, C3 1.3B): one 8-element vector
+    // per thread (32 B fp32 + 16 B bf16 per stream) at >= 3 CTAs/SM beats
+    // deeper per-thread unrolling, which costs occupancy.
     switch (fused_variant()) {
       case 1: launch_variant<M, 8, 2>(a, s); break;
-      case 2: launch_variant<M, 4, 2>(a, s); break;
-      case 3: launch_variant<M, 4, 8>(a, s); break;
+      case 2: launch_variant<M, 4, 4>(a, s); break;
+      case 3: launch_variant<M, 4, 1>(a, s); break;
       case 4: launch_variant<M, 8, 1>(a, s); break;
-      default: launch_variant<M, 4, 4>(a, s); break;
+      case 5: launch_variant<M, 4, 2, 3>(a, s); break;
+      default: launch_variant<M, 8, 1, 4>(a, s); break;
     }
   } else if constexpr (std::is_same<M, ModeF32>::value) {
     switch (fused_variant()) {
-      case 1: launch_variant<M, 4, 4>(a, s); break;
+      case 1: launch_variant<M, 4, 2>(a, s); break;
       case 2: launch_variant<M, 4, 1>(a, s); break;
-      case 3: launch_variant<M, 8, 2>(a, s); break;
-      default: launch_variant<M, 4, 2>(a, s); break;
+      case 3: launch_variant<M, 8, 1>(a, s); break;
+      case 4: launch_variant<M, 8, 1, 4>(a, s); break;
+      default: launch_variant<M, 4, 1, 4>(a, s); break;
     }
   } else {
     switch (fused_variant()) {
       case 1: launch_variant<M, 2, 2>(a, s); break;
-      case 2: launch_variant<M, 2, 8>(a, s); break;
-      default: launch_variant<M, 2, 4>(a, s); break;
+      case 2: launch_variant<M, 2, 1>(a, s); break;
+      case 3: launch_variant<M, 4, 1>(a, s); break;
+      case 4: launch_variant<M, 2, 2, 3>(a, s); break;
+      default: launch_variant<M, 2, 1, 4>(a, s); break;
     }
   }
   CO2_CUDA(cudaGetLastError());

@@ -1,0 +1,151 @@
+"""C5: tau sweep of the one-step-stale schedule against a fixed-duration
+synthetic local-compute kernel; reports exposed all-reduce time per tau next
+to the analytic simulate_timeline prediction (proj/src/timing_model.cpp:
+76-123,167-173).
+
+  torchrun --nproc-per-node N tools/overlap_sweep.py [--mode 1] [--n 125000000]
+
+exposed% = 100 * sum(stall) / sum(waited comm), the reference definition
+(1 - overlap_ratio_achieved).  stall = device time the compute stream waited
+on the reduce (events straddling the wait); comm = device duration of the
+reduce on the comm stream.  "interference" = mean round time with the
+all-reduce minus the same schedule with a world-1 (no-op) engine.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", type=int, default=1)
+    ap.add_argument("--n", type=int, default=125_000_000)
+    ap.add_argument("--taus", default="1,2,3,4,6,8,12,16,24,32")
+    ap.add_argument("--rounds", type=int, default=6)
+    ap.add_argument("--knee", type=float, default=4.0, help="tau at which tau*t_comp = t_comm")
+    ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_16265_b200 import co2
+    from paper_2401_16265_b200.dist import broadcast_nccl_id, env_rank, max_over_ranks
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
+    eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
+                               max_ctas=a.max_ctas)
+    solo = co2.CollectiveEngine(1, transport="nccl", rank=0, nccl_id=bytes(128))
+    hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    stream = torch.cuda.current_stream()
+    lo = co2.LOW_TORCH[a.mode]
+
+    # t_comm: the reduce alone (scratch buffer, same size and dtype)
+    scratch = torch.zeros(a.n, dtype=lo, device="cuda")
+    comms = []
+    for i in range(6):
+        h = eng.launch_all_reduce([scratch], scratch)
+        eng.wait(h)
+        torch.cuda.synchronize()
+        if i >= 2:
+            comms.append(eng.stall(h)[1])
+    t_comm = max_over_ranks([statistics.median(comms)], device="cpu")[0] if world > 1 else 0.0
+    del scratch
+
+    # t_comp: calibrate the synthetic inner step to t_comm / knee
+    w = co2.Worker(a.mode, a.n, co2.synth(a.mode, a.n, worker=rank)[3], keep_gap=False)
+
+    def time_inner(repeat, iters=5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        co2.synthetic_inner_step(w.params, lr=1e-6, repeat=repeat, worker=rank, step=0)
+        e0.record(stream)
+        for k in range(iters):
+            co2.synthetic_inner_step(w.params, lr=1e-6, repeat=repeat, worker=rank, step=k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / iters
+
+    target = t_comm / a.knee if t_comm > 0 else 0.0
+    repeat = 1
+    t1 = time_inner(1)
+    while repeat < 256 and t1 * repeat < target * 0.8:
+        repeat *= 2
+    t_comp = time_inner(repeat)
+    t_comp = max_over_ranks([t_comp], device="cpu")[0] if world > 1 else t_comp
+
+    def run(engine, tau):
+        w2 = co2.Worker(a.mode, a.n, w.params, keep_gap=False)
+        w2.enable_timing(4 * a.rounds)
+        n_ev0 = len(engine.events())
+        walls = []
+        for t in range(a.rounds):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            e0.record(stream)
+            w2.snapshot_start()
+            for k in range(tau):
+                co2.synthetic_inner_step(w2.params, lr=1e-6, repeat=repeat, worker=rank,
+                                         step=t * tau + k)
+                if k == 0:
+                    w2.snapshot_first()
+            co2.co2_round([w2], engine, hyper, tau, sync=False)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            walls.append(e0.elapsed_time(e1) * 1e-3)
+        kt = w2.step_times()
+        ev = engine.events()[n_ev0:]
+        launches = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "launch"}
+        completes = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "complete"}
+        waits = [e for e in ev if e["event"] == "wait"][1:]  # drop the first (warm-up) wait
+        stall = sum(e["stall"] for e in waits)
+        waited = sum(completes[e["handle_id"]] - launches[e["handle_id"]] for e in waits)
+        w2.close()
+        return statistics.mean(walls[2:]), stall, waited, len(waits), \
+            (statistics.mean(kt) if kt else 0.0)
+
+    rows = []
+    for tau in [int(x) for x in a.taus.split(",")]:
+        wall, stall, waited, nw, t_outer = run(eng, tau)
+        wall0, _, _, _, _ = run(solo, tau)
+        wall, stall, waited, wall0, t_outer = max_over_ranks(
+            [wall, stall, waited, wall0, t_outer], device="cpu") if world > 1 else \
+            (wall, stall, waited, wall0, t_outer)
+        pred = co2.simulate_timeline_co2(
+            co2.ClusterSpec(workers=world, t_comp=t_comp, t_outer=t_outer,
+                            measured_override=t_comm), tau, a.rounds)
+        row = {"tau": tau, "world": world, "n": a.n, "mode": a.mode,
+               "t_comm_ms": 1e3 * t_comm, "t_comp_ms": 1e3 * t_comp, "t_outer_ms": 1e3 * t_outer,
+               "inner_repeat": repeat, "exposed_pct": 100.0 * stall / waited if waited else 0.0,
+               "stall_ms_per_round": 1e3 * stall / max(nw, 1),
+               "comm_ms_measured": 1e3 * waited / max(nw, 1),
+               "round_ms": 1e3 * wall, "round_ms_no_allreduce": 1e3 * wall0,
+               "interference_ms": 1e3 * (wall - wall0),
+               "predicted_exposed_pct": 100.0 * (1.0 - pred.overlap_ratio_achieved),
+               "predicted_overlap": co2.overlap_ratio(tau, t_comp, t_comm) if t_comm else 1.0}
+        rows.append(row)
+        if rank == 0:
+            print(json.dumps(row), flush=True)
+    if rank == 0 and a.out:
+        with open(a.out, "w") as f:
+            for r in rows:
+                f.write(json.dumps(r) + "\n")
+    eng.close()
+    solo.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
