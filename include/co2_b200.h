@@ -292,6 +292,10 @@ co2_status_t co2_round(co2_worker_t* const* workers, int32_t g, co2_aar_t* engin
                        co2_round_result_t* result);
 co2_status_t co2_round_finish(co2_worker_t* const* workers, int32_t g, void* stream,
                               co2_round_result_t* result);
+/* End of a run: consume (wait on, without applying) the reduce the last
+ * round launched, releasing its slot in the engine's two-handle window. */
+co2_status_t co2_round_drain(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,
+                             void* stream);
 /* Device timing of the fused outer-step launch inside co2_round: events
  * bracket the kernel on the round's stream (a ring of `cap` pairs).
  * co2_worker_step_times synchronizes on the recorded events and returns the

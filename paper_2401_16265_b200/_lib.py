@@ -115,6 +115,7 @@ SIGNATURES = {
     "co2_worker_snapshot_first": (ST, [P, P]),
     "co2_round": (ST, [C.POINTER(P), I32, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),
     "co2_round_finish": (ST, [C.POINTER(P), I32, P, C.POINTER(RoundResult)]),
+    "co2_round_drain": (ST, [C.POINTER(P), I32, P, P]),
     "co2_worker_enable_timing": (ST, [P, I32]),
     "co2_worker_step_times": (ST, [P, C.POINTER(D), I32, C.POINTER(I32)]),
 }

@@ -472,3 +472,9 @@ def co2_round(workers: list[Worker], engine: CollectiveEngine, hyper: Co2Hyper, 
     check(lib().co2_round(arr, len(workers), engine.handle, C.byref(h), _stream(stream), int(sync),
                           C.byref(r)))
     return r
+
+
+def co2_round_drain(workers: list[Worker], engine: CollectiveEngine, *, stream=None) -> None:
+    """Consume the reduce launched by the last round (end of a run)."""
+    arr = (C.c_void_p * len(workers))(*[w.handle.value for w in workers])
+    check(lib().co2_round_drain(arr, len(workers), engine.handle, _stream(stream)))

@@ -482,6 +482,16 @@ extern "C" co2_status_t co2_round_finish(co2_worker_t* const* ws, int32_t g, voi
   return CO2_OK;
 }
 
+extern "C" co2_status_t co2_round_drain(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
+                                        void* stream) {
+  if (!ws || g < 1 || !e) return fail(CO2_ERR_VALIDATION, "co2_round_drain: bad arguments");
+  if (!ws[0]->has_pending) return CO2_OK;
+  const uint64_t h = ws[0]->pending;
+  CO2_TRY(co2_aar_wait(e, h, stream));
+  for (int i = 0; i < g; ++i) ws[i]->has_pending = false;
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
                                   const co2_hyper_t* hyper, void* stream, int32_t sync,
                                   co2_round_result_t* res) {
@@ -585,6 +595,8 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
   }
 
   // 3. Rounds t >= 1: poll, then wait on the previous reduce (:153-159).
+  if (!w0->has_pending)  // shared_pending, outer_algorithms.cpp:22-26
+    return fail(CO2_ERR_VALIDATION, "outer round: no pending reduce to consume");
   const uint64_t prev = w0->pending;
   int32_t done = 0;
   CO2_TRY(co2_aar_poll(e, prev, &done));

@@ -103,11 +103,14 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             walls.append(e0.elapsed_time(e1) * 1e-3)
+        co2.co2_round_drain([w2], engine)
+        torch.cuda.synchronize()
         kt = w2.step_times()
         ev = engine.events()[n_ev0:]
         launches = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "launch"}
         completes = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "complete"}
-        waits = [e for e in ev if e["event"] == "wait"][1:]  # drop the first (warm-up) wait
+        # drop the first (warm-up) wait and the final drain
+        waits = [e for e in ev if e["event"] == "wait"][1:-1]
         stall = sum(e["stall"] for e in waits)
         waited = sum(completes[e["handle_id"]] - launches[e["handle_id"]] for e in waits)
         w2.close()
