@@ -296,6 +296,45 @@ co2_status_t co2_round_finish(co2_worker_t* const* workers, int32_t g, void* str
  * round launched, releasing its slot in the engine's two-handle window. */
 co2_status_t co2_round_drain(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,
                              void* stream);
+/* ---- ghost-consistent, sharded outer state (C4; outer_algorithms.cpp:
+ *      126-145,161-184) ------------------------------------------------------
+ * The fused step on one shard where x_t0 is the average of `ghost_copies`
+ * identical anchors (ghost_copies == 0: x_t0 is the consumed average itself,
+ * the round-1 case x_{1,0} = x_{0,tau}), prev_x1 is a worker SUM divided once
+ * by prev_x1_divisor and xbar a worker sum divided by xbar_divisor.  bar0_out
+ * (state dtype, may alias prev_x0) receives the x_t0 used, i.e. the next
+ * prev_x0; anchor_out (may alias anchor_in) receives x_{t+1,0}. */
+co2_status_t co2_outer_step_ghost(co2_mode_t mode, int64_t n, const void* anchor_in,
+                                  const void* prev_x0, const void* prev_x1_sum,
+                                  int32_t prev_x1_divisor, const void* xbar_sum,
+                                  int32_t xbar_divisor, int32_t ghost_copies, void* momentum,
+                                  void* anchor_out, void* bar0_out, void* params_out,
+                                  void* gap_out, const co2_hyper_t* hyper, void* workspace,
+                                  void* stream);
+/* Sharded worker over the NCCL engine: params and the x_{t,1} snapshot are
+ * replicated (low dtype, full length); x_{t,0}, prev_x0, prev_x1, momentum
+ * and gap live only for this rank's contiguous shard.  Per round:
+ * reduce-scatter of x_{t,tau} (async, consumed next round), reduce-scatter
+ * of x_{t,1}, the ghost step on the shard, and an in-place all-gather of
+ * x_{t+1,0} into the params.  Requires hyper.ghost_consistent. */
+typedef struct co2_sharded co2_sharded_t;
+co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode, int64_t n,
+                                co2_aar_t* engine, const void* init_params, void* stream);
+co2_status_t co2_sharded_destroy(co2_sharded_t* s);
+/* which: CO2_BUF_PARAMS / CO2_BUF_XFIRST (full length), CO2_BUF_ANCHOR,
+ * CO2_BUF_PREV_X0, CO2_BUF_MOMENTUM, CO2_BUF_GAP (shard), CO2_BUF_PREV_X1
+ * (shard, worker sum), CO2_BUF_XBAR (shard, last consumed worker sum). */
+void* co2_sharded_buffer(co2_sharded_t* s, int32_t which);
+/* Shard geometry: returns the shard capacity; *offset and *length give the
+ * global offset and the real coordinate count of this rank's shard. */
+int64_t co2_sharded_shard(const co2_sharded_t* s, int64_t* offset, int64_t* length);
+co2_status_t co2_sharded_snapshot_first(co2_sharded_t* s, void* stream);
+co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* engine, const co2_hyper_t* hyper,
+                               void* stream, int32_t sync, co2_round_result_t* result);
+co2_status_t co2_sharded_drain(co2_sharded_t* s, co2_aar_t* engine, void* stream);
+co2_status_t co2_sharded_enable_timing(co2_sharded_t* s, int32_t cap);
+co2_status_t co2_sharded_step_times(co2_sharded_t* s, double* out, int32_t cap, int32_t* count);
+
 /* Device timing of the fused outer-step launch inside co2_round: events
  * bracket the kernel on the round's stream (a ring of `cap` pairs).
  * co2_worker_step_times synchronizes on the recorded events and returns the

@@ -396,6 +396,86 @@ int orc_outer_step(int mode, int64_t n, const void* x_t0v, const void* p0v, cons
   return orc_diag_status(diag);
 }
 
+/* Ghost-consistent / sharded step (outer_algorithms.cpp:161-184) in the
+ * same op order as the GPU: x_t0 = average of `ghost` identical anchors (or
+ * xbar itself when ghost == 0), prev_x1 = p1sum / p1_div, xbar = xsum / xdiv;
+ * bar0_out receives the x_t0 used.  Storage as orc_outer_step. */
+int orc_outer_step_ghost(int mode, int64_t n, const void* anchorv, const void* p0v,
+                         const void* p1v, int p1_div, const void* xsumv, int xdiv, int ghost,
+                         void* mv, void* anchor_out, void* bar0_out, void* paramsv, void* gapv,
+                         const orc_hyper* h, orc_diag* diag) {
+  int s = orc_hyper_validate(h);
+  if (s) return s;
+  uint32_t flags = 0;
+  int64_t n_floored = 0, n_clipped = 0;
+  double min_gap = INFINITY, max_step = 0.0;
+  if (mode == ORC_MODE_F64) {
+    const double *AN = anchorv, *P0 = p0v, *P1 = p1v, *XS = xsumv;
+    double *M = mv, *A = anchor_out, *B0 = bar0_out, *PR = paramsv, *G = gapv;
+    double tf = (double)h->tau, epsf = h->epsilon, betaf = h->beta, phif = h->phi,
+           alphaf = h->alpha;
+    for (int64_t j = 0; j < n; ++j) {
+      double xb = XS[j];
+      if (xdiv > 1) xb = xb / (double)xdiv;
+      double x;
+      if (ghost == 0) {
+        x = xb;
+      } else {
+        double sum = AN[j];
+        for (int i = 1; i < ghost; ++i) sum = sum + AN[j];
+        x = sum / (double)ghost;
+      }
+      double q0 = P0[j], q1 = P1[j], mo = M[j];
+      if (p1_div > 1) q1 = q1 / (double)p1_div;
+      FUSED_BODY(double, fabs, isfinite, max_std, min_std)
+      M[j] = mn;
+      if (B0) B0[j] = x;
+      if (A) A[j] = xn;
+      if (PR) PR[j] = xn;
+      if (G) G[j] = lam;
+    }
+  } else {
+    int bf = mode == ORC_MODE_BF16_MIXED;
+    const float *AN = anchorv, *P0 = p0v;
+    float *M = mv, *A = anchor_out, *B0 = bar0_out, *G = gapv;
+    float tf = (float)h->tau, epsf = (float)h->epsilon, betaf = (float)h->beta,
+          phif = (float)h->phi, alphaf = (float)h->alpha;
+    for (int64_t j = 0; j < n; ++j) {
+      float xb = bf ? orc_bf16_to_f32(((const uint16_t*)xsumv)[j]) : ((const float*)xsumv)[j];
+      if (xdiv > 1) xb = xb / (float)xdiv;
+      float x;
+      if (ghost == 0) {
+        x = xb;
+      } else {
+        float sum = AN[j];
+        for (int i = 1; i < ghost; ++i) sum = sum + AN[j];
+        x = sum / (float)ghost;
+      }
+      float q0 = P0[j], mo = M[j];
+      float q1 = bf ? orc_bf16_to_f32(((const uint16_t*)p1v)[j]) : ((const float*)p1v)[j];
+      if (p1_div > 1) q1 = q1 / (float)p1_div;
+      FUSED_BODY(float, fabsf, isfinite, max_stdf, min_stdf)
+      M[j] = mn;
+      if (B0) B0[j] = x;
+      if (A) A[j] = xn;
+      if (paramsv) {
+        if (bf)
+          ((uint16_t*)paramsv)[j] = orc_f32_to_bf16(xn);
+        else
+          ((float*)paramsv)[j] = xn;
+      }
+      if (G) G[j] = lam;
+    }
+  }
+  diag->min_gap = min_gap;
+  diag->max_outer_step = max_step;
+  diag->n_clipped = n_clipped;
+  diag->n_floored = n_floored;
+  diag->flags = flags;
+  diag->pad = 0;
+  return orc_diag_status(diag);
+}
+
 int orc_diag_status(const orc_diag* d) {
   /* Reference precedence: staleness_gap numeric (cpp:62) -> gap<1
    * validation (cpp:81-83) -> momentum numeric (cpp:88) -> clip input

@@ -118,6 +118,13 @@ int orc_outer_step(int mode, int64_t n, const void* x_t0, const void* p0,
                    const void* p1, const void* xbar, int divisor, void* m,
                    void* anchor_out, void* params_out, void* gap_out,
                    const orc_hyper* h, orc_diag* diag);
+/* Ghost-consistent / sharded step (outer_algorithms.cpp:161-184): x_t0 =
+ * average of `ghost` identical anchors (ghost == 0: the consumed average),
+ * prev_x1 = p1sum / p1_div, xbar = xsum / xdiv; bar0_out gets the x_t0 used. */
+int orc_outer_step_ghost(int mode, int64_t n, const void* anchor, const void* p0,
+                         const void* p1sum, int p1_div, const void* xsum, int xdiv, int ghost,
+                         void* m, void* anchor_out, void* bar0_out, void* params_out,
+                         void* gap_out, const orc_hyper* h, orc_diag* diag);
 /* Reference error precedence over a diag's flags. */
 int orc_diag_status(const orc_diag* d);
 

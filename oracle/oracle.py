@@ -293,6 +293,34 @@ def outer_step(mode: int, x_t0, p0, p1, xbar, m, h: Hyper, divisor: int = 1) -> 
     return FusedResult(mm, anchor, params, gap, d, code, msg)
 
 
+def outer_step_ghost(mode: int, anchor, p0, p1sum, p1_div: int, xsum, xdiv: int, ghost: int, m,
+                     h: Hyper) -> FusedResult:
+    """Ghost-consistent / sharded step (outer_algorithms.cpp:161-184); the
+    FusedResult's `anchor` field holds x_{t+1,0} and `gap` the Lambda; the
+    x_t0 used (next prev_x0) is returned as result.bar0."""
+    lib().orc_outer_step_ghost.argtypes = [C.c_int, C.c_int64] + [C.c_void_p] * 3 + \
+        [C.c_int, C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 5 + \
+        [C.POINTER(Hyper), C.POINTER(Diag)]
+    st = np.float64 if mode == MODE_F64 else np.float32
+    lo = np.float64 if mode == MODE_F64 else (np.uint16 if mode == MODE_BF16_MIXED else np.float32)
+    an = np.ascontiguousarray(anchor, st)
+    q0 = np.ascontiguousarray(p0, st)
+    q1 = np.ascontiguousarray(p1sum, lo)
+    xs = np.ascontiguousarray(xsum, lo)
+    mm = np.array(m, dtype=st, copy=True)
+    n = q0.size
+    a_out, b0, gap = np.empty(n, st), np.empty(n, st), np.empty(n, st)
+    params = np.empty(n, lo)
+    d = Diag()
+    code = lib().orc_outer_step_ghost(mode, n, _p(an), _p(q0), _p(q1), p1_div, _p(xs), xdiv, ghost,
+                                      _p(mm), _p(a_out), _p(b0), _p(params), _p(gap), C.byref(h),
+                                      C.byref(d))
+    msg = lib().orc_last_error().decode() if code else ""
+    r = FusedResult(mm, a_out, params, gap, d, code, msg)
+    r.bar0 = b0
+    return r
+
+
 def synth(mode: int, n: int, seed: int = 7, worker: int = 0, j0: int = 0):
     """Synthetic inputs of SURVEY.md 8(d): returns (x_t0, p0, p1, x_end, m)."""
     st = np.float64 if mode == MODE_F64 else np.float32

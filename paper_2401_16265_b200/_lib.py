@@ -116,6 +116,17 @@ SIGNATURES = {
     "co2_round": (ST, [C.POINTER(P), I32, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),
     "co2_round_finish": (ST, [C.POINTER(P), I32, P, C.POINTER(RoundResult)]),
     "co2_round_drain": (ST, [C.POINTER(P), I32, P, P]),
+    "co2_outer_step_ghost": (ST, [I32, I64, P, P, P, I32, P, I32, I32, P, P, P, P, P,
+                                  C.POINTER(Hyper), P, P]),
+    "co2_sharded_create": (ST, [C.POINTER(P), I32, I64, P, P, P]),
+    "co2_sharded_destroy": (ST, [P]),
+    "co2_sharded_buffer": (P, [P, I32]),
+    "co2_sharded_shard": (I64, [P, C.POINTER(I64), C.POINTER(I64)]),
+    "co2_sharded_snapshot_first": (ST, [P, P]),
+    "co2_sharded_round": (ST, [P, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),
+    "co2_sharded_drain": (ST, [P, P, P]),
+    "co2_sharded_enable_timing": (ST, [P, I32]),
+    "co2_sharded_step_times": (ST, [P, C.POINTER(D), I32, C.POINTER(I32)]),
     "co2_worker_enable_timing": (ST, [P, I32]),
     "co2_worker_step_times": (ST, [P, C.POINTER(D), I32, C.POINTER(I32)]),
 }

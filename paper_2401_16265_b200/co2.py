@@ -478,3 +478,82 @@ def co2_round_drain(workers: list[Worker], engine: CollectiveEngine, *, stream=N
     """Consume the reduce launched by the last round (end of a run)."""
     arr = (C.c_void_p * len(workers))(*[w.handle.value for w in workers])
     check(lib().co2_round_drain(arr, len(workers), engine.handle, _stream(stream)))
+
+
+def outer_step_ghost(mode: int, anchor, prev_x0, prev_x1_sum, xbar_sum, momentum,
+                     hyper: Co2Hyper, tau: int, *, workers: int, ghost_copies: int,
+                     anchor_out=None, bar0_out=None, params_out=None, gap_out=None,
+                     workspace: Workspace | None = None, stream=None, check_flags: bool = True):
+    """Ghost-consistent / sharded fused step on one shard
+    (proj/src/outer_algorithms.cpp:161-184)."""
+    n = prev_x0.numel()
+    ws = workspace or _ws(prev_x0.device)
+    h = hyper.c(tau)
+    check(lib().co2_outer_step_ghost(mode, n, _ptr(anchor), _ptr(prev_x0), _ptr(prev_x1_sum),
+                                     workers, _ptr(xbar_sum), workers, ghost_copies,
+                                     _ptr(momentum), _ptr(anchor_out), _ptr(bar0_out),
+                                     _ptr(params_out), _ptr(gap_out), C.byref(h), ws.ptr,
+                                     _stream(stream)))
+    return ws.fetch(stream) if check_flags else None
+
+
+class ShardedWorker:
+    """Ghost-consistent CO2 worker with the outer state sharded across the
+    NCCL engine's ranks (BASELINE config C4)."""
+
+    def __init__(self, mode: int, n: int, engine: CollectiveEngine, init=None, *, stream=None):
+        self.handle = C.c_void_p()
+        self.mode, self.n = mode, n
+        check(lib().co2_sharded_create(C.byref(self.handle), mode, n, engine.handle, _ptr(init),
+                                       _stream(stream)))
+        off, ln = C.c_int64(), C.c_int64()
+        self.shard = lib().co2_sharded_shard(self.handle, C.byref(off), C.byref(ln))
+        self.offset, self.length = off.value, ln.value
+
+    def close(self):
+        if self.handle:
+            lib().co2_sharded_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def buffer(self, which: int, length: int | None = None) -> torch.Tensor | None:
+        ptr = lib().co2_sharded_buffer(self.handle, which)
+        if not ptr:
+            return None
+        full = which in (L.BUF_PARAMS, L.BUF_XFIRST)
+        state = which in (L.BUF_ANCHOR, L.BUF_PREV_X0, L.BUF_MOMENTUM, L.BUF_GAP)
+        dt = STATE_TORCH[self.mode] if state else LOW_TORCH[self.mode]
+        n = length if length is not None else (self.n if full else self.length)
+        return _view(ptr, n, dt)
+
+    @property
+    def params(self):
+        return self.buffer(L.BUF_PARAMS)
+
+    def snapshot_first(self, stream=None):
+        check(lib().co2_sharded_snapshot_first(self.handle, _stream(stream)))
+
+    def round(self, engine: CollectiveEngine, hyper: Co2Hyper, tau: int, *, stream=None,
+              sync: bool = True) -> L.RoundResult:
+        h = hyper.c(tau)
+        r = L.RoundResult()
+        check(lib().co2_sharded_round(self.handle, engine.handle, C.byref(h), _stream(stream),
+                                      int(sync), C.byref(r)))
+        return r
+
+    def drain(self, engine: CollectiveEngine, stream=None):
+        check(lib().co2_sharded_drain(self.handle, engine.handle, _stream(stream)))
+
+    def enable_timing(self, cap: int = 4096):
+        check(lib().co2_sharded_enable_timing(self.handle, cap))
+
+    def step_times(self, cap: int = 4096) -> list[float]:
+        out = (C.c_double * cap)()
+        cnt = C.c_int32()
+        check(lib().co2_sharded_step_times(self.handle, out, cap, C.byref(cnt)))
+        return [out[i] for i in range(cnt.value)]

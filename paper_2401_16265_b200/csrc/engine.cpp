@@ -54,6 +54,7 @@ struct co2_aar {
   int transport = T_LOCAL;
   int rank = 0, world = 1, workers = 1;
   ncclComm_t comm = nullptr;
+  ncclComm_t comm2 = nullptr;  // blocking collectives issued on the caller's stream
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t epoch = nullptr;
   void* ws = nullptr;
@@ -132,6 +133,7 @@ extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
       if (ev) cudaEventDestroy(ev);
     if (h.diag) cudaFreeHost(h.diag);
   }
+  if (e->comm2) ncclCommDestroy(e->comm2);
   if (e->comm) ncclCommDestroy(e->comm);
   if (e->ws) cudaFree(e->ws);
   if (e->epoch) cudaEventDestroy(e->epoch);
@@ -148,8 +150,10 @@ static co2_status_t record_for(co2_aar* e, uint64_t h, Handle** out) {
   return CO2_OK;
 }
 
-extern "C" co2_status_t co2_aar_launch(co2_aar_t* e, co2_dtype_t dt, const void* const* bufs,
-                                       void* out, int64_t n, void* producer, uint64_t* handle_out) {
+// kind 0: all-reduce (NCCL in place / LOCAL average); kind 1: reduce-scatter
+// (sum) of the full buffer bufs[0] (n = world * shard) into out (one shard).
+static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const void* const* bufs,
+                                void* out, int64_t n, void* producer, uint64_t* handle_out) {
   // launch_all_reduce, collective.cpp:31-58
   if (!e) return fail(CO2_ERR_VALIDATION, "aar: null engine");
   if (e->live >= 2)
@@ -168,7 +172,17 @@ extern "C" co2_status_t co2_aar_launch(co2_aar_t* e, co2_dtype_t dt, const void*
   CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, fence, 0));
   CO2_CUDA(cudaEventDestroy(fence));
   CO2_CUDA(cudaEventRecord(h.start, e->comm_stream));
-  if (e->transport == T_NCCL) {
+  if (kind == 1) {
+    if (e->transport != T_NCCL)
+      return fail(CO2_ERR_VALIDATION, "reduce-scatter: NCCL transport only");
+    const int64_t shard = n / e->world;
+    if (e->world > 1 && shard > 0)
+      CO2_NCCL(ncclReduceScatter(bufs[0], out, (size_t)shard, nccl_dtype(dt), ncclSum, e->comm,
+                                 e->comm_stream));
+    else if (shard > 0)
+      CO2_CUDA(cudaMemcpyAsync(out, bufs[0], dtype_bytes(dt) * (size_t)shard,
+                               cudaMemcpyDeviceToDevice, e->comm_stream));
+  } else if (e->transport == T_NCCL) {
     if (out && out != bufs[0])
       return fail(CO2_ERR_VALIDATION, "launch_all_reduce: NCCL transport reduces in place");
     if (e->world > 1 && n > 0)
@@ -185,6 +199,11 @@ extern "C" co2_status_t co2_aar_launch(co2_aar_t* e, co2_dtype_t dt, const void*
   e->live += 1;
   *handle_out = e->handles.size() - 1;
   return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_launch(co2_aar_t* e, co2_dtype_t dt, const void* const* bufs,
+                                       void* out, int64_t n, void* producer, uint64_t* handle_out) {
+  return launch_impl(e, 0, dt, bufs, out, n, producer, handle_out);
 }
 
 extern "C" co2_status_t co2_aar_poll(co2_aar_t* e, uint64_t handle, int32_t* done) {
@@ -674,6 +693,290 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     r.stall_seconds = stall;
     if (res) *res = r;
     if (s != CO2_OK) return s;
+    return s2;
+  }
+  if (res) *res = r;
+  return CO2_OK;
+}
+
+// ============================================================ sharded (C4)
+// Ghost-consistent CO2 (outer_algorithms.cpp:126-145,161-184) with the outer
+// state sharded across ranks: every worker shares one outer state, so rank r
+// keeps only coordinates [r*shard, (r+1)*shard) of x_{t,0}, prev_x0,
+// prev_x1, momentum and gap.
+struct co2_sharded {
+  co2_mode_t mode = CO2_MODE_F32;
+  int64_t n = 0, n_pad = 0, shard = 0, offset = 0, length = 0;
+  int world = 1, rank = 0;
+  int t = 0, cur = 0;
+  void* params[2] = {nullptr, nullptr};  // full, low dtype, n_pad
+  void* xfirst = nullptr;                // full, low dtype
+  void* anchor = nullptr;                // shard, state
+  void* prev_x0 = nullptr;               // shard, state
+  void* m = nullptr;                     // shard, state
+  void* gap = nullptr;                   // shard, state
+  void* p1sum[2] = {nullptr, nullptr};   // shard, low: sum over workers of x_{t,1}
+  void* xsum[2] = {nullptr, nullptr};    // shard, low: sum over workers of x_{t,tau}
+  void* xbar = nullptr;
+  void* ws = nullptr;
+  co2_diag_t* host_diag = nullptr;
+  cudaEvent_t sync_ev = nullptr;
+  bool has_pending = false;
+  uint64_t pending = 0;
+  std::vector<cudaEvent_t> tev;
+  int64_t tev_recorded = 0, tev_read = 0;
+};
+
+static co2_status_t ensure_comm2(co2_aar* e) {
+  if (e->transport != T_NCCL)
+    return fail(CO2_ERR_VALIDATION, "sharded outer state: NCCL transport only");
+  if (e->world > 1 && !e->comm2) CO2_NCCL(ncclCommSplit(e->comm, 0, e->rank, &e->comm2, nullptr));
+  return CO2_OK;
+}
+
+// Blocking (stream-ordered) collectives on the caller's stream over comm2.
+static co2_status_t rs_blocking(co2_aar* e, co2_dtype_t dt, const void* full, void* shard_out,
+                                int64_t shard, cudaStream_t st) {
+  if (shard <= 0) return CO2_OK;
+  if (e->world > 1)
+    CO2_NCCL(ncclReduceScatter(full, shard_out, (size_t)shard, nccl_dtype(dt), ncclSum, e->comm2,
+                               st));
+  else
+    CO2_CUDA(cudaMemcpyAsync(shard_out, full, dtype_bytes(dt) * (size_t)shard,
+                             cudaMemcpyDeviceToDevice, st));
+  return CO2_OK;
+}
+
+static co2_status_t ag_inplace(co2_aar* e, co2_dtype_t dt, void* full, int64_t shard,
+                               cudaStream_t st) {
+  if (shard <= 0 || e->world == 1) return CO2_OK;
+  char* base = static_cast<char*>(full);
+  CO2_NCCL(ncclAllGather(base + (size_t)e->rank * shard * dtype_bytes(dt), full, (size_t)shard,
+                         nccl_dtype(dt), e->comm2, st));
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode, int64_t n,
+                                           co2_aar_t* e, const void* init, void* stream) {
+  if (!e) return fail(CO2_ERR_VALIDATION, "sharded: null engine");
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "sharded: negative dimension");
+  if (mode != CO2_MODE_F64 && mode != CO2_MODE_F32 && mode != CO2_MODE_BF16_MIXED)
+    return fail(CO2_ERR_VALIDATION, "sharded: unknown mode %d", (int)mode);
+  CO2_TRY(ensure_comm2(e));
+  co2_sharded* s = new co2_sharded();
+  s->mode = mode;
+  s->n = n;
+  s->world = e->world;
+  s->rank = e->rank;
+  // 8-element (16-byte bf16) aligned shards, equal capacity for NCCL.
+  const int64_t per = ((n + s->world - 1) / s->world + 7) / 8 * 8;
+  s->shard = per;
+  s->n_pad = per * s->world;
+  s->offset = (int64_t)s->rank * per;
+  s->length = std::max<int64_t>(0, std::min<int64_t>(per, n - s->offset));
+  const size_t sb = state_bytes(mode), lb = low_bytes(mode);
+  co2_status_t st = CO2_OK;
+  auto A = [&](void** p, size_t b) {
+    if (st == CO2_OK) st = walloc(p, b);
+  };
+  A(&s->params[0], lb * s->n_pad);
+  A(&s->params[1], lb * s->n_pad);
+  A(&s->xfirst, lb * s->n_pad);
+  A(&s->anchor, sb * per);
+  A(&s->prev_x0, sb * per);
+  A(&s->m, sb * per);
+  A(&s->gap, sb * per);
+  A(&s->p1sum[0], lb * per);
+  A(&s->p1sum[1], lb * per);
+  A(&s->xsum[0], lb * per);
+  A(&s->xsum[1], lb * per);
+  A(&s->ws, co2_workspace_bytes());
+  if (st != CO2_OK) {
+    co2_sharded_destroy(s);
+    return st;
+  }
+  cudaStream_t cs = S(stream);
+  CO2_CUDA(cudaMallocHost(&s->host_diag, sizeof(co2_diag_t)));
+  CO2_CUDA(cudaEventCreateWithFlags(&s->sync_ev, cudaEventDisableTiming));
+  CO2_CUDA(cudaMemsetAsync(s->ws, 0, co2_workspace_bytes(), cs));
+  CO2_CUDA(cudaMemsetAsync(s->m, 0, sb * per, cs));
+  CO2_CUDA(cudaMemsetAsync(s->params[0], 0, lb * s->n_pad, cs));
+  CO2_CUDA(cudaMemsetAsync(s->params[1], 0, lb * s->n_pad, cs));
+  CO2_CUDA(cudaMemsetAsync(s->xfirst, 0, lb * s->n_pad, cs));
+  if (init && n > 0) CO2_CUDA(cudaMemcpyAsync(s->params[0], init, lb * n, cudaMemcpyDeviceToDevice, cs));
+  if (mode == CO2_MODE_F64) {
+    std::vector<double> ones(per, 1.0);
+    CO2_CUDA(cudaMemcpy(s->gap, ones.data(), sb * per, cudaMemcpyHostToDevice));
+  } else {
+    CO2_TRY(co2_fill_u32(s->gap, 0x3f800000u, per, stream));
+  }
+  *out = s;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_sharded_destroy(co2_sharded_t* s) {
+  if (!s) return CO2_OK;
+  for (void* p : {s->params[0], s->params[1], s->xfirst, s->anchor, s->prev_x0, s->m, s->gap,
+                  s->p1sum[0], s->p1sum[1], s->xsum[0], s->xsum[1], s->ws})
+    if (p) cudaFree(p);
+  if (s->host_diag) cudaFreeHost(s->host_diag);
+  if (s->sync_ev) cudaEventDestroy(s->sync_ev);
+  for (cudaEvent_t ev : s->tev) cudaEventDestroy(ev);
+  delete s;
+  return CO2_OK;
+}
+
+extern "C" void* co2_sharded_buffer(co2_sharded_t* s, int32_t which) {
+  if (!s) return nullptr;
+  switch (which) {
+    case CO2_BUF_PARAMS: return s->params[s->cur];
+    case CO2_BUF_XFIRST: return s->xfirst;
+    case CO2_BUF_ANCHOR: return s->anchor;
+    case CO2_BUF_PREV_X0: return s->prev_x0;
+    case CO2_BUF_PREV_X1: return s->t > 0 ? s->p1sum[(s->t - 1) % 2] : nullptr;
+    case CO2_BUF_MOMENTUM: return s->m;
+    case CO2_BUF_GAP: return s->gap;
+    case CO2_BUF_XBAR: return s->xbar;
+  }
+  return nullptr;
+}
+
+extern "C" int64_t co2_sharded_shard(const co2_sharded_t* s, int64_t* offset, int64_t* length) {
+  if (!s) return 0;
+  if (offset) *offset = s->offset;
+  if (length) *length = s->length;
+  return s->shard;
+}
+
+extern "C" co2_status_t co2_sharded_snapshot_first(co2_sharded_t* s, void* stream) {
+  if (!s) return fail(CO2_ERR_VALIDATION, "sharded: null");
+  if (s->n == 0) return CO2_OK;
+  CO2_CUDA(cudaMemcpyAsync(s->xfirst, s->params[s->cur], low_bytes(s->mode) * s->n,
+                           cudaMemcpyDeviceToDevice, S(stream)));
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_sharded_enable_timing(co2_sharded_t* s, int32_t cap) {
+  if (!s || cap < 1) return fail(CO2_ERR_VALIDATION, "timing: bad arguments");
+  for (cudaEvent_t ev : s->tev) cudaEventDestroy(ev);
+  s->tev.assign(2 * (size_t)cap, nullptr);
+  for (cudaEvent_t& ev : s->tev) CO2_CUDA(cudaEventCreate(&ev));
+  s->tev_recorded = s->tev_read = 0;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_sharded_step_times(co2_sharded_t* s, double* out, int32_t cap,
+                                               int32_t* count) {
+  if (!s) return fail(CO2_ERR_VALIDATION, "timing: null");
+  const int64_t ring = (int64_t)s->tev.size() / 2;
+  int64_t first = s->tev_read;
+  if (ring && s->tev_recorded - first > ring) first = s->tev_recorded - ring;
+  int32_t k = 0;
+  for (int64_t i = first; ring && i < s->tev_recorded && k < cap; ++i) {
+    const int64_t sl = i % ring;
+    CO2_CUDA(cudaEventSynchronize(s->tev[2 * sl + 1]));
+    float ms = 0.f;
+    CO2_CUDA(cudaEventElapsedTime(&ms, s->tev[2 * sl], s->tev[2 * sl + 1]));
+    if (out) out[k] = ms * 1e-3;
+    ++k;
+  }
+  s->tev_read = s->tev_recorded;
+  *count = k;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_sharded_drain(co2_sharded_t* s, co2_aar_t* e, void* stream) {
+  if (!s || !e) return fail(CO2_ERR_VALIDATION, "sharded: bad arguments");
+  if (!s->has_pending) return CO2_OK;
+  CO2_TRY(co2_aar_wait(e, s->pending, stream));
+  s->has_pending = false;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
+                                          const co2_hyper_t* hyper, void* stream, int32_t sync,
+                                          co2_round_result_t* res) {
+  CO2_TRY(co2_hyper_validate(hyper));  // outer_algorithms.cpp:115
+  if (!s || !e) return fail(CO2_ERR_VALIDATION, "sharded: bad arguments");
+  if (hyper->tau < 1) return fail(CO2_ERR_VALIDATION, "staleness_gap: tau must be >= 1");
+  if (!hyper->ghost_consistent)
+    return fail(CO2_ERR_VALIDATION, "sharded outer state requires ghost_consistent semantics");
+  if (e->transport != T_NCCL || e->world != s->world || e->rank != s->rank)
+    return fail(CO2_ERR_VALIDATION, "sharded: engine does not match the shard layout");
+  cudaStream_t st = S(stream);
+  const co2_dtype_t ldt = low_dtype(s->mode);
+  const size_t lb = low_bytes(s->mode);
+  co2_round_result_t r{};
+  r.min_gap = INFINITY;
+  const int t = s->t;
+  if (t == 0) {
+    // x_{1,0} = x_{0,tau} stays worker-local: continue on the other buffer.
+    CO2_CUDA(cudaMemcpyAsync(s->params[1 - s->cur], s->params[s->cur], lb * s->n_pad,
+                             cudaMemcpyDeviceToDevice, st));
+  }
+  // bar1 of this round: the worker sum of x_{t,1} for this shard (consumed
+  // as prev_x1 next round; the reference's average(firsts), :133-145/:167).
+  CO2_TRY(rs_blocking(e, ldt, s->xfirst, s->p1sum[t % 2], s->shard, st));
+  // The one-step-stale reduce of x_{t,tau}, scattered by shard (:120).
+  uint64_t launched = 0;
+  const void* bufs[1] = {s->params[s->cur]};
+  CO2_TRY(launch_impl(e, 1, ldt, bufs, s->xsum[t % 2], s->n_pad, stream, &launched));
+  if (t == 0) {
+    // :133-145: prev_x0 <- average(x_{0,0}) over identical starts.
+    CO2_TRY(ghost_init_impl(s->mode, s->length,
+                            static_cast<char*>(s->params[s->cur]) + lb * s->offset, s->anchor,
+                            s->prev_x0, s->world, st));
+    s->cur = 1 - s->cur;
+    s->pending = launched;
+    s->has_pending = true;
+    s->t = 1;
+    r.outer_applied = 0;
+    if (sync) CO2_CUDA(cudaStreamSynchronize(st));
+    if (res) *res = r;
+    return CO2_OK;
+  }
+  if (!s->has_pending)
+    return fail(CO2_ERR_VALIDATION, "outer round: no pending reduce to consume");
+  const uint64_t prev = s->pending;
+  int32_t done = 0;
+  CO2_TRY(co2_aar_poll(e, prev, &done));
+  CO2_TRY(co2_aar_wait(e, prev, stream));
+  void* xsum = s->xsum[(t - 1) % 2];
+  void* p1 = s->p1sum[(t - 1) % 2];
+  char* out_params = static_cast<char*>(s->params[1 - s->cur]) + lb * s->offset;
+  // Round 1: x_{1,0} = x_{0,tau} differ per worker and their average is the
+  // consumed reduce itself; later rounds start from identical x_{t,0}.
+  const int ghost_copies = t == 1 ? 0 : s->world;
+  const int64_t cap = (int64_t)s->tev.size() / 2;
+  const int64_t slot = cap ? s->tev_recorded % cap : 0;
+  if (cap) CO2_CUDA(cudaEventRecord(s->tev[2 * slot], st));
+  CO2_TRY(outer_step_ghost_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, s->world, xsum,
+                                s->world, ghost_copies, s->m, s->anchor, s->prev_x0, out_params,
+                                s->gap, hyper, s->ws, st));
+  if (cap) {
+    CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));
+    s->tev_recorded += 1;
+  }
+  CO2_TRY(co2_diag_fetch_async(s->ws, s->host_diag, stream));
+  // x_{t+1,0} for every worker: in-place all-gather of the updated shards.
+  CO2_TRY(ag_inplace(e, ldt, s->params[1 - s->cur], s->shard, st));
+  s->xbar = xsum;
+  s->cur = 1 - s->cur;
+  s->pending = launched;
+  s->t += 1;
+  r.outer_applied = 1;
+  if (sync) {
+    CO2_CUDA(cudaStreamSynchronize(st));
+    const co2_diag_t& d = *s->host_diag;
+    r.min_gap = d.min_gap;
+    r.max_outer_step = d.max_outer_step;
+    r.n_clipped = d.n_clipped;
+    r.n_floored = d.n_floored;
+    double stall = 0.0;
+    co2_status_t s2 = co2_aar_stall(e, prev, &stall, nullptr);
+    r.stall_seconds = stall;
+    if (res) *res = r;
+    if (d.flags) return co2_diag_status(&d);
     return s2;
   }
   if (res) *res = r;

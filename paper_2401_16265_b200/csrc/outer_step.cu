@@ -300,9 +300,23 @@ struct StepArgs {
   double alpha, beta, phi, eps;
   int tau, divisor, penalty, clip;
   void* ws;
+  // ghost-consistent / sharded extension (GHOST instantiations only)
+  int p1_div;       // prev_x1 holds a worker sum: divide once by p1_div
+  int ghost_g;      // x_t0 = average of ghost_g identical copies of x_t0
+  int x_from_xbar;  // x_t0 = the consumed average itself (round 1)
+  void* bar0_out;   // receives the x_t0 actually used (next prev_x0)
 };
 
-template <class M, int V, int U, int NT, int MINB>
+// average() of g identical copies (param_ops.cpp:26-30 with every
+// contribution equal): ascending-order sum, one division.
+template <typename TC>
+__device__ __forceinline__ TC ghost_avg(TC v, int g) {
+  TC s = v;
+  for (int i = 1; i < g; ++i) s = s + v;
+  return s / (TC)g;
+}
+
+template <class M, int V, int U, int NT, int MINB, bool GHOST = false>
 __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
@@ -317,6 +331,10 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
   h.penalty = a.penalty;
   h.clip = a.clip;
   h.divide = a.divisor > 1;
+  Hyp<TC> hg = h;  // GHOST: xbar is divided before the element body
+  hg.divide = 0;
+  const TC p1d = (TC)a.p1_div;
+  TS* B0 = static_cast<TS*>(a.bar0_out);
 
   const TS* __restrict__ X = static_cast<const TS*>(a.x_t0);
   const TS* __restrict__ P0 = static_cast<const TS*>(a.p0);
@@ -350,13 +368,23 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
     for (int u = 0; u < U; ++u) {
       if (u < cnt) {
         const int64_t e = idx[u] * V;
-        TS mn[V], xs[V], gs[V];
+        TS mn[V], xs[V], gs[V], b0[V];
         TL xl[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           TC m = to_c(mo[u][v]), xn, lam;
-          co2_elem<TC>(to_c(x[u][v]), to_c(q0[u][v]), to_c(q1[u][v]), to_c(xb[u][v]), m, xn,
-                       lam, h, acc);
+          if constexpr (GHOST) {
+            TC xbv = to_c(xb[u][v]);
+            if (h.divide) xbv = xbv / h.divisor;
+            TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(x[u][v]), a.ghost_g);
+            TC p1v = to_c(q1[u][v]);
+            if (a.p1_div > 1) p1v = p1v / p1d;
+            b0[v] = (TS)xv;
+            co2_elem<TC>(xv, to_c(q0[u][v]), p1v, xbv, m, xn, lam, hg, acc);
+          } else {
+            co2_elem<TC>(to_c(x[u][v]), to_c(q0[u][v]), to_c(q1[u][v]), to_c(xb[u][v]), m, xn,
+                         lam, h, acc);
+          }
           mn[v] = (TS)m;
           xs[v] = (TS)xn;
           gs[v] = (TS)lam;
@@ -366,6 +394,9 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
         if (A) st_vec<TS, V>(A + e, xs);
         if (PR) st_vec<TL, V>(PR + e, xl);
         if (G) st_vec<TS, V>(G + e, gs);
+        if constexpr (GHOST) {
+          if (B0) st_vec<TS, V>(B0 + e, b0);
+        }
       }
     }
   };
@@ -386,7 +417,17 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
   const int64_t t = nv * V + (int64_t)blockIdx.x * NT + threadIdx.x;
   if (V > 1 && t < a.n) {
     TC m = to_c(Mm[t]), xn, lam;
-    co2_elem<TC>(to_c(X[t]), to_c(P0[t]), to_c(P1[t]), to_c(XB[t]), m, xn, lam, h, acc);
+    if constexpr (GHOST) {
+      TC xbv = to_c(XB[t]);
+      if (h.divide) xbv = xbv / h.divisor;
+      TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(X[t]), a.ghost_g);
+      TC p1v = to_c(P1[t]);
+      if (a.p1_div > 1) p1v = p1v / p1d;
+      if (B0) B0[t] = (TS)xv;
+      co2_elem<TC>(xv, to_c(P0[t]), p1v, xbv, m, xn, lam, hg, acc);
+    } else {
+      co2_elem<TC>(to_c(X[t]), to_c(P0[t]), to_c(P1[t]), to_c(XB[t]), m, xn, lam, h, acc);
+    }
     Mm[t] = (TS)m;
     if (A) A[t] = (TS)xn;
     if (PR) PR[t] = Store<TL>::from(xn);
@@ -418,6 +459,23 @@ void launch_variant(const StepArgs& a, cudaStream_t s) {
   auto k = fused_step_kernel<M, V, U, kThreads, MINB>;
   int grid = grid_for(k, (a.n / V + U - 1) / U, kThreads);
   k<<<grid, kThreads, 0, s>>>(a);
+}
+
+template <class M>
+co2_status_t launch_ghost(const StepArgs& a, cudaStream_t s) {
+  bool vec_ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
+                aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) &&
+                aligned16(a.gap) && aligned16(a.bar0_out);
+  if (!vec_ok) {
+    auto k = fused_step_kernel<M, 1, 4, kThreads, 1, true>;
+    k<<<grid_for(k, (a.n + 3) / 4, kThreads), kThreads, 0, s>>>(a);
+  } else {
+    constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+    auto k = fused_step_kernel<M, V, 1, kThreads, 3, true>;
+    k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
 }
 
 // Tuning knob: CO2_FUSED_VARIANT selects the (elements per vector, vectors
@@ -700,11 +758,28 @@ co2_status_t outer_step_impl(co2_mode_t mode, int64_t n, const void* x_t0, const
                              void* anchor, void* params, void* gap, const co2_hyper_t* h,
                              void* ws, cudaStream_t s) {
   StepArgs a{x_t0, p0, p1, xbar, m, anchor, params, gap, n, h->alpha, h->beta, h->phi,
-             h->epsilon, h->tau, divisor, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws};
+             h->epsilon, h->tau, divisor, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, 0, 0,
+             nullptr};
   switch (mode) {
     case CO2_MODE_F64: return launch_fused<ModeF64>(a, s);
     case CO2_MODE_F32: return launch_fused<ModeF32>(a, s);
     case CO2_MODE_BF16_MIXED: return launch_fused<ModeBF16>(a, s);
+  }
+  return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
+}
+
+co2_status_t outer_step_ghost_impl(co2_mode_t mode, int64_t n, const void* anchor_in,
+                                   const void* p0, const void* p1_sum, int32_t p1_div,
+                                   const void* xbar_sum, int32_t divisor, int32_t ghost_copies,
+                                   void* m, void* anchor_out, void* bar0_out, void* params,
+                                   void* gap, const co2_hyper_t* h, void* ws, cudaStream_t s) {
+  StepArgs a{anchor_in, p0, p1_sum, xbar_sum, m, anchor_out, params, gap, n, h->alpha, h->beta,
+             h->phi, h->epsilon, h->tau, divisor, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws,
+             p1_div, ghost_copies, ghost_copies == 0 ? 1 : 0, bar0_out};
+  switch (mode) {
+    case CO2_MODE_F64: return launch_ghost<ModeF64>(a, s);
+    case CO2_MODE_F32: return launch_ghost<ModeF32>(a, s);
+    case CO2_MODE_BF16_MIXED: return launch_ghost<ModeBF16>(a, s);
   }
   return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
 }
@@ -893,4 +968,65 @@ extern "C" co2_status_t co2_fill_u32(void* dst, uint32_t value, int64_t count, v
                                                                              count);
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
+}
+
+// ------------------------------------------------ sharded-mode helpers
+namespace co2 {
+namespace {
+// Round 0 of the sharded ghost driver: anchor <- x_{0,0} (the params shard,
+// widened) and prev_x0 <- average of g identical copies of it
+// (outer_algorithms.cpp:133-145 with identical starts).
+template <typename TS, typename TL>
+__global__ void ghost_init_kernel(const TL* params, TS* anchor, TS* prev_x0, int64_t n, int g) {
+  using TC = decltype(to_c(TS{}));
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    TC v = (TC)to_c(params[j]);
+    anchor[j] = (TS)v;
+    prev_x0[j] = (TS)ghost_avg<TC>(v, g);
+  }
+}
+}  // namespace
+
+co2_status_t ghost_init_impl(co2_mode_t mode, int64_t n, const void* params, void* anchor,
+                             void* prev_x0, int g, cudaStream_t s) {
+  if (n <= 0) return CO2_OK;
+  int grid = simple_grid(n, kThreads);
+  switch (mode) {
+    case CO2_MODE_F64:
+      ghost_init_kernel<double, double><<<grid, kThreads, 0, s>>>(
+          (const double*)params, (double*)anchor, (double*)prev_x0, n, g);
+      break;
+    case CO2_MODE_F32:
+      ghost_init_kernel<float, float><<<grid, kThreads, 0, s>>>(
+          (const float*)params, (float*)anchor, (float*)prev_x0, n, g);
+      break;
+    default:
+      ghost_init_kernel<float, bf16s><<<grid, kThreads, 0, s>>>(
+          (const bf16s*)params, (float*)anchor, (float*)prev_x0, n, g);
+      break;
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+}  // namespace co2
+
+extern "C" co2_status_t co2_outer_step_ghost(co2_mode_t mode, int64_t n, const void* anchor_in,
+                                             const void* prev_x0, const void* prev_x1_sum,
+                                             int32_t p1_div, const void* xbar_sum,
+                                             int32_t xbar_div, int32_t ghost_copies,
+                                             void* momentum, void* anchor_out, void* bar0_out,
+                                             void* params_out, void* gap_out,
+                                             const co2_hyper_t* h, void* ws, void* stream) {
+  CO2_TRY(co2_hyper_validate(h));
+  if (h->tau < 1) return fail(CO2_ERR_VALIDATION, "staleness_gap: tau must be >= 1");
+  if (n < 0 || p1_div < 1 || xbar_div < 1 || ghost_copies < 0)
+    return fail(CO2_ERR_VALIDATION, "ghost step: bad sizes or divisors");
+  if (!ws) return fail(CO2_ERR_VALIDATION, "null workspace");
+  if (n > 0 && (!prev_x0 || !prev_x1_sum || !xbar_sum || !momentum ||
+                (ghost_copies > 0 && !anchor_in)))
+    return fail(CO2_ERR_VALIDATION, "outer step: null input buffer");
+  return outer_step_ghost_impl(mode, n, ghost_copies > 0 ? anchor_in : xbar_sum, prev_x0,
+                               prev_x1_sum, p1_div, xbar_sum, xbar_div, ghost_copies, momentum,
+                               anchor_out, bar0_out, params_out, gap_out, h, ws, S(stream));
 }

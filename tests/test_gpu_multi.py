@@ -35,3 +35,17 @@ def test_nccl_rounds_bitwise_world2(mode):
     res = json.loads(line)
     assert res["ok"], res
     assert res["waits"] == 3
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_nccl_sharded_ghost_bitwise_world2(mode):
+    env = dict(os.environ, CO2_TEST_MODE=str(mode))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_nccl_sharded.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    res = json.loads(line)
+    assert res["ok"], res

@@ -239,3 +239,61 @@ def test_round_rejects_bad_hyper_and_counts():
         co2.co2_round(ws, eng, co2.Co2Hyper(beta=1.5), 2)
     with pytest.raises(co2.ValidationError, match="contribution count"):
         co2.co2_round(ws[:1], eng, co2.Co2Hyper(), 2)
+
+
+@pytest.mark.parametrize("mode", [co2.MODE_F64, co2.MODE_F32, co2.MODE_BF16_MIXED])
+@pytest.mark.parametrize("ghost", [0, 1, 2, 3, 4, 8])
+def test_ghost_step_bitwise(mode, ghost):
+    """The sharded/ghost fused step vs the oracle (outer_algorithms.cpp:161-184)."""
+    n, G = 70001, max(ghost, 2)
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    ox, op0, op1, oxe, om = O.synth(mode, n)
+    oh = O.hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12, tau=6)
+    ref = O.outer_step_ghost(mode, ox, op0, op1, G, oxe, G, ghost, om, oh)
+    assert ref.status == 0
+    h = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    a_out, b0, params = torch.empty_like(x), torch.empty_like(x), torch.empty_like(xe)
+    co2.check(co2.lib().co2_outer_step_ghost(
+        mode, n, x.data_ptr(), p0.data_ptr(), p1.data_ptr(), G, xe.data_ptr(), G, ghost,
+        m.data_ptr(), a_out.data_ptr(), b0.data_ptr(), params.data_ptr(), None,
+        co2.C.byref(h.c(6)), co2._ws().ptr, torch.cuda.current_stream().cuda_stream))
+    d = co2._ws().fetch()
+    assert to_np(m).tobytes() == ref.m.tobytes()
+    assert to_np(a_out).tobytes() == ref.anchor.tobytes()
+    assert to_np(b0).tobytes() == ref.bar0.tobytes()
+    assert to_np(params).tobytes() == ref.params.tobytes()
+    assert d.n_clipped == ref.diag.n_clipped and d.min_gap == ref.diag.min_gap
+
+
+@pytest.mark.parametrize("mode", [co2.MODE_F64, co2.MODE_F32])
+def test_sharded_world1_equals_worker_local(mode):
+    """With one rank, ghost-consistent sharded rounds reduce to worker-local
+    co2_round (average of one worker is the identity): bitwise."""
+    n, tau = 200_003, 3
+    eng_s = co2.CollectiveEngine(1, transport="nccl", rank=0, nccl_id=bytes(128))
+    eng_w = co2.CollectiveEngine(1, transport="nccl", rank=0, nccl_id=bytes(128))
+    init = co2.synth(mode, n)[3]
+    sw = co2.ShardedWorker(mode, n, eng_s, init)
+    w = co2.Worker(mode, n, init)
+    hs = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12, ghost_consistent=True)
+    hw = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    assert sw.length == n and sw.offset == 0
+    for t in range(5):
+        w.snapshot_start()
+        for k in range(tau):
+            co2.synthetic_inner_step(sw.params, lr=1e-3, step=t * tau + k)
+            co2.synthetic_inner_step(w.params, lr=1e-3, step=t * tau + k)
+            if k == 0:
+                sw.snapshot_first()
+                w.snapshot_first()
+        rs = sw.round(eng_s, hs, tau)
+        rw = co2.co2_round([w], eng_w, hw, tau)
+        assert to_np(sw.params).tobytes() == to_np(w.params).tobytes(), t
+        if t >= 1:
+            assert to_np(sw.buffer(L.BUF_MOMENTUM)).tobytes() == \
+                to_np(w.buffer(L.BUF_MOMENTUM)).tobytes()
+            assert rs.min_gap == rw.min_gap and rs.max_outer_step == rw.max_outer_step
+    with pytest.raises(co2.ValidationError, match="ghost_consistent"):
+        sw.round(eng_s, hw, tau)
+    sw.drain(eng_s)
+    co2.co2_round_drain([w], eng_w)
