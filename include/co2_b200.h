@@ -328,6 +328,9 @@ void* co2_sharded_buffer(co2_sharded_t* s, int32_t which);
 /* Shard geometry: returns the shard capacity; *offset and *length give the
  * global offset and the real coordinate count of this rank's shard. */
 int64_t co2_sharded_shard(const co2_sharded_t* s, int64_t* offset, int64_t* length);
+/* x_{0,0} snapshot of round 0 (call before the first inner step; no-op
+ * afterwards) and x_{t,1} snapshot (call after the first inner step). */
+co2_status_t co2_sharded_snapshot_start(co2_sharded_t* s, void* stream);
 co2_status_t co2_sharded_snapshot_first(co2_sharded_t* s, void* stream);
 co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* engine, const co2_hyper_t* hyper,
                                void* stream, int32_t sync, co2_round_result_t* result);

@@ -122,6 +122,7 @@ SIGNATURES = {
     "co2_sharded_destroy": (ST, [P]),
     "co2_sharded_buffer": (P, [P, I32]),
     "co2_sharded_shard": (I64, [P, C.POINTER(I64), C.POINTER(I64)]),
+    "co2_sharded_snapshot_start": (ST, [P, P]),
     "co2_sharded_snapshot_first": (ST, [P, P]),
     "co2_sharded_round": (ST, [P, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),
     "co2_sharded_drain": (ST, [P, P, P]),

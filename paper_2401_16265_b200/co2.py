@@ -535,6 +535,9 @@ class ShardedWorker:
     def params(self):
         return self.buffer(L.BUF_PARAMS)
 
+    def snapshot_start(self, stream=None):
+        check(lib().co2_sharded_snapshot_start(self.handle, _stream(stream)))
+
     def snapshot_first(self, stream=None):
         check(lib().co2_sharded_snapshot_first(self.handle, _stream(stream)))
 

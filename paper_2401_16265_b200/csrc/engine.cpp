@@ -722,6 +722,7 @@ struct co2_sharded {
   co2_diag_t* host_diag = nullptr;
   cudaEvent_t sync_ev = nullptr;
   bool has_pending = false;
+  bool started = false;
   uint64_t pending = 0;
   std::vector<cudaEvent_t> tev;
   int64_t tev_recorded = 0, tev_read = 0;
@@ -848,6 +849,20 @@ extern "C" int64_t co2_sharded_shard(const co2_sharded_t* s, int64_t* offset, in
   return s->shard;
 }
 
+extern "C" co2_status_t co2_sharded_snapshot_start(co2_sharded_t* s, void* stream) {
+  // InnerTrace::x_start (inner_loop.cpp:73).  Round 0 only: every worker
+  // starts from the same init, so the ghost snapshot average of :133-145 is
+  // the average of identical copies of this shard of x_{0,0}.  For t >= 1 the
+  // step itself maintains x_{t,0} (anchor) and prev_x0.
+  if (!s) return fail(CO2_ERR_VALIDATION, "sharded: null");
+  if (s->t > 0) return CO2_OK;
+  CO2_TRY(ghost_init_impl(s->mode, s->length,
+                          static_cast<char*>(s->params[s->cur]) + low_bytes(s->mode) * s->offset,
+                          s->anchor, s->prev_x0, s->world, S(stream)));
+  s->started = true;
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_sharded_snapshot_first(co2_sharded_t* s, void* stream) {
   if (!s) return fail(CO2_ERR_VALIDATION, "sharded: null");
   if (s->n == 0) return CO2_OK;
@@ -909,6 +924,8 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
   co2_round_result_t r{};
   r.min_gap = INFINITY;
   const int t = s->t;
+  if (t == 0 && !s->started)
+    return fail(CO2_ERR_VALIDATION, "sharded: snapshot_start must precede round 0");
   if (t == 0) {
     // x_{1,0} = x_{0,tau} stays worker-local: continue on the other buffer.
     CO2_CUDA(cudaMemcpyAsync(s->params[1 - s->cur], s->params[s->cur], lb * s->n_pad,
@@ -922,10 +939,7 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
   const void* bufs[1] = {s->params[s->cur]};
   CO2_TRY(launch_impl(e, 1, ldt, bufs, s->xsum[t % 2], s->n_pad, stream, &launched));
   if (t == 0) {
-    // :133-145: prev_x0 <- average(x_{0,0}) over identical starts.
-    CO2_TRY(ghost_init_impl(s->mode, s->length,
-                            static_cast<char*>(s->params[s->cur]) + lb * s->offset, s->anchor,
-                            s->prev_x0, s->world, st));
+    // prev_x0 <- average(x_{0,0}) was computed by co2_sharded_snapshot_start.
     s->cur = 1 - s->cur;
     s->pending = launched;
     s->has_pending = true;

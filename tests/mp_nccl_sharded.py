@@ -61,6 +61,7 @@ def main():
         m = np.zeros(n, st)
         anchor = prev_x0 = p1sum = xsum = None
     for t in range(rounds):
+        sw.snapshot_start()
         for k in range(tau):
             co2.synthetic_inner_step(sw.params, lr=1e-3, worker=rank, step=t * tau + k)
             if k == 0:
@@ -92,11 +93,15 @@ def main():
                 anchor, prev_x0, m = res.anchor, res.bar0, res.m
                 expect = [res.params] * world
                 for off, ln, mm in shards:
-                    if mm[:ln].tobytes() != m[off:off + ln].tobytes():
-                        ok, mismatch = False, (t, "momentum", off)
+                    if mm[:ln].tobytes() != m[off:off + ln].tobytes() and ok:
+                        bad = np.nonzero(mm[:ln] != m[off:off + ln])[0]
+                        ok, mismatch = False, (t, "momentum", off, int(bad.size), int(bad[0]),
+                                               float(mm[bad[0]]), float(m[off + bad[0]]))
             for i in range(world):
-                if afters[i][:n].tobytes() != expect[i].tobytes():
-                    ok, mismatch = False, (t, "params", i)
+                if afters[i][:n].tobytes() != expect[i].tobytes() and ok:
+                    bad = np.nonzero(afters[i][:n] != expect[i])[0]
+                    ok, mismatch = False, (t, "params", i, int(bad.size), int(bad[0]),
+                                           float(afters[i][bad[0]]), float(expect[i][bad[0]]))
             p1sum = storage_sum(firsts, mode)
             xsum = storage_sum(ends, mode)
         if t >= 1:

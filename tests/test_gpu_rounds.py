@@ -280,6 +280,7 @@ def test_sharded_world1_equals_worker_local(mode):
     assert sw.length == n and sw.offset == 0
     for t in range(5):
         w.snapshot_start()
+        sw.snapshot_start()
         for k in range(tau):
             co2.synthetic_inner_step(sw.params, lr=1e-3, step=t * tau + k)
             co2.synthetic_inner_step(w.params, lr=1e-3, step=t * tau + k)
