@@ -423,8 +423,9 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
       TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(X[t]), a.ghost_g);
       TC p1v = to_c(P1[t]);
       if (a.p1_div > 1) p1v = p1v / p1d;
+      const TC q0 = to_c(P0[t]);  // read before bar0_out (may alias prev_x0) is written
       if (B0) B0[t] = (TS)xv;
-      co2_elem<TC>(xv, to_c(P0[t]), p1v, xbv, m, xn, lam, hg, acc);
+      co2_elem<TC>(xv, q0, p1v, xbv, m, xn, lam, hg, acc);
     } else {
       co2_elem<TC>(to_c(X[t]), to_c(P0[t]), to_c(P1[t]), to_c(XB[t]), m, xn, lam, h, acc);
     }
