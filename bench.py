@@ -39,9 +39,15 @@ CONFIGS = {
     "c2": {"workload": "C2: 125M-param fp32 flat buffer, tau=12 (BASELINE.json configs[1])",
            "mode": 1, "n": 125_000_000, "tau": 12, "bytes_per_param": 32,
            "storage": "fp32"},
-    "c4": {"workload": "C4 shard: 7B/8 = 875M-param bf16-mixed outer-state shard per B200",
-           "mode": 2, "n": 875_000_000, "tau": 12, "bytes_per_param": 26,
-           "storage": "bf16 params + fp32 state"},
+    "c4": {"workload": "C4: 7B-param bf16 params, ghost-consistent outer state (fp32 x_{t,0}, "
+                       "prev_x0, momentum) sharded across the GPUs (BASELINE.json configs[3]); "
+                       "needs >= 2 GPUs",
+           "mode": 2, "n": 7_000_000_000, "tau": 12, "bytes_per_param": 30, "sharded": True,
+           "storage": "bf16 params/x_{t,1} (replicated) + fp32 shard state"},
+    "c4shard": {"workload": "C4 shard on one GPU: 7B/8 = 875M-param bf16-mixed shard, "
+                            "worker-local step",
+                "mode": 2, "n": 875_000_000, "tau": 12, "bytes_per_param": 26,
+                "storage": "bf16 params + fp32 state"},
 }
 HYPER = dict(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
 
@@ -213,22 +219,43 @@ def main():
                                max_ctas=args.max_ctas)
 
     # --- worker state resident in HBM, synthetic inputs
-    init = co2.synth(mode, n, worker=rank)[3]  # x_{0,tau}: the params the reduce sums
-    w = co2.Worker(mode, n, init, keep_gap=False)
-    del init
-    w.snapshot_start()
-    w.snapshot_first()
-    co2.co2_round([w], eng, hyper, tau)  # round 0: snapshots, launches the first reduce
     from paper_2401_16265_b200 import _lib as L
-    co2.check(co2.lib().co2_synth(mode, 7, rank, 0, n, w.buffer(L.BUF_ANCHOR).data_ptr(),
-                                  w.buffer(L.BUF_PREV_X0).data_ptr(),
-                                  w.buffer(L.BUF_PREV_X1).data_ptr(), None,
-                                  w.buffer(L.BUF_MOMENTUM).data_ptr(), stream.cuda_stream))
+    sharded = cfg.get("sharded", False)
+    if sharded:
+        hyper = co2.Co2Hyper(ghost_consistent=True, **HYPER)
+        init = co2.synth(mode, n, worker=0)[3]  # identical x_{0,0} on every worker
+        w = co2.ShardedWorker(mode, n, eng, init, keep_gap=False)
+        del init
+        w.snapshot_start()
+        w.snapshot_first()
+        w.round(eng, hyper, tau)  # round 0: snapshots, launches the first reduce-scatter
+        co2.check(co2.lib().co2_synth(mode, 7, rank, w.offset, w.length, None,
+                                      w.buffer(L.BUF_PREV_X0).data_ptr(), None, None,
+                                      w.buffer(L.BUF_MOMENTUM).data_ptr(), stream.cuda_stream))
+        units = n  # every coordinate of the replicated params is updated per step
+
+        def one_round():
+            w.round(eng, hyper, tau, sync=False)
+    else:
+        init = co2.synth(mode, n, worker=rank)[3]  # x_{0,tau}: the params the reduce sums
+        w = co2.Worker(mode, n, init, keep_gap=False)
+        del init
+        w.snapshot_start()
+        w.snapshot_first()
+        co2.co2_round([w], eng, hyper, tau)  # round 0: snapshots, launches the first reduce
+        co2.check(co2.lib().co2_synth(mode, 7, rank, 0, n, w.buffer(L.BUF_ANCHOR).data_ptr(),
+                                      w.buffer(L.BUF_PREV_X0).data_ptr(),
+                                      w.buffer(L.BUF_PREV_X1).data_ptr(), None,
+                                      w.buffer(L.BUF_MOMENTUM).data_ptr(), stream.cuda_stream))
+        units = world * n  # one full replica per worker
+
+        def one_round():
+            co2.co2_round([w], eng, hyper, tau, sync=False)
     torch.cuda.synchronize()
     w.enable_timing(max(args.steps, 1) + max(args.warmup, 0) + 8)
 
     for _ in range(args.warmup):
-        co2.co2_round([w], eng, hyper, tau, sync=False)
+        one_round()
     torch.cuda.synchronize()
     w.step_times()  # drop warm-up launches
     n_events_before = len(eng.events()) if world > 1 else 0
@@ -239,7 +266,7 @@ def main():
     with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            co2.co2_round([w], eng, hyper, tau, sync=False)
+            one_round()
         e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -247,8 +274,11 @@ def main():
     elapsed = e0.elapsed_time(e1) * 1e-3
     kt = w.step_times()
     r = co2.L.RoundResult()
-    arr = (co2.C.c_void_p * 1)(w.handle.value)
-    co2.check(co2.lib().co2_round_finish(arr, 1, stream.cuda_stream, co2.C.byref(r)))
+    if sharded:
+        r = w.round(eng, hyper, tau, sync=True)  # one checked round: diagnostics + flags
+    else:
+        arr = (co2.C.c_void_p * 1)(w.handle.value)
+        co2.check(co2.lib().co2_round_finish(arr, 1, stream.cuda_stream, co2.C.byref(r)))
 
     # exposed communication (reference definition: 100 * sum(stall) / sum(waited comm))
     comm = None
@@ -273,13 +303,14 @@ def main():
     if world > 1:
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
     t_max, k_max = t_tensor.tolist()
-    value = world * n * args.steps / t_max
+    value = units * args.steps / t_max
     peak, peak_kind = peaks()
-    achieved = bpp * n / k_max / 1e9 if k_max else None
+    per_rank = w.length if sharded else n  # coordinates one fused launch processes
+    achieved = bpp * per_rank / k_max / 1e9 if k_max else None
 
     # --- e2e through the host-buffer entry (pinned H2D + kernel + D2H timed)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not sharded:
         e2e = run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist)
 
     # --- CPU baseline (rank 0, N=1 only): single-core reference restatement
@@ -296,18 +327,25 @@ def main():
             "metric": "CO2 outer-step params/s", "value": value, "unit": "params/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if mode != 0 else "f64",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "f32" if mode != 0 else "f64",
             "data": "synthetic (counter-SplitMix64 uniforms, SURVEY.md 8d)",
-            "config": {"workload": cfg["workload"], "n_params_per_gpu": n, "tau": tau,
+            "config": {"workload": cfg["workload"],
+                       "n_params_per_gpu": per_rank, "n_params_total": units, "tau": tau,
                        "storage": cfg["storage"], "hyper": HYPER,
-                       "parallelism": f"dp{world} (one CO2 worker per GPU, NCCL all-reduce)",
+                       "parallelism": (f"dp{world} ghost-consistent, outer state sharded "
+                                       "(NCCL reduce-scatter + all-gather)") if sharded else
+                       f"dp{world} (one CO2 worker per GPU, NCCL all-reduce)",
                        "l2": "inputs larger than L2 (no flush needed)",
-                       "step": "co2_round: AAR launch + stale wait + fused outer step"},
+                       "step": ("sharded co2_round: RS(x_{t,1}) + async RS(x_{t,tau}) + stale "
+                                "wait + fused ghost step on the shard + AG(x_{t+1,0})")
+                       if sharded else "co2_round: AAR launch + stale wait + fused outer step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
                          "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "fused_step_kernel<ModeBF16>" if mode == 2 else
-                         "fused_step_kernel", "kernel_ms": k_max * 1e3,
+                         "kernel": ("fused_step_kernel<ModeBF16%s>" % (", GHOST" if sharded
+                                                                        else ""))
+                         if mode == 2 else "fused_step_kernel", "kernel_ms": k_max * 1e3,
                          "bytes_per_param": bpp},
             "e2e": e2e, "cpu_baseline": cpu, "comm": comm,
             "gpu_launches": world * args.steps,

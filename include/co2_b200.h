@@ -319,7 +319,8 @@ co2_status_t co2_outer_step_ghost(co2_mode_t mode, int64_t n, const void* anchor
  * x_{t+1,0} into the params.  Requires hyper.ghost_consistent. */
 typedef struct co2_sharded co2_sharded_t;
 co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode, int64_t n,
-                                co2_aar_t* engine, const void* init_params, void* stream);
+                                co2_aar_t* engine, const void* init_params, int32_t keep_gap,
+                                void* stream);
 co2_status_t co2_sharded_destroy(co2_sharded_t* s);
 /* which: CO2_BUF_PARAMS / CO2_BUF_XFIRST (full length), CO2_BUF_ANCHOR,
  * CO2_BUF_PREV_X0, CO2_BUF_MOMENTUM, CO2_BUF_GAP (shard), CO2_BUF_PREV_X1

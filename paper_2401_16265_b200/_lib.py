@@ -118,7 +118,7 @@ SIGNATURES = {
     "co2_round_drain": (ST, [C.POINTER(P), I32, P, P]),
     "co2_outer_step_ghost": (ST, [I32, I64, P, P, P, I32, P, I32, I32, P, P, P, P, P,
                                   C.POINTER(Hyper), P, P]),
-    "co2_sharded_create": (ST, [C.POINTER(P), I32, I64, P, P, P]),
+    "co2_sharded_create": (ST, [C.POINTER(P), I32, I64, P, P, I32, P]),
     "co2_sharded_destroy": (ST, [P]),
     "co2_sharded_buffer": (P, [P, I32]),
     "co2_sharded_shard": (I64, [P, C.POINTER(I64), C.POINTER(I64)]),

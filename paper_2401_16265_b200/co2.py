@@ -501,11 +501,12 @@ class ShardedWorker:
     """Ghost-consistent CO2 worker with the outer state sharded across the
     NCCL engine's ranks (BASELINE config C4)."""
 
-    def __init__(self, mode: int, n: int, engine: CollectiveEngine, init=None, *, stream=None):
+    def __init__(self, mode: int, n: int, engine: CollectiveEngine, init=None, *,
+                 keep_gap: bool = True, stream=None):
         self.handle = C.c_void_p()
         self.mode, self.n = mode, n
         check(lib().co2_sharded_create(C.byref(self.handle), mode, n, engine.handle, _ptr(init),
-                                       _stream(stream)))
+                                       int(keep_gap), _stream(stream)))
         off, ln = C.c_int64(), C.c_int64()
         self.shard = lib().co2_sharded_shard(self.handle, C.byref(off), C.byref(ln))
         self.offset, self.length = off.value, ln.value

@@ -758,7 +758,8 @@ static co2_status_t ag_inplace(co2_aar* e, co2_dtype_t dt, void* full, int64_t s
 }
 
 extern "C" co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode, int64_t n,
-                                           co2_aar_t* e, const void* init, void* stream) {
+                                           co2_aar_t* e, const void* init, int32_t keep_gap,
+                                           void* stream) {
   if (!e) return fail(CO2_ERR_VALIDATION, "sharded: null engine");
   if (n < 0) return fail(CO2_ERR_VALIDATION, "sharded: negative dimension");
   if (mode != CO2_MODE_F64 && mode != CO2_MODE_F32 && mode != CO2_MODE_BF16_MIXED)
@@ -786,7 +787,7 @@ extern "C" co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode,
   A(&s->anchor, sb * per);
   A(&s->prev_x0, sb * per);
   A(&s->m, sb * per);
-  A(&s->gap, sb * per);
+  if (keep_gap) A(&s->gap, sb * per);
   A(&s->p1sum[0], lb * per);
   A(&s->p1sum[1], lb * per);
   A(&s->xsum[0], lb * per);
@@ -805,10 +806,10 @@ extern "C" co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode,
   CO2_CUDA(cudaMemsetAsync(s->params[1], 0, lb * s->n_pad, cs));
   CO2_CUDA(cudaMemsetAsync(s->xfirst, 0, lb * s->n_pad, cs));
   if (init && n > 0) CO2_CUDA(cudaMemcpyAsync(s->params[0], init, lb * n, cudaMemcpyDeviceToDevice, cs));
-  if (mode == CO2_MODE_F64) {
+  if (s->gap && mode == CO2_MODE_F64) {
     std::vector<double> ones(per, 1.0);
     CO2_CUDA(cudaMemcpy(s->gap, ones.data(), sb * per, cudaMemcpyHostToDevice));
-  } else {
+  } else if (s->gap) {
     CO2_TRY(co2_fill_u32(s->gap, 0x3f800000u, per, stream));
   }
   *out = s;
