@@ -223,7 +223,7 @@ def main():
     sharded = cfg.get("sharded", False)
     if sharded:
         hyper = co2.Co2Hyper(ghost_consistent=True, **HYPER)
-        init = co2.synth(mode, n, worker=0)[3]  # identical x_{0,0} on every worker
+        init = co2.synth_params(mode, n, worker=0)  # identical x_{0,0} on every worker
         w = co2.ShardedWorker(mode, n, eng, init, keep_gap=False)
         del init
         w.snapshot_start()
@@ -237,7 +237,7 @@ def main():
         def one_round():
             w.round(eng, hyper, tau, sync=False)
     else:
-        init = co2.synth(mode, n, worker=rank)[3]  # x_{0,tau}: the params the reduce sums
+        init = co2.synth_params(mode, n, worker=rank)  # x_{0,tau}: the params the reduce sums
         w = co2.Worker(mode, n, init, keep_gap=False)
         del init
         w.snapshot_start()

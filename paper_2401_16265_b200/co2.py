@@ -243,6 +243,16 @@ def synth(mode: int, n: int, *, seed: int = 7, worker: int = 0, j0: int = 0, dev
     return x, p0, p1, xe, m
 
 
+def synth_params(mode: int, n: int, *, seed: int = 7, worker: int = 0, device="cuda",
+                 stream=None):
+    """Only the x_end-style draws (params dtype) of `synth`, without
+    allocating the other four buffers."""
+    xe = torch.empty(n, dtype=LOW_TORCH[mode], device=device)
+    check(lib().co2_synth(mode, seed, worker, 0, n, None, None, None, _ptr(xe), None,
+                          _stream(stream)))
+    return xe
+
+
 def synthetic_inner_step(params, *, lr: float, scale: float = 1.0, seed: int = 7, worker: int = 0,
                          step: int = 0, repeat: int = 1, stream=None):
     check(lib().co2_synthetic_inner_step(_dtype(params), params.numel(), _ptr(params), lr, scale,
