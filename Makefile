@@ -13,7 +13,7 @@ NCCL_HOME ?= $(shell python -c "import nvidia.nccl,os;print(nvidia.nccl.__path__
 NCCL_INC = $(if $(NCCL_HOME),-I$(NCCL_HOME)/include,)
 NCCL_LIB = $(if $(NCCL_HOME),-L$(NCCL_HOME)/lib -Xlinker -rpath -Xlinker $(NCCL_HOME)/lib -l:libnccl.so.2,-lnccl)
 LIB = paper_2401_16265_b200/libco2b200.so
-OBJS = build/outer_step.o build/capi.o build/engine.o
+OBJS = build/outer_step.o build/capi.o build/engine.o build/p2p.o
 
 all: $(LIB) oracle
 

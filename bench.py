@@ -186,6 +186,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="all-reduce transport at N > 1 (worker-local configs)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -215,8 +217,12 @@ def main():
         uid = obj[0]
     else:
         uid = bytes(128)
-    eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
-                               max_ctas=args.max_ctas)
+    transport = args.transport if world > 1 and not cfg.get("sharded") else "nccl"
+    if transport == "p2p":
+        eng = co2.CollectiveEngine(world, transport="p2p", rank=rank, max_ctas=args.max_ctas)
+    else:
+        eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
+                                   max_ctas=args.max_ctas)
 
     # --- worker state resident in HBM, synthetic inputs
     from paper_2401_16265_b200 import _lib as L
@@ -240,6 +246,8 @@ def main():
         init = co2.synth_params(mode, n, worker=rank)  # x_{0,tau}: the params the reduce sums
         w = co2.Worker(mode, n, init, keep_gap=False)
         del init
+        if transport == "p2p":
+            eng.register_worker(w)
         w.snapshot_start()
         w.snapshot_first()
         co2.co2_round([w], eng, hyper, tau)  # round 0: snapshots, launches the first reduce
@@ -335,7 +343,10 @@ def main():
                        "storage": cfg["storage"], "hyper": HYPER,
                        "parallelism": (f"dp{world} ghost-consistent, outer state sharded "
                                        "(NCCL reduce-scatter + all-gather)") if sharded else
-                       f"dp{world} (one CO2 worker per GPU, NCCL all-reduce)",
+                       (f"dp{world} (one CO2 worker per GPU, "
+                        + ("fixed-order NVLink P2P all-reduce)" if transport == "p2p"
+                           else "NCCL all-reduce)")),
+                       "transport": transport,
                        "l2": "inputs larger than L2 (no flush needed)",
                        "step": ("sharded co2_round: RS(x_{t,1}) + async RS(x_{t,tau}) + stale "
                                 "wait + fused ghost step on the shard + AG(x_{t+1,0})")

@@ -219,6 +219,25 @@ co2_status_t co2_nccl_unique_id(uint8_t id_out[CO2_NCCL_ID_BYTES]);
 co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO2_NCCL_ID_BYTES],
                                  int32_t rank, int32_t world, int32_t max_ctas);
 co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers);
+/* P2P transport: a deterministic fixed-order average
+ * over NVLink peer memory.  Rank r reduces slice r from every rank's buffer
+ * in ascending rank order, divides by G once (average(), param_ops.cpp:16-33)
+ * and stores the result into slice r of every rank's buffer, so the result
+ * is bitwise the reference's average for any G and the consumer uses
+ * xbar_divisor = 1.  Setup (collective, same order on every rank):
+ *   1. co2_aar_create_p2p;
+ *   2. export co2_aar_signal_buffer with co2_ipc_export, exchange the
+ *      handles (rank-indexed, world * CO2_IPC_HANDLE_BYTES), call
+ *      co2_aar_p2p_attach_signals;
+ *   3. for every buffer that will be reduced (e.g. both ping-pong params of
+ *      a worker): export, exchange, co2_aar_p2p_attach.
+ * `ctas` bounds the SMs the reduce occupies while it overlaps compute. */
+#define CO2_IPC_HANDLE_BYTES 64
+co2_status_t co2_ipc_export(const void* dev_ptr, uint8_t handle_out[CO2_IPC_HANDLE_BYTES]);
+co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_t world, int32_t ctas);
+void* co2_aar_signal_buffer(co2_aar_t* engine);
+co2_status_t co2_aar_p2p_attach_signals(co2_aar_t* engine, const uint8_t* handles);
+co2_status_t co2_aar_p2p_attach(co2_aar_t* engine, const void* local_buf, const uint8_t* handles);
 co2_status_t co2_aar_destroy(co2_aar_t* engine);
 int32_t co2_aar_world(const co2_aar_t* engine);
 /* launch_all_reduce (collective.cpp:31-58).  NCCL: bufs[0] is reduced in
@@ -263,7 +282,8 @@ enum {
   CO2_BUF_PREV_X1 = 4, /* low dtype */
   CO2_BUF_MOMENTUM = 5,/* state dtype */
   CO2_BUF_GAP = 6,     /* state dtype */
-  CO2_BUF_XBAR = 7     /* last consumed all-reduce result (low dtype; NCCL: the sum) */
+  CO2_BUF_XBAR = 7,    /* last consumed all-reduce result (low dtype; NCCL: the sum) */
+  CO2_BUF_PARAMS_ALT = 8 /* the other ping-pong params buffer (P2P registration) */
 };
 /* init_params: device buffer in the low dtype (or NULL for zeros). */
 co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, int64_t n,

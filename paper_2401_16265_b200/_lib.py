@@ -18,7 +18,8 @@ DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
 FLAG_GAP_NONFINITE, FLAG_GAP_BELOW_ONE, FLAG_M_NONFINITE = 1, 2, 4
 FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
 BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
-BUF_MOMENTUM, BUF_GAP, BUF_XBAR = 5, 6, 7
+BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT = 5, 6, 7, 8
+IPC_HANDLE_BYTES = 64
 NCCL_ID_BYTES = 128
 
 
@@ -98,6 +99,11 @@ SIGNATURES = {
     "co2_nccl_unique_id": (ST, [C.POINTER(C.c_uint8)]),
     "co2_aar_create_nccl": (ST, [C.POINTER(P), C.POINTER(C.c_uint8), I32, I32, I32]),
     "co2_aar_create_local": (ST, [C.POINTER(P), I32]),
+    "co2_ipc_export": (ST, [P, C.POINTER(C.c_uint8)]),
+    "co2_aar_create_p2p": (ST, [C.POINTER(P), I32, I32, I32]),
+    "co2_aar_signal_buffer": (P, [P]),
+    "co2_aar_p2p_attach_signals": (ST, [P, C.POINTER(C.c_uint8)]),
+    "co2_aar_p2p_attach": (ST, [P, P, C.POINTER(C.c_uint8)]),
     "co2_aar_destroy": (ST, [P]),
     "co2_aar_world": (I32, [P]),
     "co2_aar_launch": (ST, [P, I32, C.POINTER(P), P, I64, P, C.POINTER(U64)]),

@@ -328,12 +328,16 @@ class CollectiveEngine:
     """One-step-stale all-reduce (proj/include/co2sim/collective.hpp:54-93).
 
     transport "local": G simulated workers on this GPU, fixed-order average.
-    transport "nccl":  one rank per GPU; in-place ncclAllReduce(sum)."""
+    transport "nccl":  one rank per GPU; in-place ncclAllReduce(sum).
+    transport "p2p":   one rank per GPU; deterministic fixed-order average over
+                       NVLink peer memory (CUDA IPC).  Needs an initialized
+                       torch.distributed group to exchange IPC handles."""
 
     def __init__(self, workers: int = 1, *, transport: str = "local", rank: int = 0,
                  nccl_id: bytes | None = None, max_ctas: int = 0):
         self.handle = C.c_void_p()
         self.transport = transport
+        self.rank = rank
         if transport == "local":
             check(lib().co2_aar_create_local(C.byref(self.handle), workers))
         elif transport == "nccl":
@@ -341,9 +345,36 @@ class CollectiveEngine:
                 raise ValidationError("nccl transport needs the rank-0 unique id")
             uid = (C.c_uint8 * L.NCCL_ID_BYTES)(*nccl_id)
             check(lib().co2_aar_create_nccl(C.byref(self.handle), uid, rank, workers, max_ctas))
+        elif transport == "p2p":
+            check(lib().co2_aar_create_p2p(C.byref(self.handle), rank, workers, max_ctas))
+            self.workers = workers
+            sig = lib().co2_aar_signal_buffer(self.handle)
+            check(lib().co2_aar_p2p_attach_signals(self.handle, self._exchange(sig)))
         else:
             raise ValidationError(f"unknown transport {transport}")
         self.workers = workers
+
+    def _exchange(self, ptr: int):
+        """Export `ptr` and all-gather every rank's IPC handle (rank order)."""
+        h = (C.c_uint8 * L.IPC_HANDLE_BYTES)()
+        check(lib().co2_ipc_export(ptr, h))
+        if self.workers == 1:
+            return h
+        import torch.distributed as dist
+        got = [None] * self.workers
+        dist.all_gather_object(got, bytes(h))
+        flat = b"".join(got)
+        return (C.c_uint8 * len(flat))(*flat)
+
+    def register(self, ptr: int) -> None:
+        """P2P: make a device buffer (the same logical buffer on every rank)
+        reducible; collective over the group."""
+        check(lib().co2_aar_p2p_attach(self.handle, ptr, self._exchange(ptr)))
+
+    def register_worker(self, worker: "Worker") -> None:
+        """P2P: register both ping-pong params buffers of a worker."""
+        for which in (L.BUF_PARAMS, L.BUF_PARAMS_ALT):
+            self.register(lib().co2_worker_buffer(worker.handle, which))
 
     @staticmethod
     def unique_id() -> bytes:

@@ -35,13 +35,21 @@ static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
 namespace {
 
-enum { T_NCCL = 0, T_LOCAL = 1 };
+enum { T_NCCL = 0, T_LOCAL = 1, T_P2P = 2 };
 
 struct Handle {
   cudaEvent_t start = nullptr, done = nullptr, wait_begin = nullptr, wait_end = nullptr;
   bool consumed = false, polled = false, last_poll = false, completion_logged = false;
   bool waited = false;
   co2_diag_t* diag = nullptr;  // LOCAL: pinned copy of the average's flags
+  uint32_t* p2p_error = nullptr;  // P2P: pinned copy of the signal area's error word
+};
+
+// A buffer registered with the P2P transport: the same logical buffer on
+// every rank (rank-indexed device pointers, peers opened via CUDA IPC).
+struct P2PBuffer {
+  const void* local = nullptr;
+  std::vector<void*> ptrs;
 };
 
 ncclDataType_t nccl_dtype(co2_dtype_t d) {
@@ -60,6 +68,13 @@ struct co2_aar {
   void* ws = nullptr;
   int live = 0;
   std::vector<Handle> handles;
+  // P2P transport
+  int ctas = 0;
+  uint32_t p2p_epoch = 0;
+  void* signals = nullptr;        // this rank's signal area (cudaMalloc, IPC-exported)
+  std::vector<void*> peer_signals;  // rank-indexed (opened IPC pointers; own = signals)
+  std::vector<P2PBuffer> p2p_bufs;
+  std::vector<void*> opened;      // IPC pointers to close
 };
 
 static co2_status_t engine_common_init(co2_aar* e) {
@@ -110,6 +125,76 @@ extern "C" co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO
   return CO2_OK;
 }
 
+extern "C" co2_status_t co2_ipc_export(const void* dev_ptr, uint8_t handle_out[CO2_IPC_HANDLE_BYTES]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == CO2_IPC_HANDLE_BYTES, "IPC handle size");
+  if (!dev_ptr) return fail(CO2_ERR_VALIDATION, "ipc export: null pointer");
+  cudaIpcMemHandle_t h;
+  CO2_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  memcpy(handle_out, &h, sizeof h);
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_t world,
+                                           int32_t ctas) {
+  if (world < 1 || world > 8 || rank < 0 || rank >= world)
+    return fail(CO2_ERR_VALIDATION, "aar: bad rank %d / world %d (p2p supports <= 8)", rank,
+                world);
+  co2_aar* e = new co2_aar();
+  e->transport = T_P2P;
+  e->rank = rank;
+  e->world = world;
+  e->workers = world;
+  e->ctas = ctas > 0 ? ctas : 64;
+  co2_status_t s = engine_common_init(e);
+  if (s == CO2_OK) {
+    cudaError_t ce = cudaMalloc(&e->signals, p2p_signal_bytes());
+    if (ce == cudaSuccess) ce = cudaMemset(e->signals, 0, p2p_signal_bytes());
+    if (ce != cudaSuccess) s = cuda_fail(ce, "cudaMalloc(signals)");
+  }
+  if (s != CO2_OK) {
+    co2_aar_destroy(e);
+    return s;
+  }
+  *out = e;
+  return CO2_OK;
+}
+
+extern "C" void* co2_aar_signal_buffer(co2_aar_t* e) { return e ? e->signals : nullptr; }
+
+static co2_status_t open_peers(co2_aar* e, const void* local, const uint8_t* handles,
+                               std::vector<void*>* out) {
+  out->assign(e->world, nullptr);
+  for (int p = 0; p < e->world; ++p) {
+    if (p == e->rank) {
+      (*out)[p] = const_cast<void*>(local);
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + (size_t)p * CO2_IPC_HANDLE_BYTES, sizeof h);
+    void* ptr = nullptr;
+    CO2_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    e->opened.push_back(ptr);
+    (*out)[p] = ptr;
+  }
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_p2p_attach_signals(co2_aar_t* e, const uint8_t* handles) {
+  if (!e || e->transport != T_P2P) return fail(CO2_ERR_VALIDATION, "attach: not a P2P engine");
+  return open_peers(e, e->signals, handles, &e->peer_signals);
+}
+
+extern "C" co2_status_t co2_aar_p2p_attach(co2_aar_t* e, const void* local,
+                                           const uint8_t* handles) {
+  if (!e || e->transport != T_P2P) return fail(CO2_ERR_VALIDATION, "attach: not a P2P engine");
+  if (!local) return fail(CO2_ERR_VALIDATION, "attach: null buffer");
+  P2PBuffer b;
+  b.local = local;
+  CO2_TRY(open_peers(e, local, handles, &b.ptrs));
+  e->p2p_bufs.push_back(b);
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers) {
   if (workers < 1 || workers > 64)
     return fail(CO2_ERR_VALIDATION, "aar: local workers must lie in [1, 64]");
@@ -132,10 +217,13 @@ extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
     for (cudaEvent_t ev : {h.start, h.done, h.wait_begin, h.wait_end})
       if (ev) cudaEventDestroy(ev);
     if (h.diag) cudaFreeHost(h.diag);
+    if (h.p2p_error) cudaFreeHost(h.p2p_error);
   }
   if (e->comm2) ncclCommDestroy(e->comm2);
   if (e->comm) ncclCommDestroy(e->comm);
   if (e->ws) cudaFree(e->ws);
+  for (void* p : e->opened) cudaIpcCloseMemHandle(p);
+  if (e->signals) cudaFree(e->signals);
   if (e->epoch) cudaEventDestroy(e->epoch);
   if (e->comm_stream) cudaStreamDestroy(e->comm_stream);
   delete e;
@@ -182,6 +270,25 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     else if (shard > 0)
       CO2_CUDA(cudaMemcpyAsync(out, bufs[0], dtype_bytes(dt) * (size_t)shard,
                                cudaMemcpyDeviceToDevice, e->comm_stream));
+  } else if (e->transport == T_P2P) {
+    if (out && out != bufs[0])
+      return fail(CO2_ERR_VALIDATION, "launch_all_reduce: P2P transport reduces in place");
+    const P2PBuffer* pb = nullptr;
+    for (const P2PBuffer& b : e->p2p_bufs)
+      if (b.local == bufs[0]) pb = &b;
+    if (!pb) return fail(CO2_ERR_VALIDATION, "launch_all_reduce: buffer not registered for P2P");
+    if (e->world > 1 && (int)e->peer_signals.size() != e->world)
+      return fail(CO2_ERR_VALIDATION, "launch_all_reduce: P2P signals not attached");
+    CO2_CUDA(cudaMallocHost(&h.p2p_error, sizeof(uint32_t)));
+    *h.p2p_error = 0;
+    if (e->world > 1 && n > 0) {
+      e->p2p_epoch += 1;
+      CO2_TRY(p2p_average_launch(dt, pb->ptrs.data(), e->peer_signals.data(), e->world, e->rank,
+                                 n, e->p2p_epoch, e->ctas, e->comm_stream));
+      // the kernel records a timed-out barrier in the signal area's error word
+      CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + 36, 4,
+                               cudaMemcpyDeviceToHost, e->comm_stream));
+    }
   } else if (e->transport == T_NCCL) {
     if (out && out != bufs[0])
       return fail(CO2_ERR_VALIDATION, "launch_all_reduce: NCCL transport reduces in place");
@@ -252,6 +359,9 @@ extern "C" co2_status_t co2_aar_stall(co2_aar_t* e, uint64_t handle, double* sta
     *comm = ms * 1e-3;
   }
   if (h->diag && h->diag->flags) return co2_diag_status(h->diag);
+  if (h->p2p_error && *h->p2p_error)
+    return fail(CO2_ERR_CUDA, "p2p all-reduce: cross-GPU barrier timed out (code %u)",
+                *h->p2p_error);
   return CO2_OK;
 }
 
@@ -448,6 +558,7 @@ extern "C" void* co2_worker_buffer(co2_worker_t* w, int32_t which) {
     case CO2_BUF_MOMENTUM: return w->m;
     case CO2_BUF_GAP: return w->gap;
     case CO2_BUF_XBAR: return w->xbar;
+    case CO2_BUF_PARAMS_ALT: return w->params[1 - w->cur];
   }
   return nullptr;
 }
@@ -622,7 +733,9 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
   CO2_TRY(co2_aar_wait(e, prev, stream));
   const int t = w0->t;
   void* xbar = local ? w0->avg[(t - 1) % 2] : ws[0]->params[1 - ws[0]->cur];
-  const int32_t divisor = local ? 1 : e->world;
+  // NCCL delivers the worker sum (divided once in the step); LOCAL and P2P
+  // deliver the fixed-order average itself.
+  const int32_t divisor = (local || e->transport == T_P2P) ? 1 : e->world;
 
   if (hyper->ghost_consistent && g > 1) {
     // :161-184 -- one shared state driven by the averaged snapshots.

@@ -1,0 +1,216 @@
+// Deterministic fixed-order all-reduce over NVLink peer memory (SURVEY.md
+// 8f item 1): the one-step-stale average of x_{t,tau} computed exactly as the
+// reference's average() (proj/src/param_ops.cpp:16-33) -- contributions summed
+// in ascending worker order, one division by G -- so the result is bitwise
+// the oracle's for ANY worker count, which NCCL's ring/tree order is not.
+//
+// Rank r owns slice r of the buffer.  Each CTA grid-strides over slice r in
+// 16-byte vectors: it loads the slice from every rank's buffer (peer pointers
+// opened with CUDA IPC, loads over NVLink 5 / NVSwitch), accumulates in the
+// compute type in rank order, divides once, and stores the rounded average
+// into slice r of EVERY rank's buffer (a fused all-gather by P2P stores).
+// Per GPU that moves S/G*(G-1) bytes in and out over NVLink and ~2S bytes of
+// HBM (own slice read + peer reads served, own write + peer writes received)
+// -- half of a ring all-reduce's HBM traffic.
+//
+// Cross-GPU ordering uses flag words in IPC-shared signal memory:
+//   entry  : every CTA publishes ready[rank] = epoch in each peer's signal
+//            area (release, system scope) and waits for all ready[p] >= epoch;
+//   exit   : every CTA adds 1 to done in each peer's area after its stores
+//            (release) and waits until its own done reaches epoch*G*grid.
+// All spins are bounded (~4 s): on timeout the kernel records a flag and
+// exits instead of hanging the GPU.
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace co2 {
+namespace {
+
+struct bf16raw {
+  uint16_t b;
+};
+
+__device__ __forceinline__ float ld_c(const bf16raw* p) {
+  return __uint_as_float(((uint32_t)p->b) << 16);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int kMaxRanks = 8;
+constexpr int kP2PThreads = 512;
+
+// Signal area layout (per rank, 256 B): ready[kMaxRanks], done, error.
+struct Signals {
+  uint32_t ready[kMaxRanks];
+  uint32_t done;
+  uint32_t error;
+  uint32_t pad[54];
+};
+
+struct P2PArgs {
+  void* bufs[kMaxRanks];      // rank-indexed pointers to the same logical buffer
+  Signals* sig[kMaxRanks];    // rank-indexed signal areas (sig[rank] is local)
+  int64_t n;                  // elements in the buffer
+  int64_t shard;              // elements per slice (multiple of the vector width)
+  int world, rank;
+  uint32_t epoch;             // 1, 2, ... (same sequence on every rank)
+};
+
+__device__ bool spin_until(const uint32_t* p, uint32_t target, long long budget) {
+  long long t0 = clock64();
+  while (ld_acquire_sys(p) < target) {
+    if (clock64() - t0 > budget) return false;
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// TL storage, TC compute, V elements per 16-byte vector.
+template <typename TL, typename TC, int V>
+__global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs a) {
+  const long long kBudget = 4000000000LL;  // ~2 s at 1.9 GHz
+  Signals* mine = a.sig[a.rank];
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    for (int p = 0; p < a.world; ++p) st_release_sys(&a.sig[p]->ready[a.rank], a.epoch);
+    bool ok = true;
+    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch, kBudget);
+    if (!ok) mine->error = 1;
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (s_ok) {
+    const int64_t lo = (int64_t)a.rank * a.shard;
+    int64_t hi = lo + a.shard;
+    if (hi > a.n) hi = a.n;
+    const TC g = (TC)a.world;
+    const int64_t nvec = hi > lo ? (hi - lo) / V : 0;
+    const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
+    for (int64_t i = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x; i < nvec; i += stride) {
+      const int64_t e = lo + i * V;
+      uint4 raw[kMaxRanks];
+#pragma unroll
+      for (int p = 0; p < kMaxRanks; ++p)
+        if (p < a.world) raw[p] = __ldcg(reinterpret_cast<const uint4*>(static_cast<const TL*>(a.bufs[p]) + e));
+      TC acc[V];
+      {
+        const TL* v0 = reinterpret_cast<const TL*>(&raw[0]);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          if constexpr (sizeof(TL) == 2) acc[k] = ld_c(reinterpret_cast<const bf16raw*>(v0 + k));
+          else acc[k] = (TC)v0[k];
+        }
+      }
+#pragma unroll
+      for (int p = 1; p < kMaxRanks; ++p) {
+        if (p < a.world) {
+          const TL* vp = reinterpret_cast<const TL*>(&raw[p]);
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            TC x;
+            if constexpr (sizeof(TL) == 2) x = ld_c(reinterpret_cast<const bf16raw*>(vp + k));
+            else x = (TC)vp[k];
+            acc[k] = acc[k] + x;  // ascending worker order, param_ops.cpp:26-28
+          }
+        }
+      }
+      uint4 out;
+      TL* o = reinterpret_cast<TL*>(&out);
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        TC r = acc[k] / g;  // one division, param_ops.cpp:30
+        if constexpr (sizeof(TL) == 2) {
+          __nv_bfloat16 h = __float2bfloat16_rn((float)r);
+          reinterpret_cast<uint16_t*>(o)[k] = __bfloat16_as_ushort(h);
+        } else {
+          o[k] = (TL)r;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < kMaxRanks; ++p)
+        if (p < a.world) __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.bufs[p]) + e), out);
+    }
+    // scalar tail of the last slice (n not a multiple of V)
+    if (blockIdx.x == 0) {
+      for (int64_t j = lo + nvec * V + threadIdx.x; j < hi; j += kP2PThreads) {
+        TC acc;
+        if constexpr (sizeof(TL) == 2)
+          acc = ld_c(static_cast<const bf16raw*>(a.bufs[0]) + j);
+        else
+          acc = (TC)__ldcg(static_cast<const TL*>(a.bufs[0]) + j);
+        for (int p = 1; p < a.world; ++p) {
+          TC x;
+          if constexpr (sizeof(TL) == 2)
+            x = ld_c(static_cast<const bf16raw*>(a.bufs[p]) + j);
+          else
+            x = (TC)__ldcg(static_cast<const TL*>(a.bufs[p]) + j);
+          acc = acc + x;
+        }
+        TC r = acc / g;
+        for (int p = 0; p < a.world; ++p) {
+          if constexpr (sizeof(TL) == 2) {
+            __nv_bfloat16 h = __float2bfloat16_rn((float)r);
+            static_cast<bf16raw*>(a.bufs[p])[j].b = __bfloat16_as_ushort(h);
+          } else {
+            static_cast<TL*>(a.bufs[p])[j] = (TL)r;
+          }
+        }
+      }
+    }
+  }
+  // Exit barrier: our slice is in every peer's buffer before any rank's
+  // consumer may read the result.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
+    const uint32_t target = a.epoch * (uint32_t)a.world * gridDim.x;
+    if (!spin_until(&mine->done, target, kBudget)) mine->error = 2;
+  }
+}
+
+}  // namespace
+
+co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* sigs, int world,
+                                int rank, int64_t n, uint32_t epoch, int ctas, cudaStream_t s) {
+  if (world < 1 || world > kMaxRanks)
+    return fail(CO2_ERR_VALIDATION, "p2p: world must lie in [1, %d]", kMaxRanks);
+  P2PArgs a{};
+  for (int p = 0; p < world; ++p) {
+    a.bufs[p] = bufs[p];
+    a.sig[p] = static_cast<Signals*>(sigs[p]);
+  }
+  a.n = n;
+  a.world = world;
+  a.rank = rank;
+  a.epoch = epoch;
+  const int V = dt == CO2_DTYPE_F64 ? 2 : (dt == CO2_DTYPE_F32 ? 4 : 8);
+  int64_t per = (n + world - 1) / world;
+  per = (per + V - 1) / V * V;
+  a.shard = per;
+  if (ctas < 1) ctas = 1;
+  if (ctas > sm_count()) ctas = sm_count();  // all CTAs co-resident (they spin)
+  switch (dt) {
+    case CO2_DTYPE_F64: p2p_average_kernel<double, double, 2><<<ctas, kP2PThreads, 0, s>>>(a); break;
+    case CO2_DTYPE_F32: p2p_average_kernel<float, float, 4><<<ctas, kP2PThreads, 0, s>>>(a); break;
+    default: p2p_average_kernel<bf16raw, float, 8><<<ctas, kP2PThreads, 0, s>>>(a); break;
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+size_t p2p_signal_bytes() { return sizeof(Signals); }
+
+}  // namespace co2

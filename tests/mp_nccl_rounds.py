@@ -43,11 +43,17 @@ def main():
     dist.init_process_group("gloo")
     mode = int(os.environ.get("CO2_TEST_MODE", "1"))
     n, tau, rounds = 1 << 20, 4, 4
-    uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
-    eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid)
+    transport = os.environ.get("CO2_TEST_TRANSPORT", "nccl")
+    if transport == "p2p":
+        eng = co2.CollectiveEngine(world, transport="p2p", rank=rank)
+    else:
+        uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
+        eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid)
     hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
     init = co2.synth(mode, n, worker=rank)[3]
     w = co2.Worker(mode, n, init)
+    if transport == "p2p":
+        eng.register_worker(w)
     ok, worst = True, None
     if rank == 0:
         from oracle import oracle as O
@@ -81,7 +87,7 @@ def main():
             stalls.append(e["stall"])
     if rank == 0:
         print(json.dumps({"ok": ok, "first_mismatch": worst, "world": world, "mode": mode,
-                          "waits": len(stalls)}), flush=True)
+                          "transport": transport, "waits": len(stalls)}), flush=True)
     eng.close()
     dist.barrier()
     dist.destroy_process_group()

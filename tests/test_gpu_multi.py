@@ -24,9 +24,16 @@ def _port():
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("mode", [1, 2])
-def test_nccl_rounds_bitwise_world2(mode):
-    env = dict(os.environ, CO2_TEST_MODE=str(mode))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+@pytest.mark.parametrize("transport,world", [("nccl", 2), ("p2p", 2), ("p2p", 4)])
+def test_multi_rank_rounds_bitwise(mode, transport, world):
+    """Worker-local co2_round across ranks, bitwise against the oracle.  NCCL's
+    sum is order-free only for G = 2; the P2P transport's fixed-order average
+    is bitwise the reference's average() for any G."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT=transport)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "mp_nccl_rounds.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
