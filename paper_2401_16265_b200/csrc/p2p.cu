@@ -78,7 +78,7 @@ __device__ bool spin_until(const uint32_t* p, uint32_t target, long long budget)
 }
 
 // TL storage, TC compute, V elements per 16-byte vector.
-template <typename TL, typename TC, int V>
+template <typename TL, typename TC, int V, int R, int U>
 __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs a) {
   const long long kBudget = 4000000000LL;  // ~2 s at 1.9 GHz
   Signals* mine = a.sig[a.rank];
@@ -98,12 +98,9 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs 
     const TC g = (TC)a.world;
     const int64_t nvec = hi > lo ? (hi - lo) / V : 0;
     const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
-    for (int64_t i = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x; i < nvec; i += stride) {
-      const int64_t e = lo + i * V;
-      uint4 raw[kMaxRanks];
-#pragma unroll
-      for (int p = 0; p < kMaxRanks; ++p)
-        if (p < a.world) raw[p] = __ldcg(reinterpret_cast<const uint4*>(static_cast<const TL*>(a.bufs[p]) + e));
+    // U vectors per thread in flight, each gathered from every rank: the
+    // remote (NVLink) loads are issued back to back before any arithmetic.
+    auto reduce_store = [&](const uint4 (&raw)[R], int64_t e) {
       TC acc[V];
       {
         const TL* v0 = reinterpret_cast<const TL*>(&raw[0]);
@@ -114,7 +111,7 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs 
         }
       }
 #pragma unroll
-      for (int p = 1; p < kMaxRanks; ++p) {
+      for (int p = 1; p < R; ++p) {
         if (p < a.world) {
           const TL* vp = reinterpret_cast<const TL*>(&raw[p]);
 #pragma unroll
@@ -139,8 +136,29 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs 
         }
       }
 #pragma unroll
-      for (int p = 0; p < kMaxRanks; ++p)
+      for (int p = 0; p < R; ++p)
         if (p < a.world) __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.bufs[p]) + e), out);
+    };
+    int64_t i = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x;
+    for (; i + (int64_t)(U - 1) * stride < nvec; i += (int64_t)U * stride) {
+      uint4 raw[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int p = 0; p < R; ++p)
+          if (p < a.world)
+            raw[u][p] = __ldcg(reinterpret_cast<const uint4*>(
+                static_cast<const TL*>(a.bufs[p]) + lo + (i + (int64_t)u * stride) * V));
+#pragma unroll
+      for (int u = 0; u < U; ++u) reduce_store(raw[u], lo + (i + (int64_t)u * stride) * V);
+    }
+    for (; i < nvec; i += stride) {
+      uint4 raw[R];
+#pragma unroll
+      for (int p = 0; p < R; ++p)
+        if (p < a.world)
+          raw[p] = __ldcg(reinterpret_cast<const uint4*>(static_cast<const TL*>(a.bufs[p]) + lo + i * V));
+      reduce_store(raw, lo + i * V);
     }
     // scalar tail of the last slice (n not a multiple of V)
     if (blockIdx.x == 0) {
@@ -202,11 +220,21 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
   a.shard = per;
   if (ctas < 1) ctas = 1;
   if (ctas > sm_count()) ctas = sm_count();  // all CTAs co-resident (they spin)
+  // R = rank capacity of the instantiation, U = vectors in flight per thread
+  // (fewer ranks -> more vectors, keeping ~R*U*16 B of loads per thread).
+#define CO2_P2P_LAUNCH(TL, TC, V)                                                        \
+  if (world <= 2)                                                                       \
+    p2p_average_kernel<TL, TC, V, 2, 4><<<ctas, kP2PThreads, 0, s>>>(a);                \
+  else if (world <= 4)                                                                  \
+    p2p_average_kernel<TL, TC, V, 4, 2><<<ctas, kP2PThreads, 0, s>>>(a);                \
+  else                                                                                  \
+    p2p_average_kernel<TL, TC, V, 8, 1><<<ctas, kP2PThreads, 0, s>>>(a);
   switch (dt) {
-    case CO2_DTYPE_F64: p2p_average_kernel<double, double, 2><<<ctas, kP2PThreads, 0, s>>>(a); break;
-    case CO2_DTYPE_F32: p2p_average_kernel<float, float, 4><<<ctas, kP2PThreads, 0, s>>>(a); break;
-    default: p2p_average_kernel<bf16raw, float, 8><<<ctas, kP2PThreads, 0, s>>>(a); break;
+    case CO2_DTYPE_F64: CO2_P2P_LAUNCH(double, double, 2) break;
+    case CO2_DTYPE_F32: CO2_P2P_LAUNCH(float, float, 4) break;
+    default: CO2_P2P_LAUNCH(bf16raw, float, 8) break;
   }
+#undef CO2_P2P_LAUNCH
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }
