@@ -186,7 +186,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--max-ctas", type=int, default=0)
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
                     help="all-reduce transport at N > 1 (worker-local configs)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -218,9 +218,22 @@ def main():
     else:
         uid = bytes(128)
     transport = args.transport if world > 1 and not cfg.get("sharded") else "nccl"
+    transport_note = None
+    eng = None
     if transport == "p2p":
-        eng = co2.CollectiveEngine(world, transport="p2p", rank=rank, max_ctas=args.max_ctas)
-    else:
+        try:
+            eng = co2.CollectiveEngine(world, transport="p2p", rank=rank, max_ctas=args.max_ctas)
+        except Exception as exc:  # IPC unavailable: report it and use NCCL instead
+            transport_note = f"p2p setup failed ({exc}); NCCL used"
+            transport = "nccl"
+        ok = torch.tensor([1 if eng is not None else 0], device="cuda")
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0 and eng is not None:
+            eng.close()
+            eng, transport = None, "nccl"
+            transport_note = transport_note or "p2p setup failed on a peer; NCCL used"
+    if eng is None:
         eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
                                    max_ctas=args.max_ctas)
 
@@ -346,7 +359,7 @@ def main():
                        (f"dp{world} (one CO2 worker per GPU, "
                         + ("fixed-order NVLink P2P all-reduce)" if transport == "p2p"
                            else "NCCL all-reduce)")),
-                       "transport": transport,
+                       "transport": transport, "transport_note": transport_note,
                        "l2": "inputs larger than L2 (no flush needed)",
                        "step": ("sharded co2_round: RS(x_{t,1}) + async RS(x_{t,tau}) + stale "
                                 "wait + fused ghost step on the shard + AG(x_{t+1,0})")

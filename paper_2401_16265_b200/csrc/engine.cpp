@@ -144,7 +144,9 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
   e->rank = rank;
   e->world = world;
   e->workers = world;
-  e->ctas = ctas > 0 ? ctas : 64;
+  // 96 CTAs measured best while the reduce shares HBM and SMs with the fused
+  // outer step (tools/aar_bench.py, bench.py --max-ctas sweep at N = 2, 4).
+  e->ctas = ctas > 0 ? ctas : 96;
   co2_status_t s = engine_common_init(e);
   if (s == CO2_OK) {
     cudaError_t ce = cudaMalloc(&e->signals, p2p_signal_bytes());
