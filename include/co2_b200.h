@@ -283,7 +283,8 @@ enum {
   CO2_BUF_MOMENTUM = 5,/* state dtype */
   CO2_BUF_GAP = 6,     /* state dtype */
   CO2_BUF_XBAR = 7,    /* last consumed all-reduce result (low dtype; NCCL: the sum) */
-  CO2_BUF_PARAMS_ALT = 8 /* the other ping-pong params buffer (P2P registration) */
+  CO2_BUF_PARAMS_ALT = 8, /* the other ping-pong params buffer (P2P registration) */
+  CO2_BUF_XFIRST_ALT = 9  /* sharded + P2P: the other x_{t,1} snapshot buffer */
 };
 /* init_params: device buffer in the low dtype (or NULL for zeros). */
 co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, int64_t n,

@@ -18,7 +18,7 @@ DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
 FLAG_GAP_NONFINITE, FLAG_GAP_BELOW_ONE, FLAG_M_NONFINITE = 1, 2, 4
 FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
 BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
-BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT = 5, 6, 7, 8
+BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT, BUF_XFIRST_ALT = 5, 6, 7, 8, 9
 IPC_HANDLE_BYTES = 64
 NCCL_ID_BYTES = 128
 

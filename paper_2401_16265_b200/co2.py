@@ -551,6 +551,9 @@ class ShardedWorker:
         off, ln = C.c_int64(), C.c_int64()
         self.shard = lib().co2_sharded_shard(self.handle, C.byref(off), C.byref(ln))
         self.offset, self.length = off.value, ln.value
+        if engine.transport == "p2p":  # peers read / write these over NVLink
+            for which in (L.BUF_PARAMS, L.BUF_PARAMS_ALT, L.BUF_XFIRST, L.BUF_XFIRST_ALT):
+                engine.register(lib().co2_sharded_buffer(self.handle, which))
 
     def close(self):
         if self.handle:

@@ -310,6 +310,51 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
   return CO2_OK;
 }
 
+static const P2PBuffer* find_p2p(const co2_aar* e, const void* local) {
+  for (const P2PBuffer& b : e->p2p_bufs)
+    if (b.local == local) return &b;
+  return nullptr;
+}
+
+// P2P sharded layout: one handle covering the deterministic slice averages of
+// x_{t,tau} (src0) and x_{t,1} (src1) into local slices dst0 / dst1.
+static co2_status_t launch_slice(co2_aar* e, co2_dtype_t dt, const void* src0, const void* src1,
+                                 void* dst0, void* dst1, int64_t lo, int64_t len, void* producer,
+                                 uint64_t* handle_out) {
+  if (e->live >= 2)
+    return fail(CO2_ERR_VALIDATION,
+                "launch_all_reduce: overlap window exceeded, two reduces already live");
+  const P2PBuffer* b0 = find_p2p(e, src0);
+  const P2PBuffer* b1 = find_p2p(e, src1);
+  if (!b0 || !b1) return fail(CO2_ERR_VALIDATION, "slice reduce: buffer not registered for P2P");
+  if ((int)e->peer_signals.size() != e->world)
+    return fail(CO2_ERR_VALIDATION, "slice reduce: P2P signals not attached");
+  Handle h;
+  CO2_CUDA(cudaEventCreateWithFlags(&h.start, cudaEventDefault));
+  CO2_CUDA(cudaEventCreateWithFlags(&h.done, cudaEventDefault));
+  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_begin, cudaEventDefault));
+  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_end, cudaEventDefault));
+  cudaEvent_t fence;
+  CO2_CUDA(cudaEventCreateWithFlags(&fence, cudaEventDisableTiming));
+  CO2_CUDA(cudaEventRecord(fence, S(producer)));
+  CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, fence, 0));
+  CO2_CUDA(cudaEventDestroy(fence));
+  CO2_CUDA(cudaEventRecord(h.start, e->comm_stream));
+  CO2_CUDA(cudaMallocHost(&h.p2p_error, sizeof(uint32_t)));
+  *h.p2p_error = 0;
+  e->p2p_epoch += 1;
+  CO2_TRY(p2p_slice_average_launch(dt, 2, b0->ptrs.data(), b1->ptrs.data(), dst0, dst1,
+                                   e->peer_signals.data(), e->world, e->rank, lo, len,
+                                   e->p2p_epoch, e->ctas, e->comm_stream));
+  CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + 36, 4,
+                           cudaMemcpyDeviceToHost, e->comm_stream));
+  CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
+  e->handles.push_back(h);
+  e->live += 1;
+  *handle_out = e->handles.size() - 1;
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_aar_launch(co2_aar_t* e, co2_dtype_t dt, const void* const* bufs,
                                        void* out, int64_t n, void* producer, uint64_t* handle_out) {
   return launch_impl(e, 0, dt, bufs, out, n, producer, handle_out);
@@ -841,6 +886,14 @@ struct co2_sharded {
   uint64_t pending = 0;
   std::vector<cudaEvent_t> tev;
   int64_t tev_recorded = 0, tev_read = 0;
+  // P2P transport: fixed-order slice averages (p1sum / xsum then hold the
+  // averages, divisor 1), ping-pong x_{t,1} snapshots read asynchronously,
+  // and the fused step's all-gather epoch.
+  bool p2p = false;
+  void* xfirst2 = nullptr;
+  uint32_t exit_epoch = 0;
+  void* xfirst_cur() { return (t % 2 == 0 || !p2p) ? xfirst : xfirst2; }
+  void* xfirst_alt() { return (t % 2 == 0) ? xfirst2 : xfirst; }
 };
 
 static co2_status_t ensure_comm2(co2_aar* e) {
@@ -879,8 +932,10 @@ extern "C" co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode,
   if (n < 0) return fail(CO2_ERR_VALIDATION, "sharded: negative dimension");
   if (mode != CO2_MODE_F64 && mode != CO2_MODE_F32 && mode != CO2_MODE_BF16_MIXED)
     return fail(CO2_ERR_VALIDATION, "sharded: unknown mode %d", (int)mode);
-  CO2_TRY(ensure_comm2(e));
+  const bool p2p = e->transport == T_P2P;
+  if (!p2p) CO2_TRY(ensure_comm2(e));
   co2_sharded* s = new co2_sharded();
+  s->p2p = p2p;
   s->mode = mode;
   s->n = n;
   s->world = e->world;
@@ -899,6 +954,7 @@ extern "C" co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode,
   A(&s->params[0], lb * s->n_pad);
   A(&s->params[1], lb * s->n_pad);
   A(&s->xfirst, lb * s->n_pad);
+  if (p2p) A(&s->xfirst2, lb * s->n_pad);
   A(&s->anchor, sb * per);
   A(&s->prev_x0, sb * per);
   A(&s->m, sb * per);
@@ -933,7 +989,7 @@ extern "C" co2_status_t co2_sharded_create(co2_sharded_t** out, co2_mode_t mode,
 
 extern "C" co2_status_t co2_sharded_destroy(co2_sharded_t* s) {
   if (!s) return CO2_OK;
-  for (void* p : {s->params[0], s->params[1], s->xfirst, s->anchor, s->prev_x0, s->m, s->gap,
+  for (void* p : {s->params[0], s->params[1], s->xfirst, s->xfirst2, s->anchor, s->prev_x0, s->m, s->gap,
                   s->p1sum[0], s->p1sum[1], s->xsum[0], s->xsum[1], s->ws})
     if (p) cudaFree(p);
   if (s->host_diag) cudaFreeHost(s->host_diag);
@@ -947,7 +1003,9 @@ extern "C" void* co2_sharded_buffer(co2_sharded_t* s, int32_t which) {
   if (!s) return nullptr;
   switch (which) {
     case CO2_BUF_PARAMS: return s->params[s->cur];
-    case CO2_BUF_XFIRST: return s->xfirst;
+    case CO2_BUF_XFIRST: return s->xfirst_cur();
+    case CO2_BUF_PARAMS_ALT: return s->params[1 - s->cur];
+    case CO2_BUF_XFIRST_ALT: return s->p2p ? s->xfirst_alt() : nullptr;
     case CO2_BUF_ANCHOR: return s->anchor;
     case CO2_BUF_PREV_X0: return s->prev_x0;
     case CO2_BUF_PREV_X1: return s->t > 0 ? s->p1sum[(s->t - 1) % 2] : nullptr;
@@ -982,7 +1040,7 @@ extern "C" co2_status_t co2_sharded_snapshot_start(co2_sharded_t* s, void* strea
 extern "C" co2_status_t co2_sharded_snapshot_first(co2_sharded_t* s, void* stream) {
   if (!s) return fail(CO2_ERR_VALIDATION, "sharded: null");
   if (s->n == 0) return CO2_OK;
-  CO2_CUDA(cudaMemcpyAsync(s->xfirst, s->params[s->cur], low_bytes(s->mode) * s->n,
+  CO2_CUDA(cudaMemcpyAsync(s->xfirst_cur(), s->params[s->cur], low_bytes(s->mode) * s->n,
                            cudaMemcpyDeviceToDevice, S(stream)));
   return CO2_OK;
 }
@@ -1032,7 +1090,7 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
   if (hyper->tau < 1) return fail(CO2_ERR_VALIDATION, "staleness_gap: tau must be >= 1");
   if (!hyper->ghost_consistent)
     return fail(CO2_ERR_VALIDATION, "sharded outer state requires ghost_consistent semantics");
-  if (e->transport != T_NCCL || e->world != s->world || e->rank != s->rank)
+  if (e->transport != (s->p2p ? T_P2P : T_NCCL) || e->world != s->world || e->rank != s->rank)
     return fail(CO2_ERR_VALIDATION, "sharded: engine does not match the shard layout");
   cudaStream_t st = S(stream);
   const co2_dtype_t ldt = low_dtype(s->mode);
@@ -1047,13 +1105,21 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
     CO2_CUDA(cudaMemcpyAsync(s->params[1 - s->cur], s->params[s->cur], lb * s->n_pad,
                              cudaMemcpyDeviceToDevice, st));
   }
-  // bar1 of this round: the worker sum of x_{t,1} for this shard (consumed
-  // as prev_x1 next round; the reference's average(firsts), :133-145/:167).
-  CO2_TRY(rs_blocking(e, ldt, s->xfirst, s->p1sum[t % 2], s->shard, st));
-  // The one-step-stale reduce of x_{t,tau}, scattered by shard (:120).
   uint64_t launched = 0;
-  const void* bufs[1] = {s->params[s->cur]};
-  CO2_TRY(launch_impl(e, 1, ldt, bufs, s->xsum[t % 2], s->n_pad, stream, &launched));
+  if (s->p2p) {
+    // bar1 (average of x_{t,1}) is first used as prev_x1 NEXT round, so it is
+    // reduced asynchronously together with the one-step-stale x_{t,tau}: one
+    // deterministic slice-average launch on the comm stream.
+    CO2_TRY(launch_slice(e, ldt, s->params[s->cur], s->xfirst_cur(), s->xsum[t % 2],
+                         s->p1sum[t % 2], s->offset, s->length, stream, &launched));
+  } else {
+    // bar1 of this round: the worker sum of x_{t,1} for this shard (consumed
+    // as prev_x1 next round; the reference's average(firsts), :133-145/:167).
+    CO2_TRY(rs_blocking(e, ldt, s->xfirst, s->p1sum[t % 2], s->shard, st));
+    // The one-step-stale reduce of x_{t,tau}, scattered by shard (:120).
+    const void* bufs[1] = {s->params[s->cur]};
+    CO2_TRY(launch_impl(e, 1, ldt, bufs, s->xsum[t % 2], s->n_pad, stream, &launched));
+  }
   if (t == 0) {
     // prev_x0 <- average(x_{0,0}) was computed by co2_sharded_snapshot_start.
     s->cur = 1 - s->cur;
@@ -1080,16 +1146,31 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
   const int64_t cap = (int64_t)s->tev.size() / 2;
   const int64_t slot = cap ? s->tev_recorded % cap : 0;
   if (cap) CO2_CUDA(cudaEventRecord(s->tev[2 * slot], st));
-  CO2_TRY(outer_step_ghost_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, s->world, xsum,
-                                s->world, ghost_copies, s->m, s->anchor, s->prev_x0, out_params,
-                                s->gap, hyper, s->ws, st));
+  if (s->p2p) {
+    // Fused step + all-gather: the x_{t+1,0} slice goes straight into every
+    // rank's next params buffer over NVLink; the kernel's exit barrier makes
+    // all slices visible before this stream's next work (the inner loop).
+    const P2PBuffer* pb = find_p2p(e, s->params[1 - s->cur]);
+    if (!pb) return fail(CO2_ERR_VALIDATION, "sharded: params not registered for P2P");
+    std::vector<void*> outs(s->world);
+    for (int p = 0; p < s->world; ++p) outs[p] = static_cast<char*>(pb->ptrs[p]) + lb * s->offset;
+    s->exit_epoch += 1;
+    CO2_TRY(outer_step_ghost_p2p_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, xsum,
+                                      ghost_copies, s->m, s->anchor, s->prev_x0, outs.data(),
+                                      e->peer_signals.data(), s->world, s->rank, s->exit_epoch,
+                                      s->gap, hyper, s->ws, st));
+  } else {
+    CO2_TRY(outer_step_ghost_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, s->world, xsum,
+                                  s->world, ghost_copies, s->m, s->anchor, s->prev_x0,
+                                  out_params, s->gap, hyper, s->ws, st));
+  }
   if (cap) {
     CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));
     s->tev_recorded += 1;
   }
   CO2_TRY(co2_diag_fetch_async(s->ws, s->host_diag, stream));
   // x_{t+1,0} for every worker: in-place all-gather of the updated shards.
-  CO2_TRY(ag_inplace(e, ldt, s->params[1 - s->cur], s->shard, st));
+  if (!s->p2p) CO2_TRY(ag_inplace(e, ldt, s->params[1 - s->cur], s->shard, st));
   s->xbar = xsum;
   s->cur = 1 - s->cur;
   s->pending = launched;

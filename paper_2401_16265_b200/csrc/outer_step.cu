@@ -26,6 +26,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "p2p_sync.cuh"
 
 namespace co2 {
 namespace {
@@ -145,7 +146,7 @@ struct AccT {
 };
 
 template <int NT>
-__device__ void block_finish(const Acc& a, void* ws) {
+__device__ void block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr) {
   // Warp level.
   double mg = a.min_gap, ms = a.max_step;
   unsigned long long cl = a.clipped, fl = a.floored;
@@ -178,7 +179,10 @@ __device__ void block_finish(const Acc& a, void* ws) {
       b.flags |= sh[w].flags;
     }
     parts[blockIdx.x] = b;
-    __threadfence();
+    if (px)
+      __threadfence_system();  // this CTA's peer stores before the ticket
+    else
+      __threadfence();
     unsigned int t = atomicAdd(&hdr->ticket, 1u);
     s_last = (t == gridDim.x - 1);
   }
@@ -227,6 +231,7 @@ __device__ void block_finish(const Acc& a, void* ws) {
     hdr->diag.pad = 0;
     hdr->ticket = 0;  // self-reset for the next launch on this workspace
     __threadfence();
+    if (px) p2p_exit_barrier(*px);
   }
 }
 
@@ -305,6 +310,9 @@ struct StepArgs {
   int ghost_g;      // x_t0 = average of ghost_g identical copies of x_t0
   int x_from_xbar;  // x_t0 = the consumed average itself (round 1)
   void* bar0_out;   // receives the x_t0 actually used (next prev_x0)
+  // P2P fused all-gather (P2POUT instantiations only)
+  void* out_peers[kMaxRanks];
+  P2PExit exit;
 };
 
 // average() of g identical copies (param_ops.cpp:26-30 with every
@@ -316,7 +324,7 @@ __device__ __forceinline__ TC ghost_avg(TC v, int g) {
   return s / (TC)g;
 }
 
-template <class M, int V, int U, int NT, int MINB, bool GHOST = false>
+template <class M, int V, int U, int NT, int MINB, bool GHOST = false, bool P2POUT = false>
 __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
@@ -397,6 +405,10 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
         if constexpr (GHOST) {
           if (B0) st_vec<TS, V>(B0 + e, b0);
         }
+        if constexpr (P2POUT) {  // fused all-gather: x_{t+1,0} into every rank's params
+          for (int p = 0; p < a.exit.world; ++p)
+            st_vec<TL, V>(static_cast<TL*>(a.out_peers[p]) + e, xl);
+        }
       }
     }
   };
@@ -432,9 +444,16 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
     Mm[t] = (TS)m;
     if (A) A[t] = (TS)xn;
     if (PR) PR[t] = Store<TL>::from(xn);
+    if constexpr (P2POUT) {
+      for (int p = 0; p < a.exit.world; ++p)
+        static_cast<TL*>(a.out_peers[p])[t] = Store<TL>::from(xn);
+    }
     if (G) G[t] = (TS)lam;
   }
-  block_finish<NT>(acc.widen(), a.ws);
+  if constexpr (P2POUT)
+    block_finish<NT>(acc.widen(), a.ws, &a.exit);
+  else
+    block_finish<NT>(acc.widen(), a.ws);
 }
 
 constexpr int kThreads = 256;
@@ -460,6 +479,20 @@ void launch_variant(const StepArgs& a, cudaStream_t s) {
   auto k = fused_step_kernel<M, V, U, kThreads, MINB>;
   int grid = grid_for(k, (a.n / V + U - 1) / U, kThreads);
   k<<<grid, kThreads, 0, s>>>(a);
+}
+
+template <class M>
+co2_status_t launch_ghost_p2p(const StepArgs& a, cudaStream_t s) {
+  bool vec_ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
+                aligned16(a.m) && aligned16(a.anchor) && aligned16(a.gap) &&
+                aligned16(a.bar0_out);
+  for (int p = 0; p < a.exit.world; ++p) vec_ok = vec_ok && aligned16(a.out_peers[p]);
+  if (!vec_ok) return fail(CO2_ERR_VALIDATION, "p2p sharded step: buffers must be 16-byte aligned");
+  constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+  auto k = fused_step_kernel<M, V, 1, kThreads, 3, true, true>;
+  k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
 }
 
 template <class M>
@@ -765,6 +798,34 @@ co2_status_t outer_step_impl(co2_mode_t mode, int64_t n, const void* x_t0, const
     case CO2_MODE_F64: return launch_fused<ModeF64>(a, s);
     case CO2_MODE_F32: return launch_fused<ModeF32>(a, s);
     case CO2_MODE_BF16_MIXED: return launch_fused<ModeBF16>(a, s);
+  }
+  return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
+}
+
+co2_status_t outer_step_ghost_p2p_impl(co2_mode_t mode, int64_t n, const void* anchor_in,
+                                       const void* p0, const void* p1_avg, const void* xbar_avg,
+                                       int32_t ghost_copies, void* m, void* anchor_out,
+                                       void* bar0_out, void* const* out_peers,
+                                       void* const* sigs, int world, int rank, uint32_t epoch,
+                                       void* gap, const co2_hyper_t* h, void* ws,
+                                       cudaStream_t s) {
+  if (world < 1 || world > kMaxRanks)
+    return fail(CO2_ERR_VALIDATION, "p2p sharded step: world must lie in [1, %d]", kMaxRanks);
+  StepArgs a{ghost_copies > 0 ? anchor_in : xbar_avg, p0, p1_avg, xbar_avg, m, anchor_out,
+             nullptr, gap, n, h->alpha, h->beta, h->phi, h->epsilon, h->tau, 1,
+             h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, ghost_copies,
+             ghost_copies == 0 ? 1 : 0, bar0_out};
+  for (int p = 0; p < world; ++p) {
+    a.out_peers[p] = out_peers[p];
+    a.exit.sig[p] = static_cast<Signals*>(sigs[p]);
+  }
+  a.exit.world = world;
+  a.exit.rank = rank;
+  a.exit.epoch = epoch;
+  switch (mode) {
+    case CO2_MODE_F64: return launch_ghost_p2p<ModeF64>(a, s);
+    case CO2_MODE_F32: return launch_ghost_p2p<ModeF32>(a, s);
+    case CO2_MODE_BF16_MIXED: return launch_ghost_p2p<ModeBF16>(a, s);
   }
   return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
 }

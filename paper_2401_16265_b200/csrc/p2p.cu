@@ -24,6 +24,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "p2p_sync.cuh"
 
 namespace co2 {
 namespace {
@@ -36,28 +37,7 @@ __device__ __forceinline__ float ld_c(const bf16raw* p) {
   return __uint_as_float(((uint32_t)p->b) << 16);
 }
 
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-constexpr int kMaxRanks = 8;
 constexpr int kP2PThreads = 512;
-
-// Signal area layout (per rank, 256 B): ready[kMaxRanks], done, error.
-struct Signals {
-  uint32_t ready[kMaxRanks];
-  uint32_t done;
-  uint32_t error;
-  uint32_t pad[54];
-};
 
 struct P2PArgs {
   void* bufs[kMaxRanks];      // rank-indexed pointers to the same logical buffer
@@ -68,25 +48,15 @@ struct P2PArgs {
   uint32_t epoch;             // 1, 2, ... (same sequence on every rank)
 };
 
-__device__ bool spin_until(const uint32_t* p, uint32_t target, long long budget) {
-  long long t0 = clock64();
-  while (ld_acquire_sys(p) < target) {
-    if (clock64() - t0 > budget) return false;
-    __nanosleep(64);
-  }
-  return true;
-}
-
 // TL storage, TC compute, V elements per 16-byte vector.
 template <typename TL, typename TC, int V, int R, int U>
 __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs a) {
-  const long long kBudget = 4000000000LL;  // ~2 s at 1.9 GHz
   Signals* mine = a.sig[a.rank];
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     for (int p = 0; p < a.world; ++p) st_release_sys(&a.sig[p]->ready[a.rank], a.epoch);
     bool ok = true;
-    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch, kBudget);
+    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch);
     if (!ok) mine->error = 1;
     s_ok = ok;
   }
@@ -195,11 +165,139 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs 
     __threadfence_system();
     for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
     const uint32_t target = a.epoch * (uint32_t)a.world * gridDim.x;
-    if (!spin_until(&mine->done, target, kBudget)) mine->error = 2;
+    if (!spin_until(&mine->done, target)) mine->error = 2;
+  }
+}
+
+// Slice reduce for the sharded (ghost-consistent) layout: rank r averages
+// slice r of `nb` logical buffers (x_{t,tau} and x_{t,1}) over all ranks in
+// ascending rank order into local slice outputs -- a deterministic
+// reduce-scatter that delivers the average itself.  Entry barrier only:
+// the fused sharded step's exit barrier orders every later overwrite of the
+// buffers read here (see engine.cpp, co2_sharded_round).
+struct SliceArgs {
+  const void* src[2][kMaxRanks];
+  void* dst[2];
+  int nb;
+  int64_t lo, len;
+  int world, rank;
+  uint32_t epoch;
+  Signals* sig[kMaxRanks];
+};
+
+template <typename TL, typename TC, int V, int R, int U>
+__global__ void __launch_bounds__(kP2PThreads) p2p_slice_average_kernel(const SliceArgs a) {
+  Signals* mine = a.sig[a.rank];
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    for (int p = 0; p < a.world; ++p) st_release_sys(&a.sig[p]->ready[a.rank], a.epoch);
+    bool ok = true;
+    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch);
+    if (!ok) mine->error = 1;
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const TC g = (TC)a.world;
+  const int64_t nvec = a.len / V;
+  const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
+  auto to_c = [](const TL* v, int k) -> TC {
+    if constexpr (sizeof(TL) == 2)
+      return ld_c(reinterpret_cast<const bf16raw*>(v + k));
+    else
+      return (TC)v[k];
+  };
+  auto store = [](TL* o, int k, TC r) {
+    if constexpr (sizeof(TL) == 2) {
+      __nv_bfloat16 h = __float2bfloat16_rn((float)r);
+      reinterpret_cast<uint16_t*>(o)[k] = __bfloat16_as_ushort(h);
+    } else {
+      o[k] = (TL)r;
+    }
+  };
+  for (int b = 0; b < a.nb; ++b) {
+    int64_t i = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x;
+    for (; i < nvec; i += (int64_t)U * stride) {
+      uint4 raw[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t iv = i + (int64_t)u * stride;
+#pragma unroll
+        for (int p = 0; p < R; ++p)
+          if (p < a.world && iv < nvec)
+            raw[u][p] = __ldcg(reinterpret_cast<const uint4*>(
+                static_cast<const TL*>(a.src[b][p]) + a.lo + iv * V));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t iv = i + (int64_t)u * stride;
+        if (iv >= nvec) break;
+        TC acc[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = to_c(reinterpret_cast<const TL*>(&raw[u][0]), k);
+#pragma unroll
+        for (int p = 1; p < R; ++p)
+          if (p < a.world)
+#pragma unroll
+            for (int k = 0; k < V; ++k)
+              acc[k] = acc[k] + to_c(reinterpret_cast<const TL*>(&raw[u][p]), k);
+        uint4 out;
+#pragma unroll
+        for (int k = 0; k < V; ++k) store(reinterpret_cast<TL*>(&out), k, acc[k] / g);
+        *reinterpret_cast<uint4*>(static_cast<TL*>(a.dst[b]) + iv * V) = out;
+      }
+    }
+    if (blockIdx.x == 0) {  // scalar tail
+      for (int64_t j = nvec * V + threadIdx.x; j < a.len; j += kP2PThreads) {
+        TC acc = to_c(static_cast<const TL*>(a.src[b][0]) + a.lo + j, 0);
+        for (int p = 1; p < a.world; ++p)
+          acc = acc + to_c(static_cast<const TL*>(a.src[b][p]) + a.lo + j, 0);
+        store(static_cast<TL*>(a.dst[b]) + j, 0, acc / g);
+      }
+    }
   }
 }
 
 }  // namespace
+
+co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const* src0,
+                                      const void* const* src1, void* dst0, void* dst1,
+                                      void* const* sigs, int world, int rank, int64_t lo,
+                                      int64_t len, uint32_t epoch, int ctas, cudaStream_t s) {
+  if (world < 1 || world > kMaxRanks)
+    return fail(CO2_ERR_VALIDATION, "p2p: world must lie in [1, %d]", kMaxRanks);
+  SliceArgs a{};
+  for (int p = 0; p < world; ++p) {
+    a.src[0][p] = src0[p];
+    a.src[1][p] = nb > 1 ? src1[p] : nullptr;
+    a.sig[p] = static_cast<Signals*>(sigs[p]);
+  }
+  a.dst[0] = dst0;
+  a.dst[1] = dst1;
+  a.nb = nb;
+  a.lo = lo;
+  a.len = len;
+  a.world = world;
+  a.rank = rank;
+  a.epoch = epoch;
+  if (ctas < 1) ctas = 1;
+  if (ctas > sm_count()) ctas = sm_count();
+#define CO2_SLICE_LAUNCH(TL, TC, V)                                                       \
+  if (world <= 2)                                                                        \
+    p2p_slice_average_kernel<TL, TC, V, 2, 4><<<ctas, kP2PThreads, 0, s>>>(a);           \
+  else if (world <= 4)                                                                   \
+    p2p_slice_average_kernel<TL, TC, V, 4, 2><<<ctas, kP2PThreads, 0, s>>>(a);           \
+  else                                                                                   \
+    p2p_slice_average_kernel<TL, TC, V, 8, 1><<<ctas, kP2PThreads, 0, s>>>(a);
+  switch (dt) {
+    case CO2_DTYPE_F64: CO2_SLICE_LAUNCH(double, double, 2) break;
+    case CO2_DTYPE_F32: CO2_SLICE_LAUNCH(float, float, 4) break;
+    default: CO2_SLICE_LAUNCH(bf16raw, float, 8) break;
+  }
+#undef CO2_SLICE_LAUNCH
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
 
 co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* sigs, int world,
                                 int rank, int64_t n, uint32_t epoch, int ctas, cudaStream_t s) {

@@ -48,8 +48,14 @@ def main():
     dist.init_process_group("gloo")
     mode = int(os.environ.get("CO2_TEST_MODE", "1"))
     n, tau, rounds = 300_007, 3, 5
-    uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
-    eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid)
+    transport = os.environ.get("CO2_TEST_TRANSPORT", "nccl")
+    if transport == "p2p":
+        eng = co2.CollectiveEngine(world, transport="p2p", rank=rank)
+        div = 1  # the P2P slice reduce delivers the fixed-order average
+    else:
+        uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
+        eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid)
+        div = world  # NCCL delivers the worker sum
     hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12, ghost_consistent=True)
     init = co2.synth(mode, n, worker=0)[3]  # identical x_{0,0} on every worker
     sw = co2.ShardedWorker(mode, n, eng, init)
@@ -87,7 +93,7 @@ def main():
                                              np.zeros(n, st), oh).bar0
                 expect = ends  # worker-local x_{1,0} = x_{0,tau}
             else:
-                res = O.outer_step_ghost(mode, anchor, prev_x0, p1sum, world, xsum, world,
+                res = O.outer_step_ghost(mode, anchor, prev_x0, p1sum, div, xsum, div,
                                          0 if t == 1 else world, m, oh)
                 assert res.status == 0, res.message
                 anchor, prev_x0, m = res.anchor, res.bar0, res.m
@@ -102,12 +108,20 @@ def main():
                     bad = np.nonzero(afters[i][:n] != expect[i])[0]
                     ok, mismatch = False, (t, "params", i, int(bad.size), int(bad[0]),
                                            float(afters[i][bad[0]]), float(expect[i][bad[0]]))
-            p1sum = storage_sum(firsts, mode)
-            xsum = storage_sum(ends, mode)
+            if transport == "p2p":  # fixed-order averages (param_ops.cpp:16-33)
+                if mode == O.MODE_F64:
+                    p1sum, xsum = O.average(firsts), O.average(ends)
+                else:
+                    bf = mode == O.MODE_BF16_MIXED
+                    p1sum, xsum = O.average_lp(firsts, bf), O.average_lp(ends, bf)
+            else:
+                p1sum = storage_sum(firsts, mode)
+                xsum = storage_sum(ends, mode)
         if t >= 1:
             assert r.outer_applied == 1
     if rank == 0:
-        print(json.dumps({"ok": ok, "first_mismatch": mismatch, "world": world, "mode": mode}),
+        print(json.dumps({"ok": ok, "first_mismatch": mismatch, "world": world, "mode": mode,
+                          "transport": transport}),
               flush=True)
     sw.drain(eng)
     torch.cuda.synchronize()

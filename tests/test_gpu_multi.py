@@ -46,9 +46,16 @@ def test_multi_rank_rounds_bitwise(mode, transport, world):
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("mode", [0, 1, 2])
-def test_nccl_sharded_ghost_bitwise_world2(mode):
-    env = dict(os.environ, CO2_TEST_MODE=str(mode))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+@pytest.mark.parametrize("transport,world", [("nccl", 2), ("p2p", 2), ("p2p", 4)])
+def test_sharded_ghost_bitwise(mode, transport, world):
+    """Sharded ghost-consistent rounds (C4 layout) against the oracle: NCCL
+    reduce-scatter/all-gather at G = 2, and the fused P2P step (slice average
+    + ghost step + NVLink all-gather) at G = 2 and 4, bitwise."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT=transport)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "mp_nccl_sharded.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
