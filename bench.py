@@ -217,7 +217,7 @@ def main():
         uid = obj[0]
     else:
         uid = bytes(128)
-    transport = args.transport if world > 1 and not cfg.get("sharded") else "nccl"
+    transport = args.transport if world > 1 else "nccl"
     transport_note = None
     eng = None
     if transport == "p2p":
@@ -354,15 +354,21 @@ def main():
             "config": {"workload": cfg["workload"],
                        "n_params_per_gpu": per_rank, "n_params_total": units, "tau": tau,
                        "storage": cfg["storage"], "hyper": HYPER,
-                       "parallelism": (f"dp{world} ghost-consistent, outer state sharded "
-                                       "(NCCL reduce-scatter + all-gather)") if sharded else
+                       "parallelism": (f"dp{world} ghost-consistent, outer state sharded ("
+                                       + ("async fixed-order P2P slice averages + fused "
+                                          "NVLink all-gather)" if transport == "p2p" else
+                                          "NCCL reduce-scatter + all-gather)")) if sharded else
                        (f"dp{world} (one CO2 worker per GPU, "
                         + ("fixed-order NVLink P2P all-reduce)" if transport == "p2p"
                            else "NCCL all-reduce)")),
                        "transport": transport, "transport_note": transport_note,
                        "l2": "inputs larger than L2 (no flush needed)",
-                       "step": ("sharded co2_round: RS(x_{t,1}) + async RS(x_{t,tau}) + stale "
-                                "wait + fused ghost step on the shard + AG(x_{t+1,0})")
+                       "step": (("sharded co2_round: async P2P slice average of x_{t,tau} and "
+                                 "x_{t,1} + stale wait + ONE kernel: ghost step on the shard "
+                                 "storing x_{t+1,0} into every rank's params over NVLink")
+                                if transport == "p2p" else
+                                ("sharded co2_round: RS(x_{t,1}) + async RS(x_{t,tau}) + stale "
+                                 "wait + fused ghost step on the shard + AG(x_{t+1,0})"))
                        if sharded else "co2_round: AAR launch + stale wait + fused outer step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
