@@ -188,12 +188,12 @@ def main():
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
                     help="all-reduce transport at N > 1 (worker-local configs)")
-    ap.add_argument("--n", type=int, default=0, help="override the config's parameter count")
+    ap.add_argument("--nparams", type=int, default=0, help="override the config's parameter count")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
-    if args.n > 0:
-        cfg["n"] = args.n
-        cfg["workload"] += f" [n overridden to {args.n}]"
+    if args.nparams > 0:
+        cfg["n"] = args.nparams
+        cfg["workload"] += f" [n overridden to {args.nparams}]"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
