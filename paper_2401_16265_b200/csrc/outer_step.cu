@@ -811,7 +811,9 @@ co2_status_t outer_step_ghost_p2p_impl(co2_mode_t mode, int64_t n, const void* a
                                        cudaStream_t s) {
   if (world < 1 || world > kMaxRanks)
     return fail(CO2_ERR_VALIDATION, "p2p sharded step: world must lie in [1, %d]", kMaxRanks);
-  StepArgs a{ghost_copies > 0 ? anchor_in : xbar_avg, p0, p1_avg, xbar_avg, m, anchor_out,
+  // x_t0 is loaded as the STATE dtype even when unused (x_from_xbar): never
+  // alias it to the low-dtype average, which is half as long in bytes.
+  StepArgs a{anchor_in ? anchor_in : p0, p0, p1_avg, xbar_avg, m, anchor_out,
              nullptr, gap, n, h->alpha, h->beta, h->phi, h->epsilon, h->tau, 1,
              h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, ghost_copies,
              ghost_copies == 0 ? 1 : 0, bar0_out};
@@ -1088,7 +1090,7 @@ extern "C" co2_status_t co2_outer_step_ghost(co2_mode_t mode, int64_t n, const v
   if (n > 0 && (!prev_x0 || !prev_x1_sum || !xbar_sum || !momentum ||
                 (ghost_copies > 0 && !anchor_in)))
     return fail(CO2_ERR_VALIDATION, "outer step: null input buffer");
-  return outer_step_ghost_impl(mode, n, ghost_copies > 0 ? anchor_in : xbar_sum, prev_x0,
+  return outer_step_ghost_impl(mode, n, anchor_in ? anchor_in : prev_x0, prev_x0,
                                prev_x1_sum, p1_div, xbar_sum, xbar_div, ghost_copies, momentum,
                                anchor_out, bar0_out, params_out, gap_out, h, ws, S(stream));
 }
