@@ -186,8 +186,10 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--max-ctas", type=int, default=0)
-    ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"],
-                    help="all-reduce transport at N > 1 (worker-local configs)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="collective transport at N > 1; auto = the measured faster one: the "
+                         "fixed-order P2P all-reduce for worker-local configs, NCCL "
+                         "reduce-scatter/all-gather for the sharded C4")
     ap.add_argument("--nparams", type=int, default=0, help="override the config's parameter count")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -221,7 +223,11 @@ def main():
         uid = obj[0]
     else:
         uid = bytes(128)
-    transport = args.transport if world > 1 else "nccl"
+    transport = args.transport
+    if transport == "auto":
+        transport = "nccl" if cfg.get("sharded") else "p2p"
+    if world == 1:
+        transport = "nccl"  # one rank: no collective, the engine's reduce is a no-op
     transport_note = None
     eng = None
     if transport == "p2p":
