@@ -116,6 +116,12 @@ co2_status_t co2_outer_step(co2_mode_t mode, int64_t n, const void* x_t0, const 
                             void* momentum, void* anchor_out, void* params_out, void* gap_out,
                             const co2_hyper_t* hyper, void* workspace, void* stream);
 
+/* Tuning knob: select the fused kernel's instantiation (elements per vector,
+ * vectors in flight per thread, CTAs per SM); 0 = the measured default.
+ * Also settable once per process with CO2_FUSED_VARIANT.  See
+ * tools/tune_fused.py. */
+co2_status_t co2_set_fused_variant(int32_t variant);
+
 /* End-to-end form of co2_outer_step over HOST buffers (the reference's own
  * calling convention: host vectors in, host vectors out).  Streams the
  * coordinates through the GPU in chunks with H2D / compute / D2H overlapped

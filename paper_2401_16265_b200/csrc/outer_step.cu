@@ -514,12 +514,13 @@ co2_status_t launch_ghost(const StepArgs& a, cudaStream_t s) {
 
 // Tuning knob: CO2_FUSED_VARIANT selects the (elements per vector, vectors
 // in flight per thread) instantiation; 0 is the measured default.
+int g_variant = -1;
 int fused_variant() {
-  static int v = [] {
+  if (g_variant < 0) {
     const char* e = getenv("CO2_FUSED_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
+    g_variant = e ? atoi(e) : 0;
+  }
+  return g_variant;
 }
 
 template <class M>
@@ -851,6 +852,12 @@ co2_status_t outer_step_ghost_impl(co2_mode_t mode, int64_t n, const void* ancho
 }  // namespace co2
 
 using namespace co2;
+
+extern "C" co2_status_t co2_set_fused_variant(int32_t variant) {
+  if (variant < 0 || variant > 15) return fail(CO2_ERR_VALIDATION, "variant out of range");
+  g_variant = variant;
+  return CO2_OK;
+}
 
 extern "C" co2_status_t co2_staleness_gap(co2_dtype_t dt, int64_t n, const void* x_t0,
                                           const void* prev_x0, const void* prev_x1, int32_t tau,
