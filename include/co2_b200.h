@@ -57,7 +57,10 @@ enum {
   CO2_FLAG_M_NONFINITE = 4u,     /* outer_algorithms.cpp:88  numeric  */
   CO2_FLAG_CLIP_NONFINITE = 8u,  /* param_ops.cpp:41         numeric  */
   CO2_FLAG_X_NONFINITE = 16u,    /* outer_algorithms.cpp:106 numeric  */
-  CO2_FLAG_AVG_NONFINITE = 32u   /* param_ops.cpp:31         numeric  */
+  CO2_FLAG_AVG_NONFINITE = 32u,  /* param_ops.cpp:31         numeric  */
+  CO2_FLAG_SLOWMO_M = 64u,       /* outer_algorithms.cpp:231 numeric  */
+  CO2_FLAG_SLOWMO_X = 128u,      /* outer_algorithms.cpp:233 numeric  */
+  CO2_FLAG_OVERLAP = 256u        /* outer_algorithms.cpp:279 numeric  */
 };
 
 /* Co2Hyper (proj/include/co2sim/outer_algorithms.hpp:17-30) plus tau. */
@@ -323,6 +326,37 @@ co2_status_t co2_round_finish(co2_worker_t* const* workers, int32_t g, void* str
  * round launched, releasing its slot in the engine's two-handle window. */
 co2_status_t co2_round_drain(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,
                              void* stream);
+/* ---- baseline outer algorithms on the same kernel family (SURVEY.md 8f
+ *      item 3; proj/src/outer_algorithms.cpp:213-313) ----------------------
+ * Per-worker bodies (one HBM pass, reference op order, reference messages
+ * "non-finite value in slowmo momentum" / "slowmo outer iterate" /
+ * "overlap correction"; diag.max_outer_step as RoundResult). */
+/* slowmo_round body (:228-236): m = beta*m + (x_start - xbar);
+ * params = x_start - alpha*m (anchor_out, nullable, receives it too). */
+co2_status_t co2_slowmo_step(co2_mode_t mode, int64_t n, const void* x_start, const void* xbar,
+                             int32_t xbar_divisor, void* momentum, void* params_out,
+                             void* anchor_out, double alpha, double beta, void* workspace,
+                             void* stream);
+/* local_sgd_round body (:251-256): params = xbar. */
+co2_status_t co2_local_sgd_step(co2_mode_t mode, int64_t n, const void* x_start,
+                                const void* xbar, int32_t xbar_divisor, void* params_out,
+                                void* anchor_out, void* workspace, void* stream);
+/* overlap_local_sgd correction (:277-280, :293-296): params -= anchor - xbar. */
+co2_status_t co2_overlap_correction(co2_mode_t mode, int64_t n, void* params,
+                                    const void* anchor, const void* xbar, int32_t xbar_divisor,
+                                    void* workspace, void* stream);
+/* Round drivers over co2_worker_t and the engine (blocking reduce for SlowMo
+ * and Local-SGD; Overlap-Local-SGD consumes the anchor reduce next round
+ * unless `instant`, the reference's zero-cost-reduce case). */
+co2_status_t co2_slowmo_round(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,
+                              double alpha, double beta, void* stream, int32_t sync,
+                              co2_round_result_t* result);
+co2_status_t co2_local_sgd_round(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,
+                                 void* stream, int32_t sync, co2_round_result_t* result);
+co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* workers, int32_t g,
+                                         co2_aar_t* engine, int32_t instant, void* stream,
+                                         int32_t sync, co2_round_result_t* result);
+
 /* ---- ghost-consistent, sharded outer state (C4; outer_algorithms.cpp:
  *      126-145,161-184) ------------------------------------------------------
  * The fused step on one shard where x_t0 is the average of `ghost_copies`

@@ -488,7 +488,155 @@ int orc_diag_status(const orc_diag* d) {
   if (f & ORC_FLAG_CLIP_NONFINITE)
     return fail(ORC_NUMERIC, "non-finite value in clip_elementwise input");
   if (f & ORC_FLAG_X_NONFINITE) return fail(ORC_NUMERIC, "non-finite value in outer_iterate");
+  if (f & ORC_FLAG_SLOWMO_M) return fail(ORC_NUMERIC, "non-finite value in slowmo momentum");
+  if (f & ORC_FLAG_SLOWMO_X) return fail(ORC_NUMERIC, "non-finite value in slowmo outer iterate");
+  if (f & ORC_FLAG_OVERLAP) return fail(ORC_NUMERIC, "non-finite value in overlap correction");
   return ORC_OK;
+}
+
+/* ------------------------------------------------ baseline outer steps */
+/* Element access in the mode's storage types (see orc_outer_step). */
+static double ld_state(int mode, const void* p, int64_t j) {
+  return mode == ORC_MODE_F64 ? ((const double*)p)[j] : (double)((const float*)p)[j];
+}
+static double ld_low(int mode, const void* p, int64_t j) {
+  if (mode == ORC_MODE_F64) return ((const double*)p)[j];
+  if (mode == ORC_MODE_F32) return ((const float*)p)[j];
+  return orc_bf16_to_f32(((const uint16_t*)p)[j]);
+}
+static void st_state(int mode, void* p, int64_t j, double v) {
+  if (mode == ORC_MODE_F64)
+    ((double*)p)[j] = v;
+  else
+    ((float*)p)[j] = (float)v;
+}
+static void st_low(int mode, void* p, int64_t j, double v) {
+  if (mode == ORC_MODE_F64)
+    ((double*)p)[j] = v;
+  else if (mode == ORC_MODE_F32)
+    ((float*)p)[j] = (float)v;
+  else
+    ((uint16_t*)p)[j] = orc_f32_to_bf16((float)v);
+}
+
+static void diag_init(orc_diag* d) {
+  d->min_gap = INFINITY;
+  d->max_outer_step = 0.0;
+  d->n_clipped = d->n_floored = 0;
+  d->flags = 0;
+  d->pad = 0;
+}
+
+/* Arithmetic in the mode's compute type: fp64 for F64, fp32 otherwise (every
+ * fp32 op below rounds exactly as the GPU's). */
+
+int orc_slowmo_step(int mode, int64_t n, const void* x_start, const void* xbar, int divisor,
+                    void* m, void* params_out, double alpha, double beta, orc_diag* diag) {
+  /* slowmo_round, outer_algorithms.cpp:219-236 */
+  if (!(alpha > 0.0)) return fail(ORC_VALIDATION, "slowmo: alpha must be positive");
+  if (beta < 0.0 || beta >= 1.0) return fail(ORC_VALIDATION, "slowmo: beta must lie in [0, 1)");
+  diag_init(diag);
+  if (mode == ORC_MODE_F64) {
+    double mx = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      double x = ld_state(mode, x_start, j), xb = ld_low(mode, xbar, j);
+      if (divisor > 1) xb = xb / (double)divisor;
+      double delta = x - xb;
+      double mn = beta * ld_state(mode, m, j) + delta;
+      double xn = x - alpha * mn;
+      if (!isfinite(mn)) diag->flags |= ORC_FLAG_SLOWMO_M;
+      if (!isfinite(xn)) diag->flags |= ORC_FLAG_SLOWMO_X;
+      st_state(mode, m, j, mn);
+      st_low(mode, params_out, j, xn);
+      double s = fabs(xn - x);
+      if (s > mx) mx = s;
+    }
+    diag->max_outer_step = mx;
+  } else {
+    float mx = 0.0f, af = (float)alpha, bf = (float)beta, gd = (float)divisor;
+    for (int64_t j = 0; j < n; ++j) {
+      float x = (float)ld_state(mode, x_start, j), xb = (float)ld_low(mode, xbar, j);
+      if (divisor > 1) xb = xb / gd;
+      float delta = x - xb;
+      float bm = bf * (float)ld_state(mode, m, j);
+      float mn = bm + delta;
+      float am = af * mn;
+      float xn = x - am;
+      if (!isfinite(mn)) diag->flags |= ORC_FLAG_SLOWMO_M;
+      if (!isfinite(xn)) diag->flags |= ORC_FLAG_SLOWMO_X;
+      st_state(mode, m, j, mn);
+      st_low(mode, params_out, j, xn);
+      float s = fabsf(xn - x);
+      if (s > mx) mx = s;
+    }
+    diag->max_outer_step = mx;
+  }
+  return orc_diag_status(diag);
+}
+
+int orc_local_sgd_step(int mode, int64_t n, const void* x_start, const void* xbar, int divisor,
+                       void* params_out, orc_diag* diag) {
+  /* local_sgd_round, outer_algorithms.cpp:251-256 */
+  diag_init(diag);
+  if (mode == ORC_MODE_F64) {
+    double mx = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      double xb = ld_low(mode, xbar, j);
+      if (divisor > 1) xb = xb / (double)divisor;
+      double s = fabs(xb - ld_state(mode, x_start, j));
+      if (s > mx) mx = s;
+      st_low(mode, params_out, j, xb);
+    }
+    diag->max_outer_step = mx;
+  } else {
+    float mx = 0.0f, gd = (float)divisor;
+    for (int64_t j = 0; j < n; ++j) {
+      float xb = (float)ld_low(mode, xbar, j);
+      if (divisor > 1) xb = xb / gd;
+      float s = fabsf(xb - (float)ld_state(mode, x_start, j));
+      if (s > mx) mx = s;
+      st_low(mode, params_out, j, xb);
+    }
+    diag->max_outer_step = mx;
+  }
+  return orc_diag_status(diag);
+}
+
+int orc_overlap_correction(int mode, int64_t n, void* params, const void* anchor,
+                           const void* xbar, int divisor, orc_diag* diag) {
+  /* overlap_local_sgd_round, outer_algorithms.cpp:277-280 / :293-296 */
+  diag_init(diag);
+  if (mode == ORC_MODE_F64) {
+    double mx = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      double xb = ld_low(mode, xbar, j);
+      if (divisor > 1) xb = xb / (double)divisor;
+      double p = ld_low(mode, params, j);
+      double pn = p - (ld_state(mode, anchor, j) - xb);
+      if (!isfinite(pn)) diag->flags |= ORC_FLAG_OVERLAP;
+      st_low(mode, params, j, pn);
+      double s = fabs(pn - p);
+      if (s > mx) mx = s;
+    }
+    diag->max_outer_step = mx;
+  } else {
+    float mx = 0.0f, gd = (float)divisor;
+    for (int64_t j = 0; j < n; ++j) {
+      float xb = (float)ld_low(mode, xbar, j);
+      if (divisor > 1) xb = xb / gd;
+      float p = (float)ld_low(mode, params, j);
+      float d = (float)ld_state(mode, anchor, j) - xb;
+      float pn = p - d;
+      if (!isfinite(pn)) diag->flags |= ORC_FLAG_OVERLAP;
+      st_low(mode, params, j, pn);
+      /* the step actually stored (bf16 params round pn) */
+      float stored = (float)ld_low(mode, params, j);
+      float s = fabsf(stored - p);
+      if (s > mx) mx = s;
+    }
+    diag->max_outer_step = mx;
+  }
+  return orc_diag_status(diag);
 }
 
 int orc_average_lp(int bf, int g, const void* const* c, int64_t n, void* out) {

@@ -128,6 +128,24 @@ int orc_outer_step_ghost(int mode, int64_t n, const void* anchor, const void* p0
 /* Reference error precedence over a diag's flags. */
 int orc_diag_status(const orc_diag* d);
 
+/* ---- baseline outer steps (outer_algorithms.cpp:213-313) -------------- */
+/* Same storage convention as orc_outer_step (mode); xbar is the average
+ * (divisor 1) or a worker sum (divisor G).  Each returns the reference's
+ * status and message for its ensure_finite checks and fills diag
+ * (max_outer_step and flags only). */
+enum { ORC_FLAG_SLOWMO_M = 64u, ORC_FLAG_SLOWMO_X = 128u, ORC_FLAG_OVERLAP = 256u };
+/* slowmo_round body (cpp:228-236): m = beta*m + (x_start - xbar);
+ * params = x_start - alpha*m. */
+int orc_slowmo_step(int mode, int64_t n, const void* x_start, const void* xbar, int divisor,
+                    void* m, void* params_out, double alpha, double beta, orc_diag* diag);
+/* local_sgd_round body (cpp:251-256): params = xbar. */
+int orc_local_sgd_step(int mode, int64_t n, const void* x_start, const void* xbar, int divisor,
+                       void* params_out, orc_diag* diag);
+/* overlap_local_sgd correction (cpp:277-280 / :293-296):
+ * params -= anchor - xbar; diag.max_outer_step = max |params' - params|. */
+int orc_overlap_correction(int mode, int64_t n, void* params, const void* anchor,
+                           const void* xbar, int divisor, orc_diag* diag);
+
 /* ---- fixed-order average in the storage type (param_ops.cpp:16-33) ---- */
 int orc_average_lp(int dtype_bf16, int g, const void* const* contrib, int64_t n,
                    void* out);

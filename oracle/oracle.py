@@ -321,6 +321,58 @@ def outer_step_ghost(mode: int, anchor, p0, p1sum, p1_div: int, xsum, xdiv: int,
     return r
 
 
+def _dts(mode):
+    st = np.float64 if mode == MODE_F64 else np.float32
+    lo = np.float64 if mode == MODE_F64 else (np.uint16 if mode == MODE_BF16_MIXED else np.float32)
+    return st, lo
+
+
+def slowmo_step(mode: int, x_start, xbar, m, alpha: float, beta: float, divisor: int = 1):
+    """slowmo_round per-worker body (proj/src/outer_algorithms.cpp:228-236).
+    Returns (m', params, diag, status, message)."""
+    st, lo = _dts(mode)
+    L = lib()
+    L.orc_slowmo_step.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int,
+                                  C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                  C.POINTER(Diag)]
+    x = np.ascontiguousarray(x_start, st)
+    xb = np.ascontiguousarray(xbar, lo)
+    mm = np.array(m, dtype=st, copy=True)
+    out = np.empty(x.size, lo)
+    d = Diag()
+    code = L.orc_slowmo_step(mode, x.size, _p(x), _p(xb), divisor, _p(mm), _p(out), alpha, beta,
+                             C.byref(d))
+    return mm, out, d, code, (L.orc_last_error().decode() if code else "")
+
+
+def local_sgd_step(mode: int, x_start, xbar, divisor: int = 1):
+    """local_sgd_round per-worker body (proj/src/outer_algorithms.cpp:251-256)."""
+    st, lo = _dts(mode)
+    L = lib()
+    L.orc_local_sgd_step.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int,
+                                     C.c_void_p, C.POINTER(Diag)]
+    x = np.ascontiguousarray(x_start, st)
+    xb = np.ascontiguousarray(xbar, lo)
+    out = np.empty(x.size, lo)
+    d = Diag()
+    code = L.orc_local_sgd_step(mode, x.size, _p(x), _p(xb), divisor, _p(out), C.byref(d))
+    return out, d, code
+
+
+def overlap_correction(mode: int, params, anchor, xbar, divisor: int = 1):
+    """overlap_local_sgd correction (proj/src/outer_algorithms.cpp:277-280)."""
+    st, lo = _dts(mode)
+    L = lib()
+    L.orc_overlap_correction.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int, C.POINTER(Diag)]
+    p = np.array(params, dtype=lo, copy=True)
+    a = np.ascontiguousarray(anchor, st)
+    xb = np.ascontiguousarray(xbar, lo)
+    d = Diag()
+    code = L.orc_overlap_correction(mode, p.size, _p(p), _p(a), _p(xb), divisor, C.byref(d))
+    return p, d, code, (L.orc_last_error().decode() if code else "")
+
+
 def synth(mode: int, n: int, seed: int = 7, worker: int = 0, j0: int = 0):
     """Synthetic inputs of SURVEY.md 8(d): returns (x_t0, p0, p1, x_end, m)."""
     st = np.float64 if mode == MODE_F64 else np.float32

@@ -123,6 +123,13 @@ SIGNATURES = {
     "co2_round": (ST, [C.POINTER(P), I32, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),
     "co2_round_finish": (ST, [C.POINTER(P), I32, P, C.POINTER(RoundResult)]),
     "co2_round_drain": (ST, [C.POINTER(P), I32, P, P]),
+    "co2_slowmo_step": (ST, [I32, I64, P, P, I32, P, P, P, D, D, P, P]),
+    "co2_local_sgd_step": (ST, [I32, I64, P, P, I32, P, P, P, P]),
+    "co2_overlap_correction": (ST, [I32, I64, P, P, P, I32, P, P]),
+    "co2_slowmo_round": (ST, [C.POINTER(P), I32, P, D, D, P, I32, C.POINTER(RoundResult)]),
+    "co2_local_sgd_round": (ST, [C.POINTER(P), I32, P, P, I32, C.POINTER(RoundResult)]),
+    "co2_overlap_local_sgd_round": (ST, [C.POINTER(P), I32, P, I32, P, I32,
+                                         C.POINTER(RoundResult)]),
     "co2_outer_step_ghost": (ST, [I32, I64, P, P, P, I32, P, I32, I32, P, P, P, P, P,
                                   C.POINTER(Hyper), P, P]),
     "co2_sharded_create": (ST, [C.POINTER(P), I32, I64, P, P, I32, P]),

@@ -515,6 +515,39 @@ def co2_round(workers: list[Worker], engine: CollectiveEngine, hyper: Co2Hyper, 
     return r
 
 
+def _arr(workers):
+    return (C.c_void_p * len(workers))(*[w.handle.value for w in workers])
+
+
+def slowmo_round(workers: list[Worker], engine: CollectiveEngine, alpha: float, beta: float, *,
+                 stream=None, sync: bool = True) -> L.RoundResult:
+    """slowmo_round (proj/src/outer_algorithms.cpp:213-240)."""
+    r = L.RoundResult()
+    check(lib().co2_slowmo_round(_arr(workers), len(workers), engine.handle, alpha, beta,
+                                 _stream(stream), int(sync), C.byref(r)))
+    return r
+
+
+def local_sgd_round(workers: list[Worker], engine: CollectiveEngine, *, stream=None,
+                    sync: bool = True) -> L.RoundResult:
+    """local_sgd_round (proj/src/outer_algorithms.cpp:242-260)."""
+    r = L.RoundResult()
+    check(lib().co2_local_sgd_round(_arr(workers), len(workers), engine.handle, _stream(stream),
+                                    int(sync), C.byref(r)))
+    return r
+
+
+def overlap_local_sgd_round(workers: list[Worker], engine: CollectiveEngine, *,
+                            instant: bool = False, stream=None,
+                            sync: bool = True) -> L.RoundResult:
+    """overlap_local_sgd_round (proj/src/outer_algorithms.cpp:262-313)."""
+    r = L.RoundResult()
+    check(lib().co2_overlap_local_sgd_round(_arr(workers), len(workers), engine.handle,
+                                            int(instant), _stream(stream), int(sync),
+                                            C.byref(r)))
+    return r
+
+
 def co2_round_drain(workers: list[Worker], engine: CollectiveEngine, *, stream=None) -> None:
     """Consume the reduce launched by the last round (end of a run)."""
     arr = (C.c_void_p * len(workers))(*[w.handle.value for w in workers])

@@ -85,6 +85,10 @@ extern "C" co2_status_t co2_diag_status(const co2_diag_t* d) {
     return fail(CO2_ERR_NUMERIC, "non-finite value in clip_elementwise input");
   if (f & CO2_FLAG_X_NONFINITE) return fail(CO2_ERR_NUMERIC, "non-finite value in outer_iterate");
   if (f & CO2_FLAG_AVG_NONFINITE) return fail(CO2_ERR_NUMERIC, "non-finite value in average");
+  if (f & CO2_FLAG_SLOWMO_M) return fail(CO2_ERR_NUMERIC, "non-finite value in slowmo momentum");
+  if (f & CO2_FLAG_SLOWMO_X)
+    return fail(CO2_ERR_NUMERIC, "non-finite value in slowmo outer iterate");
+  if (f & CO2_FLAG_OVERLAP) return fail(CO2_ERR_NUMERIC, "non-finite value in overlap correction");
   return CO2_OK;
 }
 

@@ -1193,3 +1193,196 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
   if (res) *res = r;
   return CO2_OK;
 }
+
+// ================================================ baseline round drivers
+// SlowMo / Local-SGD (blocking reduce every round) and Overlap-Local-SGD
+// (anchor correction consumed one round late), outer_algorithms.cpp:213-313,
+// over the same worker state and CollectiveEngine as co2_round.
+namespace {
+
+co2_status_t check_workers(co2_worker_t* const* ws, int32_t g, co2_aar* e) {
+  if (!e || !ws || g < 1) return fail(CO2_ERR_VALIDATION, "round: bad arguments");
+  const int expect = e->transport == T_LOCAL ? e->workers : 1;
+  if (g != expect)
+    return fail(CO2_ERR_VALIDATION,
+                "launch_all_reduce: contribution count %d does not match worker count %d", g,
+                expect);
+  for (int i = 1; i < g; ++i)
+    if (ws[i]->mode != ws[0]->mode || ws[i]->n != ws[0]->n)
+      return fail(CO2_ERR_VALIDATION, "round: worker dimensions differ");
+  return CO2_OK;
+}
+
+// Launch the reduce of one buffer per worker; returns where the consumer
+// reads it and with which divisor.
+co2_status_t launch_reduce(co2_worker_t* const* ws, int32_t g, co2_aar* e,
+                           const void* const* bufs, int slot, cudaStream_t st,
+                           uint64_t* handle, const void** xbar, int32_t* divisor) {
+  co2_worker* w0 = ws[0];
+  const size_t lb = low_bytes(w0->mode) * w0->n;
+  const bool local = e->transport == T_LOCAL;
+  if (local && !w0->avg[0]) {
+    CO2_TRY(walloc(&w0->avg[0], lb));
+    CO2_TRY(walloc(&w0->avg[1], lb));
+  }
+  void* out = local ? w0->avg[slot] : const_cast<void*>(bufs[0]);
+  CO2_TRY(co2_aar_launch(e, low_dtype(w0->mode), bufs, out, w0->n, st, handle));
+  *xbar = out;
+  *divisor = e->transport == T_NCCL ? e->world : 1;
+  return CO2_OK;
+}
+
+co2_status_t finish_round(co2_worker_t* const* ws, int32_t g, cudaStream_t st, int32_t sync,
+                          co2_round_result_t* r) {
+  if (!sync) return CO2_OK;
+  return co2_round_finish(ws, g, st, r);
+}
+
+}  // namespace
+
+extern "C" co2_status_t co2_slowmo_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
+                                         double alpha, double beta, void* stream, int32_t sync,
+                                         co2_round_result_t* res) {
+  // slowmo_round, outer_algorithms.cpp:213-240
+  if (!(alpha > 0.0)) return fail(CO2_ERR_VALIDATION, "slowmo: alpha must be positive");
+  if (beta < 0.0 || beta >= 1.0) return fail(CO2_ERR_VALIDATION, "slowmo: beta must lie in [0, 1)");
+  CO2_TRY(check_workers(ws, g, e));
+  cudaStream_t st = S(stream);
+  const void* bufs[64];
+  for (int i = 0; i < g; ++i) bufs[i] = ws[i]->params[ws[i]->cur];
+  uint64_t h = 0;
+  const void* xbar = nullptr;
+  int32_t div = 1;
+  CO2_TRY(launch_reduce(ws, g, e, bufs, 0, st, &h, &xbar, &div));
+  int32_t done = 0;
+  CO2_TRY(co2_aar_poll(e, h, &done));
+  CO2_TRY(co2_aar_wait(e, h, stream));  // blocking: consumed in the same round
+  for (int i = 0; i < g; ++i) {
+    co2_worker* w = ws[i];
+    // x_start = x_{t,0} (anchor); the new iterate is also the next anchor.
+    CO2_TRY(slowmo_impl(w->mode, w->n, w->anchor, xbar, div, w->m, w->params[w->cur], w->anchor,
+                        alpha, beta, w->ws, st));
+    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    w->xbar = const_cast<void*>(xbar);
+    w->t += 1;
+  }
+  co2_round_result_t r{};
+  r.outer_applied = 1;
+  CO2_TRY(finish_round(ws, g, st, sync, &r));
+  if (sync) {
+    double stall = 0.0;
+    CO2_TRY(co2_aar_stall(e, h, &stall, nullptr));
+    r.stall_seconds = stall;
+  }
+  if (res) *res = r;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_local_sgd_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
+                                            void* stream, int32_t sync,
+                                            co2_round_result_t* res) {
+  // local_sgd_round, outer_algorithms.cpp:242-260
+  CO2_TRY(check_workers(ws, g, e));
+  cudaStream_t st = S(stream);
+  const void* bufs[64];
+  for (int i = 0; i < g; ++i) bufs[i] = ws[i]->params[ws[i]->cur];
+  uint64_t h = 0;
+  const void* xbar = nullptr;
+  int32_t div = 1;
+  CO2_TRY(launch_reduce(ws, g, e, bufs, 0, st, &h, &xbar, &div));
+  int32_t done = 0;
+  CO2_TRY(co2_aar_poll(e, h, &done));
+  CO2_TRY(co2_aar_wait(e, h, stream));
+  for (int i = 0; i < g; ++i) {
+    co2_worker* w = ws[i];
+    CO2_TRY(local_sgd_impl(w->mode, w->n, w->anchor, xbar, div, w->params[w->cur], w->anchor,
+                           w->ws, st));
+    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    w->xbar = const_cast<void*>(xbar);
+    w->t += 1;
+  }
+  co2_round_result_t r{};
+  r.outer_applied = 1;
+  CO2_TRY(finish_round(ws, g, st, sync, &r));
+  if (res) *res = r;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int32_t g,
+                                                    co2_aar_t* e, int32_t instant, void* stream,
+                                                    int32_t sync, co2_round_result_t* res) {
+  // overlap_local_sgd_round, outer_algorithms.cpp:262-313.  The anchors are
+  // reduced from a snapshot copy in each worker's spare params buffer, so the
+  // next inner loop can keep mutating the working params.  `instant` selects
+  // the reference's zero-cost-reduce behaviour (consumed in the same round,
+  // :283-297); otherwise the reduce is consumed next round (:267-281).
+  CO2_TRY(check_workers(ws, g, e));
+  cudaStream_t st = S(stream);
+  co2_worker* w0 = ws[0];
+  const co2_mode_t mode = w0->mode;
+  const int64_t n = w0->n;
+  const size_t lb = low_bytes(mode) * n;
+  // Per-worker max |params' - x_end| accumulates over this round's corrections.
+  std::vector<double> step(g, 0.0);
+  bool applied = false;
+  auto correct = [&](const void* xbar, int32_t div) -> co2_status_t {
+    for (int i = 0; i < g; ++i) {
+      co2_worker* w = ws[i];
+      CO2_TRY(overlap_correction_impl(mode, n, w->params[w->cur], w->anchor, xbar, div, w->ws,
+                                      st));
+      CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    }
+    applied = true;
+    return CO2_OK;
+  };
+  if (w0->has_pending) {  // :267-281
+    const uint64_t prev = w0->pending;
+    int32_t done = 0;
+    CO2_TRY(co2_aar_poll(e, prev, &done));
+    CO2_TRY(co2_aar_wait(e, prev, stream));
+    const void* xbar = e->transport == T_LOCAL ? w0->avg[(w0->t + 1) % 2]
+                                               : ws[0]->params[1 - ws[0]->cur];
+    CO2_TRY(correct(xbar, e->transport == T_NCCL ? e->world : 1));
+    for (int i = 0; i < g; ++i) ws[i]->has_pending = false;
+  }
+  // Fresh anchors (:284-288), snapshotted into the spare buffer for the reduce.
+  const void* bufs[64];
+  for (int i = 0; i < g; ++i) {
+    co2_worker* w = ws[i];
+    CO2_TRY(co2_convert(state_dtype(mode), w->anchor, low_dtype(mode), w->params[w->cur], n,
+                        stream));
+    CO2_TRY(copy_dev(w->params[1 - w->cur], w->params[w->cur], lb, st));
+    bufs[i] = w->params[1 - w->cur];
+  }
+  uint64_t h = 0;
+  const void* xbar = nullptr;
+  int32_t div = 1;
+  CO2_TRY(launch_reduce(ws, g, e, bufs, w0->t % 2, st, &h, &xbar, &div));
+  if (instant) {  // :290-297
+    int32_t done = 0;
+    CO2_TRY(co2_aar_poll(e, h, &done));
+    CO2_TRY(co2_aar_wait(e, h, stream));
+    CO2_TRY(correct(xbar, div));
+  } else {
+    for (int i = 0; i < g; ++i) {
+      ws[i]->pending = h;
+      ws[i]->has_pending = true;
+    }
+  }
+  for (int i = 0; i < g; ++i) {
+    ws[i]->xbar = const_cast<void*>(xbar);
+    ws[i]->t += 1;
+    if (!applied) {
+      ws[i]->host_diag->flags = 0;
+      ws[i]->host_diag->min_gap = INFINITY;
+      ws[i]->host_diag->max_outer_step = 0.0;
+      ws[i]->host_diag->n_clipped = ws[i]->host_diag->n_floored = 0;
+    }
+  }
+  (void)step;
+  co2_round_result_t r{};
+  r.outer_applied = 1;  // :309 -- every overlap round counts as an outer update
+  CO2_TRY(finish_round(ws, g, st, sync, &r));
+  if (res) *res = r;
+  return CO2_OK;
+}

@@ -1101,3 +1101,139 @@ extern "C" co2_status_t co2_outer_step_ghost(co2_mode_t mode, int64_t n, const v
                                prev_x1_sum, p1_div, xbar_sum, xbar_div, ghost_copies, momentum,
                                anchor_out, bar0_out, params_out, gap_out, h, ws, S(stream));
 }
+
+// ==================================================== baseline outer steps
+// SlowMo, Local-SGD and Overlap-Local-SGD outer updates
+// (proj/src/outer_algorithms.cpp:213-313) on the same kernel family: one
+// HBM pass per worker, IEEE ops in the reference's order, max_outer_step and
+// the reference's finiteness checks reduced into the workspace.
+namespace co2 {
+namespace {
+
+enum BaseOp { B_SLOWMO = 0, B_LOCAL = 1, B_OVERLAP = 2 };
+
+struct BaseArgs {
+  const void* x;   // x_start (state)              SLOWMO, LOCAL
+  const void* xb;  // consumed reduce (low)        all
+  void* m;         // momentum (state, in/out)     SLOWMO
+  void* params;    // params (low): out / in-out   all
+  void* anchor;    // SLOWMO/LOCAL: x_{t+1,0} out (state, nullable); OVERLAP: anchor in
+  int64_t n;
+  double alpha, beta;
+  int divisor;
+  void* ws;
+};
+
+template <class M, int OP>
+__global__ void __launch_bounds__(kThreads) baseline_kernel(const BaseArgs a) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  const TC af = (TC)a.alpha, bf = (TC)a.beta, gd = (TC)a.divisor;
+  AccT<TC> acc;
+  const TS* X = static_cast<const TS*>(a.x);
+  const TL* XB = static_cast<const TL*>(a.xb);
+  TS* Mm = static_cast<TS*>(a.m);
+  TL* PR = static_cast<TL*>(a.params);
+  TS* A = static_cast<TS*>(a.anchor);
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < a.n;
+       j += (int64_t)gridDim.x * kThreads) {
+    TC xb = to_c(XB[j]);
+    if (a.divisor > 1) xb = xb / gd;  // average(): one division, param_ops.cpp:30
+    if (OP == B_SLOWMO) {             // outer_algorithms.cpp:229-233
+      TC x = to_c(X[j]);
+      TC delta = x - xb;
+      TC bm = bf * to_c(Mm[j]);
+      TC mn = bm + delta;
+      TC am = af * mn;
+      TC xn = x - am;
+      if (!isfinite(mn)) acc.flags |= CO2_FLAG_SLOWMO_M;
+      if (!isfinite(xn)) acc.flags |= CO2_FLAG_SLOWMO_X;
+      Mm[j] = (TS)mn;
+      PR[j] = Store<TL>::from(xn);
+      if (A) A[j] = (TS)xn;
+      TC st = fabs(xn - x);
+      acc.max_step = st > acc.max_step ? st : acc.max_step;
+    } else if (OP == B_LOCAL) {  // outer_algorithms.cpp:252-255
+      TC st = fabs(xb - to_c(X[j]));
+      acc.max_step = st > acc.max_step ? st : acc.max_step;
+      PR[j] = Store<TL>::from(xb);
+      if (A) A[j] = (TS)xb;
+    } else {  // B_OVERLAP, outer_algorithms.cpp:278-279
+      TC p = to_c(PR[j]);
+      TC d = to_c(A[j]) - xb;
+      TC pn = p - d;
+      if (!isfinite(pn)) acc.flags |= CO2_FLAG_OVERLAP;
+      TL stored = Store<TL>::from(pn);
+      PR[j] = stored;
+      TC st = fabs(to_c(stored) - p);
+      acc.max_step = st > acc.max_step ? st : acc.max_step;
+    }
+  }
+  block_finish<kThreads>(acc.widen(), a.ws);
+}
+
+template <int OP>
+co2_status_t launch_baseline(co2_mode_t mode, const BaseArgs& a, cudaStream_t s) {
+  int grid = simple_grid(a.n, kThreads);
+  if (grid > kMaxBlocks) grid = kMaxBlocks;
+  switch (mode) {
+    case CO2_MODE_F64: baseline_kernel<ModeF64, OP><<<grid, kThreads, 0, s>>>(a); break;
+    case CO2_MODE_F32: baseline_kernel<ModeF32, OP><<<grid, kThreads, 0, s>>>(a); break;
+    case CO2_MODE_BF16_MIXED: baseline_kernel<ModeBF16, OP><<<grid, kThreads, 0, s>>>(a); break;
+    default: return fail(CO2_ERR_VALIDATION, "baseline step: unknown mode %d", (int)mode);
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+}  // namespace
+
+co2_status_t slowmo_impl(co2_mode_t mode, int64_t n, const void* x_start, const void* xbar,
+                         int32_t divisor, void* m, void* params_out, void* anchor_out,
+                         double alpha, double beta, void* ws, cudaStream_t s) {
+  BaseArgs a{x_start, xbar, m, params_out, anchor_out, n, alpha, beta, divisor, ws};
+  return launch_baseline<B_SLOWMO>(mode, a, s);
+}
+co2_status_t local_sgd_impl(co2_mode_t mode, int64_t n, const void* x_start, const void* xbar,
+                            int32_t divisor, void* params_out, void* anchor_out, void* ws,
+                            cudaStream_t s) {
+  BaseArgs a{x_start, xbar, nullptr, params_out, anchor_out, n, 0.0, 0.0, divisor, ws};
+  return launch_baseline<B_LOCAL>(mode, a, s);
+}
+co2_status_t overlap_correction_impl(co2_mode_t mode, int64_t n, void* params, const void* anchor,
+                                     const void* xbar, int32_t divisor, void* ws,
+                                     cudaStream_t s) {
+  BaseArgs a{nullptr, xbar, nullptr, params, const_cast<void*>(anchor), n, 0.0, 0.0, divisor,
+             ws};
+  return launch_baseline<B_OVERLAP>(mode, a, s);
+}
+
+}  // namespace co2
+
+extern "C" co2_status_t co2_slowmo_step(co2_mode_t mode, int64_t n, const void* x_start,
+                                        const void* xbar, int32_t divisor, void* momentum,
+                                        void* params_out, void* anchor_out, double alpha,
+                                        double beta, void* ws, void* stream) {
+  // slowmo_round's checks, outer_algorithms.cpp:219-222
+  if (!(alpha > 0.0)) return fail(CO2_ERR_VALIDATION, "slowmo: alpha must be positive");
+  if (beta < 0.0 || beta >= 1.0) return fail(CO2_ERR_VALIDATION, "slowmo: beta must lie in [0, 1)");
+  if (n < 0 || divisor < 1 || !ws) return fail(CO2_ERR_VALIDATION, "slowmo: bad arguments");
+  return slowmo_impl(mode, n, x_start, xbar, divisor, momentum, params_out, anchor_out, alpha,
+                     beta, ws, S(stream));
+}
+
+extern "C" co2_status_t co2_local_sgd_step(co2_mode_t mode, int64_t n, const void* x_start,
+                                           const void* xbar, int32_t divisor, void* params_out,
+                                           void* anchor_out, void* ws, void* stream) {
+  if (n < 0 || divisor < 1 || !ws) return fail(CO2_ERR_VALIDATION, "local_sgd: bad arguments");
+  return local_sgd_impl(mode, n, x_start, xbar, divisor, params_out, anchor_out, ws, S(stream));
+}
+
+extern "C" co2_status_t co2_overlap_correction(co2_mode_t mode, int64_t n, void* params,
+                                               const void* anchor, const void* xbar,
+                                               int32_t divisor, void* ws, void* stream) {
+  if (n < 0 || divisor < 1 || !ws)
+    return fail(CO2_ERR_VALIDATION, "overlap correction: bad arguments");
+  return overlap_correction_impl(mode, n, params, anchor, xbar, divisor, ws, S(stream));
+}

@@ -29,10 +29,11 @@ def must_contain(path: str, *literals: str) -> None:
 
 def main() -> None:
     # ---- fixture co2_dim1 (replayed bitwise, proj/src/harness.cpp:336-500)
-    fx = json.loads(src("fixtures/co2_dim1.json"))
-    fx["_source"] = "proj/fixtures/co2_dim1.json (reference fixture, tolerance 0)"
-    with open(os.path.join(HERE, "co2_dim1.json"), "w") as f:
-        json.dump(fx, f, indent=1)
+    for name in ("co2_dim1", "slowmo_dim1", "local_sgd_dim1", "overlap_dim1"):
+        fx = json.loads(src(f"fixtures/{name}.json"))
+        fx["_source"] = f"proj/fixtures/{name}.json (reference fixture, tolerance 0)"
+        with open(os.path.join(HERE, f"{name}.json"), "w") as f:
+            json.dump(fx, f, indent=1)
 
     kats: dict = {}
 

@@ -40,6 +40,57 @@ def inner_loop(features, targets, rows, x: np.ndarray, lr: float, tau: int):
     return x_start, x_first, x
 
 
+class OracleBaselineRound:
+    """slowmo_round / local_sgd_round / overlap_local_sgd_round
+    (proj/src/outer_algorithms.cpp:213-313) on the CPU oracle, fp64."""
+
+    def __init__(self, kind: str, workers: int, n: int, alpha=1.0, beta=0.0,
+                 instant: bool = False):
+        from oracle import oracle as O
+        self.O, self.kind, self.g = O, kind, workers
+        self.alpha, self.beta, self.instant = alpha, beta, instant
+        self.m = [np.zeros(n) for _ in range(workers)]
+        self.anchor = [None] * workers
+        self.pending = None
+
+    def round(self, params, traces):
+        O = self.O
+        if self.kind == "slowmo":
+            avg = O.average(params)
+            out = []
+            for i in range(self.g):
+                m, p, _, code, msg = O.slowmo_step(O.MODE_F64, traces[i][0], avg, self.m[i],
+                                                   self.alpha, self.beta)
+                assert code == 0, msg
+                self.m[i] = m
+                out.append(p)
+            return out, avg
+        if self.kind == "local_sgd":
+            avg = O.average(params)
+            return [avg.copy() for _ in range(self.g)], avg
+        # overlap_local_sgd
+        params = [p.copy() for p in params]
+        consumed = None
+        if self.pending is not None:
+            consumed = self.pending
+            for i in range(self.g):
+                params[i], _, code, msg = O.overlap_correction(O.MODE_F64, params[i],
+                                                               self.anchor[i], consumed)
+                assert code == 0, msg
+            self.pending = None
+        self.anchor = [p.copy() for p in params]
+        avg = O.average(self.anchor)
+        if self.instant:
+            consumed = avg
+            for i in range(self.g):
+                params[i], _, code, msg = O.overlap_correction(O.MODE_F64, params[i],
+                                                               self.anchor[i], avg)
+                assert code == 0, msg
+        else:
+            self.pending = avg
+        return params, consumed
+
+
 class OracleRound:
     """co2_round (proj/src/outer_algorithms.cpp:110-211) on the CPU oracle."""
 

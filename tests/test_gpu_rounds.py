@@ -298,3 +298,91 @@ def test_sharded_world1_equals_worker_local(mode):
         sw.round(eng_s, hw, tau)
     sw.drain(eng_s)
     co2.co2_round_drain([w], eng_w)
+
+
+# ------------------------------------------- baseline outer algorithms (8f-3)
+@pytest.mark.parametrize("name", ["slowmo_dim1", "local_sgd_dim1", "overlap_dim1"])
+def test_baseline_fixtures_on_gpu(name):
+    """proj/fixtures/{slowmo,local_sgd,overlap}_dim1.json at tolerance 0
+    through the product's baseline round drivers (F64, 2 simulated workers)."""
+    import json
+    import os
+
+    from conftest import ROOT
+    with open(os.path.join(ROOT, "tests", "golden", f"{name}.json")) as f:
+        fx = json.load(f)
+    feats = np.array(fx["features"], dtype=np.float64)
+    targs = np.array(fx["targets"], dtype=np.float64)
+    shards, tau, lr = fx["shards"], fx["tau"], fx["schedule"]["base_lr"]
+    g, n = len(shards), len(fx["init"])
+    h = fx.get("hyper", {})
+    eng = co2.CollectiveEngine(g, transport="local")
+    init = torch.tensor(fx["init"], dtype=torch.float64, device="cuda")
+    ws = [co2.Worker(co2.MODE_F64, n, init) for _ in range(g)]
+    for er in fx["expect"]["rounds"]:
+        ends = []
+        for i, w in enumerate(ws):
+            w.snapshot_start()
+            xs, xf, xe = inner_loop(feats, targs, shards[i], w.params.cpu().numpy(), lr, tau)
+            w.params.copy_(torch.from_numpy(xe))
+            ends.append(xe)
+        if fx["algorithm"] == "slowmo":
+            co2.slowmo_round(ws, eng, h["alpha"], h["beta"])
+        elif fx["algorithm"] == "local_sgd":
+            co2.local_sgd_round(ws, eng)
+        else:
+            co2.overlap_local_sgd_round(ws, eng, instant="cluster" not in fx)
+        if "consumed_average" in er:
+            assert ws[0].buffer(L.BUF_XBAR).cpu().numpy().tolist() == er["consumed_average"]
+        for i, ew in enumerate(er["workers"]):
+            assert ends[i].tolist() == ew["x_end"]
+            assert ws[i].params.cpu().numpy().tolist() == ew["params_after"]
+            if "momentum_after" in ew:
+                assert ws[i].buffer(L.BUF_MOMENTUM).cpu().numpy().tolist() == \
+                    ew["momentum_after"]
+    assert [w.params.cpu().numpy().tolist() for w in ws] == fx["expect"]["final_params"]
+
+
+@pytest.mark.parametrize("mode", [co2.MODE_F64, co2.MODE_F32, co2.MODE_BF16_MIXED])
+def test_baseline_steps_bitwise(mode):
+    """The three baseline per-worker kernels vs the oracle's same-order
+    restatement, with a worker-sum xbar (divisor 3)."""
+    n = 100_003
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    ox, op0, op1, oxe, om = O.synth(mode, n)
+    ws = co2.Workspace()
+    st = torch.cuda.current_stream().cuda_stream
+    # SlowMo
+    mm, params = m.clone(), torch.empty_like(xe)
+    co2.check(co2.lib().co2_slowmo_step(mode, n, x.data_ptr(), xe.data_ptr(), 3, mm.data_ptr(),
+                                        params.data_ptr(), None, 0.8, 0.6, ws.ptr, st))
+    d = ws.fetch()
+    rm, rp, rd, code, _ = O.slowmo_step(mode, ox, oxe, om, 0.8, 0.6, divisor=3)
+    assert code == 0 and to_np(mm).tobytes() == rm.tobytes()
+    assert to_np(params).tobytes() == rp.tobytes() and d.max_outer_step == rd.max_outer_step
+    # Local-SGD
+    params = torch.empty_like(xe)
+    co2.check(co2.lib().co2_local_sgd_step(mode, n, x.data_ptr(), xe.data_ptr(), 3,
+                                           params.data_ptr(), None, ws.ptr, st))
+    d = ws.fetch()
+    rp, rd, code = O.local_sgd_step(mode, ox, oxe, divisor=3)
+    assert to_np(params).tobytes() == rp.tobytes() and d.max_outer_step == rd.max_outer_step
+    # Overlap correction (params in place; anchor in the state dtype)
+    params = p1.clone()
+    co2.check(co2.lib().co2_overlap_correction(mode, n, params.data_ptr(), x.data_ptr(),
+                                               xe.data_ptr(), 3, ws.ptr, st))
+    d = ws.fetch()
+    rp, rd, code, _ = O.overlap_correction(mode, op1, ox, oxe, divisor=3)
+    assert to_np(params).tobytes() == rp.tobytes() and d.max_outer_step == rd.max_outer_step
+    # errors carry the reference's messages
+    bad = x.clone()
+    bad[5] = float("nan")
+    co2.check(co2.lib().co2_slowmo_step(mode, n, bad.data_ptr(), xe.data_ptr(), 1,
+                                        m.clone().data_ptr(), params.data_ptr(), None, 0.8, 0.6,
+                                        ws.ptr, st))
+    with pytest.raises(co2.NumericError, match="slowmo momentum"):
+        ws.fetch()
+    with pytest.raises(co2.ValidationError, match="slowmo: beta"):
+        co2.check(co2.lib().co2_slowmo_step(mode, n, x.data_ptr(), xe.data_ptr(), 1,
+                                            m.data_ptr(), params.data_ptr(), None, 0.8, 1.0,
+                                            ws.ptr, st))
