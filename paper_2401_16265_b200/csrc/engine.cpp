@@ -1343,7 +1343,12 @@ extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int
     const void* xbar = e->transport == T_LOCAL ? w0->avg[(w0->t + 1) % 2]
                                                : ws[0]->params[1 - ws[0]->cur];
     CO2_TRY(correct(xbar, e->transport == T_NCCL ? e->world : 1));
-    for (int i = 0; i < g; ++i) ws[i]->has_pending = false;
+    for (int i = 0; i < g; ++i) {
+      ws[i]->has_pending = false;
+      // LOCAL keeps the consumed average readable; in-place transports
+      // overwrite it with the next anchor snapshot below.
+      ws[i]->xbar = e->transport == T_LOCAL ? const_cast<void*>(xbar) : nullptr;
+    }
   }
   // Fresh anchors (:284-288), snapshotted into the spare buffer for the reduce.
   const void* bufs[64];
@@ -1363,6 +1368,7 @@ extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int
     CO2_TRY(co2_aar_poll(e, h, &done));
     CO2_TRY(co2_aar_wait(e, h, stream));
     CO2_TRY(correct(xbar, div));
+    for (int i = 0; i < g; ++i) ws[i]->xbar = const_cast<void*>(xbar);
   } else {
     for (int i = 0; i < g; ++i) {
       ws[i]->pending = h;
@@ -1370,7 +1376,6 @@ extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int
     }
   }
   for (int i = 0; i < g; ++i) {
-    ws[i]->xbar = const_cast<void*>(xbar);
     ws[i]->t += 1;
     if (!applied) {
       ws[i]->host_diag->flags = 0;
