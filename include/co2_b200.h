@@ -160,6 +160,13 @@ co2_status_t co2_clip_elementwise(co2_dtype_t dt, int64_t n, const void* v, doub
  * accumulation, one rounding to bf16. */
 co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const* contributions, int64_t n,
                          void* out, void* workspace, void* stream);
+/* Round diagnostic of Simulation::step (outer_algorithms.cpp:503-508):
+ * xbar = fixed-order average of the g workers' params, per_worker[i] =
+ * ||params_i - xbar||_2 (fp64 accumulation, deterministic fixed-order
+ * reduction), *max_out = max_i.  Synchronous; g <= 64.  Either output may
+ * be NULL. */
+co2_status_t co2_divergence(co2_dtype_t dt, int32_t g, const void* const* params, int64_t n,
+                            double* per_worker, double* max_out, void* workspace, void* stream);
 /* a - b elementwise (the delta of outer_algorithms.cpp:189) */
 co2_status_t co2_sub(co2_dtype_t dt, int64_t n, const void* a, const void* b, void* out,
                      void* stream);

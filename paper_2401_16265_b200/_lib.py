@@ -88,6 +88,7 @@ SIGNATURES = {
     "co2_clip_elementwise": (ST, [I32, I64, P, D, P, P, P]),
     "co2_average": (ST, [I32, I32, C.POINTER(P), I64, P, P, P]),
     "co2_sub": (ST, [I32, I64, P, P, P, P]),
+    "co2_divergence": (ST, [I32, I32, C.POINTER(P), I64, C.POINTER(D), C.POINTER(D), P, P]),
     "co2_convert": (ST, [I32, P, I32, P, I64, P]),
     "co2_synth": (ST, [I32, U64, I32, I64, I64, P, P, P, P, P, P]),
     "co2_synthetic_inner_step": (ST, [I32, I64, P, D, D, U64, I32, I64, I32, P]),

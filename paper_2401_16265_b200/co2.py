@@ -189,6 +189,20 @@ def average(contributions, *, stream=None):
     return out
 
 
+def divergence(params_list, *, stream=None) -> tuple[float, list[float]]:
+    """max_i ||x_i - xbar|| (Simulation::step, outer_algorithms.cpp:503-508);
+    returns (max, per-worker norms)."""
+    g = len(params_list)
+    n = _same_len(*params_list, msg="divergence: dimensions differ")
+    ptrs = (C.c_void_p * g)(*[_ptr(p) for p in params_list])
+    per = (C.c_double * g)()
+    mx = C.c_double()
+    ws = _ws(params_list[0].device)
+    check(lib().co2_divergence(_dtype(params_list[0]), g, ptrs, n, per, C.byref(mx), ws.ptr,
+                               _stream(stream)))
+    return mx.value, list(per)
+
+
 # ------------------------------------------------------------- fused step
 def outer_step(mode: int, x_t0, prev_x0, prev_x1, xbar, momentum, hyper: Co2Hyper, tau: int, *,
                divisor: int = 1, anchor_out=None, params_out=None, gap_out=None,
@@ -430,6 +444,17 @@ class CollectiveEngine:
         kinds = ["launch", "complete", "wait"]
         return [{"event": kinds[arr[i].kind], "handle_id": arr[i].handle, "t_sim": arr[i].t,
                  "stall": arr[i].stall} for i in range(cnt.value)]
+
+    def write_events_jsonl(self, path: str) -> int:
+        """events.jsonl in the reference's schema (proj/src/harness.cpp:151-160,
+        proj/include/co2sim/collective.hpp:24-29), times from the device
+        clock (seconds since engine creation).  Returns the line count."""
+        import json
+        ev = sorted(self.events(), key=lambda e: (e["t_sim"], e["handle_id"]))
+        with open(path, "w") as f:
+            for e in ev:
+                f.write(json.dumps(e) + "\n")
+        return len(ev)
 
 
 # ---------------------------------------------------------- worker + round

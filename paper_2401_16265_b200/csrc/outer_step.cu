@@ -1211,6 +1211,117 @@ co2_status_t overlap_correction_impl(co2_mode_t mode, int64_t n, void* params, c
 
 }  // namespace co2
 
+// ====================================================== divergence metric
+// Simulation::step's round diagnostic (proj/src/outer_algorithms.cpp:
+// 503-508): xbar = average_params() (fixed worker order, one division) and
+// divergence = max_i ||x_i - xbar||_2.  Squares accumulate in fp64 per thread
+// in grid-stride order, then a fixed shuffle tree, fixed warp order and
+// fixed block order: deterministic for a given grid (Eigen's own reduction
+// order is SIMD-shaped, so the sum is within rounding, not bitwise).
+namespace co2 {
+namespace {
+constexpr int kDivBlocks = 256;
+constexpr int kDivMaxWorkers = 64;
+
+template <typename T, typename TC>
+__global__ void __launch_bounds__(kThreads)
+    divergence_kernel(const Ptrs64<T> c, int g, int64_t n, double* partials, double* out,
+                      unsigned int* ticket) {
+  __shared__ double sh[kThreads / 32][kDivMaxWorkers];
+  __shared__ bool s_last;
+  const TC gd = (TC)g;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int w0 = 0; w0 < g; w0 += 8) {  // 8 workers per pass keeps registers bounded
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * kThreads) {
+      TC s = to_c(c.p[0][j]);
+      for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
+      const TC xb = s / gd;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (w0 + k < g) {
+          const double d = (double)(to_c(c.p[w0 + k][j]) - xb);
+          acc[k] += d * d;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double v = acc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && w0 + k < g) sh[wid][w0 + k] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < g) {
+    double b = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) b += sh[w][threadIdx.x];
+    partials[(size_t)blockIdx.x * kDivMaxWorkers + threadIdx.x] = b;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < g) {
+    double tot = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b)
+      tot += __ldcg(&partials[(size_t)b * kDivMaxWorkers + threadIdx.x]);
+    out[threadIdx.x] = sqrt(tot);
+  }
+  if (threadIdx.x == 0) *ticket = 0;
+}
+}  // namespace
+}  // namespace co2
+
+extern "C" co2_status_t co2_divergence(co2_dtype_t dt, int32_t g, const void* const* params,
+                                       int64_t n, double* per_worker, double* max_out, void* ws,
+                                       void* stream) {
+  if (g < 1 || g > kDivMaxWorkers) return fail(CO2_ERR_VALIDATION, "divergence: 1..64 workers");
+  if (n < 0 || !ws) return fail(CO2_ERR_VALIDATION, "divergence: bad arguments");
+  CO2_TRY(check_dtype(dt));
+  cudaStream_t s = S(stream);
+  // Scratch inside the workspace's partials area: per-block per-worker sums,
+  // then g results and a private ticket.
+  char* base = reinterpret_cast<char*>(ws_partials(ws));
+  double* partials = reinterpret_cast<double*>(base);
+  double* out = partials + (size_t)kDivBlocks * kDivMaxWorkers;
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(out + kDivMaxWorkers);
+  static_assert(sizeof(double) * (kDivBlocks * kDivMaxWorkers + kDivMaxWorkers) + 16 <=
+                    sizeof(Partial) * kMaxBlocks,
+                "divergence scratch exceeds the workspace");
+  CO2_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s));
+  int grid = simple_grid(n, kThreads);
+  if (grid > kDivBlocks) grid = kDivBlocks;
+  if (dt == CO2_DTYPE_F64) {
+    Ptrs64<double> p{};
+    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const double*>(params[i]);
+    divergence_kernel<double, double><<<grid, kThreads, 0, s>>>(p, g, n, partials, out, ticket);
+  } else if (dt == CO2_DTYPE_F32) {
+    Ptrs64<float> p{};
+    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const float*>(params[i]);
+    divergence_kernel<float, float><<<grid, kThreads, 0, s>>>(p, g, n, partials, out, ticket);
+  } else {
+    Ptrs64<bf16s> p{};
+    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const bf16s*>(params[i]);
+    divergence_kernel<bf16s, float><<<grid, kThreads, 0, s>>>(p, g, n, partials, out, ticket);
+  }
+  CO2_CUDA(cudaGetLastError());
+  double host[kDivMaxWorkers];
+  CO2_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * g, cudaMemcpyDeviceToHost, s));
+  CO2_CUDA(cudaStreamSynchronize(s));
+  double mx = 0.0;
+  for (int i = 0; i < g; ++i) {
+    if (per_worker) per_worker[i] = host[i];
+    mx = host[i] > mx ? host[i] : mx;
+  }
+  if (max_out) *max_out = mx;
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_slowmo_step(co2_mode_t mode, int64_t n, const void* x_start,
                                         const void* xbar, int32_t divisor, void* momentum,
                                         void* params_out, void* anchor_out, double alpha,

@@ -300,6 +300,37 @@ def test_sharded_world1_equals_worker_local(mode):
     co2.co2_round_drain([w], eng_w)
 
 
+# --------------------------------------------- round diagnostics (8f-4)
+def test_divergence_metric_and_event_log(tmp_path, fixture_co2_dim1):
+    """Simulation::step's divergence (outer_algorithms.cpp:503-508): exactly 0
+    for identical workers, matches fp64 numpy otherwise, deterministic; and
+    the engine's events.jsonl follows the reference schema."""
+    rng = np.random.default_rng(5)
+    for dt in (torch.float64, torch.float32):
+        xs = [torch.from_numpy(rng.standard_normal(300_007)).to(dt).cuda() for _ in range(3)]
+        mx, per = co2.divergence(xs)
+        a = [x.double().cpu().numpy() for x in xs]
+        if dt == torch.float64:
+            xb = O.average(a)
+        else:
+            xb = O.average_lp([x.cpu().numpy() for x in xs], False).astype(np.float64)
+        ref = [np.linalg.norm(ai - xb) for ai in a]
+        assert np.allclose(per, ref, rtol=1e-10, atol=0)
+        assert mx == max(per)
+        assert co2.divergence(xs) == (mx, per)  # deterministic
+        same = [xs[0].clone() for _ in range(4)]
+        assert co2.divergence(same)[0] == 0.0
+    # ghost-consistent rounds keep workers identical -> divergence 0
+    rounds, ws, eng = run_fixture_rounds(dict(fixture_co2_dim1, rounds=4), ghost=True)
+    assert co2.divergence([w.params for w in ws])[0] == 0.0
+    n = eng.write_events_jsonl(str(tmp_path / "events.jsonl"))
+    import json
+    lines = [json.loads(x) for x in open(tmp_path / "events.jsonl")]
+    assert n == len(lines) and n > 0
+    assert set(lines[0]) == {"event", "handle_id", "t_sim", "stall"}
+    assert {e["event"] for e in lines} == {"launch", "complete", "wait"}
+
+
 # ------------------------------------------- baseline outer algorithms (8f-3)
 @pytest.mark.parametrize("name", ["slowmo_dim1", "local_sgd_dim1", "overlap_dim1"])
 def test_baseline_fixtures_on_gpu(name):
