@@ -1241,7 +1241,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (w0 + k < g) {
-          const double d = (double)(to_c(c.p[w0 + k][j]) - xb);
+          const double d = (double)to_c(c.p[w0 + k][j]) - (double)xb;  // exact widening
           acc[k] += d * d;
         }
       }
