@@ -186,6 +186,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--schedule", default="split", choices=["split", "fused"],
+                    help="P2P worker-local rounds: 'split' = reduce kernel on the comm stream "
+                         "overlapping the step kernel; 'fused' = one kernel does both")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
                     help="collective transport at N > 1; auto = the measured faster one: the "
                          "fixed-order P2P all-reduce for worker-local configs, NCCL "
@@ -271,6 +274,8 @@ def main():
         del init
         if transport == "p2p":
             eng.register_worker(w)
+            if args.schedule == "fused":
+                eng.set_fused(True)
         w.snapshot_start()
         w.snapshot_first()
         co2.co2_round([w], eng, hyper, tau)  # round 0: snapshots, launches the first reduce
@@ -372,6 +377,8 @@ def main():
                         + ("fixed-order NVLink P2P all-reduce)" if transport == "p2p"
                            else "NCCL all-reduce)")),
                        "transport": transport, "transport_note": transport_note,
+                       "schedule": (args.schedule if transport == "p2p" and not sharded
+                                    else "split"),
                        "l2": "inputs larger than L2 (no flush needed)",
                        "step": (("sharded co2_round: async P2P slice average of x_{t,tau} and "
                                  "x_{t,1} + stale wait + ONE kernel: ghost step on the shard "

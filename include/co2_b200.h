@@ -254,6 +254,13 @@ co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_t world, in
 void* co2_aar_signal_buffer(co2_aar_t* engine);
 co2_status_t co2_aar_p2p_attach_signals(co2_aar_t* engine, const uint8_t* handles);
 co2_status_t co2_aar_p2p_attach(co2_aar_t* engine, const void* local_buf, const uint8_t* handles);
+/* P2P only: run worker-local co2_round (t >= 1) as ONE kernel that does the
+ * outer step on the previously reduced average AND the fixed-order NVLink
+ * average of this round's x_{t,tau} (consumed next round, so the schedule
+ * stays one step stale), with cross-GPU entry / exit barriers.  Results are
+ * bitwise those of the two-kernel schedule; the reduce then overlaps the
+ * outer step's HBM stream instead of the inner loop. */
+co2_status_t co2_aar_set_fused(co2_aar_t* engine, int32_t on);
 co2_status_t co2_aar_destroy(co2_aar_t* engine);
 int32_t co2_aar_world(const co2_aar_t* engine);
 /* launch_all_reduce (collective.cpp:31-58).  NCCL: bufs[0] is reduced in

@@ -106,6 +106,7 @@ SIGNATURES = {
     "co2_aar_signal_buffer": (P, [P]),
     "co2_aar_p2p_attach_signals": (ST, [P, C.POINTER(C.c_uint8)]),
     "co2_aar_p2p_attach": (ST, [P, P, C.POINTER(C.c_uint8)]),
+    "co2_aar_set_fused": (ST, [P, I32]),
     "co2_aar_destroy": (ST, [P]),
     "co2_aar_world": (I32, [P]),
     "co2_aar_launch": (ST, [P, I32, C.POINTER(P), P, I64, P, C.POINTER(U64)]),

@@ -385,6 +385,10 @@ class CollectiveEngine:
         reducible; collective over the group."""
         check(lib().co2_aar_p2p_attach(self.handle, ptr, self._exchange(ptr)))
 
+    def set_fused(self, on: bool = True) -> None:
+        """P2P: fuse the one-step-stale all-reduce into the outer-step kernel."""
+        check(lib().co2_aar_set_fused(self.handle, int(on)))
+
     def register_worker(self, worker: "Worker") -> None:
         """P2P: register both ping-pong params buffers of a worker."""
         for which in (L.BUF_PARAMS, L.BUF_PARAMS_ALT):

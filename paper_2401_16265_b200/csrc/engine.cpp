@@ -71,6 +71,8 @@ struct co2_aar {
   // P2P transport
   int ctas = 0;
   uint32_t p2p_epoch = 0;
+  bool fused = false;        // worker-local rounds use the fused all-reduce + step kernel
+  uint32_t fused_epoch = 0;
   void* signals = nullptr;        // this rank's signal area (cudaMalloc, IPC-exported)
   std::vector<void*> peer_signals;  // rank-indexed (opened IPC pointers; own = signals)
   std::vector<P2PBuffer> p2p_bufs;
@@ -162,6 +164,13 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
 }
 
 extern "C" void* co2_aar_signal_buffer(co2_aar_t* e) { return e ? e->signals : nullptr; }
+
+extern "C" co2_status_t co2_aar_set_fused(co2_aar_t* e, int32_t on) {
+  if (!e || e->transport != T_P2P)
+    return fail(CO2_ERR_VALIDATION, "fused schedule: P2P transport only");
+  e->fused = on != 0;
+  return CO2_OK;
+}
 
 static co2_status_t open_peers(co2_aar* e, const void* local, const uint8_t* handles,
                                std::vector<void*>* out) {
@@ -712,6 +721,57 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     // before the collective touches the buffer.
     for (int i = 0; i < g; ++i)
       CO2_TRY(copy_dev(ws[i]->params[1 - ws[i]->cur], ws[i]->params[ws[i]->cur], lb, st));
+  }
+  if (w0->t > 0 && e->transport == T_P2P && e->fused && !hyper->ghost_consistent) {
+    // Fused schedule (t >= 1): ONE kernel consumes the average reduced by the
+    // previous launch (in params[1-cur]) for the outer step AND averages this
+    // round's x_{t,tau} (params[cur]) over NVLink for the next round -- the
+    // compute and the collective share the HBM stream instead of competing
+    // as two kernels on two streams.
+    co2_worker* w = w0;
+    if (w->has_pending) {  // the round-0 reduce (standalone P2P kernel)
+      int32_t done = 0;
+      CO2_TRY(co2_aar_poll(e, w->pending, &done));
+      CO2_TRY(co2_aar_wait(e, w->pending, stream));
+      w->has_pending = false;
+    }
+    const P2PBuffer* pb = find_p2p(e, w->params[w->cur]);
+    if (!pb) return fail(CO2_ERR_VALIDATION, "launch_all_reduce: buffer not registered for P2P");
+    const int64_t shard = ((n + e->world - 1) / e->world + 7) / 8 * 8;
+    const int64_t lo = std::min<int64_t>((int64_t)e->rank * shard, n);
+    const int64_t len = std::max<int64_t>(0, std::min<int64_t>(shard, n - lo));
+    void* out_params = w->params[1 - w->cur];
+    e->fused_epoch += 1;
+    const int64_t cap = (int64_t)w->tev.size() / 2;
+    const int64_t slot = cap ? w->tev_recorded % cap : 0;
+    if (cap) CO2_CUDA(cudaEventRecord(w->tev[2 * slot], st));
+    CO2_TRY(outer_step_fused_aar_impl(mode, n, w->anchor, w->prev_x0, w->prev_x1, out_params,
+                                      w->m, w->prev_x0, out_params, w->gap, hyper,
+                                      pb->ptrs.data(), lo, len, e->peer_signals.data(), e->world,
+                                      e->rank, e->fused_epoch, w->ws, st));
+    if (cap) {
+      CO2_CUDA(cudaEventRecord(w->tev[2 * slot + 1], st));
+      w->tev_recorded += 1;
+    }
+    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    std::swap(w->anchor, w->prev_x0);
+    std::swap(w->prev_x1, w->xfirst);
+    w->cur = 1 - w->cur;
+    w->xbar = nullptr;
+    w->t += 1;
+    r.outer_applied = 1;
+    if (sync) {
+      co2_status_t s = co2_round_finish(ws, g, stream, &r);
+      if (res) *res = r;
+      if (s != CO2_OK) return s;
+      uint32_t err = 0;
+      CO2_CUDA(cudaMemcpy(&err, static_cast<char*>(e->signals) + 36, 4, cudaMemcpyDeviceToHost));
+      if (err)
+        return fail(CO2_ERR_CUDA, "p2p fused step: cross-GPU barrier timed out (code %u)", err);
+      return CO2_OK;
+    }
+    if (res) *res = r;
+    return CO2_OK;
   }
   const void* bufs[64];
   for (int i = 0; i < g; ++i) bufs[i] = ws[i]->params[ws[i]->cur];

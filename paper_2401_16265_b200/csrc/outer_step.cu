@@ -313,7 +313,39 @@ struct StepArgs {
   // P2P fused all-gather (P2POUT instantiations only)
   void* out_peers[kMaxRanks];
   P2PExit exit;
+  // Fused one-step-stale all-reduce (AARFUSE instantiations only): slice
+  // [aar_lo, aar_lo + aar_len) of the rank-indexed buffers aar_bufs (x_{t,tau}
+  // on every rank) is averaged in rank order and stored into every rank.
+  void* aar_bufs[kMaxRanks];
+  int64_t aar_lo, aar_len;
 };
+
+// One 16-byte vector of the fixed-order P2P average (param_ops.cpp:16-33):
+// gather from every rank, sum in rank order, divide once, store to every rank.
+template <typename TL, typename TC>
+__device__ __forceinline__ void aar_vector(const StepArgs& a, int64_t e) {
+  constexpr int VA = 16 / (int)sizeof(TL);
+  uint4 raw[kMaxRanks];
+#pragma unroll
+  for (int p = 0; p < kMaxRanks; ++p)
+    if (p < a.exit.world)
+      raw[p] = __ldcg(reinterpret_cast<const uint4*>(static_cast<const TL*>(a.aar_bufs[p]) + e));
+  TC acc[VA];
+#pragma unroll
+  for (int k = 0; k < VA; ++k) acc[k] = to_c(reinterpret_cast<const TL*>(&raw[0])[k]);
+#pragma unroll
+  for (int p = 1; p < kMaxRanks; ++p)
+    if (p < a.exit.world)
+#pragma unroll
+      for (int k = 0; k < VA; ++k) acc[k] = acc[k] + to_c(reinterpret_cast<const TL*>(&raw[p])[k]);
+  uint4 out;
+  const TC g = (TC)a.exit.world;
+#pragma unroll
+  for (int k = 0; k < VA; ++k) reinterpret_cast<TL*>(&out)[k] = Store<TL>::from(acc[k] / g);
+#pragma unroll
+  for (int p = 0; p < kMaxRanks; ++p)
+    if (p < a.exit.world) __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.aar_bufs[p]) + e), out);
+}
 
 // average() of g identical copies (param_ops.cpp:26-30 with every
 // contribution equal): ascending-order sum, one division.
@@ -324,7 +356,8 @@ __device__ __forceinline__ TC ghost_avg(TC v, int g) {
   return s / (TC)g;
 }
 
-template <class M, int V, int U, int NT, int MINB, bool GHOST = false, bool P2POUT = false>
+template <class M, int V, int U, int NT, int MINB, bool GHOST = false, bool P2POUT = false,
+          bool AARFUSE = false>
 __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
@@ -357,6 +390,24 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
   const int64_t nv = a.n / V;
   const int64_t stride = (int64_t)gridDim.x * NT;
   int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+  // AARFUSE: every rank's x_{t,tau} is final once all ranks arrived; the
+  // all-reduce vectors are interleaved with the outer-step vectors (one per
+  // world-size step vectors) so both streams share HBM and NVLink evenly.
+  constexpr int VA = 16 / (int)sizeof(TL);
+  const int64_t aar_nvec = AARFUSE ? a.aar_len / VA : 0;
+  bool aar_ok = true;
+  if constexpr (AARFUSE) {
+    __shared__ int s_go;
+    if (threadIdx.x == 0) s_go = p2p_entry_barrier(a.exit);
+    __syncthreads();
+    aar_ok = s_go != 0;
+  }
+  const int gw = AARFUSE ? a.exit.world : 1;
+  auto aar_for = [&](int64_t iv) {
+    if constexpr (AARFUSE) {
+      if (aar_ok && iv % gw == 0 && iv / gw < aar_nvec) aar_vector<TL, TC>(a, a.aar_lo + (iv / gw) * VA);
+    }
+  };
 
   auto process = [&](const int64_t (&idx)[U], int cnt) {
     TS x[U][V], q0[U][V], mo[U][V];
@@ -418,12 +469,31 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
 #pragma unroll
     for (int u = 0; u < U; ++u) idx[u] = i + (int64_t)u * stride;
     process(idx, U);
+#pragma unroll
+    for (int u = 0; u < U; ++u) aar_for(idx[u]);
   }
   for (; i < nv; i += stride) {
     int64_t idx[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) idx[u] = i;
     process(idx, 1);
+    aar_for(i);
+  }
+  if constexpr (AARFUSE) {
+    // all-reduce vectors not covered by the interleave, then its scalar tail
+    const int64_t covered = (nv + gw - 1) / gw;
+    for (int64_t ia = covered + (int64_t)blockIdx.x * NT + threadIdx.x; aar_ok && ia < aar_nvec;
+         ia += stride)
+      aar_vector<TL, TC>(a, a.aar_lo + ia * VA);
+    if (aar_ok && blockIdx.x == 0) {
+      for (int64_t j = a.aar_lo + aar_nvec * VA + threadIdx.x; j < a.aar_lo + a.aar_len;
+           j += NT) {
+        TC s0 = to_c(static_cast<const TL*>(a.aar_bufs[0])[j]);
+        for (int p = 1; p < a.exit.world; ++p) s0 = s0 + to_c(static_cast<const TL*>(a.aar_bufs[p])[j]);
+        const TL r = Store<TL>::from(s0 / (TC)a.exit.world);
+        for (int p = 0; p < a.exit.world; ++p) static_cast<TL*>(a.aar_bufs[p])[j] = r;
+      }
+    }
   }
   // Scalar tail (n % V coordinates).
   const int64_t t = nv * V + (int64_t)blockIdx.x * NT + threadIdx.x;
@@ -450,7 +520,7 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
     }
     if (G) G[t] = (TS)lam;
   }
-  if constexpr (P2POUT)
+  if constexpr (P2POUT || AARFUSE)
     block_finish<NT>(acc.widen(), a.ws, &a.exit);
   else
     block_finish<NT>(acc.widen(), a.ws);
@@ -799,6 +869,50 @@ co2_status_t outer_step_impl(co2_mode_t mode, int64_t n, const void* x_t0, const
     case CO2_MODE_F64: return launch_fused<ModeF64>(a, s);
     case CO2_MODE_F32: return launch_fused<ModeF32>(a, s);
     case CO2_MODE_BF16_MIXED: return launch_fused<ModeBF16>(a, s);
+  }
+  return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
+}
+
+namespace {
+template <class M>
+co2_status_t launch_fused_aar(const StepArgs& a, cudaStream_t s) {
+  constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+  bool ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
+            aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap);
+  for (int p = 0; p < a.exit.world; ++p) ok = ok && aligned16(a.aar_bufs[p]);
+  if (!ok) return fail(CO2_ERR_VALIDATION, "fused all-reduce step: buffers must be 16-byte aligned");
+  auto k = fused_step_kernel<M, V, 1, kThreads, 4, false, false, true>;
+  k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+}  // namespace
+
+co2_status_t outer_step_fused_aar_impl(co2_mode_t mode, int64_t n, const void* x_t0,
+                                       const void* p0, const void* p1, const void* xbar_avg,
+                                       void* m, void* anchor, void* params, void* gap,
+                                       const co2_hyper_t* h, void* const* aar_bufs,
+                                       int64_t aar_lo, int64_t aar_len, void* const* sigs,
+                                       int world, int rank, uint32_t epoch, void* ws,
+                                       cudaStream_t s) {
+  if (world < 1 || world > kMaxRanks)
+    return fail(CO2_ERR_VALIDATION, "fused all-reduce step: world must lie in [1, %d]", kMaxRanks);
+  StepArgs a{x_t0, p0, p1, xbar_avg, m, anchor, params, gap, n, h->alpha, h->beta, h->phi,
+             h->epsilon, h->tau, 1, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, 0, 0, nullptr};
+  for (int p = 0; p < world; ++p) {
+    a.aar_bufs[p] = aar_bufs[p];
+    a.exit.sig[p] = static_cast<Signals*>(sigs[p]);
+  }
+  a.exit.world = world;
+  a.exit.rank = rank;
+  a.exit.epoch = epoch;
+  a.exit.counter = 1;
+  a.aar_lo = aar_lo;
+  a.aar_len = aar_len;
+  switch (mode) {
+    case CO2_MODE_F64: return launch_fused_aar<ModeF64>(a, s);
+    case CO2_MODE_F32: return launch_fused_aar<ModeF32>(a, s);
+    case CO2_MODE_BF16_MIXED: return launch_fused_aar<ModeBF16>(a, s);
   }
   return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
 }

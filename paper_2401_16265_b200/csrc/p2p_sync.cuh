@@ -12,14 +12,17 @@ constexpr int kMaxRanks = 8;
 // Per-rank signal area (256 B, IPC-exported):
 //   ready[r]  written by rank r at the start of a slice-reduce launch
 //   done      counts finished all-reduce CTAs (fixed-order P2P average)
-//   error     1/2/3: a bounded spin timed out
+//   error     1/2/3/4/5: a bounded spin timed out
 //   done2     counts ranks that finished the fused sharded step's stores
+//   ready2[r] / done3: entry / exit of the fused all-reduce + outer step
 struct Signals {
   uint32_t ready[kMaxRanks];
   uint32_t done;
   uint32_t error;
   uint32_t done2;
-  uint32_t pad[53];
+  uint32_t ready2[kMaxRanks];
+  uint32_t done3;
+  uint32_t pad[44];
 };
 static_assert(sizeof(Signals) == 256, "signal area layout");
 
@@ -54,13 +57,27 @@ struct P2PExit {
   Signals* sig[kMaxRanks];  // rank-indexed signal areas
   int world, rank;
   uint32_t epoch;           // 1, 2, ... per fused launch, same on every rank
+  int counter;              // 0: done2 (sharded step), 1: done3 (fused all-reduce step)
 };
 
 __device__ inline void p2p_exit_barrier(const P2PExit& x) {
   __threadfence_system();
-  for (int p = 0; p < x.world; ++p) red_release_sys_add(&x.sig[p]->done2, 1u);
-  if (!spin_until(&x.sig[x.rank]->done2, x.epoch * (uint32_t)x.world))
-    x.sig[x.rank]->error = 3;
+  for (int p = 0; p < x.world; ++p)
+    red_release_sys_add(x.counter ? &x.sig[p]->done3 : &x.sig[p]->done2, 1u);
+  const uint32_t* mine = x.counter ? &x.sig[x.rank]->done3 : &x.sig[x.rank]->done2;
+  if (!spin_until(mine, x.epoch * (uint32_t)x.world)) x.sig[x.rank]->error = x.counter ? 5 : 3;
+}
+
+// Entry barrier of the fused all-reduce + outer step: every CTA publishes
+// this rank's arrival and waits for all ranks (their x_{t,tau} is final).
+__device__ inline bool p2p_entry_barrier(const P2PExit& x) {
+  for (int p = 0; p < x.world; ++p) st_release_sys(&x.sig[p]->ready2[x.rank], x.epoch);
+  for (int p = 0; p < x.world; ++p)
+    if (!spin_until(&x.sig[x.rank]->ready2[p], x.epoch)) {
+      x.sig[x.rank]->error = 4;
+      return false;
+    }
+  return true;
 }
 
 }  // namespace co2

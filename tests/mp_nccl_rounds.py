@@ -44,15 +44,17 @@ def main():
     mode = int(os.environ.get("CO2_TEST_MODE", "1"))
     n, tau, rounds = 1 << 20, 4, 4
     transport = os.environ.get("CO2_TEST_TRANSPORT", "nccl")
-    if transport == "p2p":
+    if transport in ("p2p", "p2pfused"):
         eng = co2.CollectiveEngine(world, transport="p2p", rank=rank)
+        if transport == "p2pfused":
+            eng.set_fused(True)
     else:
         uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
         eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid)
     hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
     init = co2.synth(mode, n, worker=rank)[3]
     w = co2.Worker(mode, n, init)
-    if transport == "p2p":
+    if transport in ("p2p", "p2pfused"):
         eng.register_worker(w)
     ok, worst = True, None
     if rank == 0:

@@ -24,7 +24,8 @@ def _port():
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("transport,world", [("nccl", 2), ("p2p", 2), ("p2p", 4)])
+@pytest.mark.parametrize("transport,world", [("nccl", 2), ("p2p", 2), ("p2p", 4),
+                                             ("p2pfused", 2), ("p2pfused", 4)])
 def test_multi_rank_rounds_bitwise(mode, transport, world):
     """Worker-local co2_round across ranks, bitwise against the oracle.  NCCL's
     sum is order-free only for G = 2; the P2P transport's fixed-order average
@@ -41,7 +42,9 @@ def test_multi_rank_rounds_bitwise(mode, transport, world):
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     res = json.loads(line)
     assert res["ok"], res
-    assert res["waits"] == 3
+    # two-kernel schedule: one wait per consumed reduce (rounds 1..3); fused:
+    # only the round-0 reduce is a separate handle
+    assert res["waits"] == (1 if transport == "p2pfused" else 3)
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
