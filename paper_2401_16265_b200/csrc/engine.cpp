@@ -41,9 +41,16 @@ struct Handle {
   cudaEvent_t start = nullptr, done = nullptr, wait_begin = nullptr, wait_end = nullptr;
   bool consumed = false, polled = false, last_poll = false, completion_logged = false;
   bool waited = false;
-  co2_diag_t* diag = nullptr;  // LOCAL: pinned copy of the average's flags
-  uint32_t* p2p_error = nullptr;  // P2P: pinned copy of the signal area's error word
+  co2_diag_t* diag = nullptr;  // LOCAL: pinned copy of the average's flags (pool slot)
+  uint32_t* p2p_error = nullptr;  // P2P: pinned copy of the signal area's error word (pool slot)
+  // After kRing newer launches a handle's events are recycled; its device
+  // times and status are cached first (the reference keeps every record).
+  bool cached = false;
+  double c_start = 0, c_done = 0, c_wait_end = 0, c_stall = 0, c_comm = 0;
+  uint32_t c_flags = 0, c_err = 0;
 };
+
+constexpr size_t kRing = 256;
 
 // A buffer registered with the P2P transport: the same logical buffer on
 // every rank (rank-indexed device pointers, peers opened via CUDA IPC).
@@ -77,6 +84,10 @@ struct co2_aar {
   std::vector<void*> peer_signals;  // rank-indexed (opened IPC pointers; own = signals)
   std::vector<P2PBuffer> p2p_bufs;
   std::vector<void*> opened;      // IPC pointers to close
+  // pinned per-launch slots (ring) and the reusable producer fence
+  co2_diag_t* pin_diag = nullptr;
+  uint32_t* pin_err = nullptr;
+  cudaEvent_t fence = nullptr;
 };
 
 static co2_status_t engine_common_init(co2_aar* e) {
@@ -227,9 +238,10 @@ extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
   for (Handle& h : e->handles) {
     for (cudaEvent_t ev : {h.start, h.done, h.wait_begin, h.wait_end})
       if (ev) cudaEventDestroy(ev);
-    if (h.diag) cudaFreeHost(h.diag);
-    if (h.p2p_error) cudaFreeHost(h.p2p_error);
   }
+  if (e->pin_diag) cudaFreeHost(e->pin_diag);
+  if (e->pin_err) cudaFreeHost(e->pin_err);
+  if (e->fence) cudaEventDestroy(e->fence);
   if (e->comm2) ncclCommDestroy(e->comm2);
   if (e->comm) ncclCommDestroy(e->comm);
   if (e->ws) cudaFree(e->ws);
@@ -249,6 +261,64 @@ static co2_status_t record_for(co2_aar* e, uint64_t h, Handle** out) {
   return CO2_OK;
 }
 
+static double ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms * 1e-3;
+}
+
+// Cache a finished handle's device times and status, then free its events
+// for reuse (handles older than kRing launches; at most two are ever live).
+static co2_status_t cache_handle(co2_aar* e, Handle& h) {
+  if (h.cached) return CO2_OK;
+  CO2_CUDA(cudaEventSynchronize(h.done));
+  h.c_start = ms_between(e->epoch, h.start);
+  h.c_done = ms_between(e->epoch, h.done);
+  h.c_comm = ms_between(h.start, h.done);
+  if (h.waited) {
+    CO2_CUDA(cudaEventSynchronize(h.wait_end));
+    h.c_stall = ms_between(h.wait_begin, h.wait_end);
+    h.c_wait_end = ms_between(e->epoch, h.wait_end);
+  }
+  h.c_flags = h.diag ? h.diag->flags : 0;
+  h.c_err = h.p2p_error ? *h.p2p_error : 0;
+  h.cached = true;
+  return CO2_OK;
+}
+
+// A new handle: events (recycled from the handle kRing launches back) and
+// pinned diagnostic slots from the engine's ring.
+static co2_status_t new_handle(co2_aar* e, Handle* h) {
+  const size_t id = e->handles.size();
+  if (!e->pin_diag) {
+    CO2_CUDA(cudaMallocHost(&e->pin_diag, kRing * sizeof(co2_diag_t)));
+    CO2_CUDA(cudaMallocHost(&e->pin_err, kRing * sizeof(uint32_t)));
+    CO2_CUDA(cudaEventCreateWithFlags(&e->fence, cudaEventDisableTiming));
+  }
+  if (id >= kRing) {
+    Handle& old = e->handles[id - kRing];
+    if (!old.consumed) return fail(CO2_ERR_VALIDATION, "aar: handle ring overrun");
+    CO2_TRY(cache_handle(e, old));
+    h->start = old.start;
+    h->done = old.done;
+    h->wait_begin = old.wait_begin;
+    h->wait_end = old.wait_end;
+    old.start = old.done = old.wait_begin = old.wait_end = nullptr;
+    old.diag = nullptr;
+    old.p2p_error = nullptr;
+  } else {
+    CO2_CUDA(cudaEventCreateWithFlags(&h->start, cudaEventDefault));
+    CO2_CUDA(cudaEventCreateWithFlags(&h->done, cudaEventDefault));
+    CO2_CUDA(cudaEventCreateWithFlags(&h->wait_begin, cudaEventDefault));
+    CO2_CUDA(cudaEventCreateWithFlags(&h->wait_end, cudaEventDefault));
+  }
+  h->diag = &e->pin_diag[id % kRing];
+  h->p2p_error = &e->pin_err[id % kRing];
+  h->diag->flags = 0;
+  *h->p2p_error = 0;
+  return CO2_OK;
+}
+
 // kind 0: all-reduce (NCCL in place / LOCAL average); kind 1: reduce-scatter
 // (sum) of the full buffer bufs[0] (n = world * shard) into out (one shard).
 static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const void* const* bufs,
@@ -260,16 +330,10 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
                 "launch_all_reduce: overlap window exceeded, two reduces already live");
   if (n < 0) return fail(CO2_ERR_VALIDATION, "launch_all_reduce: negative size");
   Handle h;
-  CO2_CUDA(cudaEventCreateWithFlags(&h.start, cudaEventDefault));
-  CO2_CUDA(cudaEventCreateWithFlags(&h.done, cudaEventDefault));
-  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_begin, cudaEventDefault));
-  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_end, cudaEventDefault));
+  CO2_TRY(new_handle(e, &h));
   // Fence: the reduce reads x_{t,tau} only after the producer wrote it.
-  cudaEvent_t fence;
-  CO2_CUDA(cudaEventCreateWithFlags(&fence, cudaEventDisableTiming));
-  CO2_CUDA(cudaEventRecord(fence, S(producer)));
-  CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, fence, 0));
-  CO2_CUDA(cudaEventDestroy(fence));
+  CO2_CUDA(cudaEventRecord(e->fence, S(producer)));
+  CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, e->fence, 0));
   CO2_CUDA(cudaEventRecord(h.start, e->comm_stream));
   if (kind == 1) {
     if (e->transport != T_NCCL)
@@ -290,8 +354,6 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     if (!pb) return fail(CO2_ERR_VALIDATION, "launch_all_reduce: buffer not registered for P2P");
     if (e->world > 1 && (int)e->peer_signals.size() != e->world)
       return fail(CO2_ERR_VALIDATION, "launch_all_reduce: P2P signals not attached");
-    CO2_CUDA(cudaMallocHost(&h.p2p_error, sizeof(uint32_t)));
-    *h.p2p_error = 0;
     if (e->world > 1 && n > 0) {
       e->p2p_epoch += 1;
       CO2_TRY(p2p_average_launch(dt, pb->ptrs.data(), e->peer_signals.data(), e->world, e->rank,
@@ -308,8 +370,6 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
                              e->comm, e->comm_stream));
   } else {
     CO2_TRY(co2_average(dt, e->workers, bufs, n, out, e->ws, e->comm_stream));
-    CO2_CUDA(cudaMallocHost(&h.diag, sizeof(co2_diag_t)));
-    h.diag->flags = 0;
     CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
   }
   CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
@@ -339,18 +399,10 @@ static co2_status_t launch_slice(co2_aar* e, co2_dtype_t dt, const void* src0, c
   if ((int)e->peer_signals.size() != e->world)
     return fail(CO2_ERR_VALIDATION, "slice reduce: P2P signals not attached");
   Handle h;
-  CO2_CUDA(cudaEventCreateWithFlags(&h.start, cudaEventDefault));
-  CO2_CUDA(cudaEventCreateWithFlags(&h.done, cudaEventDefault));
-  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_begin, cudaEventDefault));
-  CO2_CUDA(cudaEventCreateWithFlags(&h.wait_end, cudaEventDefault));
-  cudaEvent_t fence;
-  CO2_CUDA(cudaEventCreateWithFlags(&fence, cudaEventDisableTiming));
-  CO2_CUDA(cudaEventRecord(fence, S(producer)));
-  CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, fence, 0));
-  CO2_CUDA(cudaEventDestroy(fence));
+  CO2_TRY(new_handle(e, &h));
+  CO2_CUDA(cudaEventRecord(e->fence, S(producer)));
+  CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, e->fence, 0));
   CO2_CUDA(cudaEventRecord(h.start, e->comm_stream));
-  CO2_CUDA(cudaMallocHost(&h.p2p_error, sizeof(uint32_t)));
-  *h.p2p_error = 0;
   e->p2p_epoch += 1;
   CO2_TRY(p2p_slice_average_launch(dt, 2, b0->ptrs.data(), b1->ptrs.data(), dst0, dst1,
                                    e->peer_signals.data(), e->world, e->rank, lo, len,
@@ -404,20 +456,16 @@ extern "C" co2_status_t co2_aar_stall(co2_aar_t* e, uint64_t handle, double* sta
   Handle* h = nullptr;
   CO2_TRY(record_for(e, handle, &h));
   if (!h->waited) return fail(CO2_ERR_VALIDATION, "stall: handle not waited yet");
-  CO2_CUDA(cudaEventSynchronize(h->wait_end));
-  float ms = 0.f;
-  if (stall) {
-    CO2_CUDA(cudaEventElapsedTime(&ms, h->wait_begin, h->wait_end));
-    *stall = ms * 1e-3;
+  CO2_TRY(cache_handle(e, *h));
+  if (stall) *stall = h->c_stall;
+  if (comm) *comm = h->c_comm;
+  if (h->c_flags) {
+    co2_diag_t d{};
+    d.flags = h->c_flags;
+    return co2_diag_status(&d);
   }
-  if (comm) {
-    CO2_CUDA(cudaEventElapsedTime(&ms, h->start, h->done));
-    *comm = ms * 1e-3;
-  }
-  if (h->diag && h->diag->flags) return co2_diag_status(h->diag);
-  if (h->p2p_error && *h->p2p_error)
-    return fail(CO2_ERR_CUDA, "p2p all-reduce: cross-GPU barrier timed out (code %u)",
-                *h->p2p_error);
+  if (h->c_err)
+    return fail(CO2_ERR_CUDA, "p2p all-reduce: cross-GPU barrier timed out (code %u)", h->c_err);
   return CO2_OK;
 }
 
@@ -448,6 +496,12 @@ extern "C" co2_status_t co2_aar_events(co2_aar_t* e, co2_event_t* out, int64_t c
   };
   for (uint64_t i = 0; i < e->handles.size(); ++i) {
     Handle& h = e->handles[i];
+    if (h.cached) {  // events recycled: the cached device times
+      push(0, i, h.c_start, 0.0);
+      push(1, i, h.c_done, 0.0);
+      if (h.waited) push(2, i, h.c_wait_end, h.c_stall);
+      continue;
+    }
     CO2_CUDA(cudaEventSynchronize(h.done));
     float ms = 0.f;
     CO2_CUDA(cudaEventElapsedTime(&ms, e->epoch, h.start));
