@@ -124,6 +124,11 @@ co2_status_t co2_outer_step(co2_mode_t mode, int64_t n, const void* x_t0, const 
  * Also settable once per process with CO2_FUSED_VARIANT.  See
  * tools/tune_fused.py. */
 co2_status_t co2_set_fused_variant(int32_t variant);
+/* Tuning knob: grid size of the step kernels in waves of the idle-GPU
+ * resident CTA count (1 = persistent, the default; >1 oversubscribes so a
+ * co-running reduce kernel does not leave a late second wave).  Also
+ * CO2_GRID_WAVES. */
+co2_status_t co2_set_grid_waves(int32_t waves);
 
 /* End-to-end form of co2_outer_step over HOST buffers (the reference's own
  * calling convention: host vectors in, host vectors out).  Streams the

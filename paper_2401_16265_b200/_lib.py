@@ -80,6 +80,7 @@ SIGNATURES = {
     "co2_diag_status": (ST, [C.POINTER(Diag)]),
     "co2_outer_step": (ST, [I32, I64, P, P, P, P, I32, P, P, P, P, C.POINTER(Hyper), P, P]),
     "co2_set_fused_variant": (ST, [I32]),
+    "co2_set_grid_waves": (ST, [I32]),
     "co2_outer_step_host": (ST, [I32, I64, P, P, P, P, I32, P, P, P, C.POINTER(Hyper), I64, I32,
                                  C.POINTER(Diag)]),
     "co2_staleness_gap": (ST, [I32, I64, P, P, P, I32, D, P, P, P]),

@@ -528,16 +528,27 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
 
 constexpr int kThreads = 256;
 
+// Grid waves for the grid-stride kernels: 1 = exactly the resident CTAs of an
+// idle GPU (persistent).  When a reduce kernel co-runs on the comm stream it
+// holds registers on some SMs, so a persistent grid no longer fits in one
+// wave and its last CTAs start late; more, shorter CTAs let the hardware
+// scheduler balance instead (co2_set_grid_waves / CO2_GRID_WAVES).
+int g_waves = -1;
+int grid_waves() {
+  if (g_waves < 0) {
+    const char* e = getenv("CO2_GRID_WAVES");
+    g_waves = e ? atoi(e) : 1;
+    if (g_waves < 1) g_waves = 1;
+  }
+  return g_waves;
+}
+
 template <typename K>
 int grid_for(K kernel, int64_t work_items, int threads) {
-  static int cached_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
-  (void)cached_dev;
   if (per_sm < 1) per_sm = 1;
-  int64_t cap = (int64_t)per_sm * sm_count();
+  int64_t cap = (int64_t)per_sm * sm_count() * grid_waves();
   if (cap > kMaxBlocks) cap = kMaxBlocks;
   int64_t need = (work_items + threads - 1) / threads;
   if (need < 1) need = 1;
@@ -966,6 +977,12 @@ co2_status_t outer_step_ghost_impl(co2_mode_t mode, int64_t n, const void* ancho
 }  // namespace co2
 
 using namespace co2;
+
+extern "C" co2_status_t co2_set_grid_waves(int32_t waves) {
+  if (waves < 1 || waves > 16) return fail(CO2_ERR_VALIDATION, "waves out of range");
+  g_waves = waves;
+  return CO2_OK;
+}
 
 extern "C" co2_status_t co2_set_fused_variant(int32_t variant) {
   if (variant < 0 || variant > 15) return fail(CO2_ERR_VALIDATION, "variant out of range");
