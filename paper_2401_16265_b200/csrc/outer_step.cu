@@ -979,7 +979,7 @@ co2_status_t outer_step_ghost_impl(co2_mode_t mode, int64_t n, const void* ancho
 using namespace co2;
 
 extern "C" co2_status_t co2_set_grid_waves(int32_t waves) {
-  if (waves < 1 || waves > 16) return fail(CO2_ERR_VALIDATION, "waves out of range");
+  if (waves < 1 || waves > 64) return fail(CO2_ERR_VALIDATION, "waves out of range");
   g_waves = waves;
   return CO2_OK;
 }
