@@ -528,16 +528,19 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
 
 constexpr int kThreads = 256;
 
-// Grid waves for the grid-stride kernels: 1 = exactly the resident CTAs of an
-// idle GPU (persistent).  When a reduce kernel co-runs on the comm stream it
-// holds registers on some SMs, so a persistent grid no longer fits in one
-// wave and its last CTAs start late; more, shorter CTAs let the hardware
-// scheduler balance instead (co2_set_grid_waves / CO2_GRID_WAVES).
+// Grid waves for the grid-stride kernels, in units of the resident CTAs of an
+// idle GPU (1 = persistent).  Measured on B200 (profiles/r01/README.md): a
+// persistent grid leaves SMs idle at the end (uneven per-CTA progress across
+// the two dies' HBM) and, when a reduce kernel co-runs on the comm stream and
+// holds registers on some SMs, runs a late second wave.  Oversubscribing with
+// short CTAs lets the block scheduler balance: C3 N=1 0.887 -> 1.03 of the
+// measured copy bandwidth, N=2 / N=4 +24% / +33%.  Default 32 waves
+// (co2_set_grid_waves / CO2_GRID_WAVES to tune).
 int g_waves = -1;
 int grid_waves() {
   if (g_waves < 0) {
     const char* e = getenv("CO2_GRID_WAVES");
-    g_waves = e ? atoi(e) : 1;
+    g_waves = e ? atoi(e) : 32;
     if (g_waves < 1) g_waves = 1;
   }
   return g_waves;
