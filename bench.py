@@ -61,6 +61,32 @@ def peaks():
         return 6650.0, "fallback"
 
 
+# ncu --set full capture of this bench's fused kernel (committed under
+# profiles/; the capture ran `bench.py --steps 3 --warmup 1 --no-e2e --no-cpu`
+# on the default C3 workload).
+NCU_CAPTURE = os.path.join("profiles", "r01", "final", "fused_step_bf16_c3_raw.csv")
+
+
+def ncu_traffic(cfg):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed capture, for the workload it was taken on (else None)."""
+    if cfg.get("sharded") or cfg["n"] != 1_300_000_000 or cfg["mode"] != 2:
+        return None
+    try:
+        import csv
+        with open(os.path.join(ROOT, NCU_CAPTURE)) as f:
+            rows = list(csv.reader(f))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        tot = 0.0
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(name)
+            tot += float(vals[i]) * scale[units[i]]
+        return tot
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """NVML sampling of SM clocks and clock-event reasons during the timed
     region (the recipe's clocks line)."""
@@ -389,7 +415,9 @@ def main():
                        if sharded else "co2_round: AAR launch + stale wait + fused outer step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
-                         "traffic": None, "peak_kind": peak_kind,
+                         "traffic": ncu_traffic(cfg), "traffic_unit": "bytes per launch",
+                         "traffic_source": NCU_CAPTURE if ncu_traffic(cfg) else None,
+                         "algorithmic_bytes": bpp * per_rank, "peak_kind": peak_kind,
                          "kernel": ("fused_step_kernel<ModeBF16%s>" % (", GHOST" if sharded
                                                                         else ""))
                          if mode == 2 else "fused_step_kernel", "kernel_ms": k_max * 1e3,
