@@ -193,6 +193,14 @@ co2_status_t co2_synth(co2_mode_t mode, uint64_t seed, int32_t worker, int64_t j
 co2_status_t co2_synthetic_inner_step(co2_dtype_t dt, int64_t n, void* params, double lr,
                                       double scale, uint64_t seed, int32_t worker, int64_t step,
                                       int32_t repeat, void* stream);
+/* The same inner step with the InnerTrace x_{t,1} snapshot (inner_loop.cpp:
+ * 96-98) fused into its store: pass the worker's
+ * CO2_BUF_XFIRST as snapshot_out on the first inner step of a round instead
+ * of calling co2_worker_snapshot_first (saves a read+write pass). */
+co2_status_t co2_synthetic_inner_step_snapshot(co2_dtype_t dt, int64_t n, void* params,
+                                               double lr, double scale, uint64_t seed,
+                                               int32_t worker, int64_t step, int32_t repeat,
+                                               void* snapshot_out, void* stream);
 /* Fill a buffer with a constant (L2 flush helper for benchmarks). */
 co2_status_t co2_fill_u32(void* dst, uint32_t value, int64_t count, void* stream);
 

@@ -93,6 +93,7 @@ SIGNATURES = {
     "co2_convert": (ST, [I32, P, I32, P, I64, P]),
     "co2_synth": (ST, [I32, U64, I32, I64, I64, P, P, P, P, P, P]),
     "co2_synthetic_inner_step": (ST, [I32, I64, P, D, D, U64, I32, I64, I32, P]),
+    "co2_synthetic_inner_step_snapshot": (ST, [I32, I64, P, D, D, U64, I32, I64, I32, P, P]),
     "co2_fill_u32": (ST, [P, C.c_uint32, I64, P]),
     "co2_cluster_validate": (ST, [C.POINTER(Cluster)]),
     "co2_allreduce_time": (ST, [C.POINTER(Cluster), C.POINTER(D)]),

@@ -268,9 +268,12 @@ def synth_params(mode: int, n: int, *, seed: int = 7, worker: int = 0, device="c
 
 
 def synthetic_inner_step(params, *, lr: float, scale: float = 1.0, seed: int = 7, worker: int = 0,
-                         step: int = 0, repeat: int = 1, stream=None):
-    check(lib().co2_synthetic_inner_step(_dtype(params), params.numel(), _ptr(params), lr, scale,
-                                         seed, worker, step, repeat, _stream(stream)))
+                         step: int = 0, repeat: int = 1, snapshot_out=None, stream=None):
+    """Inner-step stand-in x <- x - lr*g; with snapshot_out the x_{t,1}
+    snapshot is written by the same pass."""
+    check(lib().co2_synthetic_inner_step_snapshot(_dtype(params), params.numel(), _ptr(params),
+                                                  lr, scale, seed, worker, step, repeat,
+                                                  _ptr(snapshot_out), _stream(stream)))
 
 
 # ------------------------------------------------------------ timing model

@@ -809,9 +809,12 @@ __global__ void synth_kernel(uint64_t kp0, uint64_t kp1, uint64_t kx, uint64_t k
   }
 }
 
+// snap (nullable): SURVEY.md 8f item 2 -- the InnerTrace snapshot x_{t,1}
+// (inner_loop.cpp:96-98) captured by the inner step's own store instead of a
+// separate copy pass over the params.
 template <typename T, typename TC>
 __global__ void inner_step_kernel(T* x, int64_t n, double lr, double scale, uint64_t key,
-                                  int64_t offset, int repeat) {
+                                  int64_t offset, int repeat, T* snap) {
   const TC lrc = (TC)lr, sc = (TC)scale;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -819,7 +822,9 @@ __global__ void inner_step_kernel(T* x, int64_t n, double lr, double scale, uint
     for (int r = 0; r < repeat; ++r) g += sc * (TC)sym_at(key, offset + j + (int64_t)r * n);
     TC v = to_c(x[j]);
     TC step = lrc * g;
-    x[j] = Store<T>::from(v - step);
+    const T out = Store<T>::from(v - step);
+    x[j] = out;
+    if (snap) snap[j] = out;
   }
 }
 
@@ -1144,10 +1149,11 @@ extern "C" co2_status_t co2_synth(co2_mode_t mode, uint64_t seed, int32_t worker
   return CO2_OK;
 }
 
-extern "C" co2_status_t co2_synthetic_inner_step(co2_dtype_t dt, int64_t n, void* params,
-                                                 double lr, double scale, uint64_t seed,
-                                                 int32_t worker, int64_t step, int32_t repeat,
-                                                 void* stream) {
+extern "C" co2_status_t co2_synthetic_inner_step_snapshot(co2_dtype_t dt, int64_t n,
+                                                          void* params, double lr, double scale,
+                                                          uint64_t seed, int32_t worker,
+                                                          int64_t step, int32_t repeat,
+                                                          void* snapshot_out, void* stream) {
   CO2_TRY(check_dtype(dt));
   if (repeat < 1) repeat = 1;
   uint64_t key = host_key(seed, (5ull << 32) | (uint64_t)(uint32_t)worker);
@@ -1155,16 +1161,24 @@ extern "C" co2_status_t co2_synthetic_inner_step(co2_dtype_t dt, int64_t n, void
   int grid = simple_grid(n, kThreads);
   cudaStream_t s = S(stream);
   if (dt == CO2_DTYPE_F64)
-    inner_step_kernel<double, double><<<grid, kThreads, 0, s>>>((double*)params, n, lr, scale, key,
-                                                                offset, repeat);
+    inner_step_kernel<double, double><<<grid, kThreads, 0, s>>>(
+        (double*)params, n, lr, scale, key, offset, repeat, (double*)snapshot_out);
   else if (dt == CO2_DTYPE_F32)
-    inner_step_kernel<float, float><<<grid, kThreads, 0, s>>>((float*)params, n, lr, scale, key,
-                                                              offset, repeat);
+    inner_step_kernel<float, float><<<grid, kThreads, 0, s>>>(
+        (float*)params, n, lr, scale, key, offset, repeat, (float*)snapshot_out);
   else
-    inner_step_kernel<bf16s, float><<<grid, kThreads, 0, s>>>((bf16s*)params, n, lr, scale, key,
-                                                              offset, repeat);
+    inner_step_kernel<bf16s, float><<<grid, kThreads, 0, s>>>(
+        (bf16s*)params, n, lr, scale, key, offset, repeat, (bf16s*)snapshot_out);
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
+}
+
+extern "C" co2_status_t co2_synthetic_inner_step(co2_dtype_t dt, int64_t n, void* params,
+                                                 double lr, double scale, uint64_t seed,
+                                                 int32_t worker, int64_t step, int32_t repeat,
+                                                 void* stream) {
+  return co2_synthetic_inner_step_snapshot(dt, n, params, lr, scale, seed, worker, step, repeat,
+                                           nullptr, stream);
 }
 
 extern "C" co2_status_t co2_fill_u32(void* dst, uint32_t value, int64_t count, void* stream) {

@@ -180,9 +180,13 @@ def test_c1_simulated_workers_bitwise(mode):
         for i, w in enumerate(ws):
             w.snapshot_start()
             for k in range(tau):
+                # odd rounds: the x_{t,1} snapshot fused into the first inner
+                # step's store (8f item 2); even rounds: the separate copy
+                fuse = k == 0 and t % 2 == 1
                 co2.synthetic_inner_step(w.params, lr=1e-3, scale=1.0, worker=i,
-                                         step=t * tau + k)
-                if k == 0:
+                                         step=t * tau + k,
+                                         snapshot_out=w.buffer(L.BUF_XFIRST) if fuse else None)
+                if k == 0 and not fuse:
                     w.snapshot_first()
             traces.append((to_np(w.buffer(L.BUF_ANCHOR)), to_np(w.buffer(L.BUF_XFIRST)),
                            to_np(w.params)))
