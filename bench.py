@@ -423,7 +423,11 @@ def main():
                          if mode == 2 else "fused_step_kernel", "kernel_ms": k_max * 1e3,
                          "bytes_per_param": bpp},
             "e2e": e2e, "cpu_baseline": cpu, "comm": comm,
-            "gpu_launches": world * args.steps,
+            # our kernels per step per rank: the fused step, plus our P2P reduce
+            # kernel when it runs as its own launch (NCCL's kernels are not ours)
+            "gpu_launches": world * args.steps * (
+                2 if world > 1 and transport == "p2p" and
+                (sharded or args.schedule == "split") else 1),
             "clocks": clk.summary(),
             "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step,
                      "n_clipped": r.n_clipped, "n_floored": r.n_floored},
