@@ -65,6 +65,8 @@ def peaks():
 # profiles/; the capture ran `bench.py --steps 3 --warmup 1 --no-e2e --no-cpu`
 # on the default C3 workload).
 NCU_CAPTURE = os.path.join("profiles", "r01", "final", "fused_step_bf16_c3_raw.csv")
+# NVLink denominator: B200_PROFILING.md's measured peer copy, GB/s per direction
+NVLINK_PEER_GBS = 770.0
 
 
 def ncu_traffic(cfg):
@@ -216,9 +218,8 @@ def main():
                     help="P2P worker-local rounds: 'split' = reduce kernel on the comm stream "
                          "overlapping the step kernel; 'fused' = one kernel does both")
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
-                    help="collective transport at N > 1; auto = the measured faster one: the "
-                         "fixed-order P2P all-reduce for worker-local configs, NCCL "
-                         "reduce-scatter/all-gather for the sharded C4")
+                    help="collective transport at N > 1; auto = the measured faster one, "
+                         "the fixed-order P2P kernels (worker-local and sharded C4)")
     ap.add_argument("--nparams", type=int, default=0, help="override the config's parameter count")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -254,7 +255,7 @@ def main():
         uid = bytes(128)
     transport = args.transport
     if transport == "auto":
-        transport = "nccl" if cfg.get("sharded") else "p2p"
+        transport = "p2p"
     if world == 1:
         transport = "nccl"  # one rank: no collective, the engine's reduce is a no-op
     transport_note = None
@@ -369,6 +370,24 @@ def main():
     peak, peak_kind = peaks()
     per_rank = w.length if sharded else n  # coordinates one fused launch processes
     achieved = bpp * per_rank / k_max / 1e9 if k_max else None
+    # Whole-step bounds at N > 1. NVLink bytes into one
+    # rank per round: the fixed-order all-reduce reads (G-1)/G of the replica
+    # from peers and receives (G-1)/G of it back; the sharded round reads two
+    # remote slices (x_{t,tau}, x_{t,1}) and receives the all-gather.
+    link, step_hbm = None, None
+    if world > 1:
+        low_bytes = {0: 8, 1: 4, 2: 2}[mode] * n
+        link_in = (3 if sharded else 2) * (world - 1) / world * low_bytes
+        link_gbs = link_in / (t_max / args.steps) / 1e9
+        link = {"bound": "nvlink", "bytes_in_per_rank": link_in, "achieved": link_gbs,
+                "peak": NVLINK_PEER_GBS, "unit": "GB/s", "frac": link_gbs / NVLINK_PEER_GBS,
+                "peak_kind": "measured peer copy per direction (B200_PROFILING.md)"}
+        if not sharded:
+            # the all-reduce reads and writes the replica once in HBM beside the step
+            bpp_step = bpp + 2 * low_bytes / n
+            hbm_gbs = bpp_step * n / (t_max / args.steps) / 1e9
+            step_hbm = {"bytes_per_param": bpp_step, "achieved": hbm_gbs, "peak": peak,
+                        "unit": "GB/s", "frac": hbm_gbs / peak}
 
     # --- e2e through the host-buffer entry (pinned H2D + kernel + D2H timed)
     e2e = None
@@ -422,6 +441,7 @@ def main():
                                                                         else ""))
                          if mode == 2 else "fused_step_kernel", "kernel_ms": k_max * 1e3,
                          "bytes_per_param": bpp},
+            "link": link, "step_hbm": step_hbm,
             "e2e": e2e, "cpu_baseline": cpu, "comm": comm,
             # our kernels per step per rank: the fused step, plus our P2P reduce
             # kernel when it runs as its own launch (NCCL's kernels are not ours)

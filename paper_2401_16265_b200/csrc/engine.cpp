@@ -77,6 +77,7 @@ struct co2_aar {
   std::vector<Handle> handles;
   // P2P transport
   int ctas = 0;
+  int slice_ctas = 0;  // sharded slice reduce; 0 = one CTA per SM
   uint32_t p2p_epoch = 0;
   bool fused = false;        // worker-local rounds use the fused all-reduce + step kernel
   uint32_t fused_epoch = 0;
@@ -157,9 +158,16 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
   e->rank = rank;
   e->world = world;
   e->workers = world;
-  // 96 CTAs measured best while the reduce shares HBM and SMs with the fused
-  // outer step (tools/aar_bench.py, bench.py --max-ctas sweep at N = 2, 4).
-  e->ctas = ctas > 0 ? ctas : 96;
+  // 64 CTAs measured best while the reduce shares HBM and SMs with the
+  // 32-wave fused outer step (bench.py --max-ctas sweep 24..148 at N = 2, 4,
+  // profiles/r01/bench/ctas_sweep.txt): fewer starve the reduce, more steal
+  // SM slots from the step.
+  e->ctas = ctas > 0 ? ctas : 64;
+  // The sharded slice reduce runs beside a step that touches 1/world of the
+  // parameters, so it wants the whole chip: 0 = the launcher's per-world
+  // default (C4 N=4: 592 CTAs 49.0 ms/round vs 64 CTAs 61.7,
+  // profiles/r01/bench/c4_ctas_sweep.txt).
+  e->slice_ctas = ctas;
   co2_status_t s = engine_common_init(e);
   if (s == CO2_OK) {
     cudaError_t ce = cudaMalloc(&e->signals, p2p_signal_bytes());
@@ -406,7 +414,7 @@ static co2_status_t launch_slice(co2_aar* e, co2_dtype_t dt, const void* src0, c
   e->p2p_epoch += 1;
   CO2_TRY(p2p_slice_average_launch(dt, 2, b0->ptrs.data(), b1->ptrs.data(), dst0, dst1,
                                    e->peer_signals.data(), e->world, e->rank, lo, len,
-                                   e->p2p_epoch, e->ctas, e->comm_stream));
+                                   e->p2p_epoch, e->slice_ctas, e->comm_stream));
   CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + 36, 4,
                            cudaMemcpyDeviceToHost, e->comm_stream));
   CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));

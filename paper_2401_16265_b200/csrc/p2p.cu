@@ -280,8 +280,13 @@ co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const*
   a.world = world;
   a.rank = rank;
   a.epoch = epoch;
-  if (ctas < 1) ctas = 1;
-  if (ctas > sm_count()) ctas = sm_count();
+  // Entry barrier only (a flag per rank, not a CTA count), so CTAs need not
+  // be co-resident and the grid may exceed one wave.
+  // Default: at G = 2 one CTA per SM (the shard step is half the chip's
+  // HBM work and competes with more), from G = 4 on 4 per SM (more remote
+  // loads in flight win) -- C4 sweep in profiles/r01/bench/c4_ctas_sweep.txt.
+  if (ctas < 1) ctas = (world <= 2 ? 1 : 4) * sm_count();
+  if (ctas > 8 * sm_count()) ctas = 8 * sm_count();
 #define CO2_SLICE_LAUNCH(TL, TC, V)                                                       \
   if (world <= 2)                                                                        \
     p2p_slice_average_kernel<TL, TC, V, 2, 4><<<ctas, kP2PThreads, 0, s>>>(a);           \
