@@ -22,6 +22,7 @@
 // exits instead of hanging the GPU.
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "p2p_sync.cuh"
@@ -258,6 +259,20 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_slice_average_kernel(const Sl
   }
 }
 
+// Rank capacity R of the kernel instantiation for a world size.  The env
+// CO2_P2P_RANK_CAP=4|8 forces a wider one, so the G = 8 instantiations
+// (guarded loads over the unused ranks) are exercised on 2- and 4-GPU boxes
+// (tests/test_gpu_multi.py); it never narrows.
+int rank_cap(int world) {
+  static const int forced = [] {
+    const char* e = getenv("CO2_P2P_RANK_CAP");
+    return e ? atoi(e) : 0;
+  }();
+  int cap = world <= 2 ? 2 : (world <= 4 ? 4 : 8);
+  if ((forced == 4 || forced == 8) && forced > cap) cap = forced;
+  return cap;
+}
+
 }  // namespace
 
 co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const* src0,
@@ -287,10 +302,11 @@ co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const*
   // loads in flight win) -- C4 sweep in profiles/r01/bench/c4_ctas_sweep.txt.
   if (ctas < 1) ctas = (world <= 2 ? 1 : 4) * sm_count();
   if (ctas > 8 * sm_count()) ctas = 8 * sm_count();
+  const int cap = rank_cap(world);
 #define CO2_SLICE_LAUNCH(TL, TC, V)                                                       \
-  if (world <= 2)                                                                        \
+  if (cap == 2)                                                                          \
     p2p_slice_average_kernel<TL, TC, V, 2, 4><<<ctas, kP2PThreads, 0, s>>>(a);           \
-  else if (world <= 4)                                                                   \
+  else if (cap == 4)                                                                     \
     p2p_slice_average_kernel<TL, TC, V, 4, 2><<<ctas, kP2PThreads, 0, s>>>(a);           \
   else                                                                                   \
     p2p_slice_average_kernel<TL, TC, V, 8, 1><<<ctas, kP2PThreads, 0, s>>>(a);
@@ -325,10 +341,11 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
   if (ctas > sm_count()) ctas = sm_count();  // all CTAs co-resident (they spin)
   // R = rank capacity of the instantiation, U = vectors in flight per thread
   // (fewer ranks -> more vectors, keeping ~R*U*16 B of loads per thread).
+  const int cap = rank_cap(world);
 #define CO2_P2P_LAUNCH(TL, TC, V)                                                        \
-  if (world <= 2)                                                                       \
+  if (cap == 2)                                                                         \
     p2p_average_kernel<TL, TC, V, 2, 4><<<ctas, kP2PThreads, 0, s>>>(a);                \
-  else if (world <= 4)                                                                  \
+  else if (cap == 4)                                                                    \
     p2p_average_kernel<TL, TC, V, 4, 2><<<ctas, kP2PThreads, 0, s>>>(a);                \
   else                                                                                  \
     p2p_average_kernel<TL, TC, V, 8, 1><<<ctas, kP2PThreads, 0, s>>>(a);

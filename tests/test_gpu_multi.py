@@ -66,3 +66,23 @@ def test_sharded_ghost_bitwise(mode, transport, world):
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     res = json.loads(line)
     assert res["ok"], res
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("script", ["mp_nccl_rounds.py", "mp_nccl_sharded.py"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_rank_cap8_bitwise(script, world):
+    """The G = 8 instantiations of the P2P reduce kernels (what an 8-GPU run
+    launches), forced at G = 2 and 4 through CO2_P2P_RANK_CAP=8: the guarded
+    loads over absent ranks must leave the fixed-order average bitwise."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, CO2_TEST_MODE="2", CO2_TEST_TRANSPORT="p2p", CO2_P2P_RANK_CAP="8")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", script)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    assert json.loads(line)["ok"]
