@@ -163,6 +163,99 @@ def test_fused_errors_follow_reference_precedence():
         co2.outer_step(mode, x, p0, p1, xe, m.clone(), co2.Co2Hyper(phi=0.0), 4)
 
 
+def special_inputs(mode: int, n: int, seed: int):
+    """Edge-value inputs in the mode's storage dtypes: p1 == p0 (gap hits
+    the epsilon floor), x == p0 (gap exactly 1), signed zeros, subnormals,
+    near-overflow magnitudes, momentum exactly at +-phi, xbar far enough off
+    to clip."""
+    rng = np.random.default_rng(seed)
+    st = np.float64 if mode == co2.MODE_F64 else np.float32
+    tiny = 1e-310 if mode == co2.MODE_F64 else 1e-39
+    big = 1e300 if mode == co2.MODE_F64 else 1e37
+    u = lambda s: rng.uniform(-1.0, 1.0, n) * s  # noqa: E731
+    p0 = u(0.02)
+    x, p1, xb, m = p0 + u(4e-3), p0 - u(1e-3), p0 - u(4e-3), u(1e-2)
+    cat = np.arange(n) % 9
+    p1 = np.where(cat == 1, p0, p1)
+    x = np.where(cat == 2, p0, x)
+    z = cat == 3
+    x, p0, p1, xb, m = (np.where(z, -0.0, a) for a in (x, p0, p1, xb, m))
+    s = cat == 4
+    p0 = np.where(s, u(tiny), p0)
+    x, p1, xb, m = (np.where(s, p0 + u(tiny), a) for a in (x, p1, xb, m))
+    b = cat == 5
+    p0 = np.where(b, u(big), p0)
+    x = np.where(b, p0 * (1 + u(1e-3)), x)
+    p1 = np.where(b, p0 * (1 - u(1e-3)), p1)
+    xb = np.where(b, p0 * (1 + u(1e-3)), xb)
+    m = np.where(cat == 6, np.where(u(1.0) > 0, 5e-3, -5e-3), m)
+    xb = np.where(cat == 7, p0 - u(10.0), xb)
+    x = np.where(cat == 8, -x, x)
+    x, p0, m = (a.astype(st) for a in (x, p0, m))
+    if mode == co2.MODE_BF16_MIXED:
+        p1, xb = O.f32_to_bf16_bits(p1.astype(np.float32)), O.f32_to_bf16_bits(xb.astype(np.float32))
+    else:
+        p1, xb = p1.astype(st), xb.astype(st)
+    return x, p0, p1, xb, m
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("penalty,clip", [(True, True), (False, False)])
+def test_fused_special_values_bitwise(mode, seed, penalty, clip):
+    """Signed zeros, subnormals (no flush: -ftz=false), near-overflow values,
+    the epsilon floor and exact clip boundaries: same bits and the same
+    status as the oracle, odd length for the scalar tail."""
+    n = 9 * 1111 + 5
+    ox, op0, op1, oxe, om = special_inputs(mode, n, seed)
+    ref = O.outer_step(mode, ox, op0, op1, oxe, om, ohyper(12, penalty, clip))
+    x, p0, p1, xe, m = (to_dev(a) for a in (ox, op0, op1, oxe, om))
+    anchor, params, gap = torch.empty_like(x), torch.empty_like(xe), torch.empty_like(x)
+    h = hyper(12, penalty, clip)
+    if ref.status != 0:
+        with pytest.raises((co2.NumericError, co2.ValidationError)) as ei:
+            co2.outer_step(mode, x, p0, p1, xe, m, h, 12, anchor_out=anchor, params_out=params,
+                           gap_out=gap)
+        assert ref.message in str(ei.value)
+        return
+    d = co2.outer_step(mode, x, p0, p1, xe, m, h, 12, anchor_out=anchor, params_out=params,
+                       gap_out=gap)
+    assert same(to_np(m), ref.m) and same(to_np(anchor), ref.anchor)
+    assert same(to_np(params), ref.params) and same(to_np(gap), ref.gap)
+    assert (d.min_gap, d.max_outer_step, d.n_clipped, d.n_floored) == (
+        ref.diag.min_gap, ref.diag.max_outer_step, ref.diag.n_clipped, ref.diag.n_floored)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("where", ["momentum", "iterate"])
+def test_fused_overflow_status_matches_oracle(mode, where):
+    """An overflow to inf inside the step raises the same error as the
+    oracle (the reference's checks, outer_algorithms.cpp:57-61,84-86)."""
+    n = 4099
+    ox, op0, op1, oxe, om = special_inputs(mode, n, 5)
+    top = np.finfo(ox.dtype).max
+    j = 2 * 9 + 1  # an ordinary coordinate; x = p0 = p1 makes its gap exactly 1
+    if where == "momentum":  # m' = 0.7*top + (0.45 + 0.45)*top overflows
+        ox[j] = op0[j] = 0.45 * top
+        om[j], xb = top, -0.45 * top
+    else:  # m' = -0.7*top is finite, x' = 0.5*top + 0.7*top is not
+        ox[j] = op0[j] = 0.5 * top
+        om[j], xb = -top, 0.5 * top
+    if mode == co2.MODE_BF16_MIXED:
+        op1[j] = O.f32_to_bf16_bits(np.array([op0[j]], np.float32))[0]
+        oxe[j] = O.f32_to_bf16_bits(np.array([xb], np.float32))[0]
+        if where != "momentum":  # keep delta = p0 - xbar exactly 0 in bf16 mode
+            ox[j] = op0[j] = O.bf16_bits_to_f32(np.array([oxe[j]], np.uint16))[0]
+    else:
+        op1[j], oxe[j] = op0[j], xb
+    ref = O.outer_step(mode, ox, op0, op1, oxe, om, ohyper(12, True, False))
+    assert ref.status == O.NUMERIC, ref.message
+    x, p0, p1, xe, m = (to_dev(a) for a in (ox, op0, op1, oxe, om))
+    with pytest.raises(co2.NumericError) as ei:
+        co2.outer_step(mode, x, p0, p1, xe, m, hyper(12, True, False), 12)
+    assert ref.message in str(ei.value)
+
+
 def test_fused_empty_and_determinism():
     mode = co2.MODE_F32
     e = torch.empty(0, device="cuda")
