@@ -99,14 +99,12 @@ class ClockSampler:
              "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
              "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, index: int, period: float = 0.01):
+    def __init__(self, torch, dev: int, period: float = 0.01):
         self.samples, self.reasons, self.ok = [], set(), False
         self.period, self._stop = period, threading.Event()
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            self.nv = nv
-            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.nv, self.h = nvml_handle(torch, dev)
+            nv = self.nv
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
             self.ok = True
         except Exception:
@@ -140,6 +138,34 @@ class ClockSampler:
         med = statistics.median(self.samples) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
+
+
+def nvml_handle(torch, dev: int):
+    """NVML handle of CUDA device `dev`, matched by PCI bus id (NVML and
+    CUDA enumerate devices in different orders in general)."""
+    import pynvml as nv
+    nv.nvmlInit()
+    p = torch.cuda.get_device_properties(dev)
+    bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    try:
+        return nv, nv.nvmlDeviceGetHandleByPciBusId(bus)
+    except Exception:
+        return nv, nv.nvmlDeviceGetHandleByIndex(dev)
+
+
+def bind_gpu_local_cpus(torch, dev: int):
+    """Pins this rank to the CPU cores NVML reports as local to its GPU, so
+    the pinned host buffers of the e2e leg are first-touched on the GPU's
+    NUMA node and its copies do not cross the socket interconnect.
+    CO2_BENCH_NUMA=0 disables it. Returns the core count, or None."""
+    if os.environ.get("CO2_BENCH_NUMA", "1") == "0":
+        return None
+    try:
+        nv, h = nvml_handle(torch, dev)
+        nv.nvmlDeviceSetCpuAffinity(h)
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return None
 
 
 def host_cores() -> int:
@@ -239,6 +265,7 @@ def main():
     from paper_2401_16265_b200 import co2
 
     torch.cuda.set_device(local)
+    numa_cores = bind_gpu_local_cpus(torch, local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -326,7 +353,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    with ClockSampler(torch, torch.cuda.current_device()) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             one_round()
@@ -393,6 +420,7 @@ def main():
     e2e = None
     if not args.no_e2e and not sharded:
         e2e = run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist)
+        e2e["numa_bound_cores"] = numa_cores  # None: not bound (CO2_BENCH_NUMA=0 / no NVML)
 
     # --- CPU baseline (rank 0, N=1 only): single-core reference restatement
     cpu = None
