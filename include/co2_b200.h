@@ -290,6 +290,20 @@ co2_status_t co2_aar_wait(co2_aar_t* engine, uint64_t handle, void* consumer_str
 co2_status_t co2_aar_stall(co2_aar_t* engine, uint64_t handle, double* stall_seconds,
                            double* comm_seconds);
 co2_status_t co2_aar_live(const co2_aar_t* engine, int32_t* live);
+/* info(handle) (collective.hpp:40-50,68): HandleInfo from device events.
+ * Times are seconds since engine creation; completion_time is valid once
+ * `completed`, stall once `consumed` and the consumer stream passed the
+ * wait (else NaN).  Never blocks. */
+typedef struct co2_handle_info {
+  uint64_t id;
+  double launch_time, completion_time, stall, comm;
+  int32_t completed, consumed;
+} co2_handle_info_t;
+co2_status_t co2_aar_info(co2_aar_t* engine, uint64_t handle, co2_handle_info_t* out);
+/* total_stall() and handle_count() (collective.hpp:64-67): the stall summed
+ * over consumed handles (synchronizes on their wait events) and the number
+ * of handles ever launched. */
+co2_status_t co2_aar_totals(co2_aar_t* engine, double* total_stall, uint64_t* handle_count);
 /* Blocking all-reduce (sum) on the given stream; used by ghost-consistent
  * mode for the averaged snapshots (outer_algorithms.cpp:163-169). */
 co2_status_t co2_aar_allreduce_blocking(co2_aar_t* engine, co2_dtype_t dt, void* buf, int64_t n,

@@ -59,6 +59,12 @@ class Event(C.Structure):
                 ("t", C.c_double), ("stall", C.c_double)]
 
 
+class HandleInfo(C.Structure):
+    _fields_ = [("id", C.c_uint64), ("launch_time", C.c_double), ("completion_time", C.c_double),
+                ("stall", C.c_double), ("comm", C.c_double), ("completed", C.c_int32),
+                ("consumed", C.c_int32)]
+
+
 class RoundResult(C.Structure):
     _fields_ = [("stall_seconds", C.c_double), ("outer_applied", C.c_int32), ("pad", C.c_int32),
                 ("min_gap", C.c_double), ("max_outer_step", C.c_double),
@@ -116,6 +122,8 @@ SIGNATURES = {
     "co2_aar_wait": (ST, [P, U64, P]),
     "co2_aar_stall": (ST, [P, U64, C.POINTER(D), C.POINTER(D)]),
     "co2_aar_live": (ST, [P, C.POINTER(I32)]),
+    "co2_aar_info": (ST, [P, U64, C.POINTER(HandleInfo)]),
+    "co2_aar_totals": (ST, [P, C.POINTER(D), C.POINTER(U64)]),
     "co2_aar_allreduce_blocking": (ST, [P, I32, P, I64, P]),
     "co2_aar_events": (ST, [P, C.POINTER(Event), I64, C.POINTER(I64)]),
     "co2_worker_create": (ST, [C.POINTER(P), I32, I64, P, I32, P]),

@@ -438,6 +438,25 @@ class CollectiveEngine:
         check(lib().co2_aar_stall(self.handle, handle, C.byref(s), C.byref(c)))
         return s.value, c.value
 
+    def info(self, handle: int) -> dict:
+        """HandleInfo (collective.hpp:40-50): device times in seconds since
+        engine creation; NaN where not yet known.  Non-blocking."""
+        r = L.HandleInfo()
+        check(lib().co2_aar_info(self.handle, handle, C.byref(r)))
+        return {"id": r.id, "launch_time": r.launch_time, "completion_time": r.completion_time,
+                "completed": bool(r.completed), "consumed": bool(r.consumed), "stall": r.stall,
+                "comm": r.comm}
+
+    def total_stall(self) -> float:
+        s = C.c_double()
+        check(lib().co2_aar_totals(self.handle, C.byref(s), None))
+        return s.value
+
+    def handle_count(self) -> int:
+        c = C.c_uint64()
+        check(lib().co2_aar_totals(self.handle, None, C.byref(c)))
+        return c.value
+
     def live_handles(self) -> int:
         v = C.c_int32()
         check(lib().co2_aar_live(self.handle, C.byref(v)))

@@ -17,6 +17,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <limits>
 #include <utility>
 #include <vector>
 
@@ -294,6 +295,15 @@ static co2_status_t cache_handle(co2_aar* e, Handle& h) {
   return CO2_OK;
 }
 
+// Non-blocking variant for info(): caches only when every event the cache
+// reads has already completed.
+static co2_status_t cache_handle_if_ready(co2_aar* e, Handle& h) {
+  if (h.cached) return CO2_OK;
+  if (cudaEventQuery(h.done) != cudaSuccess) return CO2_OK;
+  if (h.waited && cudaEventQuery(h.wait_end) != cudaSuccess) return CO2_OK;
+  return cache_handle(e, h);
+}
+
 // A new handle: events (recycled from the handle kRing launches back) and
 // pinned diagnostic slots from the engine's ring.
 static co2_status_t new_handle(co2_aar* e, Handle* h) {
@@ -480,6 +490,37 @@ extern "C" co2_status_t co2_aar_stall(co2_aar_t* e, uint64_t handle, double* sta
 extern "C" co2_status_t co2_aar_live(const co2_aar_t* e, int32_t* live) {
   if (!e) return fail(CO2_ERR_VALIDATION, "aar: null engine");
   *live = e->live;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_info(co2_aar_t* e, uint64_t handle, co2_handle_info_t* out) {
+  Handle* h = nullptr;
+  CO2_TRY(record_for(e, handle, &h));
+  if (!out) return fail(CO2_ERR_VALIDATION, "info: null output");
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  co2_handle_info_t r{handle, nan, nan, nan, nan, 0, h->consumed ? 1 : 0};
+  if (!h->cached && cudaEventQuery(h->done) == cudaSuccess) CO2_TRY(cache_handle_if_ready(e, *h));
+  if (h->cached) {
+    r.launch_time = h->c_start;
+    r.completion_time = h->c_done;
+    r.comm = h->c_comm;
+    r.completed = 1;
+    if (h->waited) r.stall = h->c_stall;
+  }
+  *out = r;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_totals(co2_aar_t* e, double* total_stall, uint64_t* count) {
+  if (!e) return fail(CO2_ERR_VALIDATION, "aar: null engine");
+  double t = 0.0;
+  for (Handle& h : e->handles)
+    if (h.waited) {
+      CO2_TRY(cache_handle(e, h));
+      t += h.c_stall;
+    }
+  if (total_stall) *total_stall = t;
+  if (count) *count = e->handles.size();
   return CO2_OK;
 }
 

@@ -234,6 +234,20 @@ def test_engine_semantics():
     kinds = [e["event"] for e in ev if e["handle_id"] == 0]
     assert kinds == ["launch", "complete", "wait"]
     assert ev[0]["t_sim"] <= ev[1]["t_sim"] <= ev[2]["t_sim"]
+    # info / total_stall / handle_count (collective.hpp:64-68)
+    i0 = eng.info(h0)
+    assert i0["id"] == h0 and i0["completed"] and i0["consumed"]
+    assert i0["launch_time"] <= i0["completion_time"] and i0["stall"] >= 0.0
+    assert eng.handle_count() == 2
+    assert eng.total_stall() == pytest.approx(i0["stall"] + eng.info(h1)["stall"])
+    h2 = eng.launch_all_reduce([a, b], out)
+    i2 = eng.info(h2)
+    assert not i2["consumed"] and np.isnan(i2["stall"])
+    with pytest.raises(co2.ValidationError, match="unknown reduce handle"):
+        eng.info(99)
+    eng.wait(h2)
+    torch.cuda.synchronize()
+    assert eng.info(h2)["consumed"] and eng.handle_count() == 3
 
 
 def test_round_rejects_bad_hyper_and_counts():
