@@ -1,6 +1,7 @@
 // C ABI glue: error reporting, validation with the reference's messages,
 // workspace / diagnostics, the fused step's entry points (device and
 // host-buffer forms) and the analytic timing model.
+#include <atomic>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -31,16 +32,17 @@ co2_status_t cuda_fail(cudaError_t e, const char* what) {
 }
 
 int sm_count() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];  // zero-initialised (static storage)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  if (cache[dev] == 0) {
-    int v = 0;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = v > 0 ? v : 148;
+    if (v <= 0) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return v;
 }
 
 }  // namespace co2
@@ -142,17 +144,21 @@ struct StageSlot {
   size_t bytes = 0;
 };
 
+// One staging pool per device (streams and buffers belong to it); calls on
+// the same device serialise on its mutex, calls on different devices run
+// concurrently.
 struct StagePool {
   std::mutex mu;
-  int device = -1;
   std::vector<StageSlot> slots;
   co2_diag_t* host_diags = nullptr;  // pinned
   size_t host_diag_cap = 0;
 };
 
-StagePool& pool() {
-  static StagePool p;
-  return p;
+constexpr int kMaxDevices = 64;
+
+StagePool& pool(int dev) {
+  static StagePool p[kMaxDevices];
+  return p[dev];
 }
 
 }  // namespace
@@ -172,18 +178,12 @@ extern "C" co2_status_t co2_outer_step_host(co2_mode_t mode, int64_t n, const vo
   auto align = [](size_t v) { return (v + 255) / 256 * 256; };
   const size_t need = align(3 * sb * chunk) + align(3 * lb * chunk) + kWsBytes + 1024;
   (void)per;
-  StagePool& P = pool();
-  std::lock_guard<std::mutex> lock(P.mu);
   int dev = 0;
   CO2_CUDA(cudaGetDevice(&dev));
-  if (P.device != dev) {
-    for (auto& s : P.slots) {
-      if (s.buf) cudaFree(s.buf);
-      if (s.stream) cudaStreamDestroy(s.stream);
-    }
-    P.slots.clear();
-    P.device = dev;
-  }
+  if (dev < 0 || dev >= kMaxDevices)
+    return fail(CO2_ERR_VALIDATION, "outer_step_host: device %d out of range", dev);
+  StagePool& P = pool(dev);
+  std::lock_guard<std::mutex> lock(P.mu);
   while ((int)P.slots.size() < nstreams) {
     StageSlot s;
     CO2_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));

@@ -18,6 +18,7 @@
 // flags) are reduced warp-shuffle -> shared memory -> per-block partials,
 // and the last block to arrive (atomic ticket) folds the partials in fixed
 // index order, so results are deterministic without a second launch.
+#include <atomic>
 #include <cuda_bf16.h>
 #include <math.h>
 #include <stdint.h>
@@ -536,14 +537,20 @@ constexpr int kThreads = 256;
 // short CTAs lets the block scheduler balance: C3 N=1 0.887 -> 1.03 of the
 // measured copy bandwidth, N=2 / N=4 +24% / +33%.  Default 32 waves
 // (co2_set_grid_waves / CO2_GRID_WAVES to tune).
-int g_waves = -1;
+// Knobs are atomics: a setter may race launches issued from other threads.
+std::atomic<int> g_waves{-1};
 int grid_waves() {
-  if (g_waves < 0) {
+  int w = g_waves.load(std::memory_order_relaxed);
+  if (w < 0) {
     const char* e = getenv("CO2_GRID_WAVES");
-    g_waves = e ? atoi(e) : 32;
-    if (g_waves < 1) g_waves = 1;
+    w = e ? atoi(e) : 32;
+    if (w < 1) w = 1;
+    if (w > 64) w = 64;
+    int expect = -1;
+    g_waves.compare_exchange_strong(expect, w, std::memory_order_relaxed);
+    w = g_waves.load(std::memory_order_relaxed);
   }
-  return g_waves;
+  return w;
 }
 
 template <typename K>
@@ -598,13 +605,18 @@ co2_status_t launch_ghost(const StepArgs& a, cudaStream_t s) {
 
 // Tuning knob: CO2_FUSED_VARIANT selects the (elements per vector, vectors
 // in flight per thread) instantiation; 0 is the measured default.
-int g_variant = -1;
+std::atomic<int> g_variant{-1};
 int fused_variant() {
-  if (g_variant < 0) {
+  int v = g_variant.load(std::memory_order_relaxed);
+  if (v < 0) {
     const char* e = getenv("CO2_FUSED_VARIANT");
-    g_variant = e ? atoi(e) : 0;
+    v = e ? atoi(e) : 0;
+    if (v < 0) v = 0;
+    int expect = -1;
+    g_variant.compare_exchange_strong(expect, v, std::memory_order_relaxed);
+    v = g_variant.load(std::memory_order_relaxed);
   }
-  return g_variant;
+  return v;
 }
 
 template <class M>
@@ -988,13 +1000,13 @@ using namespace co2;
 
 extern "C" co2_status_t co2_set_grid_waves(int32_t waves) {
   if (waves < 1 || waves > 64) return fail(CO2_ERR_VALIDATION, "waves out of range");
-  g_waves = waves;
+  g_waves.store(waves, std::memory_order_relaxed);
   return CO2_OK;
 }
 
 extern "C" co2_status_t co2_set_fused_variant(int32_t variant) {
   if (variant < 0 || variant > 15) return fail(CO2_ERR_VALIDATION, "variant out of range");
-  g_variant = variant;
+  g_variant.store(variant, std::memory_order_relaxed);
   return CO2_OK;
 }
 

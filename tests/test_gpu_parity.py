@@ -366,3 +366,42 @@ def test_cpp_facade_binary():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FACADE OK" in r.stdout
+
+
+def test_host_entry_concurrent_threads():
+    """Two host threads driving co2_outer_step_host at once (ctypes drops the
+    GIL): the per-device staging pool serialises them and both results stay
+    bitwise the oracle's."""
+    import threading
+    mode = co2.MODE_BF16_MIXED
+    n = 300_007
+    jobs = []
+    for w in (0, 1):
+        ox, op0, op1, oxe, om = O.synth(mode, n, worker=w)
+        ref = O.outer_step(mode, ox, op0, op1, oxe, om, ohyper())
+        pin = lambda a: torch.from_numpy(  # noqa: E731
+            a.view(np.int16) if a.dtype == np.uint16 else a.copy()).pin_memory()
+        hs = [pin(a) for a in (ox, op0, op1, oxe, om)]
+        jobs.append((hs, torch.empty_like(hs[0]).pin_memory(),
+                     torch.empty_like(hs[3]).pin_memory(), ref))
+    errs = []
+
+    def run(job):
+        (hx, hp0, hp1, hxe, hm), anchor, params, _ = job
+        try:
+            for _ in range(3):
+                co2.outer_step_host(mode, hx, hp0, hp1, hxe, hm.clone().pin_memory(), hyper(), 4,
+                                    anchor_out=anchor, params_out=params, chunk=50_000,
+                                    nstreams=2)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(j,)) for j in jobs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for (_, _, _, _, _), anchor, params, ref in jobs:
+        assert same(anchor.numpy(), ref.anchor)
+        assert same(params.numpy().view(np.uint16), ref.params)
