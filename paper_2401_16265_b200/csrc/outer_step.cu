@@ -553,12 +553,35 @@ int grid_waves() {
   return w;
 }
 
+// Oversubscription stops where CTAs would get shorter than min_cta_iters()
+// grid-stride iterations: below that the per-CTA fixed cost (diagnostic
+// partial + ticket atomic, CTA launch) shows.  C2 (125M fp32, 0.72 ms) at
+// 32 waves gives 6.4 iterations per CTA.  Sweep (profiles/r01/bench/
+// c2_min_iters.txt): 8 -> N=1 +1.6 %, N=2 +0.9 %, N=4 +-0; 32 -> N=1 +4 %
+// but N=2 -2.5 % (the co-running reduce wants the shorter CTAs).  C3 (33
+// iterations at 32 waves) is unaffected.  CO2_MIN_CTA_ITERS overrides
+// (0 = always the full wave count).
+int min_cta_iters() {
+  static const int v = [] {
+    const char* e = getenv("CO2_MIN_CTA_ITERS");
+    int x = e ? atoi(e) : 8;
+    return x < 0 ? 0 : x;
+  }();
+  return v;
+}
+
 template <typename K>
 int grid_for(K kernel, int64_t work_items, int threads) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
   if (per_sm < 1) per_sm = 1;
-  int64_t cap = (int64_t)per_sm * sm_count() * grid_waves();
+  const int64_t wave = (int64_t)per_sm * sm_count();
+  int64_t waves = grid_waves();
+  if (min_cta_iters() > 0) {
+    const int64_t fit = (work_items + threads - 1) / threads / (wave * min_cta_iters());
+    if (fit < waves) waves = fit < 1 ? 1 : fit;
+  }
+  int64_t cap = wave * waves;
   if (cap > kMaxBlocks) cap = kMaxBlocks;
   int64_t need = (work_items + threads - 1) / threads;
   if (need < 1) need = 1;

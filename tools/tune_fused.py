@@ -4,6 +4,10 @@ launches (the bench's steady state), CUDA events per launch, median per
 (rep, variant).  Interleaving cancels slow drifts (clocks, power cap).
 
   python tools/tune_fused.py [--mode 2] [--n 1300000000] [--iters 40] [--reps 3]
+                             [--waves 32] [--variants 0,1,...]
+
+--waves takes a comma list; every (variant, waves) pair is one interleaved
+configuration.
 """
 import argparse
 import json
@@ -28,6 +32,8 @@ def main():
     ap.add_argument("--n", type=int, default=1_300_000_000)
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--waves", default="32")
+    ap.add_argument("--variants", default="")
     a = ap.parse_args()
     import torch
 
@@ -37,11 +43,13 @@ def main():
     x, p0, p1, xe, m = co2.synth(mode, n)
     h = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
     ws = co2.Workspace()
-    variants = sorted(NAMES[mode])
+    vs = [int(v) for v in a.variants.split(",")] if a.variants else sorted(NAMES[mode])
+    variants = [(v, int(w)) for v in vs for w in a.waves.split(",")]
     res = {v: [] for v in variants}
     for rep in range(a.reps):
         for v in variants:
-            co2.check(co2.lib().co2_set_fused_variant(v))
+            co2.check(co2.lib().co2_set_fused_variant(v[0]))
+            co2.check(co2.lib().co2_set_grid_waves(v[1]))
             for _ in range(3):
                 co2.outer_step(mode, x, p0, p1, xe, m, h, 12, anchor_out=p0, params_out=xe,
                                workspace=ws, check_flags=False)
@@ -56,7 +64,8 @@ def main():
             res[v].append(statistics.median(e0.elapsed_time(e1) for e0, e1 in evs) * 1e-3)
     for v in variants:
         t = min(res[v])
-        print(json.dumps({"mode": mode, "n": n, "variant": v, "shape": NAMES[mode][v],
+        print(json.dumps({"mode": mode, "n": n, "variant": v[0], "waves": v[1],
+                          "shape": NAMES[mode][v[0]],
                           "median_ms_per_rep": [round(x * 1e3, 4) for x in res[v]],
                           "GBps_best_rep": BPP[mode] * n / t / 1e9,
                           "GBps_median_rep": BPP[mode] * n / statistics.median(res[v]) / 1e9}),
