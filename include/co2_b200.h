@@ -60,7 +60,8 @@ enum {
   CO2_FLAG_AVG_NONFINITE = 32u,  /* param_ops.cpp:31         numeric  */
   CO2_FLAG_SLOWMO_M = 64u,       /* outer_algorithms.cpp:231 numeric  */
   CO2_FLAG_SLOWMO_X = 128u,      /* outer_algorithms.cpp:233 numeric  */
-  CO2_FLAG_OVERLAP = 256u        /* outer_algorithms.cpp:279 numeric  */
+  CO2_FLAG_OVERLAP = 256u,       /* outer_algorithms.cpp:279 numeric  */
+  CO2_FLAG_NORM_NONFINITE = 512u /* global-norm clip extension numeric */
 };
 
 /* Co2Hyper (proj/include/co2sim/outer_algorithms.hpp:17-30) plus tau. */
@@ -118,6 +119,27 @@ co2_status_t co2_outer_step(co2_mode_t mode, int64_t n, const void* x_t0, const 
                             const void* prev_x1, const void* xbar, int32_t xbar_divisor,
                             void* momentum, void* anchor_out, void* params_out, void* gap_out,
                             const co2_hyper_t* hyper, void* workspace, void* stream);
+
+/* EXTENSION, outside the reference parity contract (the reference clips
+ * coordinate-wise, param_ops.cpp:35-43; SURVEY.md 8 note 3): the outer step
+ * with a GLOBAL-norm clip of the outer momentum, as the north star words it.
+ * Same buffers and hyper as co2_outer_step; with hyper->clip set,
+ *   c = m' * min(1, phi / ||m'||_2),  x' = x_t0 - alpha * c,
+ * where ||m'||_2 is summed in fp64 over fixed chunks in a fixed order (two
+ * kernels, deterministic for a given n and mode on any grid).  With clip
+ * off it equals co2_outer_step bit for bit.  n_clipped counts coordinates
+ * that were scaled (0 or n).  Async on `stream`; read the diagnostics with
+ * co2_diag_fetch and the norm with co2_global_clip_norm_fetch. */
+co2_status_t co2_outer_step_global_clip(co2_mode_t mode, int64_t n, const void* x_t0,
+                                        const void* prev_x0, const void* prev_x1,
+                                        const void* xbar, int32_t xbar_divisor, void* momentum,
+                                        void* anchor_out, void* params_out, void* gap_out,
+                                        const co2_hyper_t* hyper, void* workspace, void* stream);
+/* ||m'||_2 of the last co2_outer_step_global_clip on this workspace
+ * (synchronizes `stream`). */
+co2_status_t co2_global_clip_norm_fetch(const void* workspace, double* norm_out, void* stream);
+/* The fixed summation chunk (coordinates) that pass 1 uses for n. */
+int64_t co2_global_clip_chunk(co2_mode_t mode, int64_t n);
 
 /* Tuning knob: select the fused kernel's instantiation (elements per vector,
  * vectors in flight per thread, CTAs per SM); 0 = the measured default.

@@ -485,6 +485,7 @@ int orc_diag_status(const orc_diag* d) {
   if (f & ORC_FLAG_GAP_BELOW_ONE)
     return fail(ORC_VALIDATION, "momentum update: gap coordinate below 1");
   if (f & ORC_FLAG_M_NONFINITE) return fail(ORC_NUMERIC, "non-finite value in momentum update");
+  if (f & ORC_FLAG_NORM_NONFINITE) return fail(ORC_NUMERIC, "non-finite value in global clip norm");
   if (f & ORC_FLAG_CLIP_NONFINITE)
     return fail(ORC_NUMERIC, "non-finite value in clip_elementwise input");
   if (f & ORC_FLAG_X_NONFINITE) return fail(ORC_NUMERIC, "non-finite value in outer_iterate");
@@ -492,6 +493,162 @@ int orc_diag_status(const orc_diag* d) {
   if (f & ORC_FLAG_SLOWMO_X) return fail(ORC_NUMERIC, "non-finite value in slowmo outer iterate");
   if (f & ORC_FLAG_OVERLAP) return fail(ORC_NUMERIC, "non-finite value in overlap correction");
   return ORC_OK;
+}
+
+/* ------------------------------------- global-norm clip (extension) */
+#define GC_THREADS 256
+#define GC_MAX_CHUNKS 32768
+
+int64_t orc_gc_chunk(int64_t n, int V) {
+  const int64_t unit = (int64_t)V * GC_THREADS;
+  int64_t c = (n + GC_MAX_CHUNKS - 1) / GC_MAX_CHUNKS;
+  c = (c + unit - 1) / unit * unit;
+  return c < unit * 16 ? unit * 16 : c;
+}
+
+/* 256 per-thread partials -> xor butterfly per warp -> warps in order. */
+static double gc_block_sum(double* t) {
+  double w[GC_THREADS / 32];
+  for (int k = 0; k < GC_THREADS / 32; ++k) {
+    double* v = t + 32 * k;
+    for (int o = 16; o > 0; o >>= 1) {
+      double nv[32];
+      for (int l = 0; l < 32; ++l) nv[l] = v[l] + v[l ^ o];
+      memcpy(v, nv, sizeof nv);
+    }
+    w[k] = v[0];
+  }
+  double r = w[0];
+  for (int k = 1; k < GC_THREADS / 32; ++k) r = r + w[k];
+  return r;
+}
+
+int orc_outer_step_global_clip(int mode, int64_t n, const void* x_t0v, const void* p0v,
+                               const void* p1v, const void* xbarv, int divisor, void* mv,
+                               void* anchorv, void* paramsv, void* gapv, const orc_hyper* h,
+                               orc_diag* diag, double* norm_out) {
+  int s = orc_hyper_validate(h);
+  if (s) return s;
+  if (h->tau < 1) return fail(ORC_VALIDATION, "staleness_gap: tau must be >= 1");
+  if (divisor < 1) return fail(ORC_VALIDATION, "outer step: divisor must be >= 1");
+  if (mode != ORC_MODE_F64 && mode != ORC_MODE_F32 && mode != ORC_MODE_BF16_MIXED)
+    return fail(ORC_VALIDATION, "outer step: unknown mode");
+  const int V = mode == ORC_MODE_F64 ? 2 : (mode == ORC_MODE_F32 ? 4 : 8);
+  const int bf = mode == ORC_MODE_BF16_MIXED;
+  uint32_t flags = 0;
+  int64_t n_floored = 0, n_clipped = 0;
+  double min_gap = INFINITY, max_step = 0.0;
+  /* pass 1: m' (in place), gap, and the per-coordinate squares */
+  for (int64_t j = 0; j < n; ++j) {
+    if (mode == ORC_MODE_F64) {
+      const double x = ((const double*)x_t0v)[j], q0 = ((const double*)p0v)[j],
+                   q1 = ((const double*)p1v)[j], mo = ((double*)mv)[j];
+      double xb = ((const double*)xbarv)[j];
+      if (divisor > 1) xb = xb / (double)divisor;
+      const double tf = (double)h->tau, epsf = h->epsilon, betaf = h->beta;
+      double n0 = fabs(x - q0), a = fabs(tf * (q1 - q0));
+      int floored = a < epsf;
+      double lam = n0 / max_std(a, epsf) + 1.0;
+      double dl = q0 - xb;
+      double mn = h->penalty ? (betaf * mo + dl / lam) : (betaf * mo + dl);
+      if (!isfinite(lam)) flags |= ORC_FLAG_GAP_NONFINITE;
+      if (h->penalty && lam < 1.0) flags |= ORC_FLAG_GAP_BELOW_ONE;
+      if (!isfinite(mn)) flags |= ORC_FLAG_M_NONFINITE;
+      n_floored += floored;
+      if (lam < min_gap) min_gap = lam;
+      ((double*)mv)[j] = mn;
+      if (gapv) ((double*)gapv)[j] = lam;
+    } else {
+      const float x = ((const float*)x_t0v)[j], q0 = ((const float*)p0v)[j],
+                  mo = ((float*)mv)[j];
+      const float q1 = bf ? orc_bf16_to_f32(((const uint16_t*)p1v)[j]) : ((const float*)p1v)[j];
+      float xb = bf ? orc_bf16_to_f32(((const uint16_t*)xbarv)[j]) : ((const float*)xbarv)[j];
+      if (divisor > 1) xb = xb / (float)divisor;
+      const float tf = (float)h->tau, epsf = (float)h->epsilon, betaf = (float)h->beta;
+      float n0 = fabsf(x - q0), a = fabsf(tf * (q1 - q0));
+      int floored = a < epsf;
+      float lam = n0 / max_stdf(a, epsf) + 1.0f;
+      float dl = q0 - xb;
+      float mn = h->penalty ? (betaf * mo + dl / lam) : (betaf * mo + dl);
+      if (!isfinite(lam)) flags |= ORC_FLAG_GAP_NONFINITE;
+      if (h->penalty && lam < 1.0f) flags |= ORC_FLAG_GAP_BELOW_ONE;
+      if (!isfinite(mn)) flags |= ORC_FLAG_M_NONFINITE;
+      n_floored += floored;
+      if (lam < min_gap) min_gap = (double)lam;
+      ((float*)mv)[j] = mn;
+      if (gapv) ((float*)gapv)[j] = lam;
+    }
+  }
+  /* the norm in the GPU's fixed order */
+  const int64_t chunk = orc_gc_chunk(n, V);
+  const int64_t K = n == 0 ? 0 : (n + chunk - 1) / chunk;
+  const int64_t nvE = n / V * V;
+  double* cs = K ? malloc(sizeof(double) * (size_t)K) : NULL;
+  if (K && !cs) return fail(ORC_VALIDATION, "global clip: out of memory");
+  double t[GC_THREADS];
+  for (int64_t c = 0; c < K; ++c) {
+    const int64_t e0 = c * chunk, e1 = e0 + chunk < nvE ? e0 + chunk : nvE;
+    for (int th = 0; th < GC_THREADS; ++th) {
+      double acc = 0.0;
+      for (int64_t e = e0 + (int64_t)th * V; e < e1; e += (int64_t)GC_THREADS * V)
+        for (int v = 0; v < V; ++v) {
+          double md = mode == ORC_MODE_F64 ? ((double*)mv)[e + v] : (double)((float*)mv)[e + v];
+          acc = acc + md * md;
+        }
+      if (th == 0 && c == K - 1)
+        for (int64_t e = nvE; e < n; ++e) {
+          double md = mode == ORC_MODE_F64 ? ((double*)mv)[e] : (double)((float*)mv)[e];
+          acc = acc + md * md;
+        }
+      t[th] = acc;
+    }
+    cs[c] = gc_block_sum(t);
+  }
+  for (int th = 0; th < GC_THREADS; ++th) {
+    double acc = 0.0;
+    for (int64_t i = th; i < K; i += GC_THREADS) acc = acc + cs[i];
+    t[th] = acc;
+  }
+  const double norm = sqrt(gc_block_sum(t));
+  free(cs);
+  if (!isfinite(norm)) flags |= ORC_FLAG_NORM_NONFINITE;
+  const double sc = (h->clip && norm > h->phi) ? h->phi / norm : 1.0;
+  /* pass 2: x' = x_t0 - alpha * (m' * scale) */
+  for (int64_t j = 0; j < n; ++j) {
+    if (mode == ORC_MODE_F64) {
+      const double x = ((const double*)x_t0v)[j], m = ((double*)mv)[j];
+      const double c = m * sc;
+      const double xn = x - h->alpha * c;
+      if (!isfinite(xn)) flags |= ORC_FLAG_X_NONFINITE;
+      double st = fabs(xn - x);
+      if (st > max_step) max_step = st;
+      if (anchorv) ((double*)anchorv)[j] = xn;
+      if (paramsv) ((double*)paramsv)[j] = xn;
+    } else {
+      const float x = ((const float*)x_t0v)[j], m = ((float*)mv)[j];
+      const float c = (float)((double)m * sc);
+      const float xn = x - (float)h->alpha * c;
+      if (!isfinite(xn)) flags |= ORC_FLAG_X_NONFINITE;
+      float st = fabsf(xn - x);
+      if (st > max_step) max_step = (double)st;
+      if (anchorv) ((float*)anchorv)[j] = xn;
+      if (paramsv) {
+        if (bf)
+          ((uint16_t*)paramsv)[j] = orc_f32_to_bf16(xn);
+        else
+          ((float*)paramsv)[j] = xn;
+      }
+    }
+    n_clipped += sc < 1.0;
+  }
+  diag->min_gap = min_gap;
+  diag->max_outer_step = max_step;
+  diag->n_clipped = n_clipped;
+  diag->n_floored = n_floored;
+  diag->flags = flags;
+  diag->pad = 0;
+  if (norm_out) *norm_out = norm;
+  return orc_diag_status(diag);
 }
 
 /* ------------------------------------------------ baseline outer steps */

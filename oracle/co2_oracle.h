@@ -134,6 +134,26 @@ int orc_diag_status(const orc_diag* d);
  * status and message for its ensure_finite checks and fills diag
  * (max_outer_step and flags only). */
 enum { ORC_FLAG_SLOWMO_M = 64u, ORC_FLAG_SLOWMO_X = 128u, ORC_FLAG_OVERLAP = 256u };
+
+/* EXTENSION outside the reference parity contract (the reference clips
+ * coordinate-wise, proj/src/param_ops.cpp:35-43): the global-norm clip the
+ * north star words, restated in the GPU's exact summation order
+ * (paper_2401_16265_b200/csrc/outer_step.cu, gclip_pass1/2):
+ *   m' per coordinate as orc_outer_step; ||m'||^2 in fp64: fixed chunks of
+ *   orc_gc_chunk(n, V) coordinates; within a chunk, "thread" t (0..255) sums
+ *   (double)m'^2 over its V-wide vectors t, t+256, ... in order (the n % V
+ *   scalar tail goes to thread 0 of the last chunk, after its vectors);
+ *   a xor butterfly (16, 8, 4, 2, 1) per 32-thread warp; the 8 warps in
+ *   order.  Chunk sums fold the same way (thread t: chunks t, t+256, ...).
+ *   norm = sqrt; scale = (clip && norm > phi) ? phi / norm : 1 (fp64);
+ *   c = (T)((double)m' * scale); x' = x_t0 - alpha * c.
+ * V = 2 (fp64), 4 (fp32), 8 (bf16-mixed).  n_clipped = n when scaled. */
+enum { ORC_FLAG_NORM_NONFINITE = 512u };
+int64_t orc_gc_chunk(int64_t n, int V);
+int orc_outer_step_global_clip(int mode, int64_t n, const void* x_t0, const void* p0,
+                               const void* p1, const void* xbar, int divisor, void* m,
+                               void* anchor, void* params, void* gap, const orc_hyper* h,
+                               orc_diag* diag, double* norm_out);
 /* slowmo_round body (cpp:228-236): m = beta*m + (x_start - xbar);
  * params = x_start - alpha*m. */
 int orc_slowmo_step(int mode, int64_t n, const void* x_start, const void* xbar, int divisor,

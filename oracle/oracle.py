@@ -91,6 +91,11 @@ def lib():
                                           C.POINTER(C.c_double), C.POINTER(C.c_double), I]
         L.orc_outer_step.argtypes = [I, I64, P, P, P, P, I, P, P, P, P, C.POINTER(Hyper),
                                      C.POINTER(Diag)]
+        L.orc_outer_step_global_clip.argtypes = [I, I64, P, P, P, P, I, P, P, P, P,
+                                                 C.POINTER(Hyper), C.POINTER(Diag),
+                                                 C.POINTER(C.c_double)]
+        L.orc_gc_chunk.argtypes = [I64, I]
+        L.orc_gc_chunk.restype = I64
         L.orc_diag_status.argtypes = [C.POINTER(Diag)]
         L.orc_average_lp.argtypes = [I, I, P, I64, P]
         L.orc_synth.argtypes = [I, C.c_uint64, I, I64, I64, P, P, P, P, P]
@@ -291,6 +296,34 @@ def outer_step(mode: int, x_t0, p0, p1, xbar, m, h: Hyper, divisor: int = 1) -> 
     if code not in (OK, VALIDATION, NUMERIC):
         raise RuntimeError(msg)
     return FusedResult(mm, anchor, params, gap, d, code, msg)
+
+
+def outer_step_global_clip(mode: int, x_t0, p0, p1, xbar, m, h: Hyper, divisor: int = 1):
+    """EXTENSION outside the reference parity contract: the global-norm clip
+    in the GPU's fixed summation order (orc_outer_step_global_clip).
+    Returns (FusedResult, norm)."""
+    st = np.float64 if mode == MODE_F64 else np.float32
+    lo = np.float64 if mode == MODE_F64 else (np.uint16 if mode == MODE_BF16_MIXED else np.float32)
+    x = np.ascontiguousarray(x_t0, st)
+    q0 = np.ascontiguousarray(p0, st)
+    q1 = np.ascontiguousarray(p1, lo)
+    xb = np.ascontiguousarray(xbar, lo)
+    mm = np.array(m, dtype=st, copy=True)
+    n = x.size
+    anchor, params, gap = np.empty(n, st), np.empty(n, lo), np.empty(n, st)
+    d = Diag()
+    norm = C.c_double()
+    code = lib().orc_outer_step_global_clip(mode, n, _p(x), _p(q0), _p(q1), _p(xb), divisor,
+                                            _p(mm), _p(anchor), _p(params), _p(gap), C.byref(h),
+                                            C.byref(d), C.byref(norm))
+    msg = lib().orc_last_error().decode() if code else ""
+    if code not in (OK, VALIDATION, NUMERIC):
+        raise RuntimeError(msg)
+    return FusedResult(mm, anchor, params, gap, d, code, msg), norm.value
+
+
+def gc_chunk(n: int, v: int) -> int:
+    return lib().orc_gc_chunk(n, v)
 
 
 def outer_step_ghost(mode: int, anchor, p0, p1sum, p1_div: int, xsum, xdiv: int, ghost: int, m,

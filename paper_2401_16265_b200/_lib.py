@@ -17,6 +17,7 @@ MODE_F64, MODE_F32, MODE_BF16_MIXED = 0, 1, 2
 DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
 FLAG_GAP_NONFINITE, FLAG_GAP_BELOW_ONE, FLAG_M_NONFINITE = 1, 2, 4
 FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
+FLAG_SLOWMO_M, FLAG_SLOWMO_X, FLAG_OVERLAP, FLAG_NORM_NONFINITE = 64, 128, 256, 512
 BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
 BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT, BUF_XFIRST_ALT = 5, 6, 7, 8, 9
 IPC_HANDLE_BYTES = 64
@@ -85,6 +86,10 @@ SIGNATURES = {
     "co2_diag_fetch": (ST, [P, C.POINTER(Diag), P]),
     "co2_diag_status": (ST, [C.POINTER(Diag)]),
     "co2_outer_step": (ST, [I32, I64, P, P, P, P, I32, P, P, P, P, C.POINTER(Hyper), P, P]),
+    "co2_outer_step_global_clip": (ST, [I32, I64, P, P, P, P, I32, P, P, P, P, C.POINTER(Hyper),
+                                        P, P]),
+    "co2_global_clip_norm_fetch": (ST, [P, C.POINTER(D), P]),
+    "co2_global_clip_chunk": (I64, [I32, I64]),
     "co2_set_fused_variant": (ST, [I32]),
     "co2_set_grid_waves": (ST, [I32]),
     "co2_outer_step_host": (ST, [I32, I64, P, P, P, P, I32, P, P, P, C.POINTER(Hyper), I64, I32,

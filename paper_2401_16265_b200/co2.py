@@ -224,6 +224,28 @@ def outer_step(mode: int, x_t0, prev_x0, prev_x1, xbar, momentum, hyper: Co2Hype
     return None
 
 
+def outer_step_global_clip(mode: int, x_t0, prev_x0, prev_x1, xbar, momentum, hyper: Co2Hyper,
+                           tau: int, *, divisor: int = 1, anchor_out=None, params_out=None,
+                           gap_out=None, workspace: Workspace | None = None, stream=None):
+    """EXTENSION outside the reference parity contract: the outer step with
+    a global-norm clip of the outer momentum (c = m' * min(1, phi/||m'||_2))
+    instead of the reference's coordinate-wise clip.  Returns (Diag, norm)
+    after a stream sync."""
+    n = _same_len(x_t0, prev_x0, prev_x1, xbar, momentum, msg="staleness_gap: dimensions differ")
+    for t in (anchor_out, params_out, gap_out):
+        if t is not None and t.numel() != n:
+            raise ValidationError("outer step: output dimension differs")
+    ws = workspace or _ws(x_t0.device)
+    h = hyper.c(tau)
+    check(lib().co2_outer_step_global_clip(mode, n, _ptr(x_t0), _ptr(prev_x0), _ptr(prev_x1),
+                                           _ptr(xbar), divisor, _ptr(momentum), _ptr(anchor_out),
+                                           _ptr(params_out), _ptr(gap_out), C.byref(h), ws.ptr,
+                                           _stream(stream)))
+    norm = C.c_double()
+    check(lib().co2_global_clip_norm_fetch(ws.ptr, C.byref(norm), _stream(stream)))
+    return ws.fetch(stream), norm.value
+
+
 def outer_step_host(mode: int, x_t0, prev_x0, prev_x1, xbar, momentum, hyper: Co2Hyper, tau: int,
                     *, divisor: int = 1, anchor_out=None, params_out=None, chunk: int = 1 << 24,
                     nstreams: int = 3) -> L.Diag:

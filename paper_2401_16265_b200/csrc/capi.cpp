@@ -83,6 +83,8 @@ extern "C" co2_status_t co2_diag_status(const co2_diag_t* d) {
   if (f & CO2_FLAG_GAP_BELOW_ONE)
     return fail(CO2_ERR_VALIDATION, "momentum update: gap coordinate below 1");
   if (f & CO2_FLAG_M_NONFINITE) return fail(CO2_ERR_NUMERIC, "non-finite value in momentum update");
+  if (f & CO2_FLAG_NORM_NONFINITE)
+    return fail(CO2_ERR_NUMERIC, "non-finite value in global clip norm");
   if (f & CO2_FLAG_CLIP_NONFINITE)
     return fail(CO2_ERR_NUMERIC, "non-finite value in clip_elementwise input");
   if (f & CO2_FLAG_X_NONFINITE) return fail(CO2_ERR_NUMERIC, "non-finite value in outer_iterate");
@@ -131,6 +133,30 @@ extern "C" co2_status_t co2_outer_step(co2_mode_t mode, int64_t n, const void* x
   if (!ws) return fail(CO2_ERR_VALIDATION, "null workspace");
   return outer_step_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params, gap, h, ws,
                          S(stream));
+}
+
+extern "C" co2_status_t co2_outer_step_global_clip(co2_mode_t mode, int64_t n, const void* x_t0,
+                                                   const void* p0, const void* p1,
+                                                   const void* xbar, int32_t divisor, void* m,
+                                                   void* anchor, void* params, void* gap,
+                                                   const co2_hyper_t* h, void* ws, void* stream) {
+  CO2_TRY(validate_step(mode, n, x_t0, p0, p1, xbar, divisor, m, h));
+  if (!ws) return fail(CO2_ERR_VALIDATION, "null workspace");
+  return outer_step_global_clip_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params,
+                                     gap, h, ws, S(stream));
+}
+
+extern "C" co2_status_t co2_global_clip_norm_fetch(const void* ws, double* out, void* stream) {
+  if (!ws || !out) return fail(CO2_ERR_VALIDATION, "null workspace or output");
+  const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws);
+  CO2_CUDA(cudaMemcpyAsync(out, &hdr->gnorm, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+  CO2_CUDA(cudaStreamSynchronize(S(stream)));
+  return CO2_OK;
+}
+
+extern "C" int64_t co2_global_clip_chunk(co2_mode_t mode, int64_t n) {
+  const int V = mode == CO2_MODE_F64 ? 2 : (mode == CO2_MODE_F32 ? 4 : 8);
+  return gc_chunk(n, V);
 }
 
 // ---------------------------------------------------------------------------

@@ -146,8 +146,10 @@ struct AccT {
   }
 };
 
+// Returns true in every thread of the last block to arrive (after it wrote
+// the folded diagnostics), false elsewhere.
 template <int NT>
-__device__ void block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr) {
+__device__ bool block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr) {
   // Warp level.
   double mg = a.min_gap, ms = a.max_step;
   unsigned long long cl = a.clipped, fl = a.floored;
@@ -188,7 +190,7 @@ __device__ void block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) return false;
   // Last block: fold all partials in fixed index order (thread-strided, then
   // a fixed warp tree and fixed warp order), deterministic for a given grid.
   __threadfence();
@@ -234,6 +236,7 @@ __device__ void block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr
     __threadfence();
     if (px) p2p_exit_barrier(*px);
   }
+  return true;
 }
 
 // ---------------------------------------------------------- fused element
@@ -923,6 +926,274 @@ co2_status_t outer_step_impl(co2_mode_t mode, int64_t n, const void* x_t0, const
     case CO2_MODE_F64: return launch_fused<ModeF64>(a, s);
     case CO2_MODE_F32: return launch_fused<ModeF32>(a, s);
     case CO2_MODE_BF16_MIXED: return launch_fused<ModeBF16>(a, s);
+  }
+  return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
+}
+
+namespace {
+// ---------------------------------------------- global-norm clip extension
+// NOT part of the reference parity contract: the reference clips
+// coordinate-wise (param_ops.cpp:35-43, SURVEY.md 8 note 3).  The north
+// star's wording asks for a global-norm clip of the outer momentum; it is
+// provided as a separate entry (co2_outer_step_global_clip) with its own
+// restatement in the test oracle:
+//   pass 1: m' as in the fused step (gap, penalty), written in place, and
+//           ||m'||^2 summed in fp64 over fixed chunks (gc_chunk) -- thread t
+//           sums its vectors t, t+256, ... of the chunk in order, a fixed
+//           xor-butterfly per warp, warps in order; the last block folds
+//           the chunk sums the same way and stores sqrt into the workspace;
+//   pass 2: c = m' * min(1, phi/||m'||) (scale in fp64), x' = x_t0 - alpha*c.
+// The order depends on n and the mode only, so the norm is bitwise
+// reproducible across grids and GPUs.  34 B/param in bf16-mixed (pass 1
+// reads 16, writes 4; pass 2 reads 8, writes 6).
+__device__ __forceinline__ double warp_sum_fixed(double s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+template <typename TC>
+__device__ __forceinline__ TC gc_momentum(TC x, TC q0, TC q1, TC xb, TC m, TC& lam,
+                                          const Hyp<TC>& h, AccT<TC>& acc) {
+  if (h.divide) xb = xb / h.divisor;
+  TC n0 = fabs(x - q0);
+  TC av = fabs(h.tau * (q1 - q0));
+  bool floored = av < h.eps;
+  TC d = floored ? h.eps : av;
+  lam = n0 / d + (TC)1;
+  TC dl = q0 - xb;
+  TC bm = h.beta * m;
+  TC mn = h.penalty ? bm + dl / lam : bm + dl;
+  unsigned int f = 0;
+  if (!isfinite(lam)) f |= CO2_FLAG_GAP_NONFINITE;
+  if (h.penalty && lam < (TC)1) f |= CO2_FLAG_GAP_BELOW_ONE;
+  if (!isfinite(mn)) f |= CO2_FLAG_M_NONFINITE;
+  acc.flags |= f;
+  acc.floored += floored;
+  acc.min_gap = lam < acc.min_gap ? lam : acc.min_gap;
+  return mn;
+}
+
+template <typename T, int V, bool VEC>
+__device__ __forceinline__ void gc_load(const T* p, T (&out)[V]) {
+  if constexpr (VEC) {
+    ld_vec<T, V>(p, out);
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = p[v];
+  }
+}
+
+template <typename T, int V, bool VEC>
+__device__ __forceinline__ void gc_store(T* p, const T (&in)[V]) {
+  if constexpr (VEC) {
+    st_vec<T, V>(p, in);
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) p[v] = in[v];
+  }
+}
+
+template <class M>
+__device__ __forceinline__ Hyp<typename M::TC> make_hyp(const StepArgs& a) {
+  using TC = typename M::TC;
+  Hyp<TC> h;
+  h.tau = (TC)a.tau;
+  h.eps = (TC)a.eps;
+  h.beta = (TC)a.beta;
+  h.phi = (TC)a.phi;
+  h.alpha = (TC)a.alpha;
+  h.divisor = (TC)a.divisor;
+  h.penalty = a.penalty;
+  h.clip = a.clip;
+  h.divide = a.divisor > 1;
+  return h;
+}
+
+template <class M, int V, bool VEC>
+__global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int64_t chunk) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  constexpr int NT = kGcThreads, NW = NT / 32;
+  const Hyp<TC> h = make_hyp<M>(a);
+  const TS* X = static_cast<const TS*>(a.x_t0);
+  const TS* P0 = static_cast<const TS*>(a.p0);
+  const TL* P1 = static_cast<const TL*>(a.p1);
+  const TL* XB = static_cast<const TL*>(a.xbar);
+  TS* Mm = static_cast<TS*>(a.m);
+  TS* G = static_cast<TS*>(a.gap);
+  double* cs = ws_chunks(a.ws);
+  __shared__ double sh[NW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  AccT<TC> acc;
+  const int64_t nvE = a.n / V * V;
+  const int64_t K = (a.n + chunk - 1) / chunk;
+  for (int64_t c = blockIdx.x; c < K; c += gridDim.x) {
+    double s = 0.0;
+    const int64_t e0 = c * chunk;
+    const int64_t e1 = e0 + chunk < nvE ? e0 + chunk : nvE;
+    for (int64_t e = e0 + (int64_t)threadIdx.x * V; e < e1; e += (int64_t)NT * V) {
+      TS x[V], q0[V], mo[V], mn[V], gs[V];
+      TL q1[V], xb[V];
+      gc_load<TS, V, VEC>(X + e, x);
+      gc_load<TS, V, VEC>(P0 + e, q0);
+      gc_load<TL, V, VEC>(P1 + e, q1);
+      gc_load<TL, V, VEC>(XB + e, xb);
+      gc_load<TS, V, VEC>(Mm + e, mo);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        TC lam;
+        const TC m = gc_momentum<TC>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), to_c(xb[v]),
+                                     to_c(mo[v]), lam, h, acc);
+        mn[v] = (TS)m;
+        gs[v] = (TS)lam;
+        const double md = (double)mn[v];
+        s = s + md * md;
+      }
+      gc_store<TS, V, VEC>(Mm + e, mn);
+      if (G) gc_store<TS, V, VEC>(G + e, gs);
+    }
+    if (threadIdx.x == 0 && c == K - 1) {  // scalar tail, in index order
+      for (int64_t e = nvE; e < a.n; ++e) {
+        TC lam;
+        const TC m =
+            gc_momentum<TC>(to_c(X[e]), to_c(P0[e]), to_c(P1[e]), to_c(XB[e]), to_c(Mm[e]), lam,
+                            h, acc);
+        Mm[e] = (TS)m;
+        if (G) G[e] = (TS)lam;
+        const double md = (double)(TS)m;
+        s = s + md * md;
+      }
+    }
+    s = warp_sum_fixed(s);
+    if (lane == 0) sh[wid] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = sh[0];
+      for (int w = 1; w < NW; ++w) t = t + sh[w];
+      cs[c] = t;
+    }
+    __syncthreads();
+  }
+  if (block_finish<NT>(acc.widen(), a.ws)) {  // last block: fold the chunk sums
+    double b = 0.0;
+    for (int64_t i = threadIdx.x; i < K; i += NT) b = b + __ldcg(cs + i);
+    b = warp_sum_fixed(b);
+    __syncthreads();
+    if (lane == 0) sh[wid] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = sh[0];
+      for (int w = 1; w < NW; ++w) t = t + sh[w];
+      const double nrm = sqrt(t);
+      WsHeader* hdr = ws_header(a.ws);
+      hdr->pre = hdr->diag;
+      if (!isfinite(nrm)) hdr->pre.flags |= CO2_FLAG_NORM_NONFINITE;
+      hdr->gnorm = nrm;
+      __threadfence();
+    }
+  }
+}
+
+template <class M, int V, bool VEC>
+__global__ void __launch_bounds__(kGcThreads) gclip_pass2(const StepArgs a) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  constexpr int NT = kGcThreads;
+  const TS* X = static_cast<const TS*>(a.x_t0);
+  const TS* Mm = static_cast<const TS*>(a.m);
+  TS* A = static_cast<TS*>(a.anchor);
+  TL* PR = static_cast<TL*>(a.params);
+  const double nrm = ws_header(a.ws)->gnorm;
+  const double sc = (a.clip && nrm > a.phi) ? a.phi / nrm : 1.0;
+  const unsigned int scaled = sc < 1.0 ? 1u : 0u;
+  const TC alpha = (TC)a.alpha;
+  AccT<TC> acc;
+  auto elem = [&](TC x, TC m) -> TC {
+    TC c;
+    if constexpr (std::is_same<TC, double>::value)
+      c = m * sc;
+    else
+      c = (TC)((double)m * sc);
+    const TC ac = alpha * c;
+    const TC xn = x - ac;
+    if (!isfinite(xn)) acc.flags |= CO2_FLAG_X_NONFINITE;
+    acc.clipped += scaled;
+    const TC st = fabs(xn - x);
+    acc.max_step = st > acc.max_step ? st : acc.max_step;
+    return xn;
+  };
+  const int64_t nv = a.n / V;
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < nv; i += stride) {
+    const int64_t e = i * V;
+    TS x[V], mo[V], xs[V];
+    TL xl[V];
+    gc_load<TS, V, VEC>(X + e, x);
+    gc_load<TS, V, VEC>(Mm + e, mo);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const TC xn = elem(to_c(x[v]), to_c(mo[v]));
+      xs[v] = (TS)xn;
+      xl[v] = Store<TL>::from(xn);
+    }
+    if (A) gc_store<TS, V, VEC>(A + e, xs);
+    if (PR) gc_store<TL, V, VEC>(PR + e, xl);
+  }
+  const int64_t t = nv * V + (int64_t)blockIdx.x * NT + threadIdx.x;
+  if (V > 1 && t < a.n) {
+    const TC xn = elem(to_c(X[t]), to_c(Mm[t]));
+    if (A) A[t] = (TS)xn;
+    if (PR) PR[t] = Store<TL>::from(xn);
+  }
+  if (block_finish<NT>(acc.widen(), a.ws) && threadIdx.x == 0) {
+    // merge pass 1's gap / momentum diagnostics (stored by its last block)
+    WsHeader* hdr = ws_header(a.ws);
+    hdr->diag.min_gap = hdr->pre.min_gap;
+    hdr->diag.n_floored = hdr->pre.n_floored;
+    hdr->diag.flags |= hdr->pre.flags;
+    __threadfence();
+  }
+}
+
+template <class M>
+co2_status_t launch_global_clip(const StepArgs& a, cudaStream_t s) {
+  constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+  const bool vec = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) &&
+                   aligned16(a.xbar) && aligned16(a.m) && aligned16(a.anchor) &&
+                   aligned16(a.params) && aligned16(a.gap);
+  const int64_t chunk = gc_chunk(a.n, V);
+  const int64_t K = (a.n + chunk - 1) / chunk;
+  if (vec) {
+    auto k1 = gclip_pass1<M, V, true>;
+    k1<<<grid_for(k1, K * kGcThreads, kGcThreads), kGcThreads, 0, s>>>(a, chunk);
+    auto k2 = gclip_pass2<M, V, true>;
+    k2<<<grid_for(k2, a.n / V, kGcThreads), kGcThreads, 0, s>>>(a);
+  } else {
+    auto k1 = gclip_pass1<M, V, false>;
+    k1<<<grid_for(k1, K * kGcThreads, kGcThreads), kGcThreads, 0, s>>>(a, chunk);
+    auto k2 = gclip_pass2<M, V, false>;
+    k2<<<grid_for(k2, a.n / V, kGcThreads), kGcThreads, 0, s>>>(a);
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+}  // namespace
+
+co2_status_t outer_step_global_clip_impl(co2_mode_t mode, int64_t n, const void* x_t0,
+                                         const void* p0, const void* p1, const void* xbar,
+                                         int32_t divisor, void* m, void* anchor, void* params,
+                                         void* gap, const co2_hyper_t* h, void* ws,
+                                         cudaStream_t s) {
+  StepArgs a{x_t0, p0, p1, xbar, m, anchor, params, gap, n, h->alpha, h->beta, h->phi,
+             h->epsilon, h->tau, divisor, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, 0, 0,
+             nullptr};
+  switch (mode) {
+    case CO2_MODE_F64: return launch_global_clip<ModeF64>(a, s);
+    case CO2_MODE_F32: return launch_global_clip<ModeF32>(a, s);
+    case CO2_MODE_BF16_MIXED: return launch_global_clip<ModeBF16>(a, s);
   }
   return fail(CO2_ERR_VALIDATION, "outer step: unknown mode %d", (int)mode);
 }

@@ -405,3 +405,73 @@ def test_host_entry_concurrent_threads():
     for (_, _, _, _, _), anchor, params, ref in jobs:
         assert same(anchor.numpy(), ref.anchor)
         assert same(params.numpy().view(np.uint16), ref.params)
+
+
+# ------------------------------------------- global-norm clip (extension)
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("n", [0, 1, 7, 1000003, 3_000_001])
+@pytest.mark.parametrize("clip", [True, False])
+def test_global_clip_bitwise(mode, n, clip):
+    """EXTENSION outside the reference parity contract: the two-pass
+    global-norm clip against its oracle restatement (same fixed summation
+    order), bitwise -- m', anchor, params, gap, norm and diagnostics."""
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    o = O.synth(mode, n)
+    ref, rnorm = O.outer_step_global_clip(mode, *o, ohyper(12, True, clip))
+    assert ref.status == 0
+    anchor, params, gap = torch.empty_like(x), torch.empty_like(xe), torch.empty_like(x)
+    d, norm = co2.outer_step_global_clip(mode, x, p0, p1, xe, m, hyper(12, True, clip), 12,
+                                         anchor_out=anchor, params_out=params, gap_out=gap)
+    assert norm == rnorm or (n == 0 and norm == 0.0)
+    assert same(to_np(m), ref.m) and same(to_np(anchor), ref.anchor)
+    assert same(to_np(params), ref.params) and same(to_np(gap), ref.gap)
+    assert (d.min_gap, d.max_outer_step, d.n_clipped, d.n_floored, d.flags) == (
+        ref.diag.min_gap, ref.diag.max_outer_step, ref.diag.n_clipped, ref.diag.n_floored, 0)
+    if not clip:  # and then it is the reference-order fused step itself
+        x2, p02, p12, xe2, m2 = co2.synth(mode, n)
+        params2 = torch.empty_like(xe2)
+        co2.outer_step(mode, x2, p02, p12, xe2, m2, hyper(12, True, False), 12,
+                       params_out=params2)
+        assert same(to_np(params2), to_np(params)) and same(to_np(m2), to_np(m))
+
+
+def test_global_clip_grid_independent_and_unaligned():
+    """The norm's bits depend on n and the mode only: 1-wave and 32-wave
+    grids and the unaligned (scalar-load) path agree."""
+    mode, n = co2.MODE_BF16_MIXED, 2_000_003
+    res = []
+    try:
+        for waves in (1, 32):
+            co2.check(L.lib().co2_set_grid_waves(waves))
+            x, p0, p1, xe, m = co2.synth(mode, n)
+            params = torch.empty_like(xe)
+            _, norm = co2.outer_step_global_clip(mode, x, p0, p1, xe, m, hyper(12), 12,
+                                                 params_out=params)
+            res.append((norm, to_np(params), to_np(m)))
+    finally:
+        co2.check(L.lib().co2_set_grid_waves(32))
+    x, p0, p1, xe, m = co2.synth(mode, n + 1)
+    params = torch.empty(n + 1, dtype=xe.dtype, device="cuda")[1:]
+    mv = m[1:]
+    _, norm_u = co2.outer_step_global_clip(mode, x[1:], p0[1:], p1[1:], xe[1:], mv, hyper(12),
+                                           12, params_out=params)
+    ox, op0, op1, oxe, om = O.synth(mode, n + 1)
+    ref, rnorm = O.outer_step_global_clip(mode, ox[1:], op0[1:], op1[1:], oxe[1:], om[1:],
+                                          ohyper(12))
+    assert res[0][0] == res[1][0]
+    assert same(res[0][1], res[1][1]) and same(res[0][2], res[1][2])
+    assert norm_u == rnorm and same(to_np(params), ref.params) and same(to_np(mv), ref.m)
+
+
+def test_global_clip_errors():
+    mode, n = co2.MODE_F64, 4099
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    m.fill_(1e200)  # m' finite, ||m'||^2 overflows
+    with pytest.raises(co2.NumericError, match="non-finite value in global clip norm"):
+        co2.outer_step_global_clip(mode, x, p0, p1, xe, m, hyper(12), 12)
+    x, p0, p1, xe, m = co2.synth(mode, n)
+    m[5] = float("inf")
+    with pytest.raises(co2.NumericError, match="non-finite value in momentum update"):
+        co2.outer_step_global_clip(mode, x, p0, p1, xe, m, hyper(12), 12)
+    with pytest.raises(co2.ValidationError, match="hyper: phi must be positive"):
+        co2.outer_step_global_clip(mode, x, p0, p1, xe, m, co2.Co2Hyper(phi=0.0), 12)
