@@ -283,12 +283,20 @@ co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers);
  *   3. for every buffer that will be reduced (e.g. both ping-pong params of
  *      a worker): export, exchange, co2_aar_p2p_attach.
  * `ctas` bounds the SMs the reduce occupies while it overlaps compute. */
-#define CO2_IPC_HANDLE_BYTES 64
+/* An exported buffer: the CUDA IPC handle of the allocation that contains
+ * dev_ptr (64 bytes) followed by dev_ptr's int64 byte offset in it, so
+ * sub-allocated buffers (e.g. from a caching allocator) map correctly. */
+#define CO2_IPC_HANDLE_BYTES 72
 co2_status_t co2_ipc_export(const void* dev_ptr, uint8_t handle_out[CO2_IPC_HANDLE_BYTES]);
 co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_t world, int32_t ctas);
 void* co2_aar_signal_buffer(co2_aar_t* engine);
 co2_status_t co2_aar_p2p_attach_signals(co2_aar_t* engine, const uint8_t* handles);
 co2_status_t co2_aar_p2p_attach(co2_aar_t* engine, const void* local_buf, const uint8_t* handles);
+/* Undo co2_aar_p2p_attach for `local`: waits for this engine's reduces and
+ * closes the peer mappings.  Every rank detaches the buffer, then the group
+ * synchronises, before any rank frees it (peers must not read freed
+ * memory). */
+co2_status_t co2_aar_p2p_detach(co2_aar_t* engine, const void* local);
 /* P2P only: run worker-local co2_round (t >= 1) as ONE kernel that does the
  * outer step on the previously reduced average AND the fixed-order NVLink
  * average of this round's x_{t,tau} (consumed next round, so the schedule

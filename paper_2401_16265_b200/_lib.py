@@ -20,7 +20,7 @@ FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
 FLAG_SLOWMO_M, FLAG_SLOWMO_X, FLAG_OVERLAP, FLAG_NORM_NONFINITE = 64, 128, 256, 512
 BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
 BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT, BUF_XFIRST_ALT = 5, 6, 7, 8, 9
-IPC_HANDLE_BYTES = 64
+IPC_HANDLE_BYTES = 72  # CUDA IPC handle (64) + int64 offset
 NCCL_ID_BYTES = 128
 
 
@@ -119,6 +119,7 @@ SIGNATURES = {
     "co2_aar_signal_buffer": (P, [P]),
     "co2_aar_p2p_attach_signals": (ST, [P, C.POINTER(C.c_uint8)]),
     "co2_aar_p2p_attach": (ST, [P, P, C.POINTER(C.c_uint8)]),
+    "co2_aar_p2p_detach": (ST, [P, P]),
     "co2_aar_set_fused": (ST, [P, I32]),
     "co2_aar_destroy": (ST, [P]),
     "co2_aar_world": (I32, [P]),

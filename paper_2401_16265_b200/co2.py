@@ -410,6 +410,18 @@ class CollectiveEngine:
         reducible; collective over the group."""
         check(lib().co2_aar_p2p_attach(self.handle, ptr, self._exchange(ptr)))
 
+    def deregister(self, ptr: int) -> None:
+        """P2P: undo register(); collective.  Returns after every rank closed
+        its mapping, so the owner may then free the buffer."""
+        check(lib().co2_aar_p2p_detach(self.handle, ptr))
+        if self.workers > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def deregister_worker(self, worker: "Worker") -> None:
+        for which in (L.BUF_PARAMS, L.BUF_PARAMS_ALT):
+            self.deregister(lib().co2_worker_buffer(worker.handle, which))
+
     def set_fused(self, on: bool = True) -> None:
         """P2P: fuse the one-step-stale all-reduce into the outer-step kernel."""
         check(lib().co2_aar_set_fused(self.handle, int(on)))

@@ -10,6 +10,7 @@
 // device time between the consumer reaching the wait and the reduce finishing
 // (events straddling cudaStreamWaitEvent), the measured counterpart of the
 // reference's `stall = max(0, completion - now)` (collective.cpp:93).
+#include <cuda.h>  // CUdeviceptr / CUresult for the driver entry point below
 #include <cuda_runtime.h>
 #include <math.h>
 #include <nccl.h>
@@ -18,6 +19,8 @@
 
 #include <algorithm>
 #include <limits>
+#include <map>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -58,6 +61,7 @@ constexpr size_t kRing = 256;
 struct P2PBuffer {
   const void* local = nullptr;
   std::vector<void*> ptrs;
+  std::vector<std::pair<int, std::string>> keys;  // opened peer allocations it holds
 };
 
 ncclDataType_t nccl_dtype(co2_dtype_t d) {
@@ -85,7 +89,13 @@ struct co2_aar {
   void* signals = nullptr;        // this rank's signal area (cudaMalloc, IPC-exported)
   std::vector<void*> peer_signals;  // rank-indexed (opened IPC pointers; own = signals)
   std::vector<P2PBuffer> p2p_bufs;
-  std::vector<void*> opened;      // IPC pointers to close
+  // Opened peer allocations, keyed by (peer rank, IPC handle bytes) and
+  // reference-counted: several registered buffers may share one allocation.
+  struct Opened {
+    void* base = nullptr;
+    int refs = 0;
+  };
+  std::map<std::pair<int, std::string>, Opened> opened;
   // pinned per-launch slots (ring) and the reusable producer fence
   co2_diag_t* pin_diag = nullptr;
   uint32_t* pin_err = nullptr;
@@ -140,12 +150,38 @@ extern "C" co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO
   return CO2_OK;
 }
 
+// Base of the allocation containing p (driver cuMemGetAddressRange, reached
+// through the runtime's entry-point query so the library needs no -lcuda).
+static co2_status_t alloc_base(const void* p, char** base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CO2_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess)
+      return fail(CO2_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    fn = reinterpret_cast<Fn>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t size = 0;
+  if (fn(&b, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+    return fail(CO2_ERR_VALIDATION, "ipc export: not a device allocation");
+  *base = reinterpret_cast<char*>(b);
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_ipc_export(const void* dev_ptr, uint8_t handle_out[CO2_IPC_HANDLE_BYTES]) {
-  static_assert(sizeof(cudaIpcMemHandle_t) == CO2_IPC_HANDLE_BYTES, "IPC handle size");
+  static_assert(sizeof(cudaIpcMemHandle_t) + sizeof(int64_t) == CO2_IPC_HANDLE_BYTES,
+                "IPC handle size");
   if (!dev_ptr) return fail(CO2_ERR_VALIDATION, "ipc export: null pointer");
+  char* base = nullptr;
+  CO2_TRY(alloc_base(dev_ptr, &base));
   cudaIpcMemHandle_t h;
-  CO2_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  CO2_CUDA(cudaIpcGetMemHandle(&h, base));
+  const int64_t off = static_cast<const char*>(dev_ptr) - base;
   memcpy(handle_out, &h, sizeof h);
+  memcpy(handle_out + sizeof h, &off, sizeof off);
   return CO2_OK;
 }
 
@@ -192,20 +228,48 @@ extern "C" co2_status_t co2_aar_set_fused(co2_aar_t* e, int32_t on) {
   return CO2_OK;
 }
 
+// Drop one reference to each opened peer allocation in `keys`.
+static co2_status_t release_keys(co2_aar* e, const std::vector<std::pair<int, std::string>>& keys) {
+  for (const auto& key : keys) {
+    auto it = e->opened.find(key);
+    if (it == e->opened.end()) continue;
+    if (--it->second.refs == 0) {
+      void* base = it->second.base;
+      e->opened.erase(it);
+      CO2_CUDA(cudaIpcCloseMemHandle(base));
+    }
+  }
+  return CO2_OK;
+}
+
 static co2_status_t open_peers(co2_aar* e, const void* local, const uint8_t* handles,
-                               std::vector<void*>* out) {
+                               std::vector<void*>* out,
+                               std::vector<std::pair<int, std::string>>* keys = nullptr) {
   out->assign(e->world, nullptr);
   for (int p = 0; p < e->world; ++p) {
     if (p == e->rank) {
       (*out)[p] = const_cast<void*>(local);
       continue;
     }
+    const uint8_t* rec = handles + (size_t)p * CO2_IPC_HANDLE_BYTES;
     cudaIpcMemHandle_t h;
-    memcpy(&h, handles + (size_t)p * CO2_IPC_HANDLE_BYTES, sizeof h);
-    void* ptr = nullptr;
-    CO2_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
-    e->opened.push_back(ptr);
-    (*out)[p] = ptr;
+    int64_t off = 0;
+    memcpy(&h, rec, sizeof h);
+    memcpy(&off, rec + sizeof h, sizeof off);
+    auto key = std::make_pair(p, std::string(reinterpret_cast<const char*>(rec), sizeof h));
+    co2_aar::Opened& o = e->opened[key];
+    if (o.refs == 0) {
+      void* base = nullptr;
+      cudaError_t ce = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+      if (ce != cudaSuccess) {
+        e->opened.erase(key);
+        return cuda_fail(ce, "cudaIpcOpenMemHandle");
+      }
+      o.base = base;
+    }
+    o.refs += 1;
+    if (keys) keys->push_back(key);
+    (*out)[p] = static_cast<char*>(o.base) + off;
   }
   return CO2_OK;
 }
@@ -221,9 +285,26 @@ extern "C" co2_status_t co2_aar_p2p_attach(co2_aar_t* e, const void* local,
   if (!local) return fail(CO2_ERR_VALIDATION, "attach: null buffer");
   P2PBuffer b;
   b.local = local;
-  CO2_TRY(open_peers(e, local, handles, &b.ptrs));
+  co2_status_t st = open_peers(e, local, handles, &b.ptrs, &b.keys);
+  if (st != CO2_OK) {
+    release_keys(e, b.keys);  // keep the first error's message
+    return st;
+  }
   e->p2p_bufs.push_back(b);
   return CO2_OK;
+}
+
+extern "C" co2_status_t co2_aar_p2p_detach(co2_aar_t* e, const void* local) {
+  if (!e || e->transport != T_P2P) return fail(CO2_ERR_VALIDATION, "detach: not a P2P engine");
+  for (size_t i = 0; i < e->p2p_bufs.size(); ++i) {
+    if (e->p2p_bufs[i].local != local) continue;
+    // no reduce of ours may still read the peers' memory
+    CO2_CUDA(cudaStreamSynchronize(e->comm_stream));
+    const std::vector<std::pair<int, std::string>> keys = e->p2p_bufs[i].keys;
+    e->p2p_bufs.erase(e->p2p_bufs.begin() + (std::ptrdiff_t)i);
+    return release_keys(e, keys);
+  }
+  return fail(CO2_ERR_VALIDATION, "detach: buffer not registered for P2P");
 }
 
 extern "C" co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers) {
@@ -254,7 +335,7 @@ extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
   if (e->comm2) ncclCommDestroy(e->comm2);
   if (e->comm) ncclCommDestroy(e->comm);
   if (e->ws) cudaFree(e->ws);
-  for (void* p : e->opened) cudaIpcCloseMemHandle(p);
+  for (auto& kv : e->opened) cudaIpcCloseMemHandle(kv.second.base);
   if (e->signals) cudaFree(e->signals);
   if (e->epoch) cudaEventDestroy(e->epoch);
   if (e->comm_stream) cudaStreamDestroy(e->comm_stream);

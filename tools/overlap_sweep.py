@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=6)
     ap.add_argument("--knee", type=float, default=4.0, help="tau at which tau*t_comp = t_comm")
     ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"])
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
@@ -43,8 +44,12 @@ def main():
     if world > 1:
         dist.init_process_group("gloo")
     uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
-    eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
-                               max_ctas=a.max_ctas)
+    p2p = a.transport == "p2p" and world > 1
+    if p2p:
+        eng = co2.CollectiveEngine(world, transport="p2p", rank=rank, max_ctas=a.max_ctas)
+    else:
+        eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
+                                   max_ctas=a.max_ctas)
     solo = co2.CollectiveEngine(1, transport="nccl", rank=0, nccl_id=bytes(128))
     hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
     stream = torch.cuda.current_stream()
@@ -52,6 +57,8 @@ def main():
 
     # t_comm: the reduce alone (scratch buffer, same size and dtype)
     scratch = torch.zeros(a.n, dtype=lo, device="cuda")
+    if p2p:
+        eng.register(scratch.data_ptr())
     comms = []
     for i in range(6):
         h = eng.launch_all_reduce([scratch], scratch)
@@ -60,6 +67,8 @@ def main():
         if i >= 2:
             comms.append(eng.stall(h)[1])
     t_comm = max_over_ranks([statistics.median(comms)], device="cpu")[0] if world > 1 else 0.0
+    if p2p:
+        eng.deregister(scratch.data_ptr())
     del scratch
 
     # t_comp: calibrate the synthetic inner step to t_comm / knee
@@ -85,6 +94,8 @@ def main():
 
     def run(engine, tau):
         w2 = co2.Worker(a.mode, a.n, w.params, keep_gap=False)
+        if p2p and engine is eng:
+            engine.register_worker(w2)
         w2.enable_timing(4 * a.rounds)
         n_ev0 = len(engine.events())
         walls = []
@@ -113,6 +124,8 @@ def main():
         waits = [e for e in ev if e["event"] == "wait"][1:-1]
         stall = sum(e["stall"] for e in waits)
         waited = sum(completes[e["handle_id"]] - launches[e["handle_id"]] for e in waits)
+        if p2p and engine is eng:
+            engine.deregister_worker(w2)
         w2.close()
         return statistics.mean(walls[2:]), stall, waited, len(waits), \
             (statistics.mean(kt) if kt else 0.0)
@@ -132,6 +145,7 @@ def main():
         pst = [p[2] for p in pred.per_round[2:]]
         pred_exposed = 100.0 * sum(pst) / (t_comm * len(pst)) if t_comm and pst else 0.0
         row = {"tau": tau, "world": world, "n": a.n, "mode": a.mode,
+               "transport": "p2p" if p2p else "nccl",
                "t_comm_ms": 1e3 * t_comm, "t_comp_ms": 1e3 * t_comp, "t_outer_ms": 1e3 * t_outer,
                "inner_repeat": repeat, "exposed_pct": 100.0 * stall / waited if waited else 0.0,
                "stall_ms_per_round": 1e3 * stall / max(nw, 1),
