@@ -317,7 +317,7 @@ struct StepArgs {
   // P2P fused all-gather (P2POUT instantiations only)
   void* out_peers[kMaxRanks];
   P2PExit exit;
-  // Fused one-step-stale all-reduce (AARFUSE instantiations only): slice
+  // Fused one-step-stale all-reduce (AAR > 0 instantiations; AAR = rank capacity): slice
   // [aar_lo, aar_lo + aar_len) of the rank-indexed buffers aar_bufs (x_{t,tau}
   // on every rank) is averaged in rank order and stored into every rank.
   void* aar_bufs[kMaxRanks];
@@ -326,19 +326,19 @@ struct StepArgs {
 
 // One 16-byte vector of the fixed-order P2P average (param_ops.cpp:16-33):
 // gather from every rank, sum in rank order, divide once, store to every rank.
-template <typename TL, typename TC>
+template <typename TL, typename TC, int R>
 __device__ __forceinline__ void aar_vector(const StepArgs& a, int64_t e) {
   constexpr int VA = 16 / (int)sizeof(TL);
-  uint4 raw[kMaxRanks];
+  uint4 raw[R];
 #pragma unroll
-  for (int p = 0; p < kMaxRanks; ++p)
+  for (int p = 0; p < R; ++p)
     if (p < a.exit.world)
       raw[p] = __ldcg(reinterpret_cast<const uint4*>(static_cast<const TL*>(a.aar_bufs[p]) + e));
   TC acc[VA];
 #pragma unroll
   for (int k = 0; k < VA; ++k) acc[k] = to_c(reinterpret_cast<const TL*>(&raw[0])[k]);
 #pragma unroll
-  for (int p = 1; p < kMaxRanks; ++p)
+  for (int p = 1; p < R; ++p)
     if (p < a.exit.world)
 #pragma unroll
       for (int k = 0; k < VA; ++k) acc[k] = acc[k] + to_c(reinterpret_cast<const TL*>(&raw[p])[k]);
@@ -347,7 +347,7 @@ __device__ __forceinline__ void aar_vector(const StepArgs& a, int64_t e) {
 #pragma unroll
   for (int k = 0; k < VA; ++k) reinterpret_cast<TL*>(&out)[k] = Store<TL>::from(acc[k] / g);
 #pragma unroll
-  for (int p = 0; p < kMaxRanks; ++p)
+  for (int p = 0; p < R; ++p)
     if (p < a.exit.world) __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.aar_bufs[p]) + e), out);
 }
 
@@ -361,7 +361,7 @@ __device__ __forceinline__ TC ghost_avg(TC v, int g) {
 }
 
 template <class M, int V, int U, int NT, int MINB, bool GHOST = false, bool P2POUT = false,
-          bool AARFUSE = false>
+          int AAR = 0>
 __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
@@ -394,22 +394,22 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
   const int64_t nv = a.n / V;
   const int64_t stride = (int64_t)gridDim.x * NT;
   int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
-  // AARFUSE: every rank's x_{t,tau} is final once all ranks arrived; the
+  // AAR > 0: every rank's x_{t,tau} is final once all ranks arrived; the
   // all-reduce vectors are interleaved with the outer-step vectors (one per
   // world-size step vectors) so both streams share HBM and NVLink evenly.
   constexpr int VA = 16 / (int)sizeof(TL);
-  const int64_t aar_nvec = AARFUSE ? a.aar_len / VA : 0;
+  const int64_t aar_nvec = AAR > 0 ? a.aar_len / VA : 0;
   bool aar_ok = true;
-  if constexpr (AARFUSE) {
+  if constexpr (AAR > 0) {
     __shared__ int s_go;
     if (threadIdx.x == 0) s_go = p2p_entry_barrier(a.exit);
     __syncthreads();
     aar_ok = s_go != 0;
   }
-  const int gw = AARFUSE ? a.exit.world : 1;
+  const int gw = AAR > 0 ? a.exit.world : 1;
   auto aar_for = [&](int64_t iv) {
-    if constexpr (AARFUSE) {
-      if (aar_ok && iv % gw == 0 && iv / gw < aar_nvec) aar_vector<TL, TC>(a, a.aar_lo + (iv / gw) * VA);
+    if constexpr (AAR > 0) {
+      if (aar_ok && iv % gw == 0 && iv / gw < aar_nvec) aar_vector<TL, TC, (AAR > 0 ? AAR : 1)>(a, a.aar_lo + (iv / gw) * VA);
     }
   };
 
@@ -483,12 +483,12 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
     process(idx, 1);
     aar_for(i);
   }
-  if constexpr (AARFUSE) {
+  if constexpr (AAR > 0) {
     // all-reduce vectors not covered by the interleave, then its scalar tail
     const int64_t covered = (nv + gw - 1) / gw;
     for (int64_t ia = covered + (int64_t)blockIdx.x * NT + threadIdx.x; aar_ok && ia < aar_nvec;
          ia += stride)
-      aar_vector<TL, TC>(a, a.aar_lo + ia * VA);
+      aar_vector<TL, TC, (AAR > 0 ? AAR : 1)>(a, a.aar_lo + ia * VA);
     if (aar_ok && blockIdx.x == 0) {
       for (int64_t j = a.aar_lo + aar_nvec * VA + threadIdx.x; j < a.aar_lo + a.aar_len;
            j += NT) {
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
     }
     if (G) G[t] = (TS)lam;
   }
-  if constexpr (P2POUT || AARFUSE)
+  if constexpr (P2POUT || AAR > 0)
     block_finish<NT>(acc.widen(), a.ws, &a.exit);
   else
     block_finish<NT>(acc.widen(), a.ws);
@@ -1206,8 +1206,18 @@ co2_status_t launch_fused_aar(const StepArgs& a, cudaStream_t s) {
             aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap);
   for (int p = 0; p < a.exit.world; ++p) ok = ok && aligned16(a.aar_bufs[p]);
   if (!ok) return fail(CO2_ERR_VALIDATION, "fused all-reduce step: buffers must be 16-byte aligned");
-  auto k = fused_step_kernel<M, V, 1, kThreads, 4, false, false, true>;
-  k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  // Rank capacity of the instantiation: the gather registers scale with it
+  // (8 x 16 B spilled at 4 CTAs/SM when one instantiation served all G).
+  if (a.exit.world <= 2) {
+    auto k = fused_step_kernel<M, V, 1, kThreads, 3, false, false, 2>;
+    k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  } else if (a.exit.world <= 4) {
+    auto k = fused_step_kernel<M, V, 1, kThreads, 3, false, false, 4>;
+    k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  } else {
+    auto k = fused_step_kernel<M, V, 1, kThreads, 3, false, false, 8>;
+    k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  }
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }
