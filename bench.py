@@ -237,7 +237,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26,
+                    help="coordinates in the 1-core CPU baseline sample (~10 s of CPU work)")
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--schedule", default="split", choices=["split", "fused"],
