@@ -147,9 +147,11 @@ int64_t co2_global_clip_chunk(co2_mode_t mode, int64_t n);
  * tools/tune_fused.py. */
 co2_status_t co2_set_fused_variant(int32_t variant);
 /* Tuning knob: grid size of the step kernels in waves of the idle-GPU
- * resident CTA count (1 = persistent, the default; >1 oversubscribes so a
- * co-running reduce kernel does not leave a late second wave).  Also
- * CO2_GRID_WAVES. */
+ * resident CTA count (1 = persistent; the default 32 oversubscribes so the
+ * block scheduler balances the tail and a co-running reduce kernel does
+ * not leave a late second wave), in [1, 64].  Grids stop growing where a
+ * CTA would get fewer than 8 grid-stride iterations (CO2_MIN_CTA_ITERS).
+ * Also CO2_GRID_WAVES. */
 co2_status_t co2_set_grid_waves(int32_t waves);
 
 /* End-to-end form of co2_outer_step over HOST buffers (the reference's own
