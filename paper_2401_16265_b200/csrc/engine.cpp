@@ -195,11 +195,11 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
   e->rank = rank;
   e->world = world;
   e->workers = world;
-  // 64 CTAs measured best while the reduce shares HBM and SMs with the
-  // 32-wave fused outer step (bench.py --max-ctas sweep 24..148 at N = 2, 4,
-  // profiles/r01/bench/ctas_sweep.txt): fewer starve the reduce, more steal
-  // SM slots from the step.
-  e->ctas = ctas > 0 ? ctas : 64;
+  // 96 (G = 2) / 64 (G >= 4) CTAs of 256 threads measured best while the
+  // reduce shares HBM and SMs with the 32-wave fused outer step (bench.py
+  // --max-ctas sweeps, profiles/r01/bench/{ctas,p2p_threads}_sweep.txt):
+  // fewer starve the reduce, more steal SM slots from the step.
+  e->ctas = ctas > 0 ? ctas : (world <= 2 ? 96 : 64);
   // The sharded slice reduce runs beside a step that touches 1/world of the
   // parameters, so it wants the whole chip: 0 = the launcher's per-world
   // default (C4 N=4: 592 CTAs 49.0 ms/round vs 64 CTAs 61.7,

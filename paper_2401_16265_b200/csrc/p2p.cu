@@ -50,8 +50,8 @@ struct P2PArgs {
 };
 
 // TL storage, TC compute, V elements per 16-byte vector.
-template <typename TL, typename TC, int V, int R, int U>
-__global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs a) {
+template <typename TL, typename TC, int V, int R, int U, int NT>
+__global__ void __launch_bounds__(NT) p2p_average_kernel(const P2PArgs a) {
   Signals* mine = a.sig[a.rank];
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs 
     if (hi > a.n) hi = a.n;
     const TC g = (TC)a.world;
     const int64_t nvec = hi > lo ? (hi - lo) / V : 0;
-    const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
+    const int64_t stride = (int64_t)gridDim.x * NT;
     // U vectors per thread in flight, each gathered from every rank: the
     // remote (NVLink) loads are issued back to back before any arithmetic.
     auto reduce_store = [&](const uint4 (&raw)[R], int64_t e) {
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs 
       for (int p = 0; p < R; ++p)
         if (p < a.world) __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.bufs[p]) + e), out);
     };
-    int64_t i = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x;
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
     for (; i + (int64_t)(U - 1) * stride < nvec; i += (int64_t)U * stride) {
       uint4 raw[U][R];
 #pragma unroll
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_average_kernel(const P2PArgs 
     }
     // scalar tail of the last slice (n not a multiple of V)
     if (blockIdx.x == 0) {
-      for (int64_t j = lo + nvec * V + threadIdx.x; j < hi; j += kP2PThreads) {
+      for (int64_t j = lo + nvec * V + threadIdx.x; j < hi; j += NT) {
         TC acc;
         if constexpr (sizeof(TL) == 2)
           acc = ld_c(static_cast<const bf16raw*>(a.bufs[0]) + j);
@@ -273,6 +273,21 @@ int rank_cap(int world) {
   return cap;
 }
 
+// Threads per CTA of the all-reduce kernel (CO2_P2P_THREADS = 128 | 256 |
+// 512, default 256): its register footprint decides how many fused-step
+// CTAs still fit on the SMs it occupies (the step uses the whole register
+// file at 4 CTAs/SM).  C3 sweep, 3 interleaved passes on one box
+// (profiles/r01/bench/p2p_threads_sweep.txt): 256 threads beat 512 by
+// +1.2 % at N=2 (96 CTAs) and +4 % at N=4 (64 CTAs).
+int p2p_threads() {
+  static const int v = [] {
+    const char* e = getenv("CO2_P2P_THREADS");
+    const int x = e ? atoi(e) : 256;
+    return (x == 128 || x == 512) ? x : 256;
+  }();
+  return v;
+}
+
 }  // namespace
 
 co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const* src0,
@@ -342,19 +357,29 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
   // R = rank capacity of the instantiation, U = vectors in flight per thread
   // (fewer ranks -> more vectors, keeping ~R*U*16 B of loads per thread).
   const int cap = rank_cap(world);
-#define CO2_P2P_LAUNCH(TL, TC, V)                                                        \
-  if (cap == 2)                                                                         \
-    p2p_average_kernel<TL, TC, V, 2, 4><<<ctas, kP2PThreads, 0, s>>>(a);                \
-  else if (cap == 4)                                                                    \
-    p2p_average_kernel<TL, TC, V, 4, 2><<<ctas, kP2PThreads, 0, s>>>(a);                \
+  const int nt = p2p_threads();
+#define CO2_P2P_NT(TL, TC, V, R, U)                                                      \
+  if (nt == 128)                                                                        \
+    p2p_average_kernel<TL, TC, V, R, U, 128><<<ctas, 128, 0, s>>>(a);                   \
+  else if (nt == 256)                                                                   \
+    p2p_average_kernel<TL, TC, V, R, U, 256><<<ctas, 256, 0, s>>>(a);                   \
   else                                                                                  \
-    p2p_average_kernel<TL, TC, V, 8, 1><<<ctas, kP2PThreads, 0, s>>>(a);
+    p2p_average_kernel<TL, TC, V, R, U, 512><<<ctas, 512, 0, s>>>(a);
+#define CO2_P2P_LAUNCH(TL, TC, V)                                                        \
+  if (cap == 2) {                                                                       \
+    CO2_P2P_NT(TL, TC, V, 2, 4)                                                          \
+  } else if (cap == 4) {                                                                \
+    CO2_P2P_NT(TL, TC, V, 4, 2)                                                          \
+  } else {                                                                              \
+    CO2_P2P_NT(TL, TC, V, 8, 1)                                                          \
+  }
   switch (dt) {
     case CO2_DTYPE_F64: CO2_P2P_LAUNCH(double, double, 2) break;
     case CO2_DTYPE_F32: CO2_P2P_LAUNCH(float, float, 4) break;
     default: CO2_P2P_LAUNCH(bf16raw, float, 8) break;
   }
 #undef CO2_P2P_LAUNCH
+#undef CO2_P2P_NT
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }
