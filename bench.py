@@ -175,6 +175,21 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def host_info() -> dict:
+    """nproc / affinity / CPU model / RAM of the host the CPU arms ran on."""
+    info = {"nproc": os.cpu_count(), "affinity_cores": host_cores()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            info["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in f
+                                      if ln.startswith("model name")), None)
+        with open("/proc/meminfo") as f:
+            kb = next(int(ln.split()[1]) for ln in f if ln.startswith("MemTotal"))
+        info["mem_gb"] = round(kb / 1e6, 1)
+    except Exception:
+        pass
+    return info
+
+
 # ----------------------------------------------------------------- CPU arms
 def cpu_sample_inputs(cfg, n_sample: int):
     """fp64 upcast of the same synthetic inputs (first n_sample coordinates)."""
@@ -200,6 +215,53 @@ def time_cpu_step(cfg, n_sample: int, threads: int, steps: int, warmup: int):
     return n_sample / statistics.mean(times), statistics.mean(times)
 
 
+def time_cpu_average(n_sample: int, workers: int = 4, reps: int = 3) -> dict:
+    """The reference's CPU all-reduce arithmetic, average()
+    (proj/src/param_ops.cpp:16-33), fp64 and single-threaded as the
+    reference runs it, over `workers` contributions of n_sample."""
+    import numpy as np
+    from oracle import oracle as O
+    cs = [O.to_f64(O.synth(2, n_sample, worker=w)[3]) for w in range(workers)]
+    O.average(cs)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.average(cs)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    del cs, np
+    return {"value": n_sample / t, "unit": "params/s", "workers": workers, "cores": 1,
+            "sample": f"{n_sample} coordinates x {workers} fp64 contributions"}
+
+
+def time_cpu_fused_bound(cfg, n_sample: int, threads: int, reps: int = 3) -> dict:
+    """NOT the reference: the fused same-order step (oracle orc_outer_step,
+    the GPU's storage types) on every host core over contiguous ranges -- a
+    best-case CPU bound for the same work."""
+    import concurrent.futures as cf
+    from oracle import oracle as O
+    mode = cfg["mode"]
+    x, p0, p1, xe, m = O.synth(mode, n_sample)
+    h = O.hyper(tau=cfg["tau"], **HYPER)
+    bounds = [n_sample * i // threads for i in range(threads + 1)]
+
+    def part(i):
+        lo, hi = bounds[i], bounds[i + 1]
+        O.outer_step(mode, x[lo:hi], p0[lo:hi], p1[lo:hi], xe[lo:hi], m[lo:hi], h)
+
+    ts = []
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(part, range(threads)))
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            list(ex.map(part, range(threads)))
+            ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"value": n_sample / t, "unit": "params/s", "cores": threads,
+            "kind": "fused same-order C loop, storage dtypes of the config (not the reference)",
+            "sample": f"{n_sample} coordinates"}
+
+
 def run_reference_arm(args, cfg, rank: int):
     if rank != 0:
         return 0
@@ -221,6 +283,9 @@ def run_reference_arm(args, cfg, rank: int):
                 "d2h_bytes_per_step": 0},
         "note": "Reference (C++20/Eigen) is not buildable here (Eigen absent); this arm times "
                 "oracle/co2_oracle.c, a bit-exact restatement pinned by the reference's fixtures.",
+        "cpu_aar": time_cpu_average(min(n_sample, 1 << 24)),
+        "cpu_fused_bound": time_cpu_fused_bound(cfg, n_sample, cores),
+        "host": host_info(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -384,6 +449,8 @@ def main():
         comm = {"exposed_pct": 100.0 * stall / waited if waited > 0 else 0.0,
                 "stall_ms_per_step": 1e3 * stall / max(len(waits), 1),
                 "allreduce_ms": 1e3 * waited / max(len(waits), 1),
+                "stall_share_of_step_pct": 100.0 * stall / max(len(waits), 1) /
+                (elapsed / args.steps) if elapsed > 0 else None,
                 "allreduce_bytes": n * (2 if mode == 2 else 4 if mode == 1 else 8),
                 "note": "no inner-loop compute in this step: the reduce overlaps only the "
                         "outer step itself (tau*t_comp = 0 worst case); see "
@@ -427,7 +494,7 @@ def main():
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:
         v, t = time_cpu_step(cfg, args.cpu_sample, 1, 3, 1)
-        cpu = {"value": v, "unit": "params/s", "cores": 1, "kind": "port",
+        cpu = {"value": v, "unit": "params/s", "cores": 1, "kind": "port", "host": host_info(),
                "sample": f"{args.cpu_sample} coordinates of the same synthetic inputs (fp64 "
                          "upcast), reference unfused passes + fresh temporaries, 1 thread, "
                          f"{t:.2f} s per step"}

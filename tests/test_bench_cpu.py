@@ -31,6 +31,11 @@ def test_reference_arm_line():
     assert d["e2e"] == {"value": d["value"], "unit": "params/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("C3")
+    # the CPU AAR timed separately, a labelled best-case CPU
+    # bound, and the host the numbers came from
+    assert d["cpu_aar"]["value"] > 0 and d["cpu_aar"]["cores"] == 1
+    assert d["cpu_fused_bound"]["value"] > 0 and "not the reference" in d["cpu_fused_bound"]["kind"]
+    assert d["host"]["nproc"] >= 1
 
 
 def test_reference_arm_non_zero_rank_is_silent():
