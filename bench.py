@@ -219,7 +219,6 @@ def time_cpu_average(n_sample: int, workers: int = 4, reps: int = 3) -> dict:
     """The reference's CPU all-reduce arithmetic, average()
     (proj/src/param_ops.cpp:16-33), fp64 and single-threaded as the
     reference runs it, over `workers` contributions of n_sample."""
-    import numpy as np
     from oracle import oracle as O
     cs = [O.to_f64(O.synth(2, n_sample, worker=w)[3]) for w in range(workers)]
     O.average(cs)
@@ -229,7 +228,6 @@ def time_cpu_average(n_sample: int, workers: int = 4, reps: int = 3) -> dict:
         O.average(cs)
         ts.append(time.perf_counter() - t0)
     t = statistics.median(ts)
-    del cs, np
     return {"value": n_sample / t, "unit": "params/s", "workers": workers, "cores": 1,
             "sample": f"{n_sample} coordinates x {workers} fp64 contributions"}
 
