@@ -38,7 +38,6 @@ __device__ __forceinline__ float ld_c(const bf16raw* p) {
   return __uint_as_float(((uint32_t)p->b) << 16);
 }
 
-constexpr int kP2PThreads = 512;
 
 struct P2PArgs {
   void* bufs[kMaxRanks];      // rank-indexed pointers to the same logical buffer
@@ -186,8 +185,8 @@ struct SliceArgs {
   Signals* sig[kMaxRanks];
 };
 
-template <typename TL, typename TC, int V, int R, int U>
-__global__ void __launch_bounds__(kP2PThreads) p2p_slice_average_kernel(const SliceArgs a) {
+template <typename TL, typename TC, int V, int R, int U, int NT>
+__global__ void __launch_bounds__(NT) p2p_slice_average_kernel(const SliceArgs a) {
   Signals* mine = a.sig[a.rank];
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
@@ -201,7 +200,7 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_slice_average_kernel(const Sl
   if (!s_ok) return;
   const TC g = (TC)a.world;
   const int64_t nvec = a.len / V;
-  const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
+  const int64_t stride = (int64_t)gridDim.x * NT;
   auto to_c = [](const TL* v, int k) -> TC {
     if constexpr (sizeof(TL) == 2)
       return ld_c(reinterpret_cast<const bf16raw*>(v + k));
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_slice_average_kernel(const Sl
     }
   };
   for (int b = 0; b < a.nb; ++b) {
-    int64_t i = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x;
+    int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
     for (; i < nvec; i += (int64_t)U * stride) {
       uint4 raw[U][R];
 #pragma unroll
@@ -249,7 +248,7 @@ __global__ void __launch_bounds__(kP2PThreads) p2p_slice_average_kernel(const Sl
       }
     }
     if (blockIdx.x == 0) {  // scalar tail
-      for (int64_t j = nvec * V + threadIdx.x; j < a.len; j += kP2PThreads) {
+      for (int64_t j = nvec * V + threadIdx.x; j < a.len; j += NT) {
         TC acc = to_c(static_cast<const TL*>(a.src[b][0]) + a.lo + j, 0);
         for (int p = 1; p < a.world; ++p)
           acc = acc + to_c(static_cast<const TL*>(a.src[b][p]) + a.lo + j, 0);
@@ -288,6 +287,17 @@ int p2p_threads() {
   return v;
 }
 
+// Threads per CTA of the sharded slice reduce (CO2_P2P_SLICE_THREADS = 256
+// | 512, default 512).  At equal total threads 256 and 512 measure the same
+// (profiles/r01/bench/c4_slice_threads.txt); the slice reduce is NVLink-bound.
+int p2p_slice_threads() {
+  static const int v = [] {
+    const char* e = getenv("CO2_P2P_SLICE_THREADS");
+    return (e && atoi(e) == 256) ? 256 : 512;
+  }();
+  return v;
+}
+
 }  // namespace
 
 co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const* src0,
@@ -318,19 +328,27 @@ co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const*
   if (ctas < 1) ctas = (world <= 2 ? 1 : 4) * sm_count();
   if (ctas > 8 * sm_count()) ctas = 8 * sm_count();
   const int cap = rank_cap(world);
-#define CO2_SLICE_LAUNCH(TL, TC, V)                                                       \
-  if (cap == 2)                                                                          \
-    p2p_slice_average_kernel<TL, TC, V, 2, 4><<<ctas, kP2PThreads, 0, s>>>(a);           \
-  else if (cap == 4)                                                                     \
-    p2p_slice_average_kernel<TL, TC, V, 4, 2><<<ctas, kP2PThreads, 0, s>>>(a);           \
+  const int nt = p2p_slice_threads();
+#define CO2_SLICE_NT(TL, TC, V, R, U)                                                     \
+  if (nt == 256)                                                                         \
+    p2p_slice_average_kernel<TL, TC, V, R, U, 256><<<ctas, 256, 0, s>>>(a);              \
   else                                                                                   \
-    p2p_slice_average_kernel<TL, TC, V, 8, 1><<<ctas, kP2PThreads, 0, s>>>(a);
+    p2p_slice_average_kernel<TL, TC, V, R, U, 512><<<ctas, 512, 0, s>>>(a);
+#define CO2_SLICE_LAUNCH(TL, TC, V)                                                       \
+  if (cap == 2) {                                                                        \
+    CO2_SLICE_NT(TL, TC, V, 2, 4)                                                         \
+  } else if (cap == 4) {                                                                 \
+    CO2_SLICE_NT(TL, TC, V, 4, 2)                                                         \
+  } else {                                                                               \
+    CO2_SLICE_NT(TL, TC, V, 8, 1)                                                         \
+  }
   switch (dt) {
     case CO2_DTYPE_F64: CO2_SLICE_LAUNCH(double, double, 2) break;
     case CO2_DTYPE_F32: CO2_SLICE_LAUNCH(float, float, 4) break;
     default: CO2_SLICE_LAUNCH(bf16raw, float, 8) break;
   }
 #undef CO2_SLICE_LAUNCH
+#undef CO2_SLICE_NT
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }
