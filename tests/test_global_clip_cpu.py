@@ -69,3 +69,13 @@ def test_chunking_is_grid_independent_and_bounded():
             c = O.gc_chunk(n, v)
             assert c % (v * 256) == 0 and c >= v * 256 * 16
             assert (n + c - 1) // c <= 32768
+
+
+def test_product_chunk_formula_matches_oracle():
+    """The library's summation chunk (pure host arithmetic, no GPU call)
+    equals the oracle restatement's, so both sum in the same order."""
+    from paper_2401_16265_b200 import _lib as L
+    lib = L.lib()
+    for mode, v in ((0, 2), (1, 4), (2, 8)):
+        for n in (0, 1, 7, 8191, 100003, 3_000_001, 1_300_000_000, 7_000_000_000):
+            assert lib.co2_global_clip_chunk(mode, n) == O.gc_chunk(n, v)
