@@ -311,6 +311,10 @@ def main():
                     help="collective transport at N > 1; auto = the measured faster one, "
                          "the fixed-order P2P kernels (worker-local and sharded C4)")
     ap.add_argument("--nparams", type=int, default=0, help="override the config's parameter count")
+    ap.add_argument("--clip", default="coordinate", choices=["coordinate", "global"],
+                    help="coordinate = the reference's clip (every headline number); global = "
+                         "the global-norm clip EXTENSION (two passes, outside the parity "
+                         "contract; worker-local split schedule only)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.nparams > 0:
@@ -334,6 +338,13 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mode, n, tau, bpp = cfg["mode"], cfg["n"], cfg["tau"], cfg["bytes_per_param"]
+    gclip = args.clip == "global"
+    if gclip:
+        if cfg.get("sharded") or args.schedule == "fused":
+            raise SystemExit("--clip global: worker-local configs, split schedule only")
+        # pass 1 reads x_t0, p0, p1, xbar, m and writes m'; pass 2 reads m', x_t0
+        # and writes anchor, params
+        bpp = {0: 80, 1: 40, 2: 34}[mode]
     hyper = co2.Co2Hyper(**HYPER)
     stream = torch.cuda.current_stream()
 
@@ -390,6 +401,8 @@ def main():
         init = co2.synth_params(mode, n, worker=rank)  # x_{0,tau}: the params the reduce sums
         w = co2.Worker(mode, n, init, keep_gap=False)
         del init
+        if gclip:
+            w.set_clip_mode("global")
         if transport == "p2p":
             eng.register_worker(w)
             if args.schedule == "fused":
@@ -484,7 +497,7 @@ def main():
 
     # --- e2e through the host-buffer entry (pinned H2D + kernel + D2H timed)
     e2e = None
-    if not args.no_e2e and not sharded:
+    if not args.no_e2e and not sharded and not gclip:  # the host entry is the reference clip
         e2e = run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist)
         e2e["numa_bound_cores"] = numa_cores  # None: not bound (CO2_BENCH_NUMA=0 / no NVML)
 
@@ -516,6 +529,8 @@ def main():
                         + ("fixed-order NVLink P2P all-reduce)" if transport == "p2p"
                            else "NCCL all-reduce)")),
                        "transport": transport, "transport_note": transport_note,
+                       "clip": args.clip + (" (extension, outside the parity contract)"
+                                            if gclip else " (reference)"),
                        "schedule": (args.schedule if transport == "p2p" and not sharded
                                     else "split"),
                        "l2": "inputs larger than L2 (no flush needed)",
@@ -528,12 +543,16 @@ def main():
                        if sharded else "co2_round: AAR launch + stale wait + fused outer step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
-                         "traffic": ncu_traffic(cfg), "traffic_unit": "bytes per launch",
-                         "traffic_source": NCU_CAPTURE if ncu_traffic(cfg) else None,
+                         "traffic": None if gclip else ncu_traffic(cfg),
+                         "traffic_unit": "bytes per launch",
+                         "traffic_source": NCU_CAPTURE if ncu_traffic(cfg) and not gclip else None,
                          "algorithmic_bytes": bpp * per_rank, "peak_kind": peak_kind,
-                         "kernel": ("fused_step_kernel<ModeBF16%s>" % (", GHOST" if sharded
-                                                                        else ""))
-                         if mode == 2 else "fused_step_kernel", "kernel_ms": k_max * 1e3,
+                         "kernel": ("gclip_pass1 + gclip_pass2 (global-norm clip extension)"
+                                    if gclip else
+                                    ("fused_step_kernel<ModeBF16%s>" % (", GHOST" if sharded
+                                                                         else ""))
+                                    if mode == 2 else "fused_step_kernel"),
+                         "kernel_ms": k_max * 1e3,
                          "bytes_per_param": bpp},
             "link": link, "step_hbm": step_hbm,
             "e2e": e2e, "cpu_baseline": cpu, "comm": comm,

@@ -135,6 +135,10 @@ co2_status_t co2_outer_step_global_clip(co2_mode_t mode, int64_t n, const void* 
                                         const void* xbar, int32_t xbar_divisor, void* momentum,
                                         void* anchor_out, void* params_out, void* gap_out,
                                         const co2_hyper_t* hyper, void* workspace, void* stream);
+/* Clip mode of a worker's co2_round step: CO2_CLIP_COORDINATE is the
+ * reference (default); CO2_CLIP_GLOBAL_NORM runs co2_outer_step_global_clip
+ * instead (the extension above; not with the fused P2P schedule). */
+enum { CO2_CLIP_COORDINATE = 0, CO2_CLIP_GLOBAL_NORM = 1 };
 /* ||m'||_2 of the last co2_outer_step_global_clip on this workspace
  * (synchronizes `stream`). */
 co2_status_t co2_global_clip_norm_fetch(const void* workspace, double* norm_out, void* stream);
@@ -373,6 +377,7 @@ co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, int64_t n,
                                const void* init_params, int32_t keep_gap, void* stream);
 co2_status_t co2_worker_destroy(co2_worker_t* w);
 void* co2_worker_buffer(co2_worker_t* w, int32_t which);
+co2_status_t co2_worker_set_clip_mode(co2_worker_t* worker, int32_t clip_mode);
 int32_t co2_worker_round(const co2_worker_t* w);
 /* Snapshot hooks: x_{t,0} <- params (call before the first inner step;
  * a no-op for t >= 1 where the outer step already wrote the anchor), and

@@ -18,6 +18,7 @@ DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
 FLAG_GAP_NONFINITE, FLAG_GAP_BELOW_ONE, FLAG_M_NONFINITE = 1, 2, 4
 FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
 FLAG_SLOWMO_M, FLAG_SLOWMO_X, FLAG_OVERLAP, FLAG_NORM_NONFINITE = 64, 128, 256, 512
+CLIP_COORDINATE, CLIP_GLOBAL_NORM = 0, 1
 BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
 BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT, BUF_XFIRST_ALT = 5, 6, 7, 8, 9
 IPC_HANDLE_BYTES = 72  # CUDA IPC handle (64) + int64 offset
@@ -135,6 +136,7 @@ SIGNATURES = {
     "co2_worker_create": (ST, [C.POINTER(P), I32, I64, P, I32, P]),
     "co2_worker_destroy": (ST, [P]),
     "co2_worker_buffer": (P, [P, I32]),
+    "co2_worker_set_clip_mode": (ST, [P, I32]),
     "co2_worker_round": (I32, [P]),
     "co2_worker_snapshot_start": (ST, [P, P]),
     "co2_worker_snapshot_first": (ST, [P, P]),

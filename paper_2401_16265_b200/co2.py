@@ -555,6 +555,14 @@ class Worker:
     def t(self) -> int:
         return lib().co2_worker_round(self.handle)
 
+    def set_clip_mode(self, mode: str) -> None:
+        """'coordinate' (the reference, default) or 'global' (the global-norm
+        clip extension, outside the parity contract)."""
+        m = {"coordinate": L.CLIP_COORDINATE, "global": L.CLIP_GLOBAL_NORM}.get(mode)
+        if m is None:
+            raise ValidationError(f"worker: unknown clip mode {mode!r}")
+        check(lib().co2_worker_set_clip_mode(self.handle, m))
+
     def enable_timing(self, cap: int = 4096):
         check(lib().co2_worker_enable_timing(self.handle, cap))
 

@@ -676,6 +676,7 @@ struct co2_worker {
   // optional device timing of the fused launch (ring of event pairs)
   std::vector<cudaEvent_t> tev;  // 2 * cap
   int64_t tev_recorded = 0, tev_read = 0;
+  int clip_mode = CO2_CLIP_COORDINATE;  // CO2_CLIP_GLOBAL_NORM: the extension
 };
 
 static co2_status_t step_launch(co2_worker* w, co2_mode_t mode, int64_t n, const void* x_t0,
@@ -685,8 +686,12 @@ static co2_status_t step_launch(co2_worker* w, co2_mode_t mode, int64_t n, const
   const int64_t cap = (int64_t)w->tev.size() / 2;
   const int64_t slot = cap ? w->tev_recorded % cap : 0;
   if (cap) CO2_CUDA(cudaEventRecord(w->tev[2 * slot], st));
-  CO2_TRY(outer_step_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params, gap, h, w->ws,
-                          st));
+  if (w->clip_mode == CO2_CLIP_GLOBAL_NORM)
+    CO2_TRY(outer_step_global_clip_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params,
+                                        gap, h, w->ws, st));
+  else
+    CO2_TRY(outer_step_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params, gap, h,
+                            w->ws, st));
   if (cap) {
     CO2_CUDA(cudaEventRecord(w->tev[2 * slot + 1], st));
     w->tev_recorded += 1;
@@ -803,6 +808,14 @@ extern "C" void* co2_worker_buffer(co2_worker_t* w, int32_t which) {
   return nullptr;
 }
 
+extern "C" co2_status_t co2_worker_set_clip_mode(co2_worker_t* w, int32_t mode) {
+  if (!w) return fail(CO2_ERR_VALIDATION, "worker: null handle");
+  if (mode != CO2_CLIP_COORDINATE && mode != CO2_CLIP_GLOBAL_NORM)
+    return fail(CO2_ERR_VALIDATION, "worker: unknown clip mode %d", (int)mode);
+  w->clip_mode = mode;
+  return CO2_OK;
+}
+
 extern "C" int32_t co2_worker_round(const co2_worker_t* w) { return w ? w->t : -1; }
 
 extern "C" co2_status_t co2_worker_snapshot_start(co2_worker_t* w, void* stream) {
@@ -913,6 +926,9 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     // compute and the collective share the HBM stream instead of competing
     // as two kernels on two streams.
     co2_worker* w = w0;
+    if (w->clip_mode != CO2_CLIP_COORDINATE)
+      return fail(CO2_ERR_VALIDATION,
+                  "global-norm clip: not available with the fused all-reduce schedule");
     if (w->has_pending) {  // the round-0 reduce (standalone P2P kernel)
       int32_t done = 0;
       CO2_TRY(co2_aar_poll(e, w->pending, &done));

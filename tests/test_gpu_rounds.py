@@ -435,3 +435,44 @@ def test_baseline_steps_bitwise(mode):
         co2.check(co2.lib().co2_slowmo_step(mode, n, x.data_ptr(), xe.data_ptr(), 1,
                                             m.data_ptr(), params.data_ptr(), None, 0.8, 1.0,
                                             ws.ptr, st))
+
+
+@pytest.mark.parametrize("mode", [co2.MODE_F32, co2.MODE_BF16_MIXED])
+def test_rounds_global_clip_mode(mode):
+    """Worker clip mode 'global' (the global-norm clip extension): every
+    round's step equals co2_outer_step_global_clip replayed on the worker's
+    pre-round state and the consumed average, bitwise; m' is the same as in
+    the reference coordinate mode."""
+    n, G, tau = 300_007, 2, 3
+    hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    eng = co2.CollectiveEngine(G, transport="local")
+    ws = [co2.Worker(mode, n, co2.synth(mode, n, worker=i)[3]) for i in range(G)]
+    for w in ws:
+        w.set_clip_mode("global")
+    with pytest.raises(co2.ValidationError, match="unknown clip mode"):
+        ws[0].set_clip_mode("spectral")
+    for t in range(4):
+        pre = []
+        for i, w in enumerate(ws):
+            w.snapshot_start()
+            for k in range(tau):
+                co2.synthetic_inner_step(w.params, lr=1e-3, scale=1.0, worker=i,
+                                         step=t * tau + k)
+                if k == 0:
+                    w.snapshot_first()
+            pre.append([w.buffer(b).clone() for b in (L.BUF_ANCHOR, L.BUF_PREV_X0,
+                                                       L.BUF_PREV_X1, L.BUF_MOMENTUM)])
+        co2.co2_round(ws, eng, hyper, tau)
+        if t == 0:
+            continue
+        xbar = ws[0].buffer(L.BUF_XBAR).clone()  # the consumed average
+        for i, w in enumerate(ws):
+            x0, p0, p1, m = pre[i]
+            anchor = torch.empty_like(x0)
+            params = torch.empty_like(p1)
+            d, norm = co2.outer_step_global_clip(mode, x0, p0, p1, xbar, m, hyper, tau,
+                                                 anchor_out=anchor, params_out=params)
+            assert norm > 5e-3 and d.n_clipped == n  # the clip is active
+            assert to_np(w.buffer(L.BUF_MOMENTUM)).tobytes() == to_np(m).tobytes(), (t, i)
+            assert to_np(w.buffer(L.BUF_ANCHOR)).tobytes() == to_np(anchor).tobytes(), (t, i)
+            assert to_np(w.params).tobytes() == to_np(params).tobytes(), (t, i)
