@@ -247,4 +247,19 @@ inline co2_diag_t finish_step(void* workspace, cudaStream_t stream) {
   return d;
 }
 
+// EXTENSION, not a reference API: the same step with a global-norm clip of
+// m' (co2_outer_step_global_clip).  Returns ||m'||_2 after synchronizing;
+// finish_step() then reports the diagnostics.
+inline double outer_step_global_clip(co2_mode_t mode, int64_t n, const OuterStepBuffers& b,
+                                     int xbar_divisor, const Co2Hyper& hyper, int tau,
+                                     void* workspace, cudaStream_t stream) {
+  co2_hyper_t h = hyper.c(tau);
+  check(co2_outer_step_global_clip(mode, n, b.x_t0, b.prev_x0, b.prev_x1, b.xbar, xbar_divisor,
+                                   b.momentum, b.anchor_out, b.params_out, b.gap_out, &h,
+                                   workspace, stream));
+  double norm = 0.0;
+  check(co2_global_clip_norm_fetch(workspace, &norm, stream));
+  return norm;
+}
+
 }  // namespace co2b200

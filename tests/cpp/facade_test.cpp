@@ -123,6 +123,34 @@ int main() {
     CHECK(throws<validation_error>([&] { overlap_ratio(0, 0.1, 1.0); }));
     std::printf("ok overlap_ratio\n");
   }
+  {  // fused step and the global-norm clip extension (fp64, 3 coordinates)
+    Context& ctx = Context::get();
+    Co2Hyper h;
+    h.phi = 0.1;
+    auto x = vec({1.0, 2.0, 3.0}), p0 = vec({0.5, 2.5, 2.0}), p1 = vec({0.6, 2.4, 2.2});
+    auto xb = vec({0.2, 2.9, 1.5});
+    auto m1 = vec({0.0, 0.0, 0.0}), m2 = vec({0.0, 0.0, 0.0});
+    DeviceVector a1(3, CO2_DTYPE_F64), a2(3, CO2_DTYPE_F64);
+    OuterStepBuffers b{x.data(), p0.data(), p1.data(), xb.data(), m1.data(), a1.data(),
+                       nullptr, nullptr};
+    outer_step(CO2_MODE_F64, 3, b, 1, h, 1, ctx.ws, ctx.stream);
+    finish_step(ctx.ws, ctx.stream);
+    b.momentum = m2.data();
+    b.anchor_out = a2.data();
+    const double norm = outer_step_global_clip(CO2_MODE_F64, 3, b, 1, h, 1, ctx.ws, ctx.stream);
+    co2_diag_t d = finish_step(ctx.ws, ctx.stream);
+    auto mv = m2.to_host(), xg = a2.to_host(), xc = a1.to_host();
+    CHECK(mv == m1.to_host());  // m' does not depend on the clip
+    const double nn = std::sqrt(mv[0] * mv[0] + mv[1] * mv[1] + mv[2] * mv[2]);
+    CHECK(std::fabs(norm - nn) <= 1e-15 * nn);
+    CHECK(norm > 0.1 && d.n_clipped == 3);
+    for (int j = 0; j < 3; ++j) {
+      const double xs[3] = {1.0, 2.0, 3.0};
+      CHECK(xg[j] == xs[j] - 1.0 * (mv[j] * (0.1 / norm)));
+      CHECK(xc[j] == xs[j] - std::fmin(std::fmax(mv[j], -0.1), 0.1));
+    }
+    std::printf("ok outer_step / outer_step_global_clip\n");
+  }
   std::printf(g_fail ? "FACADE FAILED %d\n" : "FACADE OK\n", g_fail);
   return g_fail ? 1 : 0;
 }
