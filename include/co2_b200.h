@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CO2_ABI_VERSION 1
+#define CO2_ABI_VERSION 2  /* 2: 72-byte IPC export records (handle + offset) */
 
 typedef int32_t co2_status_t;
 enum {

@@ -195,7 +195,7 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.co2_abi_version() != 1:
+        if L.co2_abi_version() != 2:
             raise ImportError("libco2b200.so ABI version mismatch")
         _lib = L
     return _lib

@@ -15,6 +15,7 @@
 #include <math.h>
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -209,6 +210,14 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
   if (s == CO2_OK) {
     cudaError_t ce = cudaMalloc(&e->signals, p2p_signal_bytes());
     if (ce == cudaSuccess) ce = cudaMemset(e->signals, 0, p2p_signal_bytes());
+    if (ce == cudaSuccess) {
+      // barrier spin budget (Signals::timeout_ms): CO2_P2P_TIMEOUT_MS, else 10 s
+      const char* env = getenv("CO2_P2P_TIMEOUT_MS");
+      const long v = env ? atol(env) : 10000;
+      const uint32_t ms = (uint32_t)(v < 1 ? 1 : (v > 3600000 ? 3600000 : v));
+      ce = cudaMemcpy(static_cast<char*>(e->signals) + p2p_signal_timeout_offset(), &ms,
+                      sizeof ms, cudaMemcpyHostToDevice);
+    }
     if (ce != cudaSuccess) s = cuda_fail(ce, "cudaMalloc(signals)");
   }
   if (s != CO2_OK) {
@@ -458,7 +467,7 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
       CO2_TRY(p2p_average_launch(dt, pb->ptrs.data(), e->peer_signals.data(), e->world, e->rank,
                                  n, e->p2p_epoch, e->ctas, e->comm_stream));
       // the kernel records a timed-out barrier in the signal area's error word
-      CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + 36, 4,
+      CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
                                cudaMemcpyDeviceToHost, e->comm_stream));
     }
   } else if (e->transport == T_NCCL) {
@@ -506,7 +515,7 @@ static co2_status_t launch_slice(co2_aar* e, co2_dtype_t dt, const void* src0, c
   CO2_TRY(p2p_slice_average_launch(dt, 2, b0->ptrs.data(), b1->ptrs.data(), dst0, dst1,
                                    e->peer_signals.data(), e->world, e->rank, lo, len,
                                    e->p2p_epoch, e->slice_ctas, e->comm_stream));
-  CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + 36, 4,
+  CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
                            cudaMemcpyDeviceToHost, e->comm_stream));
   CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
   e->handles.push_back(h);
@@ -965,7 +974,7 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
       if (res) *res = r;
       if (s != CO2_OK) return s;
       uint32_t err = 0;
-      CO2_CUDA(cudaMemcpy(&err, static_cast<char*>(e->signals) + 36, 4, cudaMemcpyDeviceToHost));
+      CO2_CUDA(cudaMemcpy(&err, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4, cudaMemcpyDeviceToHost));
       if (err)
         return fail(CO2_ERR_CUDA, "p2p fused step: cross-GPU barrier timed out (code %u)", err);
       return CO2_OK;

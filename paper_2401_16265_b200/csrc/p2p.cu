@@ -18,9 +18,11 @@
 //            area (release, system scope) and waits for all ready[p] >= epoch;
 //   exit   : every CTA adds 1 to done in each peer's area after its stores
 //            (release) and waits until its own done reaches epoch*G*grid.
-// All spins are bounded (~4 s): on timeout the kernel records a flag and
+// All spins are bounded in wall-clock time (Signals::timeout_ms, 10 s by
+// default): on timeout the kernel records a flag and
 // exits instead of hanging the GPU.
 #include <cuda_bf16.h>
+#include <stddef.h>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -56,7 +58,7 @@ __global__ void __launch_bounds__(NT) p2p_average_kernel(const P2PArgs a) {
   if (threadIdx.x == 0) {
     for (int p = 0; p < a.world; ++p) st_release_sys(&a.sig[p]->ready[a.rank], a.epoch);
     bool ok = true;
-    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch);
+    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch, mine);
     if (!ok) mine->error = 1;
     s_ok = ok;
   }
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(NT) p2p_average_kernel(const P2PArgs a) {
     __threadfence_system();
     for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
     const uint32_t target = a.epoch * (uint32_t)a.world * gridDim.x;
-    if (!spin_until(&mine->done, target)) mine->error = 2;
+    if (!spin_until(&mine->done, target, mine)) mine->error = 2;
   }
 }
 
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(NT) p2p_slice_average_kernel(const SliceArgs a
   if (threadIdx.x == 0) {
     for (int p = 0; p < a.world; ++p) st_release_sys(&a.sig[p]->ready[a.rank], a.epoch);
     bool ok = true;
-    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch);
+    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch, mine);
     if (!ok) mine->error = 1;
     s_ok = ok;
   }
@@ -403,5 +405,7 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
 }
 
 size_t p2p_signal_bytes() { return sizeof(Signals); }
+size_t p2p_signal_timeout_offset() { return offsetof(Signals, timeout_ms); }
+size_t p2p_signal_error_offset() { return offsetof(Signals, error); }
 
 }  // namespace co2

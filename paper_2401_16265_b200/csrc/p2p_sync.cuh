@@ -15,6 +15,8 @@ constexpr int kMaxRanks = 8;
 //   error     1/2/3/4/5: a bounded spin timed out
 //   done2     counts ranks that finished the fused sharded step's stores
 //   ready2[r] / done3: entry / exit of the fused all-reduce + outer step
+//   timeout_ms  the spin budget of this rank's barriers (0 = 10 s); set by
+//               the host from CO2_P2P_TIMEOUT_MS when the engine is created
 struct Signals {
   uint32_t ready[kMaxRanks];
   uint32_t done;
@@ -22,7 +24,8 @@ struct Signals {
   uint32_t done2;
   uint32_t ready2[kMaxRanks];
   uint32_t done3;
-  uint32_t pad[44];
+  uint32_t timeout_ms;
+  uint32_t pad[43];
 };
 static_assert(sizeof(Signals) == 256, "signal area layout");
 
@@ -38,13 +41,20 @@ __device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// ~2 s at 1.9 GHz.
-constexpr long long kSpinBudget = 4000000000LL;
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
-__device__ inline bool spin_until(const uint32_t* p, uint32_t target) {
-  long long t0 = clock64();
+// Wall-clock bounded (globaltimer, independent of the SM clock): the
+// budget is the owning rank's timeout_ms (default 10 s).
+__device__ inline bool spin_until(const uint32_t* p, uint32_t target, const Signals* mine) {
+  const uint32_t ms = *reinterpret_cast<const volatile uint32_t*>(&mine->timeout_ms);
+  const uint64_t budget = (uint64_t)(ms ? ms : 10000u) * 1000000ull;
+  const uint64_t t0 = global_ns();
   while (ld_acquire_sys(p) < target) {
-    if (clock64() - t0 > kSpinBudget) return false;
+    if (global_ns() - t0 > budget) return false;
     __nanosleep(64);
   }
   return true;
@@ -65,7 +75,8 @@ __device__ inline void p2p_exit_barrier(const P2PExit& x) {
   for (int p = 0; p < x.world; ++p)
     red_release_sys_add(x.counter ? &x.sig[p]->done3 : &x.sig[p]->done2, 1u);
   const uint32_t* mine = x.counter ? &x.sig[x.rank]->done3 : &x.sig[x.rank]->done2;
-  if (!spin_until(mine, x.epoch * (uint32_t)x.world)) x.sig[x.rank]->error = x.counter ? 5 : 3;
+  if (!spin_until(mine, x.epoch * (uint32_t)x.world, x.sig[x.rank]))
+    x.sig[x.rank]->error = x.counter ? 5 : 3;
 }
 
 // Entry barrier of the fused all-reduce + outer step: every CTA publishes
@@ -73,7 +84,7 @@ __device__ inline void p2p_exit_barrier(const P2PExit& x) {
 __device__ inline bool p2p_entry_barrier(const P2PExit& x) {
   for (int p = 0; p < x.world; ++p) st_release_sys(&x.sig[p]->ready2[x.rank], x.epoch);
   for (int p = 0; p < x.world; ++p)
-    if (!spin_until(&x.sig[x.rank]->ready2[p], x.epoch)) {
+    if (!spin_until(&x.sig[x.rank]->ready2[p], x.epoch, x.sig[x.rank])) {
       x.sig[x.rank]->error = 4;
       return false;
     }

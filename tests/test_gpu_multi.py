@@ -99,3 +99,18 @@ def test_p2p_register_deregister_cycles():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     assert json.loads(line)["ok"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_p2p_missing_peer_times_out():
+    """A peer that never joins the reduce: the barrier gives up after
+    CO2_P2P_TIMEOUT_MS, the error is reported, and the GPU stays usable."""
+    env = dict(os.environ, CO2_P2P_TIMEOUT_MS="300")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_p2p_timeout.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert res["error"] and "timed out" in res["error"], res
+    assert res["healthy"] and res["seconds"] < 5.0, res
