@@ -900,6 +900,11 @@ template <int OP>
 co2_status_t launch_op(co2_dtype_t dt, const OpArgs& a, cudaStream_t s) {
   CO2_TRY(check_dtype(dt));
   if (!a.ws) return fail(CO2_ERR_VALIDATION, "null workspace");
+  // operands each op reads: GAP (x_t0, prev_x0, prev_x1), MOMENTUM (m, gap,
+  // delta), ITERATE (x_t0, m), CLIP (v)
+  const bool need_b = OP != OP_CLIP, need_c = OP == OP_GAP || OP == OP_MOMENTUM;
+  if (a.n > 0 && (!a.a || !a.out || (need_b && !a.b) || (need_c && !a.c)))
+    return fail(CO2_ERR_VALIDATION, "null buffer");
   int grid = simple_grid(a.n, kThreads);
   if (grid > kMaxBlocks) grid = kMaxBlocks;
   if (dt == CO2_DTYPE_F64)
@@ -1385,6 +1390,9 @@ extern "C" co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const
 extern "C" co2_status_t co2_sub(co2_dtype_t dt, int64_t n, const void* a, const void* b, void* out,
                                 void* stream) {
   CO2_TRY(check_dtype(dt));
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "sub: negative length");
+  if (n == 0) return CO2_OK;
+  if (!a || !b || !out) return fail(CO2_ERR_VALIDATION, "null buffer");
   int grid = simple_grid(n, kThreads);
   cudaStream_t s = S(stream);
   if (dt == CO2_DTYPE_F64)
@@ -1419,7 +1427,9 @@ extern "C" co2_status_t co2_convert(co2_dtype_t ddt, void* dst, co2_dtype_t sdt,
                                     int64_t n, void* stream) {
   CO2_TRY(check_dtype(ddt));
   CO2_TRY(check_dtype(sdt));
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "convert: negative length");
   if (n == 0) return CO2_OK;
+  if (!dst || !src) return fail(CO2_ERR_VALIDATION, "null buffer");
   if (ddt == sdt) {
     size_t es = ddt == CO2_DTYPE_F64 ? 8 : (ddt == CO2_DTYPE_F32 ? 4 : 2);
     CO2_CUDA(cudaMemcpyAsync(dst, src, es * (size_t)n, cudaMemcpyDeviceToDevice, S(stream)));

@@ -67,6 +67,32 @@ def test_outer_step_validates_before_launch():
     assert L.lib().co2_last_error().decode() == "staleness_gap: tau must be >= 1"
 
 
+def test_null_buffers_are_rejected_before_launch():
+    """Null device buffers with n > 0 are a validation error at the ABI, not
+    an illegal address on the GPU (checked before any device work)."""
+    import ctypes as C
+    lib = L.lib()
+    fake = C.c_void_p(0x1000)  # never dereferenced: validation fails first
+    h = co2.Co2Hyper().c(4)
+    cases = [
+        lambda: lib.co2_outer_step(L.MODE_F32, 8, None, fake, fake, fake, 1, fake, None, None,
+                                   None, C.byref(h), fake, None),
+        lambda: lib.co2_outer_step_global_clip(L.MODE_F32, 8, fake, fake, None, fake, 1, fake,
+                                               None, None, None, C.byref(h), fake, None),
+        lambda: lib.co2_staleness_gap(L.DTYPE_F64, 8, fake, None, fake, 4, 1e-12, fake, fake,
+                                      None),
+        lambda: lib.co2_penalized_momentum(L.DTYPE_F64, 8, fake, 0.5, fake, None, 1, fake, fake,
+                                           None),
+        lambda: lib.co2_outer_iterate(L.DTYPE_F64, 8, fake, 1.0, None, 1.0, 1, fake, fake, None),
+        lambda: lib.co2_clip_elementwise(L.DTYPE_F64, 8, None, 1.0, fake, fake, None),
+        lambda: lib.co2_sub(L.DTYPE_F64, 8, fake, None, fake, None),
+        lambda: lib.co2_convert(L.DTYPE_F32, None, L.DTYPE_F64, fake, 8, None),
+    ]
+    for f in cases:
+        assert f() == L.ERR_VALIDATION
+        assert "null" in lib.co2_last_error().decode()
+
+
 def test_allreduce_time_ring_formula(golden):
     """proj/tests/test_timing_model.cpp:23-47"""
     k = golden["allreduce_time"]
