@@ -1367,6 +1367,12 @@ extern "C" co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const
   if (g > 64) return fail(CO2_ERR_VALIDATION, "average: at most 64 contributions");
   CO2_TRY(check_dtype(dt));
   if (!ws) return fail(CO2_ERR_VALIDATION, "null workspace");
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "average: contribution dimensions differ");
+  if (n > 0) {
+    if (!contributions || !out) return fail(CO2_ERR_VALIDATION, "null buffer");
+    for (int i = 0; i < g; ++i)
+      if (!contributions[i]) return fail(CO2_ERR_VALIDATION, "null buffer");
+  }
   int grid = simple_grid(n, kThreads);
   if (grid > kMaxBlocks) grid = kMaxBlocks;
   cudaStream_t s = S(stream);
@@ -1757,6 +1763,9 @@ extern "C" co2_status_t co2_divergence(co2_dtype_t dt, int32_t g, const void* co
   if (g < 1 || g > kDivMaxWorkers) return fail(CO2_ERR_VALIDATION, "divergence: 1..64 workers");
   if (n < 0 || !ws) return fail(CO2_ERR_VALIDATION, "divergence: bad arguments");
   CO2_TRY(check_dtype(dt));
+  if (!params) return fail(CO2_ERR_VALIDATION, "null buffer");
+  for (int i = 0; i < g; ++i)
+    if (n > 0 && !params[i]) return fail(CO2_ERR_VALIDATION, "null buffer");
   cudaStream_t s = S(stream);
   // Scratch inside the workspace's partials area: per-block per-worker sums,
   // then g results and a private ticket.
