@@ -124,6 +124,7 @@ extern "C" co2_status_t co2_nccl_unique_id(uint8_t id_out[CO2_NCCL_ID_BYTES]) {
 
 extern "C" co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO2_NCCL_ID_BYTES],
                                             int32_t rank, int32_t world, int32_t max_ctas) {
+  if (!out) return fail(CO2_ERR_VALIDATION, "aar: null output handle");
   if (world < 1 || rank < 0 || rank >= world)
     return fail(CO2_ERR_VALIDATION, "aar: bad rank %d / world %d", rank, world);
   co2_aar* e = new co2_aar();
@@ -188,6 +189,7 @@ extern "C" co2_status_t co2_ipc_export(const void* dev_ptr, uint8_t handle_out[C
 
 extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_t world,
                                            int32_t ctas) {
+  if (!out) return fail(CO2_ERR_VALIDATION, "aar: null output handle");
   if (world < 1 || world > 8 || rank < 0 || rank >= world)
     return fail(CO2_ERR_VALIDATION, "aar: bad rank %d / world %d (p2p supports <= 8)", rank,
                 world);
@@ -317,6 +319,7 @@ extern "C" co2_status_t co2_aar_p2p_detach(co2_aar_t* e, const void* local) {
 }
 
 extern "C" co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers) {
+  if (!out) return fail(CO2_ERR_VALIDATION, "aar: null output handle");
   if (workers < 1 || workers > 64)
     return fail(CO2_ERR_VALIDATION, "aar: local workers must lie in [1, 64]");
   co2_aar* e = new co2_aar();
@@ -850,6 +853,9 @@ static co2_status_t copy_dev(void* d, const void* s, size_t bytes, cudaStream_t 
 
 extern "C" co2_status_t co2_round_finish(co2_worker_t* const* ws, int32_t g, void* stream,
                                          co2_round_result_t* res) {
+  if (!ws || !res || g < 1) return fail(CO2_ERR_VALIDATION, "co2_round_finish: bad arguments");
+  for (int i = 0; i < g; ++i)
+    if (!ws[i]) return fail(CO2_ERR_VALIDATION, "co2_round_finish: null worker");
   CO2_CUDA(cudaStreamSynchronize(S(stream)));
   co2_round_result_t r = *res;
   r.min_gap = INFINITY;
@@ -884,12 +890,22 @@ extern "C" co2_status_t co2_round_drain(co2_worker_t* const* ws, int32_t g, co2_
   return CO2_OK;
 }
 
+// Argument checks shared by the round drivers: engine, worker array and
+// every worker handle non-null, g >= 1.
+static co2_status_t check_round_args(co2_worker_t* const* ws, int32_t g, const co2_aar* e,
+                                     const char* who) {
+  if (!e || !ws || g < 1) return fail(CO2_ERR_VALIDATION, "%s: bad arguments", who);
+  for (int i = 0; i < g; ++i)
+    if (!ws[i]) return fail(CO2_ERR_VALIDATION, "%s: null worker", who);
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
                                   const co2_hyper_t* hyper, void* stream, int32_t sync,
                                   co2_round_result_t* res) {
   // co2_round, proj/src/outer_algorithms.cpp:110-211
   CO2_TRY(co2_hyper_validate(hyper));  // :115
-  if (!e || !ws || g < 1) return fail(CO2_ERR_VALIDATION, "co2_round: bad arguments");
+  CO2_TRY(check_round_args(ws, g, e, "co2_round"));
   if (hyper->tau < 1) return fail(CO2_ERR_VALIDATION, "staleness_gap: tau must be >= 1");
   if (g != (e->transport == T_LOCAL ? e->workers : 1))
     return fail(CO2_ERR_VALIDATION,
@@ -1512,6 +1528,7 @@ co2_status_t finish_round(co2_worker_t* const* ws, int32_t g, cudaStream_t st, i
 extern "C" co2_status_t co2_slowmo_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
                                          double alpha, double beta, void* stream, int32_t sync,
                                          co2_round_result_t* res) {
+  CO2_TRY(check_round_args(ws, g, e, "slowmo_round"));
   // slowmo_round, outer_algorithms.cpp:213-240
   if (!(alpha > 0.0)) return fail(CO2_ERR_VALIDATION, "slowmo: alpha must be positive");
   if (beta < 0.0 || beta >= 1.0) return fail(CO2_ERR_VALIDATION, "slowmo: beta must lie in [0, 1)");
@@ -1550,6 +1567,7 @@ extern "C" co2_status_t co2_slowmo_round(co2_worker_t* const* ws, int32_t g, co2
 extern "C" co2_status_t co2_local_sgd_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
                                             void* stream, int32_t sync,
                                             co2_round_result_t* res) {
+  CO2_TRY(check_round_args(ws, g, e, "local_sgd_round"));
   // local_sgd_round, outer_algorithms.cpp:242-260
   CO2_TRY(check_workers(ws, g, e));
   cudaStream_t st = S(stream);
@@ -1580,6 +1598,7 @@ extern "C" co2_status_t co2_local_sgd_round(co2_worker_t* const* ws, int32_t g, 
 extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int32_t g,
                                                     co2_aar_t* e, int32_t instant, void* stream,
                                                     int32_t sync, co2_round_result_t* res) {
+  CO2_TRY(check_round_args(ws, g, e, "overlap_local_sgd_round"));
   // overlap_local_sgd_round, outer_algorithms.cpp:262-313.  The anchors are
   // reduced from a snapshot copy in each worker's spare params buffer, so the
   // next inner loop can keep mutating the working params.  `instant` selects

@@ -87,10 +87,22 @@ def test_null_buffers_are_rejected_before_launch():
         lambda: lib.co2_clip_elementwise(L.DTYPE_F64, 8, None, 1.0, fake, fake, None),
         lambda: lib.co2_sub(L.DTYPE_F64, 8, fake, None, fake, None),
         lambda: lib.co2_convert(L.DTYPE_F32, None, L.DTYPE_F64, fake, 8, None),
+        lambda: lib.co2_aar_create_local(None, 2),
+        lambda: lib.co2_aar_create_p2p(None, 0, 2, 0),
     ]
     for f in cases:
         assert f() == L.ERR_VALIDATION
         assert "null" in lib.co2_last_error().decode()
+    # round drivers: a null engine / worker array / worker is rejected up front
+    arr = (C.c_void_p * 2)(None, None)
+    res = L.RoundResult()
+    for f in (lambda: lib.co2_round(arr, 2, None, C.byref(h), None, 1, C.byref(res)),
+              lambda: lib.co2_local_sgd_round(arr, 2, fake, None, 1, C.byref(res)),
+              lambda: lib.co2_slowmo_round(arr, 2, fake, 1.0, 0.5, None, 1, C.byref(res)),
+              lambda: lib.co2_round_finish(arr, 2, None, C.byref(res))):
+        assert f() == L.ERR_VALIDATION
+        msg = lib.co2_last_error().decode()
+        assert "bad arguments" in msg or "null worker" in msg, msg
 
 
 def test_allreduce_time_ring_formula(golden):
