@@ -18,7 +18,9 @@ kernels of libco2b200.so; torch supplies device memory and streams only.
 ParamVector becomes a 1-D CUDA tensor (float64 / float32 / bfloat16).  The
 per-op functions are synchronous like the reference (they return after the
 device flags were read so they can raise); the fused `outer_step` is
-asynchronous unless `check=True`.
+asynchronous when `check_flags=False`.  The default workspace is shared per
+device: launches on concurrent streams must each pass their own
+`Workspace`.
 """
 from __future__ import annotations
 
