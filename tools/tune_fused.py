@@ -65,7 +65,7 @@ def main():
     for v in variants:
         t = min(res[v])
         print(json.dumps({"mode": mode, "n": n, "variant": v[0], "waves": v[1],
-                          "shape": NAMES[mode][v[0]],
+                          "shape": NAMES[mode].get(v[0], "?"),
                           "median_ms_per_rep": [round(x * 1e3, 4) for x in res[v]],
                           "GBps_best_rep": BPP[mode] * n / t / 1e9,
                           "GBps_median_rep": BPP[mode] * n / statistics.median(res[v]) / 1e9}),
