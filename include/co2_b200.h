@@ -61,7 +61,8 @@ enum {
   CO2_FLAG_SLOWMO_M = 64u,       /* outer_algorithms.cpp:231 numeric  */
   CO2_FLAG_SLOWMO_X = 128u,      /* outer_algorithms.cpp:233 numeric  */
   CO2_FLAG_OVERLAP = 256u,       /* outer_algorithms.cpp:279 numeric  */
-  CO2_FLAG_NORM_NONFINITE = 512u /* global-norm clip extension numeric */
+  CO2_FLAG_NORM_NONFINITE = 512u, /* global-norm clip extension numeric */
+  CO2_FLAG_NONFINITE_INPUT = 1024u /* ensure_finite, param_ops.cpp:10-14 */
 };
 
 /* Co2Hyper (proj/include/co2sim/outer_algorithms.hpp:17-30) plus tau. */
@@ -191,6 +192,11 @@ co2_status_t co2_clip_elementwise(co2_dtype_t dt, int64_t n, const void* v, doub
  * HOST array of g device pointers (g <= 64), summed in ascending index
  * order and divided by g once.  F64: fp64; F32: fp32; BF16: fp32
  * accumulation, one rounding to bf16. */
+/* ensure_finite (param_ops.hpp:14, param_ops.cpp:10-14): numeric error
+ * "non-finite value in <what>" if any of the n values is NaN or +-inf.
+ * Synchronizes `stream`. */
+co2_status_t co2_ensure_finite(co2_dtype_t dt, int64_t n, const void* v, const char* what,
+                               void* workspace, void* stream);
 co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const* contributions, int64_t n,
                          void* out, void* workspace, void* stream);
 /* Round diagnostic of Simulation::step (outer_algorithms.cpp:503-508):

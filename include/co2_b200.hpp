@@ -214,6 +214,13 @@ inline DeviceVector average(const std::vector<DeviceVector>& contributions) {
   return out;
 }
 
+// ensure_finite (param_ops.hpp:14): numeric_error "non-finite value in " +
+// context.
+inline void ensure_finite(const DeviceVector& v, const std::string& context) {
+  Context& c = Context::get();
+  check(co2_ensure_finite(v.dtype(), v.size(), v.data(), context.c_str(), c.ws, c.stream));
+}
+
 inline double overlap_ratio(int tau, double t_comp, double t_comm) {
   double r = 0.0;
   check(co2_overlap_ratio(tau, t_comp, t_comm, &r));

@@ -19,6 +19,7 @@ FLAG_GAP_NONFINITE, FLAG_GAP_BELOW_ONE, FLAG_M_NONFINITE = 1, 2, 4
 FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
 FLAG_SLOWMO_M, FLAG_SLOWMO_X, FLAG_OVERLAP, FLAG_NORM_NONFINITE = 64, 128, 256, 512
 CLIP_COORDINATE, CLIP_GLOBAL_NORM = 0, 1
+FLAG_NONFINITE_INPUT = 1024
 BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
 BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT, BUF_XFIRST_ALT = 5, 6, 7, 8, 9
 IPC_HANDLE_BYTES = 72  # CUDA IPC handle (64) + int64 offset
@@ -99,6 +100,7 @@ SIGNATURES = {
     "co2_penalized_momentum": (ST, [I32, I64, P, D, P, P, I32, P, P, P]),
     "co2_outer_iterate": (ST, [I32, I64, P, D, P, D, I32, P, P, P]),
     "co2_clip_elementwise": (ST, [I32, I64, P, D, P, P, P]),
+    "co2_ensure_finite": (ST, [I32, I64, P, C.c_char_p, P, P]),
     "co2_average": (ST, [I32, I32, C.POINTER(P), I64, P, P, P]),
     "co2_sub": (ST, [I32, I64, P, P, P, P]),
     "co2_divergence": (ST, [I32, I32, C.POINTER(P), I64, C.POINTER(D), C.POINTER(D), P, P]),

@@ -176,6 +176,15 @@ def clip_elementwise(v, phi: float, *, stream=None):
     return out
 
 
+def ensure_finite(v: torch.Tensor, context: str, *, workspace: Workspace | None = None,
+                  stream=None) -> None:
+    """ensure_finite (proj/src/param_ops.cpp:10-14): raises NumericError
+    "non-finite value in <context>" if v holds a NaN or an infinity."""
+    ws = workspace or _ws(v.device)
+    check(lib().co2_ensure_finite(_dtype(v), v.numel(), _ptr(v), context.encode(), ws.ptr,
+                                  _stream(stream)))
+
+
 def average(contributions, *, stream=None):
     """average (proj/src/param_ops.cpp:16-33): ascending-order sum, one
     division by G."""
@@ -492,6 +501,15 @@ class CollectiveEngine:
         c = C.c_uint64()
         check(lib().co2_aar_totals(self.handle, None, C.byref(c)))
         return c.value
+
+    def reduce_time(self) -> float:
+        """reduce_time() (collective.hpp:64): here the measured mean device
+        duration (s) of the completed reduces, 0.0 before the first."""
+        ev = self.events()
+        start = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "launch"}
+        dur = [e["t_sim"] - start[e["handle_id"]] for e in ev
+               if e["event"] == "complete" and e["handle_id"] in start]
+        return sum(dur) / len(dur) if dur else 0.0
 
     def live_handles(self) -> int:
         v = C.c_int32()

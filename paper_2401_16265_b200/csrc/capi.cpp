@@ -93,6 +93,7 @@ extern "C" co2_status_t co2_diag_status(const co2_diag_t* d) {
   if (f & CO2_FLAG_SLOWMO_X)
     return fail(CO2_ERR_NUMERIC, "non-finite value in slowmo outer iterate");
   if (f & CO2_FLAG_OVERLAP) return fail(CO2_ERR_NUMERIC, "non-finite value in overlap correction");
+  if (f & CO2_FLAG_NONFINITE_INPUT) return fail(CO2_ERR_NUMERIC, "non-finite value");
   return CO2_OK;
 }
 

@@ -690,7 +690,7 @@ struct Ptrs64 {
   const T* p[64];
 };
 
-enum OpKind { OP_GAP = 0, OP_MOMENTUM = 1, OP_ITERATE = 2, OP_CLIP = 3 };
+enum OpKind { OP_GAP = 0, OP_MOMENTUM = 1, OP_ITERATE = 2, OP_CLIP = 3, OP_FINITE = 4 };
 
 struct OpArgs {
   const void* a;
@@ -757,13 +757,15 @@ __global__ void __launch_bounds__(kThreads) op_kernel(const OpArgs a) {
       double st = (double)fabs(xn - x);
       acc.max_step = st > acc.max_step ? st : acc.max_step;
       O[j] = Store<T>::from(xn);
-    } else {  // OP_CLIP, param_ops.cpp:35-43
+    } else if (OP == OP_CLIP) {  // param_ops.cpp:35-43
       TC phi = (TC)a.s0;
       TC v = to_c(A[j]);
       if (!isfinite(v)) acc.flags |= CO2_FLAG_CLIP_NONFINITE;
       acc.clipped += (v < -phi) || (phi < v);
       TC lo = (v < -phi) ? -phi : v;
       O[j] = Store<T>::from((phi < lo) ? phi : lo);
+    } else {  // OP_FINITE, ensure_finite (param_ops.cpp:10-14)
+      if (!isfinite(to_c(A[j]))) acc.flags |= CO2_FLAG_NONFINITE_INPUT;
     }
   }
   block_finish<kThreads>(acc, a.ws);
@@ -902,8 +904,9 @@ co2_status_t launch_op(co2_dtype_t dt, const OpArgs& a, cudaStream_t s) {
   if (!a.ws) return fail(CO2_ERR_VALIDATION, "null workspace");
   // operands each op reads: GAP (x_t0, prev_x0, prev_x1), MOMENTUM (m, gap,
   // delta), ITERATE (x_t0, m), CLIP (v)
-  const bool need_b = OP != OP_CLIP, need_c = OP == OP_GAP || OP == OP_MOMENTUM;
-  if (a.n > 0 && (!a.a || !a.out || (need_b && !a.b) || (need_c && !a.c)))
+  const bool need_b = OP != OP_CLIP && OP != OP_FINITE;
+  const bool need_c = OP == OP_GAP || OP == OP_MOMENTUM, need_out = OP != OP_FINITE;
+  if (a.n > 0 && (!a.a || (need_out && !a.out) || (need_b && !a.b) || (need_c && !a.c)))
     return fail(CO2_ERR_VALIDATION, "null buffer");
   int grid = simple_grid(a.n, kThreads);
   if (grid > kMaxBlocks) grid = kMaxBlocks;
@@ -1359,6 +1362,21 @@ extern "C" co2_status_t co2_clip_elementwise(co2_dtype_t dt, int64_t n, const vo
   if (!(phi > 0.0)) return fail(CO2_ERR_VALIDATION, "clip_elementwise: phi must be positive");
   OpArgs a{v, nullptr, nullptr, out, n, phi, 0.0, 0, ws};
   return launch_op<OP_CLIP>(dt, a, S(stream));
+}
+
+extern "C" co2_status_t co2_ensure_finite(co2_dtype_t dt, int64_t n, const void* v,
+                                         const char* what, void* ws, void* stream) {
+  // ensure_finite (param_ops.cpp:10-14): "non-finite value in " + context
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "ensure_finite: negative length");
+  OpArgs a{v, nullptr, nullptr, nullptr, n, 0.0, 0.0, 0, ws};
+  CO2_TRY(launch_op<OP_FINITE>(dt, a, S(stream)));
+  co2_diag_t d;
+  CO2_CUDA(cudaMemcpyAsync(&d, &ws_header(ws)->diag, sizeof d, cudaMemcpyDeviceToHost,
+                           S(stream)));
+  CO2_CUDA(cudaStreamSynchronize(S(stream)));
+  if (d.flags & CO2_FLAG_NONFINITE_INPUT)
+    return fail(CO2_ERR_NUMERIC, "non-finite value in %s", what ? what : "");
+  return CO2_OK;
 }
 
 extern "C" co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const* contributions,

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "co2_b200.hpp"
@@ -116,6 +117,17 @@ int main() {
     CHECK(throws<validation_error>([&] { clip_elementwise(vec({1.0}), 0.0); }));
     CHECK(throws<numeric_error>([&] { clip_elementwise(vec({NAN}), 1.0); }));
     std::printf("ok clip\n");
+  }
+  {  // ensure_finite names the failing context (test_param_ops.cpp:162-170)
+    ensure_finite(vec({1.0, 2.0}), "outer momentum");
+    bool named = false;
+    try {
+      ensure_finite(vec({1.0, NAN}), "outer momentum");
+    } catch (const numeric_error& e) {
+      named = std::string(e.what()).find("outer momentum") != std::string::npos;
+    }
+    CHECK(named);
+    std::printf("ok ensure_finite\n");
   }
   {  // overlap ratio (timing_model.cpp:36-43 via the ABI)
     CHECK(overlap_ratio(2, 0.25, 1.0) == 0.5);

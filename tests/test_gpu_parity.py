@@ -317,6 +317,19 @@ def test_unfused_kats_and_errors(golden):
         co2.outer_iterate(t([1.0]), 1.0, t([float("inf")]), 1.0, False)
 
 
+def test_ensure_finite_names_the_context():
+    """ensure_finite (param_ops.cpp:10-14; test_param_ops.cpp:162-170)."""
+    for dt in (torch.float64, torch.float32, torch.bfloat16):
+        ok = torch.linspace(-1, 1, 1001, device="cuda").to(dt)
+        co2.ensure_finite(ok, "outer momentum")
+        for bad in (float("nan"), float("inf"), float("-inf")):
+            v = ok.clone()
+            v[777] = bad
+            with pytest.raises(co2.NumericError, match="^non-finite value in outer momentum$"):
+                co2.ensure_finite(v, "outer momentum")
+    co2.ensure_finite(torch.empty(0, device="cuda"), "empty")
+
+
 def test_average_golden_and_fixed_order(golden):
     ins = [torch.tensor(v, dtype=torch.float64, device="cuda") for v in golden["average"]["inputs"]]
     assert co2.average(ins).tolist() == golden["average"]["expected"]

@@ -248,6 +248,7 @@ def test_engine_semantics():
     eng.wait(h2)
     torch.cuda.synchronize()
     assert eng.info(h2)["consumed"] and eng.handle_count() == 3
+    assert eng.reduce_time() > 0.0
 
 
 def test_round_rejects_bad_hyper_and_counts():
