@@ -197,6 +197,17 @@ co2_status_t co2_clip_elementwise(co2_dtype_t dt, int64_t n, const void* v, doub
  * Synchronizes `stream`. */
 co2_status_t co2_ensure_finite(co2_dtype_t dt, int64_t n, const void* v, const char* what,
                                void* workspace, void* stream);
+/* elementwise_abs_diff (param_ops.cpp:44-51): out = |a - b|; numeric error
+ * "non-finite value in elementwise_abs_diff".  Synchronizes `stream`. */
+co2_status_t co2_elementwise_abs_diff(co2_dtype_t dt, int64_t n, const void* a, const void* b,
+                                      void* out, void* workspace, void* stream);
+/* l2_norm (param_ops.cpp:54-60): the Euclidean norm, squares summed in fp64
+ * in a fixed order (the global-norm clip's chunked order, so it is
+ * deterministic for a given n and dtype; the reference's Eigen reduction
+ * order differs, so it agrees to fp64 rounding, not bitwise); numeric error
+ * "l2_norm: non-finite result".  Synchronizes `stream`. */
+co2_status_t co2_l2_norm(co2_dtype_t dt, int64_t n, const void* v, double* norm_out,
+                         void* workspace, void* stream);
 co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const* contributions, int64_t n,
                          void* out, void* workspace, void* stream);
 /* Round diagnostic of Simulation::step (outer_algorithms.cpp:503-508):

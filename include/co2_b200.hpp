@@ -221,6 +221,24 @@ inline void ensure_finite(const DeviceVector& v, const std::string& context) {
   check(co2_ensure_finite(v.dtype(), v.size(), v.data(), context.c_str(), c.ws, c.stream));
 }
 
+// elementwise_abs_diff / l2_norm (param_ops.hpp:26-30).
+inline DeviceVector elementwise_abs_diff(const DeviceVector& a, const DeviceVector& b) {
+  if (a.size() != b.size() || a.dtype() != b.dtype())
+    throw validation_error("elementwise_abs_diff: dimensions differ");
+  Context& c = Context::get();
+  DeviceVector out(a.size(), a.dtype());
+  check(co2_elementwise_abs_diff(a.dtype(), a.size(), a.data(), b.data(), out.data(), c.ws,
+                                 c.stream));
+  return out;
+}
+
+inline double l2_norm(const DeviceVector& v) {
+  Context& c = Context::get();
+  double r = 0.0;
+  check(co2_l2_norm(v.dtype(), v.size(), v.data(), &r, c.ws, c.stream));
+  return r;
+}
+
 inline double overlap_ratio(int tau, double t_comp, double t_comm) {
   double r = 0.0;
   check(co2_overlap_ratio(tau, t_comp, t_comm, &r));

@@ -651,6 +651,47 @@ int orc_outer_step_global_clip(int mode, int64_t n, const void* x_t0v, const voi
   return orc_diag_status(diag);
 }
 
+static double ld_any(int dtype, const void* v, int64_t j) {
+  if (dtype == 0) return ((const double*)v)[j];
+  if (dtype == 1) return (double)((const float*)v)[j];
+  return (double)orc_bf16_to_f32(((const uint16_t*)v)[j]);
+}
+
+double orc_l2_norm(int dtype, int64_t n, const void* v) {
+  const int V = dtype == 0 ? 2 : (dtype == 1 ? 4 : 8);
+  const int64_t chunk = orc_gc_chunk(n, V);
+  const int64_t K = n == 0 ? 0 : (n + chunk - 1) / chunk;
+  const int64_t nvE = n / V * V;
+  double* cs = K ? malloc(sizeof(double) * (size_t)K) : NULL;
+  if (K && !cs) return NAN;
+  double t[GC_THREADS];
+  for (int64_t c = 0; c < K; ++c) {
+    const int64_t e0 = c * chunk, e1 = e0 + chunk < nvE ? e0 + chunk : nvE;
+    for (int th = 0; th < GC_THREADS; ++th) {
+      double acc = 0.0;
+      for (int64_t e = e0 + (int64_t)th * V; e < e1; e += (int64_t)GC_THREADS * V)
+        for (int k = 0; k < V; ++k) {
+          const double d = ld_any(dtype, v, e + k);
+          acc = acc + d * d;
+        }
+      if (th == 0 && c == K - 1)
+        for (int64_t e = nvE; e < n; ++e) {
+          const double d = ld_any(dtype, v, e);
+          acc = acc + d * d;
+        }
+      t[th] = acc;
+    }
+    cs[c] = gc_block_sum(t);
+  }
+  for (int th = 0; th < GC_THREADS; ++th) {
+    double acc = 0.0;
+    for (int64_t i = th; i < K; i += GC_THREADS) acc = acc + cs[i];
+    t[th] = acc;
+  }
+  free(cs);
+  return sqrt(gc_block_sum(t));
+}
+
 /* ------------------------------------------------ baseline outer steps */
 /* Element access in the mode's storage types (see orc_outer_step). */
 static double ld_state(int mode, const void* p, int64_t j) {

@@ -150,6 +150,10 @@ enum { ORC_FLAG_SLOWMO_M = 64u, ORC_FLAG_SLOWMO_X = 128u, ORC_FLAG_OVERLAP = 256
  * V = 2 (fp64), 4 (fp32), 8 (bf16-mixed).  n_clipped = n when scaled. */
 enum { ORC_FLAG_NORM_NONFINITE = 512u };
 int64_t orc_gc_chunk(int64_t n, int V);
+/* l2_norm (proj/src/param_ops.cpp:54-60) in the GPU's fixed order (the
+ * global-clip chunked sum above, V by dtype: 0 fp64 -> 2, 1 fp32 -> 4,
+ * 2 bf16 -> 8). */
+double orc_l2_norm(int dtype, int64_t n, const void* v);
 int orc_outer_step_global_clip(int mode, int64_t n, const void* x_t0, const void* p0,
                                const void* p1, const void* xbar, int divisor, void* m,
                                void* anchor, void* params, void* gap, const orc_hyper* h,

@@ -95,6 +95,8 @@ def lib():
                                                  C.POINTER(Hyper), C.POINTER(Diag),
                                                  C.POINTER(C.c_double)]
         L.orc_gc_chunk.argtypes = [I64, I]
+        L.orc_l2_norm.argtypes = [I, I64, P]
+        L.orc_l2_norm.restype = D
         L.orc_gc_chunk.restype = I64
         L.orc_diag_status.argtypes = [C.POINTER(Diag)]
         L.orc_average_lp.argtypes = [I, I, P, I64, P]
@@ -320,6 +322,14 @@ def outer_step_global_clip(mode: int, x_t0, p0, p1, xbar, m, h: Hyper, divisor: 
     if code not in (OK, VALIDATION, NUMERIC):
         raise RuntimeError(msg)
     return FusedResult(mm, anchor, params, gap, d, code, msg), norm.value
+
+
+def l2_norm(v: np.ndarray) -> float:
+    """l2_norm (proj/src/param_ops.cpp:54-60) in the GPU's fixed order; bf16
+    inputs as uint16 bit patterns."""
+    dt = {np.dtype(np.float64): 0, np.dtype(np.float32): 1, np.dtype(np.uint16): 2}[v.dtype]
+    a = np.ascontiguousarray(v)
+    return lib().orc_l2_norm(dt, a.size, _p(a))
 
 
 def gc_chunk(n: int, v: int) -> int:

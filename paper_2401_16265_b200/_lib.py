@@ -101,6 +101,8 @@ SIGNATURES = {
     "co2_outer_iterate": (ST, [I32, I64, P, D, P, D, I32, P, P, P]),
     "co2_clip_elementwise": (ST, [I32, I64, P, D, P, P, P]),
     "co2_ensure_finite": (ST, [I32, I64, P, C.c_char_p, P, P]),
+    "co2_elementwise_abs_diff": (ST, [I32, I64, P, P, P, P, P]),
+    "co2_l2_norm": (ST, [I32, I64, P, C.POINTER(D), P, P]),
     "co2_average": (ST, [I32, I32, C.POINTER(P), I64, P, P, P]),
     "co2_sub": (ST, [I32, I64, P, P, P, P]),
     "co2_divergence": (ST, [I32, I32, C.POINTER(P), I64, C.POINTER(D), C.POINTER(D), P, P]),

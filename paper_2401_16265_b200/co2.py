@@ -176,6 +176,27 @@ def clip_elementwise(v, phi: float, *, stream=None):
     return out
 
 
+def elementwise_abs_diff(a: torch.Tensor, b: torch.Tensor, *, workspace: Workspace | None = None,
+                         stream=None) -> torch.Tensor:
+    """elementwise_abs_diff (proj/src/param_ops.cpp:44-51)."""
+    if a.numel() != b.numel() or a.dtype != b.dtype:
+        raise ValidationError("elementwise_abs_diff: dimensions differ")
+    out = torch.empty_like(a)
+    ws = workspace or _ws(a.device)
+    check(lib().co2_elementwise_abs_diff(_dtype(a), a.numel(), _ptr(a), _ptr(b), _ptr(out),
+                                         ws.ptr, _stream(stream)))
+    return out
+
+
+def l2_norm(v: torch.Tensor, *, workspace: Workspace | None = None, stream=None) -> float:
+    """l2_norm (proj/src/param_ops.cpp:54-60), fixed-order fp64 sum of squares."""
+    ws = workspace or _ws(v.device)
+    out = C.c_double()
+    check(lib().co2_l2_norm(_dtype(v), v.numel(), _ptr(v), C.byref(out), ws.ptr,
+                            _stream(stream)))
+    return out.value
+
+
 def ensure_finite(v: torch.Tensor, context: str, *, workspace: Workspace | None = None,
                   stream=None) -> None:
     """ensure_finite (proj/src/param_ops.cpp:10-14): raises NumericError

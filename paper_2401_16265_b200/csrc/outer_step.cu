@@ -690,7 +690,8 @@ struct Ptrs64 {
   const T* p[64];
 };
 
-enum OpKind { OP_GAP = 0, OP_MOMENTUM = 1, OP_ITERATE = 2, OP_CLIP = 3, OP_FINITE = 4 };
+enum OpKind { OP_GAP = 0, OP_MOMENTUM = 1, OP_ITERATE = 2, OP_CLIP = 3, OP_FINITE = 4,
+              OP_ABSDIFF = 5 };
 
 struct OpArgs {
   const void* a;
@@ -764,6 +765,10 @@ __global__ void __launch_bounds__(kThreads) op_kernel(const OpArgs a) {
       acc.clipped += (v < -phi) || (phi < v);
       TC lo = (v < -phi) ? -phi : v;
       O[j] = Store<T>::from((phi < lo) ? phi : lo);
+    } else if (OP == OP_ABSDIFF) {  // elementwise_abs_diff, param_ops.cpp:44-51
+      TC r = fabs(to_c(A[j]) - to_c(B[j]));
+      if (!isfinite(r)) acc.flags |= CO2_FLAG_NONFINITE_INPUT;
+      O[j] = Store<T>::from(r);
     } else {  // OP_FINITE, ensure_finite (param_ops.cpp:10-14)
       if (!isfinite(to_c(A[j]))) acc.flags |= CO2_FLAG_NONFINITE_INPUT;
     }
@@ -904,7 +909,7 @@ co2_status_t launch_op(co2_dtype_t dt, const OpArgs& a, cudaStream_t s) {
   if (!a.ws) return fail(CO2_ERR_VALIDATION, "null workspace");
   // operands each op reads: GAP (x_t0, prev_x0, prev_x1), MOMENTUM (m, gap,
   // delta), ITERATE (x_t0, m), CLIP (v)
-  const bool need_b = OP != OP_CLIP && OP != OP_FINITE;
+  const bool need_b = OP != OP_CLIP && OP != OP_FINITE;  // ABSDIFF reads b
   const bool need_c = OP == OP_GAP || OP == OP_MOMENTUM, need_out = OP != OP_FINITE;
   if (a.n > 0 && (!a.a || (need_out && !a.out) || (need_b && !a.b) || (need_c && !a.c)))
     return fail(CO2_ERR_VALIDATION, "null buffer");
@@ -1166,6 +1171,74 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass2(const StepArgs a) {
   }
 }
 
+// l2_norm (param_ops.cpp:54-60) in the global-norm clip's fixed order: fp64
+// squares summed per fixed chunk (thread t: vectors t, t+256, ...; the n % V
+// tail to thread 0 of the last chunk), xor butterfly per warp, warps in
+// order; the last CTA folds the chunk sums the same way and stores the sqrt
+// in the workspace header.  Deterministic for a given n and dtype.
+template <typename T, int V>
+__global__ void __launch_bounds__(kGcThreads) sumsq_kernel(const T* v, int64_t n, int64_t chunk,
+                                                          void* ws) {
+  constexpr int NT = kGcThreads, NW = NT / 32;
+  double* cs = ws_chunks(ws);
+  __shared__ double sh[NW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nvE = n / V * V;
+  const int64_t K = (n + chunk - 1) / chunk;
+  Acc acc;
+  for (int64_t c = blockIdx.x; c < K; c += gridDim.x) {
+    double s = 0.0;
+    const int64_t e0 = c * chunk;
+    const int64_t e1 = e0 + chunk < nvE ? e0 + chunk : nvE;
+    for (int64_t e = e0 + (int64_t)threadIdx.x * V; e < e1; e += (int64_t)NT * V) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const double d = (double)to_c(v[e + k]);
+        s = s + d * d;
+      }
+    }
+    if (threadIdx.x == 0 && c == K - 1)
+      for (int64_t e = nvE; e < n; ++e) {
+        const double d = (double)to_c(v[e]);
+        s = s + d * d;
+      }
+    s = warp_sum_fixed(s);
+    if (lane == 0) sh[wid] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = sh[0];
+      for (int w = 1; w < NW; ++w) t = t + sh[w];
+      cs[c] = t;
+    }
+    __syncthreads();
+  }
+  if (block_finish<NT>(acc, ws)) {
+    double b = 0.0;
+    for (int64_t i = threadIdx.x; i < K; i += NT) b = b + __ldcg(cs + i);
+    b = warp_sum_fixed(b);
+    __syncthreads();
+    if (lane == 0) sh[wid] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = sh[0];
+      for (int w = 1; w < NW; ++w) t = t + sh[w];
+      ws_header(ws)->gnorm = sqrt(t);
+      __threadfence();
+    }
+  }
+}
+
+template <typename T, int V>
+co2_status_t launch_sumsq(const void* v, int64_t n, void* ws, cudaStream_t s) {
+  const int64_t chunk = gc_chunk(n, V);
+  const int64_t K = (n + chunk - 1) / chunk;
+  auto k = sumsq_kernel<T, V>;
+  k<<<grid_for(k, K * kGcThreads, kGcThreads), kGcThreads, 0, s>>>(static_cast<const T*>(v), n,
+                                                                    chunk, ws);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
 template <class M>
 co2_status_t launch_global_clip(const StepArgs& a, cudaStream_t s) {
   constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
@@ -1376,6 +1449,39 @@ extern "C" co2_status_t co2_ensure_finite(co2_dtype_t dt, int64_t n, const void*
   CO2_CUDA(cudaStreamSynchronize(S(stream)));
   if (d.flags & CO2_FLAG_NONFINITE_INPUT)
     return fail(CO2_ERR_NUMERIC, "non-finite value in %s", what ? what : "");
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_elementwise_abs_diff(co2_dtype_t dt, int64_t n, const void* a,
+                                                 const void* b, void* out, void* ws,
+                                                 void* stream) {
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "elementwise_abs_diff: dimensions differ");
+  OpArgs oa{a, b, nullptr, out, n, 0.0, 0.0, 0, ws};
+  CO2_TRY(launch_op<OP_ABSDIFF>(dt, oa, S(stream)));
+  co2_diag_t d;
+  CO2_CUDA(cudaMemcpyAsync(&d, &ws_header(ws)->diag, sizeof d, cudaMemcpyDeviceToHost,
+                           S(stream)));
+  CO2_CUDA(cudaStreamSynchronize(S(stream)));
+  if (d.flags & CO2_FLAG_NONFINITE_INPUT)
+    return fail(CO2_ERR_NUMERIC, "non-finite value in elementwise_abs_diff");
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_l2_norm(co2_dtype_t dt, int64_t n, const void* v, double* out,
+                                   void* ws, void* stream) {
+  CO2_TRY(check_dtype(dt));
+  if (n < 0) return fail(CO2_ERR_VALIDATION, "l2_norm: negative length");
+  if (!ws || !out || (n > 0 && !v)) return fail(CO2_ERR_VALIDATION, "null buffer");
+  if (dt == CO2_DTYPE_F64)
+    CO2_TRY((launch_sumsq<double, 2>(v, n, ws, S(stream))));
+  else if (dt == CO2_DTYPE_F32)
+    CO2_TRY((launch_sumsq<float, 4>(v, n, ws, S(stream))));
+  else
+    CO2_TRY((launch_sumsq<bf16s, 8>(v, n, ws, S(stream))));
+  CO2_CUDA(cudaMemcpyAsync(out, &ws_header(ws)->gnorm, sizeof(double), cudaMemcpyDeviceToHost,
+                           S(stream)));
+  CO2_CUDA(cudaStreamSynchronize(S(stream)));
+  if (!isfinite(*out)) return fail(CO2_ERR_NUMERIC, "l2_norm: non-finite result");
   return CO2_OK;
 }
 

@@ -129,6 +129,16 @@ int main() {
     CHECK(named);
     std::printf("ok ensure_finite\n");
   }
+  {  // elementwise_abs_diff / l2_norm (test_param_ops.cpp:147-160)
+    auto d = elementwise_abs_diff(vec({1.0, -2.0, 3.5}), vec({2.5, -2.0, -1.0})).to_host();
+    CHECK(d[0] == 1.5 && d[1] == 0.0 && d[2] == 4.5);
+    CHECK(throws<validation_error>([&] { elementwise_abs_diff(vec({1.0}), vec({1.0, 2.0})); }));
+    CHECK(throws<numeric_error>([&] { elementwise_abs_diff(vec({INFINITY}), vec({1.0})); }));
+    CHECK(l2_norm(vec({3.0, 4.0})) == 5.0);
+    CHECK(l2_norm(vec({0.0, 0.0, 0.0})) == 0.0);
+    CHECK(throws<numeric_error>([&] { l2_norm(vec({1e300, 1e300})); }));
+    std::printf("ok elementwise_abs_diff / l2_norm\n");
+  }
   {  // overlap ratio (timing_model.cpp:36-43 via the ABI)
     CHECK(overlap_ratio(2, 0.25, 1.0) == 0.5);
     CHECK(overlap_ratio(8, 0.25, 1.0) == 1.0);

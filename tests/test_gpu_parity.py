@@ -330,6 +330,33 @@ def test_ensure_finite_names_the_context():
     co2.ensure_finite(torch.empty(0, device="cuda"), "empty")
 
 
+@pytest.mark.parametrize("dt", [torch.float64, torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("n", [0, 1, 7, 100_003, 3_000_001])
+def test_l2_norm_bitwise_fixed_order(dt, n):
+    """l2_norm (param_ops.cpp:54-60) in the fixed chunked order: bitwise the
+    oracle's restatement for every dtype and size."""
+    v = torch.randn(n, device="cuda", generator=torch.Generator("cuda").manual_seed(n)).to(dt)
+    got = co2.l2_norm(v)
+    assert got == O.l2_norm(to_np(v))
+
+
+def test_abs_diff_and_l2_norm_kats_and_errors():
+    """elementwise_abs_diff / l2_norm KATs (test_param_ops.cpp:147-160)."""
+    t = lambda v: torch.tensor(v, dtype=torch.float64, device="cuda")  # noqa: E731
+    assert co2.elementwise_abs_diff(t([1.0, -2.0, 3.5]), t([2.5, -2.0, -1.0])).tolist() == \
+        [1.5, 0.0, 4.5]
+    with pytest.raises(co2.ValidationError, match="elementwise_abs_diff: dimensions differ"):
+        co2.elementwise_abs_diff(t([1.0, -2.0, 3.5]), t([1.0]))
+    with pytest.raises(co2.NumericError, match="non-finite value in elementwise_abs_diff"):
+        co2.elementwise_abs_diff(t([float("inf")]), t([1.0]))
+    assert co2.l2_norm(t([3.0, 4.0])) == 5.0 and co2.l2_norm(t([0.0, 0.0, 0.0])) == 0.0
+    with pytest.raises(co2.NumericError, match="l2_norm: non-finite result"):
+        co2.l2_norm(t([1e300, 1e300]))
+    a = torch.randn(100_001, device="cuda", dtype=torch.float32)
+    b = torch.randn(100_001, device="cuda", dtype=torch.float32)
+    assert torch.equal(co2.elementwise_abs_diff(a, b), (a - b).abs())
+
+
 def test_average_golden_and_fixed_order(golden):
     ins = [torch.tensor(v, dtype=torch.float64, device="cuda") for v in golden["average"]["inputs"]]
     assert co2.average(ins).tolist() == golden["average"]["expected"]
