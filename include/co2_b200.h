@@ -273,6 +273,22 @@ co2_status_t co2_overlap_ratio(int32_t tau, double t_comp, double t_comm, double
 co2_status_t co2_simulate_timeline_co2(const co2_cluster_t* spec, int32_t tau, int32_t rounds,
                                        int32_t batch_size, co2_timeline_t* out,
                                        co2_round_timing_t* per_round);
+/* simulate_timeline for every AlgorithmKind (algorithm_kind.hpp:9,
+ * timing_model.cpp:76-173); co2_simulate_timeline_co2 is kind CO2_ALG_CO2. */
+enum {
+  CO2_ALG_CO2 = 0,
+  CO2_ALG_SLOWMO = 1,
+  CO2_ALG_LOCAL_SGD = 2,
+  CO2_ALG_OVERLAP_LOCAL_SGD = 3,
+  CO2_ALG_SYNC_SGD = 4
+};
+co2_status_t co2_simulate_timeline(int32_t kind, const co2_cluster_t* spec, int32_t tau,
+                                   int32_t rounds, int32_t batch_size, co2_timeline_t* out,
+                                   co2_round_timing_t* per_round);
+/* scalability_ratio (timing_model.cpp:45-53): throughput gain over worker
+ * gain. */
+co2_status_t co2_scalability_ratio(double throughput_small, double throughput_large,
+                                   double workers_small, double workers_large, double* out);
 
 /* ---- one-step-stale all-reduce engine (CollectiveEngine,
  *      proj/include/co2sim/collective.hpp:54-93) ----------------------------

@@ -20,6 +20,7 @@ FLAG_CLIP_NONFINITE, FLAG_X_NONFINITE, FLAG_AVG_NONFINITE = 8, 16, 32
 FLAG_SLOWMO_M, FLAG_SLOWMO_X, FLAG_OVERLAP, FLAG_NORM_NONFINITE = 64, 128, 256, 512
 CLIP_COORDINATE, CLIP_GLOBAL_NORM = 0, 1
 FLAG_NONFINITE_INPUT = 1024
+ALG_CO2, ALG_SLOWMO, ALG_LOCAL_SGD, ALG_OVERLAP_LOCAL_SGD, ALG_SYNC_SGD = 0, 1, 2, 3, 4
 BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
 BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT, BUF_XFIRST_ALT = 5, 6, 7, 8, 9
 IPC_HANDLE_BYTES = 72  # CUDA IPC handle (64) + int64 offset
@@ -116,6 +117,9 @@ SIGNATURES = {
     "co2_overlap_ratio": (ST, [I32, D, D, C.POINTER(D)]),
     "co2_simulate_timeline_co2": (ST, [C.POINTER(Cluster), I32, I32, I32, C.POINTER(Timeline),
                                        C.POINTER(RoundTiming)]),
+    "co2_simulate_timeline": (ST, [I32, C.POINTER(Cluster), I32, I32, I32, C.POINTER(Timeline),
+                                  C.POINTER(RoundTiming)]),
+    "co2_scalability_ratio": (ST, [D, D, D, D, C.POINTER(D)]),
     "co2_nccl_unique_id": (ST, [C.POINTER(C.c_uint8)]),
     "co2_aar_create_nccl": (ST, [C.POINTER(P), C.POINTER(C.c_uint8), I32, I32, I32]),
     "co2_aar_create_local": (ST, [C.POINTER(P), I32]),

@@ -381,17 +381,40 @@ class TimelineReport:
     per_round: list = field(default_factory=list)
 
 
+ALGORITHMS = {"co2": L.ALG_CO2, "slowmo": L.ALG_SLOWMO, "local_sgd": L.ALG_LOCAL_SGD,
+              "overlap_local_sgd": L.ALG_OVERLAP_LOCAL_SGD, "sync_sgd": L.ALG_SYNC_SGD}
+
+
 def simulate_timeline_co2(spec: ClusterSpec, tau: int, rounds: int,
                           batch_size: int = 1) -> TimelineReport:
     """simulate_timeline(AlgorithmKind::co2, ...) (proj/src/timing_model.cpp:76-123)."""
+    return simulate_timeline("co2", spec, tau, rounds, batch_size)
+
+
+def simulate_timeline(kind: str, spec: ClusterSpec, tau: int, rounds: int,
+                      batch_size: int = 1) -> TimelineReport:
+    """simulate_timeline (proj/src/timing_model.cpp:76-173) for kind in
+    co2 / slowmo / local_sgd / overlap_local_sgd / sync_sgd."""
+    if kind not in ALGORITHMS:
+        raise ValidationError(f"simulate_timeline: unknown algorithm {kind!r}")
     s, out = spec.c(), L.Timeline()
     per = (L.RoundTiming * max(rounds, 1))()
-    check(lib().co2_simulate_timeline_co2(C.byref(s), tau, rounds, batch_size, C.byref(out), per))
+    check(lib().co2_simulate_timeline(ALGORITHMS[kind], C.byref(s), tau, rounds, batch_size,
+                                      C.byref(out), per))
     return TimelineReport(out.workers, out.tau, out.rounds, out.batch_size, out.comm_time,
                           out.wall_time, out.total_stall, out.overlap_ratio_achieved,
                           out.throughput,
                           [(per[i].t, per[i].start, per[i].stall, per[i].end)
                            for i in range(rounds)])
+
+
+def scalability_ratio(throughput_small: float, throughput_large: float, workers_small: float,
+                      workers_large: float) -> float:
+    """scalability_ratio (proj/src/timing_model.cpp:45-53)."""
+    r = C.c_double()
+    check(lib().co2_scalability_ratio(throughput_small, throughput_large, workers_small,
+                                      workers_large, C.byref(r)))
+    return r.value
 
 
 # ------------------------------------------------------- collective engine

@@ -324,32 +324,77 @@ extern "C" co2_status_t co2_overlap_ratio(int32_t tau, double t_comp, double t_c
   return CO2_OK;
 }
 
-extern "C" co2_status_t co2_simulate_timeline_co2(const co2_cluster_t* s, int32_t tau,
-                                                  int32_t rounds, int32_t batch_size,
-                                                  co2_timeline_t* out,
-                                                  co2_round_timing_t* per_round) {
-  // simulate_timeline co2 branch, timing_model.cpp:76-123,167-173
+extern "C" co2_status_t co2_simulate_timeline(int32_t kind, const co2_cluster_t* s, int32_t tau,
+                                              int32_t rounds, int32_t batch_size,
+                                              co2_timeline_t* out,
+                                              co2_round_timing_t* per_round) {
+  // simulate_timeline, timing_model.cpp:76-173: co2 / slowmo / local_sgd /
+  // overlap_local_sgd / sync_sgd (AlgorithmKind order, algorithm_kind.hpp:9)
   CO2_TRY(co2_cluster_validate(s));
+  if (kind < CO2_ALG_CO2 || kind > CO2_ALG_SYNC_SGD)
+    return fail(CO2_ERR_VALIDATION, "simulate_timeline: unknown algorithm %d", (int)kind);
   if (tau < 1) return fail(CO2_ERR_VALIDATION, "simulate_timeline: tau must be >= 1");
   if (rounds < 1) return fail(CO2_ERR_VALIDATION, "simulate_timeline: rounds must be >= 1");
   if (batch_size < 1) return fail(CO2_ERR_VALIDATION, "simulate_timeline: batch_size must be >= 1");
+  if (!out) return fail(CO2_ERR_VALIDATION, "simulate_timeline: null output");
   double comm = 0.0;
   CO2_TRY(co2_allreduce_time(s, &comm));
   double now = 0.0, total_stall = 0.0, waited = 0.0, pending = 0.0;
+  bool has_pending = false;
   for (int t = 0; t < rounds; ++t) {
     co2_round_timing_t rt{t, now, 0.0, 0.0};
-    now += tau * s->t_comp;
-    double launched = now + comm;
-    if (t == 0) {
-      pending = launched;
-    } else {
-      double stall = std::max(0.0, pending - now);
-      now += stall;
-      rt.stall = stall;
-      total_stall += stall;
-      waited += comm;
-      pending = launched;
-      now += s->t_outer;
+    switch (kind) {
+      case CO2_ALG_CO2: {
+        now += tau * s->t_comp;
+        const double launched = now + comm;
+        if (t == 0) {  // the first round skips the outer update
+          pending = launched;
+          has_pending = true;
+          break;
+        }
+        const double stall = std::max(0.0, pending - now);
+        now += stall;
+        rt.stall = stall;
+        total_stall += stall;
+        waited += comm;
+        pending = launched;
+        now += s->t_outer;
+        break;
+      }
+      case CO2_ALG_SLOWMO:
+      case CO2_ALG_LOCAL_SGD:  // blocking reduce every round
+        now += tau * s->t_comp;
+        rt.stall = comm;
+        total_stall += comm;
+        waited += comm;
+        now += comm;
+        now += s->t_outer;
+        break;
+      case CO2_ALG_OVERLAP_LOCAL_SGD:
+        now += tau * s->t_comp;
+        if (has_pending) {
+          const double stall = std::max(0.0, pending - now);
+          now += stall;
+          rt.stall = stall;
+          total_stall += stall;
+          waited += comm;
+          has_pending = false;
+        }
+        if (comm > 0.0) {  // an instant reduce is consumed in its own round
+          pending = now + comm;
+          has_pending = true;
+        }
+        now += s->t_outer;
+        break;
+      default:  // CO2_ALG_SYNC_SGD: compute and reduce serialised per step
+        for (int k = 0; k < tau; ++k) {
+          now += s->t_comp;
+          rt.stall += comm;
+          total_stall += comm;
+          waited += comm;
+          now += comm;
+        }
+        break;
     }
     rt.end = now;
     if (per_round) per_round[t] = rt;
@@ -362,7 +407,25 @@ extern "C" co2_status_t co2_simulate_timeline_co2(const co2_cluster_t* s, int32_
   out->wall_time = now;
   out->total_stall = total_stall;
   out->overlap_ratio_achieved = waited > 0.0 ? 1.0 - total_stall / waited : 1.0;
-  double work = (double)rounds * tau * s->workers * batch_size;
+  const double work = (double)rounds * tau * s->workers * batch_size;
   out->throughput = now > 0.0 ? work / now : 0.0;
+  return CO2_OK;
+}
+
+extern "C" co2_status_t co2_simulate_timeline_co2(const co2_cluster_t* s, int32_t tau,
+                                                  int32_t rounds, int32_t batch_size,
+                                                  co2_timeline_t* out,
+                                                  co2_round_timing_t* per_round) {
+  return co2_simulate_timeline(CO2_ALG_CO2, s, tau, rounds, batch_size, out, per_round);
+}
+
+extern "C" co2_status_t co2_scalability_ratio(double throughput_small, double throughput_large,
+                                              double workers_small, double workers_large,
+                                              double* out) {
+  // scalability_ratio, timing_model.cpp:45-53
+  if (!(throughput_small > 0.0) || !(workers_small > 0.0) || !(workers_large > 0.0))
+    return fail(CO2_ERR_VALIDATION, "scalability_ratio: non-positive input");
+  if (!out) return fail(CO2_ERR_VALIDATION, "scalability_ratio: null output");
+  *out = (throughput_large / throughput_small) / (workers_large / workers_small);
   return CO2_OK;
 }

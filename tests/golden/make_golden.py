@@ -131,6 +131,35 @@ def main() -> None:
         {"_source": "proj/tests/test_timing_model.cpp:112-116", "workers": 2, "t_comp": 1.0,
          "comm": 0.0, "t_outer": 100.0, "tau": 2, "rounds": 1, "wall_time": 2.0},
     ]
+    # the other AlgorithmKind branches (proj/tests/test_timing_model.cpp:118-162)
+    must_contain("tests/test_timing_model.cpp",
+                 "doctest::Approx(3 * (2.0 + 3.0 + 0.5))", "r.total_stall == 9.0",
+                 "AlgorithmKind::overlap_local_sgd,\n                                       "
+                 "spec_with(2, 1.0, 3.0, 0.0), 2, 3", "doctest::Approx(2.0 / 3.0)",
+                 "spec_with(2, 1.0, 0.0, 0.0), 2, 4", "doctest::Approx(3 * 2 * (1.0 + 3.0))",
+                 "r.total_stall == 18.0", "doctest::Approx(12.0 / 24.0)",
+                 "spec_with(4, 1.0, 1.0, 0.0), 2, 3, 8", "doctest::Approx(8.0 * r1.throughput)",
+                 "scalability_ratio(100.0, 200.0, 2.0, 4.0) == 1.0",
+                 "scalability_ratio(100.0, 150.0, 1.0, 2.0) == 0.75")
+    kats["timeline_kinds"] = [
+        {"_source": "proj/tests/test_timing_model.cpp:118-126", "kind": k, "workers": 2,
+         "t_comp": 1.0, "comm": 3.0, "t_outer": 0.5, "tau": 2, "rounds": 3,
+         "wall_time": 3 * (2.0 + 3.0 + 0.5), "total_stall": 9.0, "overlap": 0.0}
+        for k in ("slowmo", "local_sgd")] + [
+        {"_source": "proj/tests/test_timing_model.cpp:128-137", "kind": "overlap_local_sgd",
+         "workers": 2, "t_comp": 1.0, "comm": 3.0, "t_outer": 0.0, "tau": 2, "rounds": 3,
+         "wall_time": 8.0, "total_stall": 2.0, "overlap": 2.0 / 3.0},
+        {"_source": "proj/tests/test_timing_model.cpp:139-145", "kind": "overlap_local_sgd",
+         "workers": 2, "t_comp": 1.0, "comm": 0.0, "t_outer": 0.0, "tau": 2, "rounds": 4,
+         "wall_time": 8.0, "total_stall": 0.0, "overlap": 1.0},
+        {"_source": "proj/tests/test_timing_model.cpp:147-154", "kind": "sync_sgd",
+         "workers": 2, "t_comp": 1.0, "comm": 3.0, "t_outer": 0.0, "tau": 2, "rounds": 3,
+         "wall_time": 3 * 2 * (1.0 + 3.0), "total_stall": 18.0, "overlap": 0.0,
+         "throughput": 12.0 / 24.0},
+    ]
+    kats["scalability_ratio"] = {"_source": "proj/tests/test_timing_model.cpp:73-77",
+                                 "cases": [[100.0, 200.0, 2.0, 4.0, 1.0],
+                                           [100.0, 150.0, 1.0, 2.0, 0.75]]}
     kats["allreduce_time"] = {"_source": "proj/tests/test_timing_model.cpp:23-34",
                               "workers": 4, "latency": 0.001, "param_bytes": 1e9,
                               "bandwidth": 1e9, "expected": 1.506,

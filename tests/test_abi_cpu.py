@@ -167,6 +167,33 @@ def test_co2_timeline_hand_traces(golden):
         co2.simulate_timeline_co2(co2.ClusterSpec(workers=2, measured_override=1.0), 2, 0)
 
 
+def test_timeline_every_algorithm_kind(golden):
+    """simulate_timeline's slowmo / local_sgd / overlap_local_sgd / sync_sgd
+    branches against the reference's hand traces
+    (proj/tests/test_timing_model.cpp:118-162), and scalability_ratio."""
+    for k in golden["timeline_kinds"]:
+        spec = co2.ClusterSpec(workers=k["workers"], t_comp=k["t_comp"], t_outer=k["t_outer"],
+                               measured_override=k["comm"])
+        r = co2.simulate_timeline(k["kind"], spec, k["tau"], k["rounds"])
+        assert r.wall_time == pytest.approx(k["wall_time"]) and r.total_stall == k["total_stall"]
+        assert r.overlap_ratio_achieved == pytest.approx(k["overlap"])
+        if "throughput" in k:
+            assert r.throughput == pytest.approx(k["throughput"])
+    spec = co2.ClusterSpec(workers=4, t_comp=1.0, t_outer=0.0, measured_override=1.0)
+    r1 = co2.simulate_timeline("local_sgd", spec, 2, 3, 1)
+    r8 = co2.simulate_timeline("local_sgd", spec, 2, 3, 8)
+    assert r8.throughput == pytest.approx(8.0 * r1.throughput)
+    # the co2 kind through the general entry equals the co2-only entry
+    s2 = co2.ClusterSpec(workers=2, t_comp=1.0, t_outer=0.5, measured_override=3.0)
+    assert co2.simulate_timeline("co2", s2, 2, 3) == co2.simulate_timeline_co2(s2, 2, 3)
+    for a, b, c, d, e in golden["scalability_ratio"]["cases"]:
+        assert co2.scalability_ratio(a, b, c, d) == e
+    with pytest.raises(co2.ValidationError, match="scalability_ratio: non-positive input"):
+        co2.scalability_ratio(0.0, 1.0, 1.0, 2.0)
+    with pytest.raises(co2.ValidationError, match="unknown algorithm"):
+        co2.simulate_timeline("diloco", s2, 2, 3)
+
+
 def test_overlap_flatness_acceptance():
     """proj/tests/acceptance.cpp:88-116 (co2 half): with tau*t_comp >= t_comm
     the one-round-stale pattern has zero stall and flat throughput."""
