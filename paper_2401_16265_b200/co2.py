@@ -379,6 +379,18 @@ class TimelineReport:
     overlap_ratio_achieved: float
     throughput: float
     per_round: list = field(default_factory=list)
+    algorithm: str = "co2"
+
+    def to_json(self) -> dict:
+        """to_json(TimelineReport) (proj/src/timing_model.cpp:55-74)."""
+        return {"algorithm": self.algorithm, "workers": self.workers, "tau": self.tau,
+                "rounds": self.rounds, "batch_size": self.batch_size,
+                "comm_time": self.comm_time, "wall_time": self.wall_time,
+                "total_stall": self.total_stall,
+                "overlap_ratio_achieved": self.overlap_ratio_achieved,
+                "throughput": self.throughput,
+                "per_round": [{"t": t, "start": a, "stall": b, "end": e}
+                              for t, a, b, e in self.per_round]}
 
 
 ALGORITHMS = {"co2": L.ALG_CO2, "slowmo": L.ALG_SLOWMO, "local_sgd": L.ALG_LOCAL_SGD,
@@ -405,7 +417,7 @@ def simulate_timeline(kind: str, spec: ClusterSpec, tau: int, rounds: int,
                           out.wall_time, out.total_stall, out.overlap_ratio_achieved,
                           out.throughput,
                           [(per[i].t, per[i].start, per[i].stall, per[i].end)
-                           for i in range(rounds)])
+                           for i in range(rounds)], kind)
 
 
 def scalability_ratio(throughput_small: float, throughput_large: float, workers_small: float,

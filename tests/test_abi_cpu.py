@@ -192,6 +192,11 @@ def test_timeline_every_algorithm_kind(golden):
         co2.scalability_ratio(0.0, 1.0, 1.0, 2.0)
     with pytest.raises(co2.ValidationError, match="unknown algorithm"):
         co2.simulate_timeline("diloco", s2, 2, 3)
+    # to_json (test_timing_model.cpp:164-175)
+    j = co2.simulate_timeline("co2", s2, 2, 3).to_json()
+    assert j["algorithm"] == "co2" and j["workers"] == 2 and j["tau"] == 2
+    assert j["wall_time"] == 8.0 and j["total_stall"] == 1.0
+    assert len(j["per_round"]) == 3 and j["per_round"][1]["stall"] == 1.0
 
 
 def test_overlap_flatness_acceptance():
