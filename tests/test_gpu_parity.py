@@ -515,3 +515,48 @@ def test_global_clip_errors():
         co2.outer_step_global_clip(mode, x, p0, p1, xe, m, hyper(12), 12)
     with pytest.raises(co2.ValidationError, match="hyper: phi must be positive"):
         co2.outer_step_global_clip(mode, x, p0, p1, xe, m, co2.Co2Hyper(phi=0.0), 12)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_fused_step_property_vs_oracle(mode):
+    """hypothesis: arbitrary finite inputs in the mode's storage type (any
+    magnitudes, signed zeros, subnormals, epsilon floor, clip boundaries) and
+    any hyper -- the GPU step equals the oracle bit for bit, or raises the
+    oracle's exact error."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+    big = 1e150 if mode == co2.MODE_F64 else float(np.float32(1e30))
+    w = 64 if mode == co2.MODE_F64 else 32
+    fin = st.floats(allow_nan=False, allow_infinity=False, width=w, min_value=-big, max_value=big)
+
+    @settings(max_examples=150, deadline=None, derandomize=True)
+    @given(vals=st.lists(st.tuples(fin, fin, fin, fin, fin), min_size=1, max_size=40),
+           alpha=st.floats(1e-3, 4.0), beta=st.floats(0.0, 0.999), phi=st.floats(1e-9, 1e3),
+           eps=st.sampled_from([1e-12, 1e-30, 1.0]), tau=st.integers(1, 64),
+           penalty=st.booleans(), clip=st.booleans())
+    def check(vals, alpha, beta, phi, eps, tau, penalty, clip):
+        st_dt = np.float64 if mode == co2.MODE_F64 else np.float32
+        x, p0, p1, xb, m = (np.array(c, dtype=st_dt) for c in zip(*vals))
+        if mode == co2.MODE_BF16_MIXED:
+            p1, xb = O.f32_to_bf16_bits(p1), O.f32_to_bf16_bits(xb)
+        oh = O.hyper(alpha=alpha, beta=beta, phi=phi, epsilon=eps, tau=tau, penalty=penalty,
+                     clip=clip)
+        ref = O.outer_step(mode, x, p0, p1, xb, m, oh)
+        h = co2.Co2Hyper(alpha=alpha, beta=beta, phi=phi, epsilon=eps, penalty=penalty,
+                         clip=clip)
+        dx, dp0, dp1, dxb, dm = (to_dev(a) for a in (x, p0, p1, xb, m))
+        anchor, params, gap = torch.empty_like(dx), torch.empty_like(dxb), torch.empty_like(dx)
+        if ref.status != 0:
+            with pytest.raises((co2.NumericError, co2.ValidationError)) as ei:
+                co2.outer_step(mode, dx, dp0, dp1, dxb, dm, h, tau, anchor_out=anchor,
+                               params_out=params, gap_out=gap)
+            assert str(ei.value) == ref.message
+            return
+        d = co2.outer_step(mode, dx, dp0, dp1, dxb, dm, h, tau, anchor_out=anchor,
+                           params_out=params, gap_out=gap)
+        assert same(to_np(dm), ref.m) and same(to_np(anchor), ref.anchor)
+        assert same(to_np(params), ref.params) and same(to_np(gap), ref.gap)
+        assert (d.min_gap, d.max_outer_step, d.n_clipped, d.n_floored) == (
+            ref.diag.min_gap, ref.diag.max_outer_step, ref.diag.n_clipped, ref.diag.n_floored)
+
+    check()
