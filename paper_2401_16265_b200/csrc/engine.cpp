@@ -106,7 +106,13 @@ struct co2_aar {
 static co2_status_t engine_common_init(co2_aar* e) {
   int lo = 0, hi = 0;
   CO2_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  CO2_CUDA(cudaStreamCreateWithPriority(&e->comm_stream, cudaStreamNonBlocking, hi));
+  // The comm stream runs at the highest priority so the reduce's CTAs are
+  // scheduled ahead of queued step CTAs.  CO2_COMM_PRIORITY=low inverts it:
+  // the reduce then starves behind the 32-wave step grid and 28-37 % of it
+  // is exposed (profiles/r01/bench/comm_priority.txt).
+  const char* pr = getenv("CO2_COMM_PRIORITY");
+  const int prio = (pr && strcmp(pr, "low") == 0) ? lo : hi;
+  CO2_CUDA(cudaStreamCreateWithPriority(&e->comm_stream, cudaStreamNonBlocking, prio));
   CO2_CUDA(cudaEventCreate(&e->epoch));
   CO2_CUDA(cudaEventRecord(e->epoch, e->comm_stream));
   CO2_CUDA(cudaMalloc(&e->ws, co2_workspace_bytes()));
