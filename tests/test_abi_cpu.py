@@ -231,3 +231,41 @@ def test_product_does_not_reference_oracle():
                     assert needle not in src, (fn, needle)
     out = subprocess.run(["ldd", L.LIB_PATH], capture_output=True, text=True).stdout
     assert "oracle" not in out
+
+
+def test_timeline_invariants_property():
+    """hypothesis over simulate_timeline (timing_model.cpp:76-173): for every
+    algorithm the wall time covers the compute, stalls never exceed the
+    reduce, co2's stall is the uncovered remainder of the previous reduce,
+    and the achieved overlap lies in [0, 1]."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    pos = st.floats(0.0, 100.0, allow_nan=False)
+
+    @settings(max_examples=300, deadline=None, derandomize=True)
+    @given(kind=st.sampled_from(sorted(co2.ALGORITHMS)), workers=st.integers(1, 64),
+           t_comp=pos, comm=pos, t_outer=pos, tau=st.integers(1, 48), rounds=st.integers(1, 12),
+           batch=st.integers(1, 16))
+    def check(kind, workers, t_comp, comm, t_outer, tau, rounds, batch):
+        spec = co2.ClusterSpec(workers=workers, t_comp=t_comp, t_outer=t_outer,
+                               measured_override=comm)
+        r = co2.simulate_timeline(kind, spec, tau, rounds, batch)
+        c = r.comm_time
+        assert len(r.per_round) == rounds
+        assert r.wall_time >= rounds * tau * t_comp * (1 - 1e-12)
+        assert 0.0 <= r.overlap_ratio_achieved <= 1.0
+        prev_end = 0.0
+        for t, start, stall, end in r.per_round:
+            assert start == prev_end and end >= start and stall >= 0.0
+            assert stall <= (tau if kind == "sync_sgd" else 1) * c * (1 + 1e-12)
+            prev_end = end
+        assert r.wall_time == prev_end
+        if kind == "co2":
+            assert r.per_round[0][2] == 0.0  # round 0 never stalls
+            if tau * t_comp >= c:  # the local steps alone hide the reduce
+                assert r.total_stall <= 1e-9 * max(r.wall_time, 1.0)
+        if kind in ("slowmo", "local_sgd"):
+            assert r.total_stall == pytest.approx(rounds * c)
+
+    check()
