@@ -44,6 +44,10 @@ CONFIGS = {
                        "needs >= 2 GPUs",
            "mode": 2, "n": 7_000_000_000, "tau": 12, "bytes_per_param": 30, "sharded": True,
            "storage": "bf16 params/x_{t,1} (replicated) + fp32 shard state"},
+    "c1": {"workload": "C1: 1M-param fp32 flat vector, 4 simulated CO2 workers on one GPU, "
+                       "tau=4 (BASELINE.json configs[0], the reference's CPU fixture scale)",
+           "mode": 1, "n": 1 << 20, "tau": 4, "bytes_per_param": 32, "local_workers": 4,
+           "storage": "fp32"},
     "c4shard": {"workload": "C4 shard on one GPU: 7B/8 = 875M-param bf16-mixed shard, "
                             "worker-local step",
                 "mode": 2, "n": 875_000_000, "tau": 12, "bytes_per_param": 26,
@@ -290,6 +294,60 @@ def run_reference_arm(args, cfg, rank: int):
 
 
 # ----------------------------------------------------------------- GPU arm
+def run_local_workers(args, cfg) -> int:
+    """C1: G simulated workers on one GPU through the LOCAL engine (the
+    fixed-order average kernel + G fused steps per co2_round).  The buffers
+    (G x 1M fp32 x ~7 streams) are L2-resident, so this is a launch- and
+    cache-bound number, not an HBM roofline one."""
+    import torch
+
+    from paper_2401_16265_b200 import co2
+    mode, n, tau, g = cfg["mode"], cfg["n"], cfg["tau"], cfg["local_workers"]
+    hyper = co2.Co2Hyper(**HYPER)
+    eng = co2.CollectiveEngine(g, transport="local")
+    ws = [co2.Worker(mode, n, co2.synth_params(mode, n, worker=i), keep_gap=False)
+          for i in range(g)]
+    for w in ws:
+        w.snapshot_start()
+        w.snapshot_first()
+    co2.co2_round(ws, eng, hyper, tau)  # round 0
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        co2.co2_round(ws, eng, hyper, tau, sync=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch, torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            co2.co2_round(ws, eng, hyper, tau, sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    r = co2.L.RoundResult()
+    arr = (co2.C.c_void_p * g)(*[w.handle.value for w in ws])
+    co2.check(co2.lib().co2_round_finish(arr, g, stream.cuda_stream, co2.C.byref(r)))
+    value = g * n * args.steps / t
+    line = {
+        "metric": "CO2 outer-step params/s", "value": value, "unit": "params/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-SplitMix64 uniforms, SURVEY.md 8d)",
+        "config": {"workload": cfg["workload"], "n_params_per_worker": n, "workers": g,
+                   "tau": tau, "hyper": HYPER,
+                   "l2": "L2-resident working set: a launch/cache-bound number, not HBM",
+                   "step": "co2_round over 4 simulated workers: fixed-order average kernel + "
+                           "4 fused outer steps"},
+        "roofline": None, "e2e": None, "cpu_baseline": None,
+        "gpu_launches": args.steps * (g + 1), "clocks": clk.summary(),
+        "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step},
+    }
+    print(json.dumps(line), flush=True)
+    for w in ws:
+        w.close()
+    eng.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -326,6 +384,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference_arm(args, cfg, rank)
+    if cfg.get("local_workers"):
+        if world > 1:
+            raise SystemExit("--config c1 runs simulated workers on one GPU")
+        import torch
+        torch.cuda.set_device(local)
+        return run_local_workers(args, cfg)
 
     import torch
     import torch.distributed as dist
