@@ -12,6 +12,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libco2b200.so")
 
+ABI_VERSION = 2
 OK, ERR_VALIDATION, ERR_NUMERIC, ERR_CUDA, ERR_NCCL = 0, 2, 3, 4, 5
 MODE_F64, MODE_F32, MODE_BF16_MIXED = 0, 1, 2
 DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
@@ -203,7 +204,7 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.co2_abi_version() != 2:
+        if L.co2_abi_version() != ABI_VERSION:
             raise ImportError("libco2b200.so ABI version mismatch")
         _lib = L
     return _lib

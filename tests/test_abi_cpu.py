@@ -269,3 +269,23 @@ def test_timeline_invariants_property():
             assert r.total_stall == pytest.approx(rounds * c)
 
     check()
+
+
+def test_header_constants_match_the_python_binding():
+    """Every CO2_* constant of include/co2_b200.h (status codes, modes,
+    dtypes, flags, buffers, algorithms, clip modes, record sizes, ABI
+    version) has the same value in the ctypes binding."""
+    import re
+    text = open(os.path.join(ROOT, "include", "co2_b200.h")).read()
+    consts = {m.group(1): int(m.group(2))
+              for m in re.finditer(r"\b(CO2_[A-Z0-9_]+)\s*=\s*(\d+)u?\b", text)}
+    consts.update({m.group(1): int(m.group(2))
+                   for m in re.finditer(r"#define\s+(CO2_[A-Z0-9_]+)\s+(\d+)", text)})
+    assert len(consts) > 40
+    for name, value in consts.items():
+        py = name[len("CO2_"):]
+        if name in ("CO2_OK",):
+            py = "OK"
+        assert hasattr(L, py), f"{name} missing from _lib.py"
+        assert getattr(L, py) == value, (name, getattr(L, py), value)
+    assert L.lib().co2_abi_version() == consts["CO2_ABI_VERSION"]
