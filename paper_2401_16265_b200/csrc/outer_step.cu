@@ -6,8 +6,9 @@
 // bf16-mixed, 64 B in fp64 (versus ~264 B/param in the reference's unfused
 // fp64 passes, outer_algorithms.cpp:48-108).  Streams are 128-bit
 // coalesced with evict-first cache hints, U independent vectors per thread
-// are in flight before any arithmetic, and the grid is sized to the resident
-// CTA count of the 148 SMs (grid-stride persistent loop).
+// are in flight before any arithmetic, and the grid-stride loop runs on a
+// grid of up to 32 waves of the 148 SMs' resident CTAs (grid_for below), so
+// the block scheduler balances the tail and any co-running reduce kernel.
 //
 // Bit-exactness: built with --fmad=false and IEEE division, every element op
 // below is exactly one IEEE op in the reference's order, so the F64 mode is
