@@ -399,6 +399,16 @@ def test_host_e2e_entry_equals_device_path():
         assert d.max_outer_step == ref.diag.max_outer_step
 
 
+def test_cpp_round_driver_binary():
+    """A C++ co2_round loop over the plain C ABI (tests/cpp/round_example.cpp)."""
+    exe = os.path.join(ROOT, "build", "round_example")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", ROOT, "round_example"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ROUNDS OK" in r.stdout
+
+
 def test_cpp_facade_binary():
     exe = os.path.join(ROOT, "build", "facade_test")
     if not os.path.exists(exe):
