@@ -133,6 +133,7 @@ static int gap_f64_range(int64_t n, const double* x_t0, const double* p0, const 
   return orc_ensure_finite_f64(n, gap, "staleness_gap");
 }
 
+/* staleness_gap, proj/src/outer_algorithms.cpp:48-64 */
 int orc_staleness_gap_f64(int64_t n, const double* x_t0, const double* p0,
                           const double* p1, int tau, double epsilon, double* gap) {
   if (tau < 1) return fail(ORC_VALIDATION, "staleness_gap: tau must be >= 1");
@@ -152,6 +153,7 @@ static int momentum_f64_range(int64_t n, const double* m_prev, double beta, cons
   return orc_ensure_finite_f64(n, m, "momentum update");
 }
 
+/* penalized_momentum_update, proj/src/outer_algorithms.cpp:66-90 */
 int orc_penalized_momentum_f64(int64_t n, const double* m_prev, double beta,
                                const double* gap, const double* delta, int penalty,
                                double* m) {
@@ -177,6 +179,8 @@ static int iterate_f64_range(int64_t n, const double* x_t0, double alpha, const 
   return orc_ensure_finite_f64(n, x, "outer_iterate");
 }
 
+/* outer_iterate, proj/src/outer_algorithms.cpp:92-108 (clip through
+ * clip_elementwise, proj/src/param_ops.cpp:35-43) */
 int orc_outer_iterate_f64(int64_t n, const double* x_t0, double alpha, const double* m,
                           double phi, int clip, double* x) {
   if (!(alpha > 0.0)) return fail(ORC_VALIDATION, "outer_iterate: alpha must be positive");
@@ -239,6 +243,8 @@ static void* step_range(void* arg) {
   return NULL;
 }
 
+/* co2_round's per-worker body, proj/src/outer_algorithms.cpp:186-202, with
+ * the reference's unfused passes and temporaries */
 int orc_worker_step_f64(int64_t n, const double* x_t0, const double* p0, const double* p1,
                         const double* avg, double* m_inout, const orc_hyper* h, double* next,
                         double* gap_out, double* min_gap, double* max_step, int threads) {
@@ -338,6 +344,9 @@ int orc_worker_step_f64(int64_t n, const double* x_t0, const double* p0, const d
     if (st > max_step) max_step = (double)st;                                      \
   }
 
+/* The fused same-op-order restatement of proj/src/outer_algorithms.cpp:
+ * 186-196 (SURVEY.md 8a "Fused per-element semantics") in the GPU's storage
+ * and compute types */
 int orc_outer_step(int mode, int64_t n, const void* x_t0v, const void* p0v, const void* p1v,
                    const void* xbarv, int divisor, void* mv, void* anchorv, void* paramsv,
                    void* gapv, const orc_hyper* h, orc_diag* diag) {
@@ -891,6 +900,8 @@ static double store_low(int mode, void* p, int64_t i, double v) {
 
 static double round_state(int mode, double v) { return mode == ORC_MODE_F64 ? v : (double)(float)v; }
 
+/* SURVEY.md 8d synthetic inputs on the RngStream generator
+ * (proj/include/co2sim/rng.hpp:14-25), random-access form */
 void orc_synth(int mode, uint64_t seed, int worker, int64_t j0, int64_t count, void* x_t0,
                void* p0, void* p1, void* x_end, void* m) {
   for (int64_t i = 0; i < count; ++i) {
