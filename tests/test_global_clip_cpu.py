@@ -79,3 +79,33 @@ def test_product_chunk_formula_matches_oracle():
     for mode, v in ((0, 2), (1, 4), (2, 8)):
         for n in (0, 1, 7, 8191, 100003, 3_000_001, 1_300_000_000, 7_000_000_000):
             assert lib.co2_global_clip_chunk(mode, n) == O.gc_chunk(n, v)
+
+
+def test_global_clip_property():
+    """hypothesis: for arbitrary finite fp64 inputs the global-clip oracle's
+    m' equals the reference-order step's, its norm is the fp64 norm of m'
+    to rounding, and the update is x_t0 - alpha * m' * min(1, phi/norm)."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+    fin = st.floats(allow_nan=False, allow_infinity=False, width=64, min_value=-1e100,
+                    max_value=1e100)
+
+    @settings(max_examples=200, deadline=None, derandomize=True)
+    @given(vals=st.lists(st.tuples(fin, fin, fin, fin, fin), min_size=1, max_size=3000),
+           alpha=st.floats(1e-3, 4.0), beta=st.floats(0.0, 0.999), phi=st.floats(1e-9, 1e3))
+    def check(vals, alpha, beta, phi):
+        x, p0, p1, xb, m = (np.array(c, dtype=np.float64) for c in zip(*vals))
+        h = O.hyper(alpha=alpha, beta=beta, phi=phi, epsilon=1e-12, tau=4)
+        r, norm = O.outer_step_global_clip(O.MODE_F64, x, p0, p1, xb, m, h)
+        ref = O.outer_step(O.MODE_F64, x, p0, p1, xb, m,
+                           O.hyper(alpha=alpha, beta=beta, phi=phi, epsilon=1e-12, tau=4,
+                                   clip=False))
+        if ref.status != 0 or r.status != 0:
+            return  # overflow / non-finite paths are covered by the error tests
+        assert r.m.tobytes() == ref.m.tobytes()
+        exact = float(np.sqrt(np.sum(r.m * r.m)))
+        assert norm == pytest.approx(exact, rel=1e-13, abs=0.0)
+        sc = phi / norm if norm > phi else 1.0
+        assert r.params.tobytes() == (x - alpha * (r.m * sc)).tobytes()
+
+    check()
