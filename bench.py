@@ -265,11 +265,18 @@ def time_cpu_fused_bound(cfg, n_sample: int, threads: int, reps: int = 3) -> dic
 
 
 def run_reference_arm(args, cfg, rank: int):
+    """The reference's CPU path on this host: the fp64 restatement of
+    co2_round's per-worker body with the reference's unfused passes and fresh
+    temporaries, on ONE thread -- the reference is single-threaded (Eigen
+    cwise ops, no OpenMP or threads).
+    The same passes split over every host core are reported separately as
+    `cpu_parallel_bound` (not the reference)."""
     if rank != 0:
         return 0
     cores = host_cores()
     n_sample = args.ref_sample
-    value, t = time_cpu_step(cfg, n_sample, cores, max(args.steps, 1), max(args.warmup, 0))
+    value, t = time_cpu_step(cfg, n_sample, 1, max(args.steps, 1), max(args.warmup, 0))
+    pv, pt = time_cpu_step(cfg, n_sample, cores, 3, 1)
     line = {
         "impl": "reference", "metric": "CO2 outer-step params/s", "value": value,
         "unit": "params/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -277,15 +284,19 @@ def run_reference_arm(args, cfg, rank: int):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "n_params_per_worker": cfg["n"],
                    "tau": cfg["tau"], "sample_params": n_sample},
-        "cpu_baseline": {"value": value, "unit": "params/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "params/s", "cores": 1, "kind": "port",
                          "sample": f"{n_sample} coordinates of the {cfg['n']}-param workload, "
-                                   "fp64 upcast, reference unfused passes, coordinate ranges "
-                                   f"split over {cores} threads"},
+                                   "fp64 upcast, reference unfused passes and fresh "
+                                   "temporaries, 1 thread (the reference is single-threaded)"},
         "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "note": "Reference (C++20/Eigen) is not buildable here (Eigen absent); this arm times "
                 "oracle/co2_oracle.c, a bit-exact restatement pinned by the reference's fixtures.",
         "cpu_aar": time_cpu_average(min(n_sample, 1 << 24)),
+        "cpu_parallel_bound": {"value": pv, "unit": "params/s", "cores": cores,
+                               "ms_per_step": pt * 1e3,
+                               "kind": "NOT the reference: the same unfused fp64 passes split "
+                                       f"over {cores} host threads (coordinate ranges)"},
         "cpu_fused_bound": time_cpu_fused_bound(cfg, n_sample, cores),
         "host": host_info(),
     }
@@ -330,7 +341,9 @@ def run_local_workers(args, cfg) -> int:
     line = {
         "metric": "CO2 outer-step params/s", "value": value, "unit": "params/s", "n_gpus": 1,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": {0: "f64", 1: "f32", 2: "bf16-mixed"}[mode],
+            "compute_dtype": "f64" if mode == 0 else "f32",
         "data": "synthetic (counter-SplitMix64 uniforms, SURVEY.md 8d)",
         "config": {"workload": cfg["workload"], "n_params_per_worker": n, "workers": g,
                    "tau": tau, "hyper": HYPER,
@@ -360,7 +373,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26,
                     help="coordinates in the 1-core CPU baseline sample (~10 s of CPU work)")
-    ap.add_argument("--ref-sample", type=int, default=1 << 25)
+    ap.add_argument("--ref-sample", type=int, default=1 << 24,
+                    help="coordinates per reference-arm step (1 thread, ~0.6 s per step)")
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--schedule", default="split", choices=["split", "fused"],
                     help="P2P worker-local rounds: 'split' = reduce kernel on the comm stream "
@@ -580,7 +594,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-            "dtype": "f32" if mode != 0 else "f64",
+            "dtype": {0: "f64", 1: "f32", 2: "bf16-mixed"}[mode],
+            "compute_dtype": "f64" if mode == 0 else "f32",
             "data": "synthetic (counter-SplitMix64 uniforms, SURVEY.md 8d)",
             "config": {"workload": cfg["workload"],
                        "n_params_per_gpu": per_rank, "n_params_total": units, "tau": tau,

@@ -1616,8 +1616,6 @@ extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int
   const co2_mode_t mode = w0->mode;
   const int64_t n = w0->n;
   const size_t lb = low_bytes(mode) * n;
-  // Per-worker max |params' - x_end| accumulates over this round's corrections.
-  std::vector<double> step(g, 0.0);
   bool applied = false;
   auto correct = [&](const void* xbar, int32_t div) -> co2_status_t {
     for (int i = 0; i < g; ++i) {
@@ -1678,7 +1676,6 @@ extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int
       ws[i]->host_diag->n_clipped = ws[i]->host_diag->n_floored = 0;
     }
   }
-  (void)step;
   co2_round_result_t r{};
   r.outer_applied = 1;  // :309 -- every overlap round counts as an outer update
   CO2_TRY(finish_round(ws, g, st, sync, &r));

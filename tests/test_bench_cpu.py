@@ -27,7 +27,9 @@ def test_reference_arm_line():
     assert d["metric"] == "CO2 outer-step params/s" and d["steps"] == 2 and d["warmup"] == 1
     assert d["value"] > 0 and d["n_gpus"] == 1
     cb = d["cpu_baseline"]
-    assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
+    # the reference is single-threaded: the arm runs on 1 thread
+    assert cb["kind"] in ("port", "reference") and cb["cores"] == 1 and cb["value"] == d["value"]
+    assert d["cpu_parallel_bound"]["value"] > 0 and "NOT the reference" in d["cpu_parallel_bound"]["kind"]
     assert d["e2e"] == {"value": d["value"], "unit": "params/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("C3")
