@@ -29,7 +29,8 @@
 extern "C" {
 #endif
 
-#define CO2_ABI_VERSION 2  /* 2: 72-byte IPC export records (handle + offset) */
+#define CO2_ABI_VERSION 3  /* 2: 72-byte IPC export records (handle + offset);
+                              3: HandleInfo audit fields, NCCL algorithm, xbar capture */
 
 typedef int32_t co2_status_t;
 enum {
@@ -298,8 +299,14 @@ co2_status_t co2_scalability_ratio(double throughput_small, double throughput_la
  * wait on its completion event.  At most two handles are live (the
  * reference's overlap window, collective.cpp:39-42).
  * Transports:
- *   NCCL  one rank per GPU; in-place ncclAllReduce(sum) of the buffer; the
- *         consumer divides by world size (co2_outer_step xbar_divisor).
+ *   NCCL  one rank per GPU, in place.  Default algorithm CO2_NCCL_FIXED_ORDER:
+ *         grouped ncclSend/ncclRecv slice exchange, the fixed-order average
+ *         kernel on this rank's slice (ascending rank order, one division:
+ *         average(), param_ops.cpp:16-33), grouped send/recv all-gather --
+ *         the reference's average bit for bit at any world size, with a
+ *         ring all-reduce's NVLink volume; the consumer uses divisor 1.
+ *         CO2_NCCL_SUM: ncclAllReduce(sum) in the storage dtype (order and
+ *         per-hop rounding are NCCL's), the consumer divides by world size.
  *   LOCAL G simulated workers on one GPU; fixed-order average kernel of the
  *         G contribution buffers into `out` (bitwise the reference average).
  */
@@ -309,6 +316,10 @@ co2_status_t co2_nccl_unique_id(uint8_t id_out[CO2_NCCL_ID_BYTES]);
 co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO2_NCCL_ID_BYTES],
                                  int32_t rank, int32_t world, int32_t max_ctas);
 co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers);
+/* NCCL engines only; not while reduces are live.  Worker-local and sharded
+ * rounds pick the matching consumer divisor themselves. */
+enum { CO2_NCCL_FIXED_ORDER = 0, CO2_NCCL_SUM = 1 };
+co2_status_t co2_aar_set_nccl_algo(co2_aar_t* engine, int32_t algo);
 /* P2P transport: a deterministic fixed-order average
  * over NVLink peer memory.  Rank r reduces slice r from every rank's buffer
  * in ascending rank order, divides by G once (average(), param_ops.cpp:16-33)
@@ -367,6 +378,10 @@ typedef struct co2_handle_info {
   uint64_t id;
   double launch_time, completion_time, stall, comm;
   int32_t completed, consumed;
+  int32_t contributions;     /* worker contributions reduced (HandleInfo::contributions) */
+  int32_t polled;            /* co2_aar_poll was called at least once */
+  int32_t last_poll;         /* result of the most recent poll */
+  int32_t completion_logged; /* a poll (or the wait) observed completion */
 } co2_handle_info_t;
 co2_status_t co2_aar_info(co2_aar_t* engine, uint64_t handle, co2_handle_info_t* out);
 /* total_stall() and handle_count() (collective.hpp:64-67): the stall summed
@@ -412,6 +427,12 @@ co2_status_t co2_worker_destroy(co2_worker_t* w);
 void* co2_worker_buffer(co2_worker_t* w, int32_t which);
 co2_status_t co2_worker_set_clip_mode(co2_worker_t* worker, int32_t clip_mode);
 int32_t co2_worker_round(const co2_worker_t* w);
+/* RoundResult::consumed_average (outer_algorithms.hpp:68, outer_algorithms.cpp:
+ * 159) on the in-place transports: when on, every co2_round step also writes
+ * the reduce it consumed (low dtype; the average, also under CO2_NCCL_SUM)
+ * into a worker-owned buffer returned by co2_worker_buffer(CO2_BUF_XBAR).
+ * Costs one low-dtype write per coordinate.  LOCAL always keeps it. */
+co2_status_t co2_worker_keep_average(co2_worker_t* w, int32_t on);
 /* Snapshot hooks: x_{t,0} <- params (call before the first inner step;
  * a no-op for t >= 1 where the outer step already wrote the anchor), and
  * x_{t,1} <- params (call after the first inner step). */

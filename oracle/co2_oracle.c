@@ -316,10 +316,13 @@ int orc_worker_step_f64(int64_t n, const double* x_t0, const double* p0, const d
  * reference's element-wise passes for one coordinate, no FMA:
  *   n0 = |x_t0 - p0|; d = max(|tau*(p1 - p0)|, eps); L = n0/d + 1
  *   D = p0 - xbar; m' = beta*m + D/L  (or beta*m + D)
- *   c = min(max(m', -phi), phi)       (or m');  x' = x_t0 - alpha*c */
+ *   c = min(max(m', -phi), phi)       (or m');  x' = x_t0 - alpha*c
+ * q0s is the point the inner loop started from: q0 itself in fp64 / fp32, and
+ * bf16(q0) in bf16-mixed, where the inner loop runs on the bf16 rounding of
+ * the fp32 anchor (the GPU's start_of_inner, csrc/outer_step.cu). */
 #define FUSED_BODY(T, ABS, ISFIN, MAXF, MINF)                                      \
   T n0 = ABS(x - q0);                                                              \
-  T a = ABS(tf * (q1 - q0));                                                       \
+  T a = ABS(tf * (q1 - q0s));                                                      \
   int floored = a < epsf;                                                          \
   T d = MAXF(a, epsf);                                                             \
   T lam = n0 / d + (T)1;                                                           \
@@ -364,6 +367,7 @@ int orc_outer_step(int mode, int64_t n, const void* x_t0v, const void* p0v, cons
            alphaf = h->alpha, gd = (double)divisor;
     for (int64_t j = 0; j < n; ++j) {
       double x = X[j], q0 = P0[j], q1 = P1[j], mo = M[j];
+      double q0s = q0;
       double xb = divisor > 1 ? XB[j] / gd : XB[j];
       FUSED_BODY(double, fabs, isfinite, max_std, min_std)
       M[j] = mn;
@@ -382,6 +386,7 @@ int orc_outer_step(int mode, int64_t n, const void* x_t0v, const void* p0v, cons
       float q1 = bf ? orc_bf16_to_f32(((const uint16_t*)p1v)[j]) : ((const float*)p1v)[j];
       float xb = bf ? orc_bf16_to_f32(((const uint16_t*)xbarv)[j]) : ((const float*)xbarv)[j];
       if (divisor > 1) xb = xb / gd;
+      float q0s = bf ? orc_bf16_to_f32(orc_f32_to_bf16(q0)) : q0;
       FUSED_BODY(float, fabsf, isfinite, max_stdf, min_stdf)
       M[j] = mn;
       if (A) A[j] = xn;
@@ -435,6 +440,7 @@ int orc_outer_step_ghost(int mode, int64_t n, const void* anchorv, const void* p
         x = sum / (double)ghost;
       }
       double q0 = P0[j], q1 = P1[j], mo = M[j];
+      double q0s = q0;
       if (p1_div > 1) q1 = q1 / (double)p1_div;
       FUSED_BODY(double, fabs, isfinite, max_std, min_std)
       M[j] = mn;
@@ -463,6 +469,7 @@ int orc_outer_step_ghost(int mode, int64_t n, const void* anchorv, const void* p
       float q0 = P0[j], mo = M[j];
       float q1 = bf ? orc_bf16_to_f32(((const uint16_t*)p1v)[j]) : ((const float*)p1v)[j];
       if (p1_div > 1) q1 = q1 / (float)p1_div;
+      float q0s = bf ? orc_bf16_to_f32(orc_f32_to_bf16(q0)) : q0;
       FUSED_BODY(float, fabsf, isfinite, max_stdf, min_stdf)
       M[j] = mn;
       if (B0) B0[j] = x;
@@ -574,7 +581,8 @@ int orc_outer_step_global_clip(int mode, int64_t n, const void* x_t0v, const voi
       float xb = bf ? orc_bf16_to_f32(((const uint16_t*)xbarv)[j]) : ((const float*)xbarv)[j];
       if (divisor > 1) xb = xb / (float)divisor;
       const float tf = (float)h->tau, epsf = (float)h->epsilon, betaf = (float)h->beta;
-      float n0 = fabsf(x - q0), a = fabsf(tf * (q1 - q0));
+      const float q0s = bf ? orc_bf16_to_f32(orc_f32_to_bf16(q0)) : q0;
+      float n0 = fabsf(x - q0), a = fabsf(tf * (q1 - q0s));
       int floored = a < epsf;
       float lam = n0 / max_stdf(a, epsf) + 1.0f;
       float dl = q0 - xb;

@@ -12,7 +12,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libco2b200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 OK, ERR_VALIDATION, ERR_NUMERIC, ERR_CUDA, ERR_NCCL = 0, 2, 3, 4, 5
 MODE_F64, MODE_F32, MODE_BF16_MIXED = 0, 1, 2
 DTYPE_F64, DTYPE_F32, DTYPE_BF16 = 0, 1, 2
@@ -26,6 +26,7 @@ BUF_PARAMS, BUF_ANCHOR, BUF_XFIRST, BUF_PREV_X0, BUF_PREV_X1 = 0, 1, 2, 3, 4
 BUF_MOMENTUM, BUF_GAP, BUF_XBAR, BUF_PARAMS_ALT, BUF_XFIRST_ALT = 5, 6, 7, 8, 9
 IPC_HANDLE_BYTES = 72  # CUDA IPC handle (64) + int64 offset
 NCCL_ID_BYTES = 128
+NCCL_FIXED_ORDER, NCCL_SUM = 0, 1
 
 
 class Hyper(C.Structure):
@@ -67,7 +68,8 @@ class Event(C.Structure):
 class HandleInfo(C.Structure):
     _fields_ = [("id", C.c_uint64), ("launch_time", C.c_double), ("completion_time", C.c_double),
                 ("stall", C.c_double), ("comm", C.c_double), ("completed", C.c_int32),
-                ("consumed", C.c_int32)]
+                ("consumed", C.c_int32), ("contributions", C.c_int32), ("polled", C.c_int32),
+                ("last_poll", C.c_int32), ("completion_logged", C.c_int32)]
 
 
 class RoundResult(C.Structure):
@@ -131,6 +133,7 @@ SIGNATURES = {
     "co2_aar_p2p_attach": (ST, [P, P, C.POINTER(C.c_uint8)]),
     "co2_aar_p2p_detach": (ST, [P, P]),
     "co2_aar_set_fused": (ST, [P, I32]),
+    "co2_aar_set_nccl_algo": (ST, [P, I32]),
     "co2_aar_destroy": (ST, [P]),
     "co2_aar_world": (I32, [P]),
     "co2_aar_launch": (ST, [P, I32, C.POINTER(P), P, I64, P, C.POINTER(U64)]),
@@ -147,6 +150,7 @@ SIGNATURES = {
     "co2_worker_buffer": (P, [P, I32]),
     "co2_worker_set_clip_mode": (ST, [P, I32]),
     "co2_worker_round": (I32, [P]),
+    "co2_worker_keep_average": (ST, [P, I32]),
     "co2_worker_snapshot_start": (ST, [P, P]),
     "co2_worker_snapshot_first": (ST, [P, P]),
     "co2_round": (ST, [C.POINTER(P), I32, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),

@@ -434,13 +434,17 @@ class CollectiveEngine:
     """One-step-stale all-reduce (proj/include/co2sim/collective.hpp:54-93).
 
     transport "local": G simulated workers on this GPU, fixed-order average.
-    transport "nccl":  one rank per GPU; in-place ncclAllReduce(sum).
+    transport "nccl":  one rank per GPU, in place.  nccl_algo "fixed" (default):
+                       slice exchange + fixed-order average kernel + all-gather,
+                       bitwise the reference's average() at any G; "sum":
+                       ncclAllReduce(sum) in the storage dtype, divided by G in
+                       the consumer (NCCL's order and per-hop rounding).
     transport "p2p":   one rank per GPU; deterministic fixed-order average over
                        NVLink peer memory (CUDA IPC).  Needs an initialized
                        torch.distributed group to exchange IPC handles."""
 
     def __init__(self, workers: int = 1, *, transport: str = "local", rank: int = 0,
-                 nccl_id: bytes | None = None, max_ctas: int = 0):
+                 nccl_id: bytes | None = None, max_ctas: int = 0, nccl_algo: str = "fixed"):
         self.handle = C.c_void_p()
         self.transport = transport
         self.rank = rank
@@ -451,6 +455,10 @@ class CollectiveEngine:
                 raise ValidationError("nccl transport needs the rank-0 unique id")
             uid = (C.c_uint8 * L.NCCL_ID_BYTES)(*nccl_id)
             check(lib().co2_aar_create_nccl(C.byref(self.handle), uid, rank, workers, max_ctas))
+            if nccl_algo not in ("fixed", "sum"):
+                raise ValidationError(f"unknown nccl_algo {nccl_algo}")
+            check(lib().co2_aar_set_nccl_algo(
+                self.handle, L.NCCL_SUM if nccl_algo == "sum" else L.NCCL_FIXED_ORDER))
         elif transport == "p2p":
             check(lib().co2_aar_create_p2p(C.byref(self.handle), rank, workers, max_ctas))
             self.workers = workers
@@ -546,7 +554,8 @@ class CollectiveEngine:
         check(lib().co2_aar_info(self.handle, handle, C.byref(r)))
         return {"id": r.id, "launch_time": r.launch_time, "completion_time": r.completion_time,
                 "completed": bool(r.completed), "consumed": bool(r.consumed), "stall": r.stall,
-                "comm": r.comm}
+                "comm": r.comm, "contributions": r.contributions, "polled": bool(r.polled),
+                "last_poll": bool(r.last_poll), "completion_logged": bool(r.completion_logged)}
 
     def total_stall(self) -> float:
         s = C.c_double()
@@ -630,6 +639,12 @@ class Worker:
     @property
     def t(self) -> int:
         return lib().co2_worker_round(self.handle)
+
+    def keep_average(self, on: bool = True) -> None:
+        """RoundResult::consumed_average on the in-place transports (NCCL,
+        P2P): the step also writes the reduce it consumed into a worker-owned
+        buffer, readable as buffer(BUF_XBAR) after the round."""
+        check(lib().co2_worker_keep_average(self.handle, int(on)))
 
     def set_clip_mode(self, mode: str) -> None:
         """'coordinate' (the reference, default) or 'global' (the global-norm

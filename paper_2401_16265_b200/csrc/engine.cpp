@@ -46,6 +46,7 @@ struct Handle {
   cudaEvent_t start = nullptr, done = nullptr, wait_begin = nullptr, wait_end = nullptr;
   bool consumed = false, polled = false, last_poll = false, completion_logged = false;
   bool waited = false;
+  int contributions = 0;
   co2_diag_t* diag = nullptr;  // LOCAL: pinned copy of the average's flags (pool slot)
   uint32_t* p2p_error = nullptr;  // P2P: pinned copy of the signal area's error word (pool slot)
   // After kRing newer launches a handle's events are recycled; its device
@@ -56,6 +57,7 @@ struct Handle {
 };
 
 constexpr size_t kRing = 256;
+constexpr int kMaxNcclRanks = 64;  // fixed-order average: co2_average's contribution cap
 
 // A buffer registered with the P2P transport: the same logical buffer on
 // every rank (rank-indexed device pointers, peers opened via CUDA IPC).
@@ -76,6 +78,17 @@ struct co2_aar {
   int rank = 0, world = 1, workers = 1;
   ncclComm_t comm = nullptr;
   ncclComm_t comm2 = nullptr;  // blocking collectives issued on the caller's stream
+  // NCCL algorithm: false (default) = fixed-order average (send/recv slice
+  // exchange + ascending-rank sum kernel + send/recv all-gather), bitwise
+  // the reference's average() at any world size; true = ncclAllReduce /
+  // ncclReduceScatter sums in the storage dtype (ring / tree order, rounded
+  // per hop), divided by G in the consumer.
+  bool nccl_sum = false;
+  // staging of the slices received from peers: [0] comm stream, [1] the
+  // caller's stream (sharded x_{t,1}); a second workspace for [1]'s sum kernel
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes[2] = {0, 0};
+  void* ws2 = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t epoch = nullptr;
   void* ws = nullptr;
@@ -84,9 +97,12 @@ struct co2_aar {
   // P2P transport
   int ctas = 0;
   int slice_ctas = 0;  // sharded slice reduce; 0 = one CTA per SM
-  uint32_t p2p_epoch = 0;
+  uint32_t p2p_epoch = 0;      // ready flags of every P2P reduce launch (average and slice)
+  uint32_t p2p_done = 0;       // cumulative exit-barrier target of the average kernel
   bool fused = false;        // worker-local rounds use the fused all-reduce + step kernel
-  uint32_t fused_epoch = 0;
+  uint32_t fused_epoch = 0;  // exit barrier (done3) of the fused all-reduce + step
+  uint32_t shard_epoch = 0;  // exit barrier (done2) of the sharded P2P step: per engine,
+                             // since the counter lives in the engine's signal area
   void* signals = nullptr;        // this rank's signal area (cudaMalloc, IPC-exported)
   std::vector<void*> peer_signals;  // rank-indexed (opened IPC pointers; own = signals)
   std::vector<P2PBuffer> p2p_bufs;
@@ -138,6 +154,7 @@ extern "C" co2_status_t co2_aar_create_nccl(co2_aar_t** out, const uint8_t id[CO
   e->rank = rank;
   e->world = world;
   e->workers = world;
+  e->nccl_sum = world > kMaxNcclRanks;  // beyond the average kernel's fan-in
   co2_status_t s = engine_common_init(e);
   if (s != CO2_OK) {
     delete e;
@@ -315,8 +332,10 @@ extern "C" co2_status_t co2_aar_p2p_detach(co2_aar_t* e, const void* local) {
   if (!e || e->transport != T_P2P) return fail(CO2_ERR_VALIDATION, "detach: not a P2P engine");
   for (size_t i = 0; i < e->p2p_bufs.size(); ++i) {
     if (e->p2p_bufs[i].local != local) continue;
-    // no reduce of ours may still read the peers' memory
-    CO2_CUDA(cudaStreamSynchronize(e->comm_stream));
+    // No kernel may still touch the peers' memory: besides the reduces on
+    // the comm stream, the fused all-reduce step and the sharded P2P step
+    // run on the caller's stream(s), so wait for the whole device.
+    CO2_CUDA(cudaDeviceSynchronize());
     const std::vector<std::pair<int, std::string>> keys = e->p2p_bufs[i].keys;
     e->p2p_bufs.erase(e->p2p_bufs.begin() + (std::ptrdiff_t)i);
     return release_keys(e, keys);
@@ -342,7 +361,7 @@ extern "C" co2_status_t co2_aar_create_local(co2_aar_t** out, int32_t workers) {
 
 extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
   if (!e) return CO2_OK;
-  cudaStreamSynchronize(e->comm_stream);
+  cudaDeviceSynchronize();  // kernels on any stream may use the peer mappings
   for (Handle& h : e->handles) {
     for (cudaEvent_t ev : {h.start, h.done, h.wait_begin, h.wait_end})
       if (ev) cudaEventDestroy(ev);
@@ -353,6 +372,9 @@ extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
   if (e->comm2) ncclCommDestroy(e->comm2);
   if (e->comm) ncclCommDestroy(e->comm);
   if (e->ws) cudaFree(e->ws);
+  if (e->ws2) cudaFree(e->ws2);
+  for (void* p : e->stage)
+    if (p) cudaFree(p);
   for (auto& kv : e->opened) cudaIpcCloseMemHandle(kv.second.base);
   if (e->signals) cudaFree(e->signals);
   if (e->epoch) cudaEventDestroy(e->epoch);
@@ -366,6 +388,99 @@ extern "C" int32_t co2_aar_world(const co2_aar_t* e) { return e ? e->workers : 0
 static co2_status_t record_for(co2_aar* e, uint64_t h, Handle** out) {
   if (!e || h >= e->handles.size()) return fail(CO2_ERR_VALIDATION, "unknown reduce handle");
   *out = &e->handles[h];
+  return CO2_OK;
+}
+
+// ---- NCCL fixed-order average (the default NCCL algorithm) ---------------
+// The reference's average() (proj/src/param_ops.cpp:16-33) sums the
+// contributions in ascending worker order and divides once.  A ring or tree
+// all-reduce sums in a topology-dependent order and, in bf16, rounds after
+// every hop.  This decomposition keeps the ring's NVLink volume, (G-1)/G of
+// the buffer in and out per rank, but fixes the order:
+//   1. slice exchange: rank r sends slice p of its buffer to rank p and
+//      receives slice r of every peer's buffer into staging (grouped
+//      ncclSend / ncclRecv, an all-to-all);
+//   2. the fixed-order average kernel (co2_average) over the G copies of
+//      slice r, ascending rank order, one division, written to `dst`;
+//   3. (all-reduce only) slice all-gather with grouped send / recv.
+// Slices are ceil(n/G) rounded up to 8 elements (16-byte aligned in every
+// dtype); the last ones may be short or empty.
+static int64_t nccl_slice(int64_t n, int world) { return ((n + world - 1) / world + 7) / 8 * 8; }
+
+static co2_status_t stage_reserve(co2_aar* e, int which, size_t bytes) {
+  if (e->stage_bytes[which] >= bytes) return CO2_OK;
+  if (e->stage[which]) CO2_CUDA(cudaFree(e->stage[which]));
+  e->stage[which] = nullptr;
+  e->stage_bytes[which] = 0;
+  CO2_CUDA(cudaMalloc(&e->stage[which], bytes));
+  e->stage_bytes[which] = bytes;
+  return CO2_OK;
+}
+
+// Steps 1-2: average of slice `rank` of every rank's `src` (n elements,
+// slices of `slice`) into dst (len_r elements).  `which` selects the staging
+// buffer / workspace pair of the stream.
+static co2_status_t nccl_fixed_rs(co2_aar* e, ncclComm_t comm, int which, co2_dtype_t dt,
+                                  const void* src, int64_t n, int64_t slice, void* dst,
+                                  void* ws, cudaStream_t st) {
+  const int G = e->world, r = e->rank;
+  const size_t es = dtype_bytes(dt);
+  auto lo = [&](int p) { return std::min<int64_t>((int64_t)p * slice, n); };
+  auto len = [&](int p) { return std::max<int64_t>(0, std::min<int64_t>(slice, n - lo(p))); };
+  const int64_t mine = len(r);
+  CO2_TRY(stage_reserve(e, which, es * (size_t)slice * (size_t)G + 16));
+  char* stg = static_cast<char*>(e->stage[which]);
+  const char* s8 = static_cast<const char*>(src);
+  CO2_NCCL(ncclGroupStart());
+  for (int p = 0; p < G; ++p) {
+    if (p == r) continue;
+    if (len(p) > 0) CO2_NCCL(ncclSend(s8 + es * lo(p), (size_t)len(p), nccl_dtype(dt), p, comm, st));
+    if (mine > 0)
+      CO2_NCCL(ncclRecv(stg + es * (size_t)slice * p, (size_t)mine, nccl_dtype(dt), p, comm, st));
+  }
+  CO2_NCCL(ncclGroupEnd());
+  const void* parts[kMaxNcclRanks];
+  for (int p = 0; p < G; ++p)
+    parts[p] = p == r ? static_cast<const void*>(s8 + es * lo(r))
+                      : static_cast<const void*>(stg + es * (size_t)slice * p);
+  return co2_average(dt, G, parts, mine, dst, ws, st);
+}
+
+// Step 3: every rank's slice of `buf` into every rank (in place).
+static co2_status_t nccl_fixed_ag(co2_aar* e, ncclComm_t comm, co2_dtype_t dt, void* buf,
+                                  int64_t n, int64_t slice, cudaStream_t st) {
+  const int G = e->world, r = e->rank;
+  const size_t es = dtype_bytes(dt);
+  auto lo = [&](int p) { return std::min<int64_t>((int64_t)p * slice, n); };
+  auto len = [&](int p) { return std::max<int64_t>(0, std::min<int64_t>(slice, n - lo(p))); };
+  char* b8 = static_cast<char*>(buf);
+  CO2_NCCL(ncclGroupStart());
+  for (int p = 0; p < G; ++p) {
+    if (p == r) continue;
+    if (len(r) > 0) CO2_NCCL(ncclSend(b8 + es * lo(r), (size_t)len(r), nccl_dtype(dt), p, comm, st));
+    if (len(p) > 0) CO2_NCCL(ncclRecv(b8 + es * lo(p), (size_t)len(p), nccl_dtype(dt), p, comm, st));
+  }
+  CO2_NCCL(ncclGroupEnd());
+  return CO2_OK;
+}
+
+// Consumers divide the delivered reduce by this: NCCL's sum algorithm
+// delivers the worker sum; every other path delivers the average itself.
+static int32_t reduce_divisor(const co2_aar* e) {
+  return (e->transport == T_NCCL && e->nccl_sum) ? e->world : 1;
+}
+
+extern "C" co2_status_t co2_aar_set_nccl_algo(co2_aar_t* e, int32_t algo) {
+  if (!e || e->transport != T_NCCL)
+    return fail(CO2_ERR_VALIDATION, "nccl algorithm: NCCL transport only");
+  if (algo != CO2_NCCL_FIXED_ORDER && algo != CO2_NCCL_SUM)
+    return fail(CO2_ERR_VALIDATION, "nccl algorithm: unknown value %d", (int)algo);
+  if (algo == CO2_NCCL_FIXED_ORDER && e->world > kMaxNcclRanks)
+    return fail(CO2_ERR_VALIDATION, "nccl algorithm: fixed order supports <= %d ranks",
+                kMaxNcclRanks);
+  if (e->live > 0)
+    return fail(CO2_ERR_VALIDATION, "nccl algorithm: cannot change with reduces in flight");
+  e->nccl_sum = algo == CO2_NCCL_SUM;
   return CO2_OK;
 }
 
@@ -448,6 +563,7 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
   if (n < 0) return fail(CO2_ERR_VALIDATION, "launch_all_reduce: negative size");
   Handle h;
   CO2_TRY(new_handle(e, &h));
+  h.contributions = e->workers;
   // Fence: the reduce reads x_{t,tau} only after the producer wrote it.
   CO2_CUDA(cudaEventRecord(e->fence, S(producer)));
   CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, e->fence, 0));
@@ -456,7 +572,10 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     if (e->transport != T_NCCL)
       return fail(CO2_ERR_VALIDATION, "reduce-scatter: NCCL transport only");
     const int64_t shard = n / e->world;
-    if (e->world > 1 && shard > 0)
+    if (e->world > 1 && shard > 0 && !e->nccl_sum) {
+      CO2_TRY(nccl_fixed_rs(e, e->comm, 0, dt, bufs[0], n, shard, out, e->ws, e->comm_stream));
+      CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
+    } else if (e->world > 1 && shard > 0)
       CO2_NCCL(ncclReduceScatter(bufs[0], out, (size_t)shard, nccl_dtype(dt), ncclSum, e->comm,
                                  e->comm_stream));
     else if (shard > 0)
@@ -474,7 +593,7 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     if (e->world > 1 && n > 0) {
       e->p2p_epoch += 1;
       CO2_TRY(p2p_average_launch(dt, pb->ptrs.data(), e->peer_signals.data(), e->world, e->rank,
-                                 n, e->p2p_epoch, e->ctas, e->comm_stream));
+                                 n, e->p2p_epoch, &e->p2p_done, e->ctas, e->comm_stream));
       // the kernel records a timed-out barrier in the signal area's error word
       CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
                                cudaMemcpyDeviceToHost, e->comm_stream));
@@ -482,9 +601,18 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
   } else if (e->transport == T_NCCL) {
     if (out && out != bufs[0])
       return fail(CO2_ERR_VALIDATION, "launch_all_reduce: NCCL transport reduces in place");
-    if (e->world > 1 && n > 0)
+    if (e->world > 1 && n > 0 && !e->nccl_sum) {
+      const int64_t slice = nccl_slice(n, e->world);
+      void* buf = const_cast<void*>(bufs[0]);
+      void* mine = static_cast<char*>(buf) +
+                   dtype_bytes(dt) * (size_t)std::min<int64_t>((int64_t)e->rank * slice, n);
+      CO2_TRY(nccl_fixed_rs(e, e->comm, 0, dt, buf, n, slice, mine, e->ws, e->comm_stream));
+      CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
+      CO2_TRY(nccl_fixed_ag(e, e->comm, dt, buf, n, slice, e->comm_stream));
+    } else if (e->world > 1 && n > 0) {
       CO2_NCCL(ncclAllReduce(bufs[0], const_cast<void*>(bufs[0]), (size_t)n, nccl_dtype(dt), ncclSum,
                              e->comm, e->comm_stream));
+    }
   } else {
     CO2_TRY(co2_average(dt, e->workers, bufs, n, out, e->ws, e->comm_stream));
     CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
@@ -517,6 +645,7 @@ static co2_status_t launch_slice(co2_aar* e, co2_dtype_t dt, const void* src0, c
     return fail(CO2_ERR_VALIDATION, "slice reduce: P2P signals not attached");
   Handle h;
   CO2_TRY(new_handle(e, &h));
+  h.contributions = e->workers;
   CO2_CUDA(cudaEventRecord(e->fence, S(producer)));
   CO2_CUDA(cudaStreamWaitEvent(e->comm_stream, e->fence, 0));
   CO2_CUDA(cudaEventRecord(h.start, e->comm_stream));
@@ -597,7 +726,8 @@ extern "C" co2_status_t co2_aar_info(co2_aar_t* e, uint64_t handle, co2_handle_i
   CO2_TRY(record_for(e, handle, &h));
   if (!out) return fail(CO2_ERR_VALIDATION, "info: null output");
   const double nan = std::numeric_limits<double>::quiet_NaN();
-  co2_handle_info_t r{handle, nan, nan, nan, nan, 0, h->consumed ? 1 : 0};
+  co2_handle_info_t r{handle, nan, nan, nan, nan, 0, h->consumed ? 1 : 0, h->contributions,
+                      h->polled ? 1 : 0, h->last_poll ? 1 : 0, 0};
   if (!h->cached && cudaEventQuery(h->done) == cudaSuccess) CO2_TRY(cache_handle_if_ready(e, *h));
   if (h->cached) {
     r.launch_time = h->c_start;
@@ -606,6 +736,8 @@ extern "C" co2_status_t co2_aar_info(co2_aar_t* e, uint64_t handle, co2_handle_i
     r.completed = 1;
     if (h->waited) r.stall = h->c_stall;
   }
+  // log_completion (collective.cpp:66-71): a successful poll or the wait
+  r.completion_logged = (h->completion_logged || h->consumed) ? 1 : 0;
   *out = r;
   return CO2_OK;
 }
@@ -685,8 +817,16 @@ struct co2_worker {
   void* tmp_state = nullptr;          // ghost: bar0
   void* tmp_low = nullptr;            // ghost: bar1
   void* xbar = nullptr;               // last consumed reduce (for CO2_BUF_XBAR)
+  // RoundResult::consumed_average on the in-place transports (NCCL / P2P):
+  // the step copies the reduce it consumes here (co2_worker_keep_average).
+  void* avg_keep = nullptr;
+  bool keep_avg = false;
   void* ws = nullptr;
   co2_diag_t* host_diag = nullptr;  // pinned
+  // fused P2P schedule: pinned copy of the engine's signal error word, read
+  // back after every fused round (a timed-out barrier means the consumed
+  // average is incomplete); checked by co2_round_finish and the next round
+  uint32_t* fused_err = nullptr;
   bool has_pending = false;
   uint64_t pending = 0;
   uint64_t consumed = 0;
@@ -700,16 +840,16 @@ struct co2_worker {
 static co2_status_t step_launch(co2_worker* w, co2_mode_t mode, int64_t n, const void* x_t0,
                                 const void* p0, const void* p1, const void* xbar,
                                 int32_t divisor, void* m, void* anchor, void* params, void* gap,
-                                const co2_hyper_t* h, cudaStream_t st) {
+                                const co2_hyper_t* h, cudaStream_t st, void* xbar_out = nullptr) {
   const int64_t cap = (int64_t)w->tev.size() / 2;
   const int64_t slot = cap ? w->tev_recorded % cap : 0;
   if (cap) CO2_CUDA(cudaEventRecord(w->tev[2 * slot], st));
   if (w->clip_mode == CO2_CLIP_GLOBAL_NORM)
     CO2_TRY(outer_step_global_clip_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params,
-                                        gap, h, w->ws, st));
+                                        gap, h, w->ws, st, xbar_out));
   else
     CO2_TRY(outer_step_impl(mode, n, x_t0, p0, p1, xbar, divisor, m, anchor, params, gap, h,
-                            w->ws, st));
+                            w->ws, st, xbar_out));
   if (cap) {
     CO2_CUDA(cudaEventRecord(w->tev[2 * slot + 1], st));
     w->tev_recorded += 1;
@@ -773,9 +913,10 @@ extern "C" co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, i
 extern "C" co2_status_t co2_worker_destroy(co2_worker_t* w) {
   if (!w) return CO2_OK;
   for (void* p : {w->params[0], w->params[1], w->anchor, w->xfirst, w->prev_x0, w->prev_x1, w->m,
-                  w->gap, w->avg[0], w->avg[1], w->tmp_state, w->tmp_low, w->ws})
+                  w->gap, w->avg[0], w->avg[1], w->tmp_state, w->tmp_low, w->avg_keep, w->ws})
     if (p) cudaFree(p);
   if (w->host_diag) cudaFreeHost(w->host_diag);
+  if (w->fused_err) cudaFreeHost(w->fused_err);
   for (cudaEvent_t ev : w->tev) cudaEventDestroy(ev);
   delete w;
   return CO2_OK;
@@ -834,6 +975,13 @@ extern "C" co2_status_t co2_worker_set_clip_mode(co2_worker_t* w, int32_t mode) 
   return CO2_OK;
 }
 
+extern "C" co2_status_t co2_worker_keep_average(co2_worker_t* w, int32_t on) {
+  if (!w) return fail(CO2_ERR_VALIDATION, "worker: null handle");
+  w->keep_avg = on != 0;
+  if (w->keep_avg && !w->avg_keep) CO2_TRY(walloc(&w->avg_keep, low_bytes(w->mode) * w->n));
+  return CO2_OK;
+}
+
 extern "C" int32_t co2_worker_round(const co2_worker_t* w) { return w ? w->t : -1; }
 
 extern "C" co2_status_t co2_worker_snapshot_start(co2_worker_t* w, void* stream) {
@@ -870,6 +1018,10 @@ extern "C" co2_status_t co2_round_finish(co2_worker_t* const* ws, int32_t g, voi
   r.n_floored = 0;
   co2_status_t first = CO2_OK;
   char msg[512] = {0};
+  for (int i = 0; i < g; ++i)
+    if (ws[i]->fused_err && *ws[i]->fused_err)
+      return fail(CO2_ERR_CUDA, "p2p fused step: cross-GPU barrier timed out (code %u)",
+                  *ws[i]->fused_err);
   for (int i = 0; i < g; ++i) {  // worker order = the reference's error order (cpp:186)
     const co2_diag_t& d = *ws[i]->host_diag;
     r.min_gap = d.min_gap < r.min_gap ? d.min_gap : r.min_gap;
@@ -960,6 +1112,13 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     if (w->clip_mode != CO2_CLIP_COORDINATE)
       return fail(CO2_ERR_VALIDATION,
                   "global-norm clip: not available with the fused all-reduce schedule");
+    if (!w->fused_err) {
+      CO2_CUDA(cudaMallocHost(&w->fused_err, sizeof(uint32_t)));
+      *w->fused_err = 0;
+    }
+    if (*w->fused_err)  // an earlier async round's barrier timed out
+      return fail(CO2_ERR_CUDA, "p2p fused step: cross-GPU barrier timed out (code %u)",
+                  *w->fused_err);
     if (w->has_pending) {  // the round-0 reduce (standalone P2P kernel)
       int32_t done = 0;
       CO2_TRY(co2_aar_poll(e, w->pending, &done));
@@ -979,27 +1138,26 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     CO2_TRY(outer_step_fused_aar_impl(mode, n, w->anchor, w->prev_x0, w->prev_x1, out_params,
                                       w->m, w->prev_x0, out_params, w->gap, hyper,
                                       pb->ptrs.data(), lo, len, e->peer_signals.data(), e->world,
-                                      e->rank, e->fused_epoch, w->ws, st));
+                                      e->rank, e->fused_epoch, w->ws, st,
+                                      w->keep_avg ? w->avg_keep : nullptr));
     if (cap) {
       CO2_CUDA(cudaEventRecord(w->tev[2 * slot + 1], st));
       w->tev_recorded += 1;
     }
     CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    CO2_CUDA(cudaMemcpyAsync(w->fused_err,
+                             static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
+                             cudaMemcpyDeviceToHost, st));
     std::swap(w->anchor, w->prev_x0);
     std::swap(w->prev_x1, w->xfirst);
     w->cur = 1 - w->cur;
-    w->xbar = nullptr;
+    w->xbar = w->keep_avg ? w->avg_keep : nullptr;
     w->t += 1;
     r.outer_applied = 1;
     if (sync) {
-      co2_status_t s = co2_round_finish(ws, g, stream, &r);
+      co2_status_t s = co2_round_finish(ws, g, stream, &r);  // checks fused_err too
       if (res) *res = r;
-      if (s != CO2_OK) return s;
-      uint32_t err = 0;
-      CO2_CUDA(cudaMemcpy(&err, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4, cudaMemcpyDeviceToHost));
-      if (err)
-        return fail(CO2_ERR_CUDA, "p2p fused step: cross-GPU barrier timed out (code %u)", err);
-      return CO2_OK;
+      return s;
     }
     if (res) *res = r;
     return CO2_OK;
@@ -1073,7 +1231,7 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
   void* xbar = local ? w0->avg[(t - 1) % 2] : ws[0]->params[1 - ws[0]->cur];
   // NCCL delivers the worker sum (divided once in the step); LOCAL and P2P
   // deliver the fixed-order average itself.
-  const int32_t divisor = (local || e->transport == T_P2P) ? 1 : e->world;
+  const int32_t divisor = reduce_divisor(e);
 
   if (hyper->ghost_consistent && g > 1) {
     // :161-184 -- one shared state driven by the averaged snapshots.
@@ -1120,9 +1278,12 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     for (int i = 0; i < g; ++i) {
       co2_worker* w = ws[i];
       void* out_params = w->params[1 - w->cur];
-      void* xb = local ? xbar : out_params;  // NCCL: the sum lives in the other buffer
+      void* xb = local ? xbar : out_params;  // NCCL / P2P: the reduce lives in the other buffer
+      void* keep = (!local && w->keep_avg) ? w->avg_keep : nullptr;
       CO2_TRY(step_launch(w, mode, n, w->anchor, w->prev_x0, w->prev_x1, xb, divisor, w->m,
-                          w->prev_x0, out_params, w->gap, hyper, st));
+                          w->prev_x0, out_params, w->gap, hyper, st, keep));
+      // the sum algorithm delivered the worker sum: keep the average
+      if (keep && divisor > 1) CO2_TRY(scale_div_impl(ldt, keep, n, divisor, st));
       CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
       std::swap(w->anchor, w->prev_x0);  // anchor <- x_{t+1,0}; prev_x0 <- x_{t,0}
       std::swap(w->prev_x1, w->xfirst);  // prev_x1 <- x_{t,1}
@@ -1130,7 +1291,9 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     }
   }
   for (int i = 0; i < g; ++i) {
-    ws[i]->xbar = local ? xbar : nullptr;  // NCCL consumed its sum in place
+    // in-place transports overwrite the reduce with x_{t+1,0}: readable only
+    // through the keep-average copy
+    ws[i]->xbar = local ? xbar : (ws[i]->keep_avg ? ws[i]->avg_keep : nullptr);
     ws[i]->consumed = prev;
     ws[i]->has_consumed = true;
     ws[i]->pending = launched;
@@ -1182,7 +1345,6 @@ struct co2_sharded {
   // and the fused step's all-gather epoch.
   bool p2p = false;
   void* xfirst2 = nullptr;
-  uint32_t exit_epoch = 0;
   void* xfirst_cur() { return (t % 2 == 0 || !p2p) ? xfirst : xfirst2; }
   void* xfirst_alt() { return (t % 2 == 0) ? xfirst2 : xfirst; }
 };
@@ -1198,7 +1360,14 @@ static co2_status_t ensure_comm2(co2_aar* e) {
 static co2_status_t rs_blocking(co2_aar* e, co2_dtype_t dt, const void* full, void* shard_out,
                                 int64_t shard, cudaStream_t st) {
   if (shard <= 0) return CO2_OK;
-  if (e->world > 1)
+  if (e->world > 1 && !e->nccl_sum) {
+    if (!e->ws2) {
+      CO2_CUDA(cudaMalloc(&e->ws2, co2_workspace_bytes()));
+      CO2_CUDA(cudaMemsetAsync(e->ws2, 0, co2_workspace_bytes(), st));
+    }
+    CO2_TRY(nccl_fixed_rs(e, e->comm2, 1, dt, full, shard * e->world, shard, shard_out, e->ws2,
+                          st));
+  } else if (e->world > 1)
     CO2_NCCL(ncclReduceScatter(full, shard_out, (size_t)shard, nccl_dtype(dt), ncclSum, e->comm2,
                                st));
   else
@@ -1445,15 +1614,16 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
     if (!pb) return fail(CO2_ERR_VALIDATION, "sharded: params not registered for P2P");
     std::vector<void*> outs(s->world);
     for (int p = 0; p < s->world; ++p) outs[p] = static_cast<char*>(pb->ptrs[p]) + lb * s->offset;
-    s->exit_epoch += 1;
+    e->shard_epoch += 1;
     CO2_TRY(outer_step_ghost_p2p_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, xsum,
                                       ghost_copies, s->m, s->anchor, s->prev_x0, outs.data(),
-                                      e->peer_signals.data(), s->world, s->rank, s->exit_epoch,
+                                      e->peer_signals.data(), s->world, s->rank, e->shard_epoch,
                                       s->gap, hyper, s->ws, st));
   } else {
-    CO2_TRY(outer_step_ghost_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, s->world, xsum,
-                                  s->world, ghost_copies, s->m, s->anchor, s->prev_x0,
-                                  out_params, s->gap, hyper, s->ws, st));
+    CO2_TRY(outer_step_ghost_impl(s->mode, s->length, s->anchor, s->prev_x0, p1,
+                                  reduce_divisor(e), xsum, reduce_divisor(e), ghost_copies,
+                                  s->m, s->anchor, s->prev_x0, out_params, s->gap, hyper, s->ws,
+                                  st));
   }
   if (cap) {
     CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));
@@ -1519,7 +1689,7 @@ co2_status_t launch_reduce(co2_worker_t* const* ws, int32_t g, co2_aar* e,
   void* out = local ? w0->avg[slot] : const_cast<void*>(bufs[0]);
   CO2_TRY(co2_aar_launch(e, low_dtype(w0->mode), bufs, out, w0->n, st, handle));
   *xbar = out;
-  *divisor = e->transport == T_NCCL ? e->world : 1;
+  *divisor = reduce_divisor(e);
   return CO2_OK;
 }
 
@@ -1634,7 +1804,7 @@ extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int
     CO2_TRY(co2_aar_wait(e, prev, stream));
     const void* xbar = e->transport == T_LOCAL ? w0->avg[(w0->t + 1) % 2]
                                                : ws[0]->params[1 - ws[0]->cur];
-    CO2_TRY(correct(xbar, e->transport == T_NCCL ? e->world : 1));
+    CO2_TRY(correct(xbar, reduce_divisor(e)));
     for (int i = 0; i < g; ++i) {
       ws[i]->has_pending = false;
       // LOCAL keeps the consumed average readable; in-place transports

@@ -255,12 +255,26 @@ struct Hyp {
 //   m' = beta*m + D/L   (or beta*m + D)     :84 / :86
 //   c  = min(max(m', -phi), phi)  (or m')   param_ops.cpp:42
 //   x' = x_t0 - alpha*c                     outer_algorithms.cpp:102 / :104
-template <typename TC>
+// Bf16-mixed (LQ): the inner loop started from the bf16 params, i.e. from
+// the bf16 rounding of the fp32 anchor q0, so the first-step displacement in
+// the gap's denominator is q1 - bf16(q0) (exactly 0 at a coordinate the first
+// inner step did not move, as in the reference); the numerator and Delta
+// use the fp32 anchors.  Identity for the fp32 / fp64 modes.
+template <typename TC, bool LQ>
+__device__ __forceinline__ TC start_of_inner(TC q0) {
+  if constexpr (LQ) {
+    return __uint_as_float(((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(q0))) << 16);
+  } else {
+    return q0;
+  }
+}
+
+template <typename TC, bool LQ = false>
 __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& xn, TC& lam,
                                          const Hyp<TC>& h, AccT<TC>& acc) {
   if (h.divide) xb = xb / h.divisor;  // average(): sum / G, param_ops.cpp:30
   TC n0 = fabs(x - q0);
-  TC av = fabs(h.tau * (q1 - q0));
+  TC av = fabs(h.tau * (q1 - start_of_inner<TC, LQ>(q0)));
   bool floored = av < h.eps;
   TC d = floored ? h.eps : av;
   lam = n0 / d + (TC)1;
@@ -323,6 +337,10 @@ struct StepArgs {
   // on every rank) is averaged in rank order and stored into every rank.
   void* aar_bufs[kMaxRanks];
   int64_t aar_lo, aar_len;
+  // RoundResult::consumed_average (outer_algorithms.hpp:68): when non-null
+  // the step copies the reduce it consumed (as read: a worker sum stays a
+  // sum), so in-place transports keep it readable.
+  void* xbar_out;
 };
 
 // One 16-byte vector of the fixed-order P2P average (param_ops.cpp:16-33):
@@ -330,19 +348,28 @@ struct StepArgs {
 template <typename TL, typename TC, int R>
 __device__ __forceinline__ void aar_vector(const StepArgs& a, int64_t e) {
   constexpr int VA = 16 / (int)sizeof(TL);
-  uint4 raw[R];
-#pragma unroll
-  for (int p = 0; p < R; ++p)
-    if (p < a.exit.world)
-      raw[p] = __ldcg(reinterpret_cast<const uint4*>(static_cast<const TL*>(a.aar_bufs[p]) + e));
+  // Ranks are gathered in groups of at most 4 (ascending), so the 8-rank
+  // instantiation holds 4 x 16 B of loads, not 8, beside the step's state
+  // (it spilled 152 B at 3 CTAs/SM with all 8 in flight).
+  constexpr int RG = R < 2 ? R : 2;
   TC acc[VA];
 #pragma unroll
-  for (int k = 0; k < VA; ++k) acc[k] = to_c(reinterpret_cast<const TL*>(&raw[0])[k]);
+  for (int p0 = 0; p0 < R; p0 += RG) {
+    uint4 raw[RG];
 #pragma unroll
-  for (int p = 1; p < R; ++p)
-    if (p < a.exit.world)
+    for (int q = 0; q < RG; ++q)
+      if (p0 + q < a.exit.world)
+        raw[q] = __ldcg(
+            reinterpret_cast<const uint4*>(static_cast<const TL*>(a.aar_bufs[p0 + q]) + e));
 #pragma unroll
-      for (int k = 0; k < VA; ++k) acc[k] = acc[k] + to_c(reinterpret_cast<const TL*>(&raw[p])[k]);
+    for (int q = 0; q < RG; ++q)
+      if (p0 + q < a.exit.world)
+#pragma unroll
+        for (int k = 0; k < VA; ++k) {
+          const TC v = to_c(reinterpret_cast<const TL*>(&raw[q])[k]);
+          acc[k] = (p0 + q == 0) ? v : acc[k] + v;  // ascending rank order
+        }
+  }
   uint4 out;
   const TC g = (TC)a.exit.world;
 #pragma unroll
@@ -381,6 +408,8 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
   hg.divide = 0;
   const TC p1d = (TC)a.p1_div;
   TS* B0 = static_cast<TS*>(a.bar0_out);
+  TL* XO = static_cast<TL*>(a.xbar_out);
+  constexpr bool LQ = !std::is_same<TS, TL>::value;  // bf16-mixed: see start_of_inner
 
   const TS* __restrict__ X = static_cast<const TS*>(a.x_t0);
   const TS* __restrict__ P0 = static_cast<const TS*>(a.p0);
@@ -437,17 +466,17 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           TC m = to_c(mo[u][v]), xn, lam;
+          TC xbv = to_c(xb[u][v]);
+          if (h.divide) xbv = xbv / h.divisor;  // average(): sum / G, param_ops.cpp:30
           if constexpr (GHOST) {
-            TC xbv = to_c(xb[u][v]);
-            if (h.divide) xbv = xbv / h.divisor;
             TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(x[u][v]), a.ghost_g);
             TC p1v = to_c(q1[u][v]);
             if (a.p1_div > 1) p1v = p1v / p1d;
             b0[v] = (TS)xv;
-            co2_elem<TC>(xv, to_c(q0[u][v]), p1v, xbv, m, xn, lam, hg, acc);
+            co2_elem<TC, LQ>(xv, to_c(q0[u][v]), p1v, xbv, m, xn, lam, hg, acc);
           } else {
-            co2_elem<TC>(to_c(x[u][v]), to_c(q0[u][v]), to_c(q1[u][v]), to_c(xb[u][v]), m, xn,
-                         lam, h, acc);
+            co2_elem<TC, LQ>(to_c(x[u][v]), to_c(q0[u][v]), to_c(q1[u][v]), xbv, m, xn, lam,
+                             hg, acc);
           }
           mn[v] = (TS)m;
           xs[v] = (TS)xn;
@@ -458,6 +487,7 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
         if (A) st_vec<TS, V>(A + e, xs);
         if (PR) st_vec<TL, V>(PR + e, xl);
         if (G) st_vec<TS, V>(G + e, gs);
+        if (XO) st_vec<TL, V>(XO + e, xb[u]);  // as consumed (a sum stays a sum)
         if constexpr (GHOST) {
           if (B0) st_vec<TS, V>(B0 + e, b0);
         }
@@ -504,18 +534,19 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
   const int64_t t = nv * V + (int64_t)blockIdx.x * NT + threadIdx.x;
   if (V > 1 && t < a.n) {
     TC m = to_c(Mm[t]), xn, lam;
+    TC xbv = to_c(XB[t]);
+    if (h.divide) xbv = xbv / h.divisor;
     if constexpr (GHOST) {
-      TC xbv = to_c(XB[t]);
-      if (h.divide) xbv = xbv / h.divisor;
       TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(X[t]), a.ghost_g);
       TC p1v = to_c(P1[t]);
       if (a.p1_div > 1) p1v = p1v / p1d;
       const TC q0 = to_c(P0[t]);  // read before bar0_out (may alias prev_x0) is written
       if (B0) B0[t] = (TS)xv;
-      co2_elem<TC>(xv, q0, p1v, xbv, m, xn, lam, hg, acc);
+      co2_elem<TC, LQ>(xv, q0, p1v, xbv, m, xn, lam, hg, acc);
     } else {
-      co2_elem<TC>(to_c(X[t]), to_c(P0[t]), to_c(P1[t]), to_c(XB[t]), m, xn, lam, h, acc);
+      co2_elem<TC, LQ>(to_c(X[t]), to_c(P0[t]), to_c(P1[t]), xbv, m, xn, lam, hg, acc);
     }
+    if (XO) XO[t] = XB[t];
     Mm[t] = (TS)m;
     if (A) A[t] = (TS)xn;
     if (PR) PR[t] = Store<TL>::from(xn);
@@ -649,7 +680,8 @@ int fused_variant() {
 template <class M>
 co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
   bool vec_ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
-                aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap);
+                aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap) &&
+                aligned16(a.xbar_out);
   if (!vec_ok) {
     launch_variant<M, 1, 4>(a, s);
   } else if constexpr (std::is_same<M, ModeBF16>::value) {
@@ -794,6 +826,56 @@ __global__ void __launch_bounds__(kThreads)
   block_finish<kThreads>(acc, ws);
 }
 
+// 16-byte-vector form of average_kernel (every contribution and the output
+// 16-byte aligned): per vector the contributions are loaded four at a time
+// and accumulated in ascending worker order, then divided once -- the same
+// per-element op sequence as the scalar kernel, so results are identical.
+template <typename T, typename TC>
+__global__ void __launch_bounds__(kThreads)
+    average_vec_kernel(const Ptrs64<T> c, int g, T* out, int64_t n, void* ws) {
+  constexpr int V = 16 / (int)sizeof(T);
+  Acc acc;
+  const TC gd = (TC)g;
+  const int64_t nv = n / V;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nv; i += stride) {
+    const int64_t e = i * V;
+    TC s[V];
+    for (int i0 = 0; i0 < g; i0 += 4) {
+      uint4 raw[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (i0 + k < g) raw[k] = __ldcs(reinterpret_cast<const uint4*>(c.p[i0 + k] + e));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (i0 + k < g) {
+          const T* v = reinterpret_cast<const T*>(&raw[k]);
+#pragma unroll
+          for (int q = 0; q < V; ++q) s[q] = (i0 + k == 0) ? to_c(v[q]) : s[q] + to_c(v[q]);
+        }
+      }
+    }
+    T o[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const TC r = s[q] / gd;
+      if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
+      o[q] = Store<T>::from(r);
+    }
+    st_vec<T, V>(out + e, o);
+  }
+  if (blockIdx.x == 0) {  // scalar tail
+    for (int64_t j = nv * V + threadIdx.x; j < n; j += kThreads) {
+      TC s = to_c(c.p[0][j]);
+      for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
+      const TC r = s / gd;
+      if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
+      out[j] = Store<T>::from(r);
+    }
+  }
+  block_finish<kThreads>(acc, ws);
+}
+
 template <typename T, typename TC>
 __global__ void sub_kernel(const T* a, const T* b, T* o, int64_t n) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
@@ -932,10 +1014,11 @@ co2_status_t launch_op(co2_dtype_t dt, const OpArgs& a, cudaStream_t s) {
 co2_status_t outer_step_impl(co2_mode_t mode, int64_t n, const void* x_t0, const void* p0,
                              const void* p1, const void* xbar, int32_t divisor, void* m,
                              void* anchor, void* params, void* gap, const co2_hyper_t* h,
-                             void* ws, cudaStream_t s) {
+                             void* ws, cudaStream_t s, void* xbar_out) {
   StepArgs a{x_t0, p0, p1, xbar, m, anchor, params, gap, n, h->alpha, h->beta, h->phi,
              h->epsilon, h->tau, divisor, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, 0, 0,
              nullptr};
+  a.xbar_out = xbar_out;
   switch (mode) {
     case CO2_MODE_F64: return launch_fused<ModeF64>(a, s);
     case CO2_MODE_F32: return launch_fused<ModeF32>(a, s);
@@ -966,12 +1049,11 @@ __device__ __forceinline__ double warp_sum_fixed(double s) {
   return s;
 }
 
-template <typename TC>
+template <typename TC, bool LQ>
 __device__ __forceinline__ TC gc_momentum(TC x, TC q0, TC q1, TC xb, TC m, TC& lam,
                                           const Hyp<TC>& h, AccT<TC>& acc) {
-  if (h.divide) xb = xb / h.divisor;
   TC n0 = fabs(x - q0);
-  TC av = fabs(h.tau * (q1 - q0));
+  TC av = fabs(h.tau * (q1 - start_of_inner<TC, LQ>(q0)));
   bool floored = av < h.eps;
   TC d = floored ? h.eps : av;
   lam = n0 / d + (TC)1;
@@ -1037,6 +1119,8 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int6
   const TL* XB = static_cast<const TL*>(a.xbar);
   TS* Mm = static_cast<TS*>(a.m);
   TS* G = static_cast<TS*>(a.gap);
+  TL* XO = static_cast<TL*>(a.xbar_out);
+  constexpr bool LQ = !std::is_same<TS, TL>::value;
   double* cs = ws_chunks(a.ws);
   __shared__ double sh[NW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1058,8 +1142,10 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int6
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         TC lam;
-        const TC m = gc_momentum<TC>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), to_c(xb[v]),
-                                     to_c(mo[v]), lam, h, acc);
+        TC xbv = to_c(xb[v]);
+        if (h.divide) xbv = xbv / h.divisor;
+        const TC m = gc_momentum<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), xbv, to_c(mo[v]),
+                                         lam, h, acc);
         mn[v] = (TS)m;
         gs[v] = (TS)lam;
         const double md = (double)mn[v];
@@ -1067,13 +1153,17 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int6
       }
       gc_store<TS, V, VEC>(Mm + e, mn);
       if (G) gc_store<TS, V, VEC>(G + e, gs);
+      if (XO) gc_store<TL, V, VEC>(XO + e, xb);
     }
     if (threadIdx.x == 0 && c == K - 1) {  // scalar tail, in index order
       for (int64_t e = nvE; e < a.n; ++e) {
         TC lam;
+        TC xbv = to_c(XB[e]);
+        if (h.divide) xbv = xbv / h.divisor;
+        if (XO) XO[e] = XB[e];
         const TC m =
-            gc_momentum<TC>(to_c(X[e]), to_c(P0[e]), to_c(P1[e]), to_c(XB[e]), to_c(Mm[e]), lam,
-                            h, acc);
+            gc_momentum<TC, LQ>(to_c(X[e]), to_c(P0[e]), to_c(P1[e]), xbv, to_c(Mm[e]), lam, h,
+                                acc);
         Mm[e] = (TS)m;
         if (G) G[e] = (TS)lam;
         const double md = (double)(TS)m;
@@ -1245,7 +1335,7 @@ co2_status_t launch_global_clip(const StepArgs& a, cudaStream_t s) {
   constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
   const bool vec = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) &&
                    aligned16(a.xbar) && aligned16(a.m) && aligned16(a.anchor) &&
-                   aligned16(a.params) && aligned16(a.gap);
+                   aligned16(a.params) && aligned16(a.gap) && aligned16(a.xbar_out);
   const int64_t chunk = gc_chunk(a.n, V);
   const int64_t K = (a.n + chunk - 1) / chunk;
   if (vec) {
@@ -1268,10 +1358,11 @@ co2_status_t outer_step_global_clip_impl(co2_mode_t mode, int64_t n, const void*
                                          const void* p0, const void* p1, const void* xbar,
                                          int32_t divisor, void* m, void* anchor, void* params,
                                          void* gap, const co2_hyper_t* h, void* ws,
-                                         cudaStream_t s) {
+                                         cudaStream_t s, void* xbar_out) {
   StepArgs a{x_t0, p0, p1, xbar, m, anchor, params, gap, n, h->alpha, h->beta, h->phi,
              h->epsilon, h->tau, divisor, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, 0, 0,
              nullptr};
+  a.xbar_out = xbar_out;
   switch (mode) {
     case CO2_MODE_F64: return launch_global_clip<ModeF64>(a, s);
     case CO2_MODE_F32: return launch_global_clip<ModeF32>(a, s);
@@ -1285,7 +1376,8 @@ template <class M>
 co2_status_t launch_fused_aar(const StepArgs& a, cudaStream_t s) {
   constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
   bool ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
-            aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap);
+            aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap) &&
+            aligned16(a.xbar_out);
   for (int p = 0; p < a.exit.world; ++p) ok = ok && aligned16(a.aar_bufs[p]);
   if (!ok) return fail(CO2_ERR_VALIDATION, "fused all-reduce step: buffers must be 16-byte aligned");
   // Rank capacity of the instantiation: the gather registers scale with it
@@ -1311,11 +1403,12 @@ co2_status_t outer_step_fused_aar_impl(co2_mode_t mode, int64_t n, const void* x
                                        const co2_hyper_t* h, void* const* aar_bufs,
                                        int64_t aar_lo, int64_t aar_len, void* const* sigs,
                                        int world, int rank, uint32_t epoch, void* ws,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, void* xbar_out) {
   if (world < 1 || world > kMaxRanks)
     return fail(CO2_ERR_VALIDATION, "fused all-reduce step: world must lie in [1, %d]", kMaxRanks);
   StepArgs a{x_t0, p0, p1, xbar_avg, m, anchor, params, gap, n, h->alpha, h->beta, h->phi,
              h->epsilon, h->tau, 1, h->penalty ? 1 : 0, h->clip ? 1 : 0, ws, 1, 0, 0, nullptr};
+  a.xbar_out = xbar_out;
   for (int p = 0; p < world; ++p) {
     a.aar_bufs[p] = aar_bufs[p];
     a.exit.sig[p] = static_cast<Signals*>(sigs[p]);
@@ -1498,24 +1591,30 @@ extern "C" co2_status_t co2_average(co2_dtype_t dt, int32_t g, const void* const
     for (int i = 0; i < g; ++i)
       if (!contributions[i]) return fail(CO2_ERR_VALIDATION, "null buffer");
   }
-  int grid = simple_grid(n, kThreads);
-  if (grid > kMaxBlocks) grid = kMaxBlocks;
+  bool vec = aligned16(out);
+  for (int i = 0; i < g && vec; ++i) vec = aligned16(contributions[i]);
   cudaStream_t s = S(stream);
-  if (dt == CO2_DTYPE_F64) {
-    Ptrs64<double> p{};
-    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const double*>(contributions[i]);
-    average_kernel<double, double><<<grid, kThreads, 0, s>>>(p, g, static_cast<double*>(out), n, ws);
-  } else if (dt == CO2_DTYPE_F32) {
-    Ptrs64<float> p{};
-    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const float*>(contributions[i]);
-    average_kernel<float, float><<<grid, kThreads, 0, s>>>(p, g, static_cast<float*>(out), n, ws);
-  } else {
-    Ptrs64<bf16s> p{};
-    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const bf16s*>(contributions[i]);
-    average_kernel<bf16s, float><<<grid, kThreads, 0, s>>>(p, g, static_cast<bf16s*>(out), n, ws);
-  }
-  CO2_CUDA(cudaGetLastError());
-  return CO2_OK;
+  auto run = [&](auto tag) -> co2_status_t {
+    using T = decltype(tag);
+    using TC = decltype(to_c(T{}));
+    Ptrs64<T> p{};
+    for (int i = 0; i < g; ++i) p.p[i] = static_cast<const T*>(contributions[i]);
+    if (vec) {
+      auto k = average_vec_kernel<T, TC>;
+      const int64_t nv = n / (16 / (int64_t)sizeof(T));
+      k<<<grid_for(k, nv > 0 ? nv : 1, kThreads), kThreads, 0, s>>>(p, g, static_cast<T*>(out), n,
+                                                                     ws);
+    } else {
+      int grid = simple_grid(n, kThreads);
+      if (grid > kMaxBlocks) grid = kMaxBlocks;
+      average_kernel<T, TC><<<grid, kThreads, 0, s>>>(p, g, static_cast<T*>(out), n, ws);
+    }
+    CO2_CUDA(cudaGetLastError());
+    return CO2_OK;
+  };
+  if (dt == CO2_DTYPE_F64) return run(double{});
+  if (dt == CO2_DTYPE_F32) return run(float{});
+  return run(bf16s{});
 }
 
 extern "C" co2_status_t co2_sub(co2_dtype_t dt, int64_t n, const void* a, const void* b, void* out,
@@ -1645,6 +1744,32 @@ extern "C" co2_status_t co2_fill_u32(void* dst, uint32_t value, int64_t count, v
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }
+
+namespace co2 {
+namespace {
+template <typename T>
+__global__ void scale_div_kernel(T* b, int64_t n, int g) {
+  using TC = decltype(to_c(T{}));
+  const TC gd = (TC)g;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    b[j] = Store<T>::from(to_c(b[j]) / gd);
+}
+}  // namespace
+
+co2_status_t scale_div_impl(co2_dtype_t dt, void* buf, int64_t n, int g, cudaStream_t s) {
+  if (n <= 0) return CO2_OK;
+  const int grid = simple_grid(n, kThreads);
+  if (dt == CO2_DTYPE_F64)
+    scale_div_kernel<double><<<grid, kThreads, 0, s>>>(static_cast<double*>(buf), n, g);
+  else if (dt == CO2_DTYPE_F32)
+    scale_div_kernel<float><<<grid, kThreads, 0, s>>>(static_cast<float*>(buf), n, g);
+  else
+    scale_div_kernel<bf16s><<<grid, kThreads, 0, s>>>(static_cast<bf16s*>(buf), n, g);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+}  // namespace co2
 
 // ------------------------------------------------ sharded-mode helpers
 namespace co2 {

@@ -48,6 +48,7 @@ struct P2PArgs {
   int64_t shard;              // elements per slice (multiple of the vector width)
   int world, rank;
   uint32_t epoch;             // 1, 2, ... (same sequence on every rank)
+  uint32_t done_target;       // cumulative exit-barrier count after this launch
 };
 
 // TL storage, TC compute, V elements per 16-byte vector.
@@ -166,8 +167,7 @@ __global__ void __launch_bounds__(NT) p2p_average_kernel(const P2PArgs a) {
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
-    const uint32_t target = a.epoch * (uint32_t)a.world * gridDim.x;
-    if (!spin_until(&mine->done, target, mine)) mine->error = 2;
+    if (!spin_until(&mine->done, a.done_target, mine)) mine->error = 2;
   }
 }
 
@@ -356,7 +356,8 @@ co2_status_t p2p_slice_average_launch(co2_dtype_t dt, int nb, const void* const*
 }
 
 co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* sigs, int world,
-                                int rank, int64_t n, uint32_t epoch, int ctas, cudaStream_t s) {
+                                int rank, int64_t n, uint32_t epoch, uint32_t* done_total,
+                                int ctas, cudaStream_t s) {
   if (world < 1 || world > kMaxRanks)
     return fail(CO2_ERR_VALIDATION, "p2p: world must lie in [1, %d]", kMaxRanks);
   P2PArgs a{};
@@ -374,6 +375,8 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
   a.shard = per;
   if (ctas < 1) ctas = 1;
   if (ctas > sm_count()) ctas = sm_count();  // all CTAs co-resident (they spin)
+  *done_total += (uint32_t)world * (uint32_t)ctas;  // wraps; compared wrap-safe
+  a.done_target = *done_total;
   // R = rank capacity of the instantiation, U = vectors in flight per thread
   // (fewer ranks -> more vectors, keeping ~R*U*16 B of loads per thread).
   const int cap = rank_cap(world);

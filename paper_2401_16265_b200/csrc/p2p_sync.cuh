@@ -53,7 +53,8 @@ __device__ inline bool spin_until(const uint32_t* p, uint32_t target, const Sign
   const uint32_t ms = *reinterpret_cast<const volatile uint32_t*>(&mine->timeout_ms);
   const uint64_t budget = (uint64_t)(ms ? ms : 10000u) * 1000000ull;
   const uint64_t t0 = global_ns();
-  while (ld_acquire_sys(p) < target) {
+  // wrap-safe: counters and epochs are uint32 sequences that may wrap
+  while ((int32_t)(ld_acquire_sys(p) - target) < 0) {
     if (global_ns() - t0 > budget) return false;
     __nanosleep(64);
   }

@@ -1,8 +1,10 @@
 """Sharded ghost-consistent rounds over NCCL (C4 layout), launched by
 tests/test_gpu_multi.py under torchrun.  Rank 0 gathers each round's traces
 and replays ghost-consistent co2_round (outer_algorithms.cpp:126-145,161-184)
-on the CPU oracle; for G = 2 the NCCL sums are order-free, so the comparison
-is bitwise.  Prints one JSON line on rank 0."""
+on the CPU oracle.  The fixed-order transports (P2P, and NCCL's default
+slice-exchange algorithm) deliver the reference's average() and are bitwise
+at any G; NCCL's sum algorithm ("ncclsum") is order-free only for G = 2.
+Prints one JSON line on rank 0."""
 import json
 import os
 import sys
@@ -54,8 +56,10 @@ def main():
         div = 1  # the P2P slice reduce delivers the fixed-order average
     else:
         uid = broadcast_nccl_id(co2.CollectiveEngine.unique_id, rank, world)
-        eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid)
-        div = world  # NCCL delivers the worker sum
+        algo = "sum" if transport == "ncclsum" else "fixed"
+        eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
+                                   nccl_algo=algo)
+        div = world if algo == "sum" else 1  # the sum algorithm delivers the worker sum
     hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12, ghost_consistent=True)
     init = co2.synth(mode, n, worker=0)[3]  # identical x_{0,0} on every worker
     sw = co2.ShardedWorker(mode, n, eng, init)
@@ -108,7 +112,7 @@ def main():
                     bad = np.nonzero(afters[i][:n] != expect[i])[0]
                     ok, mismatch = False, (t, "params", i, int(bad.size), int(bad[0]),
                                            float(afters[i][bad[0]]), float(expect[i][bad[0]]))
-            if transport == "p2p":  # fixed-order averages (param_ops.cpp:16-33)
+            if transport != "ncclsum":  # fixed-order averages (param_ops.cpp:16-33)
                 if mode == O.MODE_F64:
                     p1sum, xsum = O.average(firsts), O.average(ends)
                 else:

@@ -46,10 +46,17 @@ def test_full_size_windows_bitwise(name, mode, n, tau):
     assert d.flags == 0
     assert d.min_gap >= 1.0
     assert d.max_outer_step <= np.float32(5e-3) * (1 + 2.0 ** -16)
-    # stalled coordinates j % 61 == 0, plus the rare draws where p1 rounds back
-    # onto p0 (|1e-3 * (2U-1)| below half an ulp of p0)
+    # stalled coordinates j % 61 == 0, plus the draws where p1 rounds back onto
+    # the inner loop's start (|1e-3 * (2U-1)| below half an ulp): rare against
+    # fp32 p0, a few percent against the bf16 start of bf16-mixed (measured
+    # on the first window of the oracle: the fraction is size-independent)
     stalled = (n + 60) // 61
-    assert stalled <= d.n_floored <= stalled + n // 100000
+    if mode == co2.MODE_BF16_MIXED:
+        ox, op0, op1, _, _ = O.synth(mode, 1 << 20)
+        frac = np.count_nonzero(O.to_f64(op1) == O.to_f64(O.f32_to_bf16_bits(op0))) / (1 << 20)
+        assert stalled <= d.n_floored <= n * (frac + 0.005)
+    else:
+        assert stalled <= d.n_floored <= stalled + n // 100000
     assert 0 < d.n_clipped < n
     del x, p0, p1, xe, m
     torch.cuda.empty_cache()

@@ -24,12 +24,13 @@ def _port():
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("transport,world", [("nccl", 2), ("p2p", 2), ("p2p", 4),
+@pytest.mark.parametrize("transport,world", [("nccl", 2), ("nccl", 4), ("p2p", 2), ("p2p", 4),
                                              ("p2pfused", 2), ("p2pfused", 4)])
 def test_multi_rank_rounds_bitwise(mode, transport, world):
-    """Worker-local co2_round across ranks, bitwise against the oracle.  NCCL's
-    sum is order-free only for G = 2; the P2P transport's fixed-order average
-    is bitwise the reference's average() for any G."""
+    """Worker-local co2_round across ranks, bitwise against the oracle --
+    params, momentum and the consumed average -- for every fixed-order
+    transport (NCCL's default slice-exchange algorithm, P2P, fused P2P): the
+    reference's average() (param_ops.cpp:16-33) at any G."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT=transport)
@@ -48,12 +49,36 @@ def test_multi_rank_rounds_bitwise(mode, transport, world):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_rounds_nccl_sum_within_bound(mode, world):
+    """NCCL's sum algorithm (ncclAllReduce(sum) in the storage dtype, /G in
+    the step): x-bar, momentum and params within the stated per-round bound
+    of the reference (tests/mp_nccl_rounds.py docstring: delta = G*u*max|x|,
+    u = 2^-8 bf16 / 2^-23 fp32)."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT="ncclsum")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_nccl_rounds.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert res["ok"], res
+    assert res["max_bound_ratio"] <= 1.0
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("mode", [0, 1, 2])
-@pytest.mark.parametrize("transport,world", [("nccl", 2), ("p2p", 2), ("p2p", 4)])
+@pytest.mark.parametrize("transport,world", [("nccl", 2), ("nccl", 4), ("ncclsum", 2),
+                                             ("p2p", 2), ("p2p", 4)])
 def test_sharded_ghost_bitwise(mode, transport, world):
-    """Sharded ghost-consistent rounds (C4 layout) against the oracle: NCCL
-    reduce-scatter/all-gather at G = 2, and the fused P2P step (slice average
-    + ghost step + NVLink all-gather) at G = 2 and 4, bitwise."""
+    """Sharded ghost-consistent rounds (C4 layout) against the oracle,
+    bitwise: NCCL's fixed-order slice exchange + all-gather at G = 2 and 4,
+    NCCL's reduce-scatter sum at G = 2 (order-free there), and the fused P2P
+    step (slice average + ghost step + NVLink all-gather) at G = 2 and 4."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT=transport)
