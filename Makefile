@@ -37,6 +37,11 @@ facade_test: tests/cpp/facade_test.cpp include/co2_b200.hpp $(LIB)
 	    -o build/facade_test -L$(CSRC)/.. -lco2b200 -L/usr/local/cuda/lib64 -lcudart \
 	    -Wl,-rpath,'$$ORIGIN/../paper_2401_16265_b200'
 
+co2sim_round_test: tests/cpp/co2sim_round_test.cpp include/co2sim_b200.hpp include/co2_b200.hpp $(LIB)
+	g++ -std=c++17 -O2 -ffp-contract=off -Iinclude -I/usr/local/cuda/include \
+	    tests/cpp/co2sim_round_test.cpp -o build/co2sim_round_test -L$(CSRC)/.. -lco2b200 \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../paper_2401_16265_b200'
+
 round_example: tests/cpp/round_example.cpp include/co2_b200.h $(LIB)
 	g++ -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include tests/cpp/round_example.cpp \
 	    -o build/round_example -L$(CSRC)/.. -lco2b200 -L/usr/local/cuda/lib64 -lcudart \
@@ -45,4 +50,4 @@ round_example: tests/cpp/round_example.cpp include/co2_b200.h $(LIB)
 clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
-.PHONY: all oracle clean facade_test round_example
+.PHONY: all oracle clean facade_test round_example co2sim_round_test

@@ -306,10 +306,12 @@ def run_reference_arm(args, cfg, rank: int):
 
 # ----------------------------------------------------------------- GPU arm
 def run_local_workers(args, cfg) -> int:
-    """C1: G simulated workers on one GPU through the LOCAL engine (the
-    fixed-order average kernel + G fused steps per co2_round).  The buffers
-    (G x 1M fp32 x ~7 streams) are L2-resident, so this is a launch- and
-    cache-bound number, not an HBM roofline one."""
+    """C1: G simulated workers on one GPU through the LOCAL engine.  Every
+    co2_round (t >= 1) is ONE kernel (local_round_kernel): this round's
+    fixed-order average of the G contributions plus the G fused outer steps
+    on the previous average.  The working set (~120 MB) is about the L2
+    size, so L2 is flushed (a 512 MB write) before every timed round and
+    only the round itself is inside the CUDA events."""
     import torch
 
     from paper_2401_16265_b200 import co2
@@ -323,35 +325,54 @@ def run_local_workers(args, cfg) -> int:
         w.snapshot_first()
     co2.co2_round(ws, eng, hyper, tau)  # round 0
     stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(max(args.warmup, 3)):
         co2.co2_round(ws, eng, hyper, tau, sync=False)
+    ws[0].enable_timing(args.steps + 8)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
     with ClockSampler(torch, torch.cuda.current_device()) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
+        for e0, e1 in ev:
+            flush.zero_()  # evict the previous round's lines from L2
+            e0.record(stream)
             co2.co2_round(ws, eng, hyper, tau, sync=False)
-        e1.record(stream)
+            e1.record(stream)
         torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) * 1e-3
+    t = sum(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3
+    kt = ws[0].step_times()
+    k_mean = statistics.mean(kt) if kt else None
     r = co2.L.RoundResult()
     arr = (co2.C.c_void_p * g)(*[w.handle.value for w in ws])
     co2.check(co2.lib().co2_round_finish(arr, g, stream.cuda_stream, co2.C.byref(r)))
     value = g * n * args.steps / t
+    sb, lb = (8, 8) if mode == 0 else ((4, 4) if mode == 1 else (4, 2))
+    # per coordinate and round: G steps (x_t0, p0, m state + p1 low read;
+    # m, anchor state + params low written) + the consumed xbar once + the
+    # launched average (G contributions read, one written)
+    bytes_round = n * (g * (3 * sb + lb + 2 * sb + lb) + lb + g * lb + lb)
+    peak, peak_kind = peaks()
+    achieved = bytes_round / k_mean / 1e9 if k_mean else None
     line = {
         "metric": "CO2 outer-step params/s", "value": value, "unit": "params/s", "n_gpus": 1,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": {0: "f64", 1: "f32", 2: "bf16-mixed"}[mode],
-            "compute_dtype": "f64" if mode == 0 else "f32",
+        "compute_dtype": "f64" if mode == 0 else "f32",
         "data": "synthetic (counter-SplitMix64 uniforms, SURVEY.md 8d)",
         "config": {"workload": cfg["workload"], "n_params_per_worker": n, "workers": g,
                    "tau": tau, "hyper": HYPER,
-                   "l2": "L2-resident working set: a launch/cache-bound number, not HBM",
-                   "step": "co2_round over 4 simulated workers: fixed-order average kernel + "
-                           "4 fused outer steps"},
-        "roofline": None, "e2e": None, "cpu_baseline": None,
-        "gpu_launches": args.steps * (g + 1), "clocks": clk.summary(),
+                   "l2": "L2 flushed (512 MB write) before every timed round; the flush is "
+                         "outside the per-round CUDA events",
+                   "step": f"co2_round over {g} simulated workers: ONE kernel = fixed-order "
+                           f"average of x_t,tau + {g} fused outer steps on the stale average"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "algorithmic_bytes": bytes_round, "peak_kind": peak_kind,
+                     "kernel": "local_round_kernel", "kernel_ms": k_mean * 1e3 if k_mean else None,
+                     "bytes_per_param": bytes_round / (g * n)},
+        "e2e": None, "cpu_baseline": None,
+        "gpu_launches": args.steps, "clocks": clk.summary(),
         "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step},
     }
     print(json.dumps(line), flush=True)

@@ -369,6 +369,11 @@ co2_status_t co2_aar_poll(co2_aar_t* engine, uint64_t handle, int32_t* done);
 co2_status_t co2_aar_wait(co2_aar_t* engine, uint64_t handle, void* consumer_stream);
 co2_status_t co2_aar_stall(co2_aar_t* engine, uint64_t handle, double* stall_seconds,
                            double* comm_seconds);
+/* Make `stream` wait for the reduce to finish WITHOUT consuming the handle,
+ * so the caller may overwrite the contributions afterwards (the reference's
+ * launch snapshots them, collective.cpp:44-50; the C++ facade's value-
+ * semantics launch_all_reduce uses this). */
+co2_status_t co2_aar_order_after(co2_aar_t* engine, uint64_t handle, void* stream);
 co2_status_t co2_aar_live(const co2_aar_t* engine, int32_t* live);
 /* info(handle) (collective.hpp:40-50,68): HandleInfo from device events.
  * Times are seconds since engine creation; completion_time is valid once

@@ -134,6 +134,7 @@ SIGNATURES = {
     "co2_aar_p2p_detach": (ST, [P, P]),
     "co2_aar_set_fused": (ST, [P, I32]),
     "co2_aar_set_nccl_algo": (ST, [P, I32]),
+    "co2_aar_order_after": (ST, [P, U64, P]),
     "co2_aar_destroy": (ST, [P]),
     "co2_aar_world": (I32, [P]),
     "co2_aar_launch": (ST, [P, I32, C.POINTER(P), P, I64, P, C.POINTER(U64)]),

@@ -115,6 +115,7 @@ struct co2_aar {
   std::map<std::pair<int, std::string>, Opened> opened;
   // pinned per-launch slots (ring) and the reusable producer fence
   co2_diag_t* pin_diag = nullptr;
+  co2_diag_t* pin_diag_dev = nullptr;  // device mapping of pin_diag
   uint32_t* pin_err = nullptr;
   cudaEvent_t fence = nullptr;
 };
@@ -524,6 +525,7 @@ static co2_status_t new_handle(co2_aar* e, Handle* h) {
   const size_t id = e->handles.size();
   if (!e->pin_diag) {
     CO2_CUDA(cudaMallocHost(&e->pin_diag, kRing * sizeof(co2_diag_t)));
+    CO2_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->pin_diag_dev), e->pin_diag, 0));
     CO2_CUDA(cudaMallocHost(&e->pin_err, kRing * sizeof(uint32_t)));
     CO2_CUDA(cudaEventCreateWithFlags(&e->fence, cudaEventDisableTiming));
   }
@@ -697,6 +699,17 @@ extern "C" co2_status_t co2_aar_wait(co2_aar_t* e, uint64_t handle, void* consum
   return CO2_OK;
 }
 
+extern "C" co2_status_t co2_aar_order_after(co2_aar_t* e, uint64_t handle, void* stream) {
+  // Orders `stream`'s later work after the reduce without consuming it: the
+  // reference's launch snapshots its contributions (collective.cpp:44-50),
+  // so a value-semantics caller may overwrite them right after the launch.
+  Handle* h = nullptr;
+  CO2_TRY(record_for(e, handle, &h));
+  if (h->consumed) return fail(CO2_ERR_VALIDATION, "order_after: handle already consumed");
+  CO2_CUDA(cudaStreamWaitEvent(S(stream), h->done, 0));
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_aar_stall(co2_aar_t* e, uint64_t handle, double* stall,
                                       double* comm) {
   Handle* h = nullptr;
@@ -823,6 +836,7 @@ struct co2_worker {
   bool keep_avg = false;
   void* ws = nullptr;
   co2_diag_t* host_diag = nullptr;  // pinned
+  co2_diag_t* host_diag_dev = nullptr;  // its device mapping (kernels write it directly)
   // fused P2P schedule: pinned copy of the engine's signal error word, read
   // back after every fused round (a timed-out barrier means the consumed
   // average is incomplete); checked by co2_round_finish and the next round
@@ -890,6 +904,7 @@ extern "C" co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, i
   }
   cudaStream_t st = S(stream);
   CO2_CUDA(cudaMallocHost(&w->host_diag, sizeof(co2_diag_t)));
+  CO2_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&w->host_diag_dev), w->host_diag, 0));
   CO2_CUDA(cudaMemsetAsync(w->ws, 0, co2_workspace_bytes(), st));
   // OuterState init, outer_algorithms.cpp:416-418: momentum zeros, gap ones.
   CO2_CUDA(cudaMemsetAsync(w->m, 0, sb ? sb : 1, st));
@@ -1058,6 +1073,99 @@ static co2_status_t check_round_args(co2_worker_t* const* ws, int32_t g, const c
   return CO2_OK;
 }
 
+// Single-launch LOCAL round (C1): rounds t >= 1 of the
+// worker-local branch with up to kMaxLocalRound simulated workers run as one
+// kernel that both averages this round's x_{t,tau} (the launch) and applies
+// every worker's step on the previous average (the consume) -- see
+// local_round_kernel.  CO2_LOCAL_ROUND=split keeps the two-kernel schedule.
+static bool local_round_fused_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("CO2_LOCAL_ROUND");
+    return !(v && strcmp(v, "split") == 0);
+  }();
+  return on;
+}
+
+static co2_status_t local_round_fused(co2_worker_t* const* ws, int32_t g, co2_aar* e,
+                                      const co2_hyper_t* hyper, void* stream, int32_t sync,
+                                      co2_round_result_t* res) {
+  co2_worker* w0 = ws[0];
+  cudaStream_t st = S(stream);
+  if (!w0->has_pending)  // shared_pending, outer_algorithms.cpp:22-26
+    return fail(CO2_ERR_VALIDATION, "outer round: no pending reduce to consume");
+  if (e->live >= 2)
+    return fail(CO2_ERR_VALIDATION,
+                "launch_all_reduce: overlap window exceeded, two reduces already live");
+  const uint64_t prev = w0->pending;
+  int32_t done = 0;
+  CO2_TRY(co2_aar_poll(e, prev, &done));  // :155-157
+  CO2_TRY(co2_aar_wait(e, prev, stream));
+  const int t = w0->t;
+  void* xbar = w0->avg[(t - 1) % 2];
+  void* avg_out = w0->avg[t % 2];
+  const void *x0[kMaxLocalRound], *p0[kMaxLocalRound], *p1[kMaxLocalRound],
+      *cur[kMaxLocalRound];
+  void *m[kMaxLocalRound], *an[kMaxLocalRound], *pr[kMaxLocalRound], *gp[kMaxLocalRound],
+      *wsp[kMaxLocalRound];
+  co2_diag_t* hd[kMaxLocalRound];
+  for (int i = 0; i < g; ++i) {
+    co2_worker* w = ws[i];
+    x0[i] = w->anchor;
+    p0[i] = w->prev_x0;
+    p1[i] = w->prev_x1;
+    cur[i] = w->params[w->cur];
+    m[i] = w->m;
+    an[i] = w->prev_x0;  // x_{t+1,0} over prev_x0 (the rotation swaps it in)
+    pr[i] = w->params[1 - w->cur];
+    gp[i] = w->gap;
+    wsp[i] = w->ws;
+    hd[i] = w->host_diag_dev;
+  }
+  Handle h;
+  CO2_TRY(new_handle(e, &h));
+  h.contributions = g;
+  const size_t slot = e->handles.size() % kRing;
+  CO2_CUDA(cudaEventRecord(h.start, st));
+  const int64_t cap = (int64_t)w0->tev.size() / 2;
+  const int64_t tslot = cap ? w0->tev_recorded % cap : 0;
+  if (cap) CO2_CUDA(cudaEventRecord(w0->tev[2 * tslot], st));
+  CO2_TRY(local_round_impl(w0->mode, g, w0->n, x0, p0, p1, m, an, pr, gp, cur, wsp, hd,
+                           e->pin_diag_dev + slot, xbar, avg_out, hyper, st));
+  if (cap) {
+    CO2_CUDA(cudaEventRecord(w0->tev[2 * tslot + 1], st));
+    w0->tev_recorded += 1;
+  }
+  CO2_CUDA(cudaEventRecord(h.done, st));
+  e->handles.push_back(h);
+  e->live += 1;
+  const uint64_t launched = e->handles.size() - 1;
+  for (int i = 0; i < g; ++i) {
+    co2_worker* w = ws[i];
+    std::swap(w->anchor, w->prev_x0);  // anchor <- x_{t+1,0}; prev_x0 <- x_{t,0}
+    std::swap(w->prev_x1, w->xfirst);  // prev_x1 <- x_{t,1}
+    w->cur = 1 - w->cur;
+    w->xbar = xbar;
+    w->consumed = prev;
+    w->has_consumed = true;
+    w->pending = launched;
+    w->t += 1;
+  }
+  co2_round_result_t r{};
+  r.min_gap = INFINITY;
+  r.outer_applied = 1;
+  if (sync) {
+    co2_status_t s1 = co2_round_finish(ws, g, stream, &r);
+    double stall = 0.0;
+    co2_status_t s2 = co2_aar_stall(e, prev, &stall, nullptr);
+    r.stall_seconds = stall;
+    if (res) *res = r;
+    if (s1 != CO2_OK) return s1;
+    return s2;
+  }
+  if (res) *res = r;
+  return CO2_OK;
+}
+
 extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
                                   const co2_hyper_t* hyper, void* stream, int32_t sync,
                                   co2_round_result_t* res) {
@@ -1088,6 +1196,12 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
   const bool local = e->transport == T_LOCAL;
   co2_round_result_t r{};
   r.min_gap = INFINITY;
+  if (local && w0->t > 0 && !hyper->ghost_consistent && g <= kMaxLocalRound && w0->avg[0] &&
+      local_round_fused_enabled()) {
+    bool coord = true;
+    for (int i = 0; i < g; ++i) coord = coord && ws[i]->clip_mode == CO2_CLIP_COORDINATE;
+    if (coord) return local_round_fused(ws, g, e, hyper, stream, sync, res);
+  }
 
   // 1. Launch the reduce of x_{t,tau} (:120).
   if (local && !w0->avg[0]) {

@@ -1941,6 +1941,358 @@ co2_status_t overlap_correction_impl(co2_mode_t mode, int64_t n, void* params, c
 
 }  // namespace co2
 
+namespace co2 {
+namespace {
+// ================================================ single-launch LOCAL round
+// C1 (BASELINE configs[0]): G simulated workers on one GPU.  One co2_round
+// (outer_algorithms.cpp:110-211, worker-local branch, t >= 1) as ONE grid:
+//   * this round's launch_all_reduce of x_{t,tau} (collect_params, :120):
+//     the fixed-order average of every worker's params into avg_out
+//     (param_ops.cpp:16-33: ascending worker order, one division);
+//   * every worker's fused outer step consuming the previous round's
+//     average xbar (:186-202), in worker order per tile, so xbar is read from
+//     HBM once per tile and from L1 for the other workers.
+// The two halves touch disjoint buffers (the average reads params[cur] and
+// writes avg[t%2]; the steps read avg[(t-1)%2] and write params[1-cur],
+// m and the anchor), so one grid is exactly the two-kernel schedule.  Per
+// element every op is the fused step's / average_kernel's, so results and
+// per-worker diagnostics are bitwise those of the separate launches.
+// Diagnostics: per worker, warp -> smem -> per-CTA partials in that worker's
+// workspace; the last CTA (ticket in worker 0's workspace) folds each in
+// fixed order and also writes it straight into the worker's pinned host
+// diag (device-mapped), so no per-worker D2H copy is issued.
+struct LocalRoundArgs {
+  const void* x_t0[kMaxLocalRound];
+  const void* p0[kMaxLocalRound];
+  const void* p1[kMaxLocalRound];
+  void* m[kMaxLocalRound];
+  void* anchor[kMaxLocalRound];
+  void* params[kMaxLocalRound];
+  void* gap[kMaxLocalRound];
+  const void* cur[kMaxLocalRound];  // x_{t,tau}: this round's contributions
+  void* ws[kMaxLocalRound];
+  co2_diag_t* host_diag[kMaxLocalRound];  // device-mapped pinned (nullable)
+  co2_diag_t* avg_diag;                   // device-mapped pinned (nullable)
+  const void* xbar;                       // the average consumed this round
+  void* avg_out;                          // this round's average
+  int g;
+  int64_t n;
+  double alpha, beta, phi, eps;
+  int tau, penalty, clip;
+};
+
+template <class M, int KG, int V, int NT>
+__global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  constexpr bool LQ = !std::is_same<TS, TL>::value;
+  Hyp<TC> h;
+  h.tau = (TC)a.tau;
+  h.eps = (TC)a.eps;
+  h.beta = (TC)a.beta;
+  h.phi = (TC)a.phi;
+  h.alpha = (TC)a.alpha;
+  h.divisor = (TC)1;
+  h.penalty = a.penalty;
+  h.clip = a.clip;
+  h.divide = 0;
+  const TC gd = (TC)a.g;
+  AccT<TC> acc[KG];
+  unsigned int avg_flags = 0;
+  const int64_t nv = a.n / V;
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  const TL* XB = static_cast<const TL*>(a.xbar);
+  TL* AO = static_cast<TL*>(a.avg_out);
+  auto step_one = [&](int w, int64_t e, int cnt) {
+    // cnt = V (vector) or 1 (scalar tail element e)
+    const TS* X = static_cast<const TS*>(a.x_t0[w]);
+    const TS* P0 = static_cast<const TS*>(a.p0[w]);
+    const TL* P1 = static_cast<const TL*>(a.p1[w]);
+    TS* Mm = static_cast<TS*>(a.m[w]);
+    TS* A = static_cast<TS*>(a.anchor[w]);
+    TL* PR = static_cast<TL*>(a.params[w]);
+    TS* G = static_cast<TS*>(a.gap[w]);
+    TS x[V], q0[V], mo[V], mn[V], xs[V], gs[V];
+    TL q1[V], xb[V], xl[V];
+    if (cnt == V) {
+      ld_vec<TS, V>(X + e, x);
+      ld_vec<TS, V>(P0 + e, q0);
+      ld_vec<TL, V>(P1 + e, q1);
+      ld_vec<TS, V>(Mm + e, mo);
+      // xbar: default-cached, so the first worker's load brings the tile
+      // into L1 for the others
+      constexpr int XBYTES = V * (int)sizeof(TL);
+      if constexpr (XBYTES % 16 == 0) {
+        uint4 r[XBYTES / 16];
+#pragma unroll
+        for (int k = 0; k < XBYTES / 16; ++k) r[k] = reinterpret_cast<const uint4*>(XB + e)[k];
+        memcpy(xb, r, XBYTES);
+      } else if constexpr (XBYTES == 8) {
+        uint2 r = *reinterpret_cast<const uint2*>(XB + e);
+        memcpy(xb, &r, 8);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) xb[v] = XB[e + v];
+      }
+    } else {
+      x[0] = X[e];
+      q0[0] = P0[e];
+      q1[0] = P1[e];
+      mo[0] = Mm[e];
+      xb[0] = XB[e];
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (v < cnt) {
+        TC m = to_c(mo[v]), xn, lam;
+        co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), to_c(xb[v]), m, xn, lam, h,
+                         acc[w]);
+        mn[v] = (TS)m;
+        xs[v] = (TS)xn;
+        gs[v] = (TS)lam;
+        xl[v] = Store<TL>::from(xn);
+      }
+    }
+    if (cnt == V) {
+      st_vec<TS, V>(Mm + e, mn);
+      if (A) st_vec<TS, V>(A + e, xs);
+      st_vec<TL, V>(PR + e, xl);
+      if (G) st_vec<TS, V>(G + e, gs);
+    } else {
+      Mm[e] = mn[0];
+      if (A) A[e] = xs[0];
+      PR[e] = xl[0];
+      if (G) G[e] = gs[0];
+    }
+  };
+  auto average_one = [&](int64_t e, int cnt) {
+    TC sacc[V];
+#pragma unroll
+    for (int w = 0; w < KG; ++w) {
+      if (w < a.g) {
+        const TL* C = static_cast<const TL*>(a.cur[w]);
+        TL c[V];
+        if (cnt == V) {
+          ld_vec<TL, V>(C + e, c);
+        } else {
+          c[0] = C[e];
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) sacc[v] = (w == 0) ? to_c(c[v]) : sacc[v] + to_c(c[v]);
+      }
+    }
+    TL o[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (v < cnt) {
+        const TC r = sacc[v] / gd;
+        if (!isfinite(r)) avg_flags |= CO2_FLAG_AVG_NONFINITE;
+        o[v] = Store<TL>::from(r);
+      }
+    }
+    if (cnt == V)
+      st_vec<TL, V>(AO + e, o);
+    else
+      AO[e] = o[0];
+  };
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < nv; i += stride) {
+    const int64_t e = i * V;
+    average_one(e, V);
+#pragma unroll
+    for (int w = 0; w < KG; ++w)
+      if (w < a.g) step_one(w, e, V);
+  }
+  {  // scalar tail (n % V coordinates), one per thread
+    const int64_t t = nv * V + (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (V > 1 && t < a.n) {
+      average_one(t, 1);
+#pragma unroll
+      for (int w = 0; w < KG; ++w)
+        if (w < a.g) step_one(w, t, 1);
+    }
+  }
+  // ---- per-worker diagnostics: the block_finish fold, once per worker
+  constexpr int NW = NT / 32;
+  __shared__ Partial sh[KG][NW];
+  __shared__ unsigned int sh_avg[NW];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int w = 0; w < KG; ++w) {
+    const Acc b = acc[w].widen();
+    double mg = b.min_gap, ms = b.max_step;
+    unsigned long long cl = b.clipped, fl = b.floored;
+    unsigned int fg = b.flags;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double omg = __shfl_xor_sync(0xffffffffu, mg, o);
+      double oms = __shfl_xor_sync(0xffffffffu, ms, o);
+      mg = omg < mg ? omg : mg;
+      ms = oms > ms ? oms : ms;
+      cl += __shfl_xor_sync(0xffffffffu, cl, o);
+      fl += __shfl_xor_sync(0xffffffffu, fl, o);
+      fg |= __shfl_xor_sync(0xffffffffu, fg, o);
+    }
+    if (lane == 0) sh[w][wid] = Partial{mg, ms, cl, fl, fg, 0u};
+  }
+  {
+    unsigned int af = avg_flags;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) af |= __shfl_xor_sync(0xffffffffu, af, o);
+    if (lane == 0) sh_avg[wid] = af;
+  }
+  __syncthreads();
+  WsHeader* hdr0 = ws_header(a.ws[0]);
+  if (threadIdx.x < KG && (int)threadIdx.x < a.g) {
+    const int w = threadIdx.x;
+    Partial b = sh[w][0];
+    for (int k = 1; k < NW; ++k) {  // fixed order
+      b.min_gap = sh[w][k].min_gap < b.min_gap ? sh[w][k].min_gap : b.min_gap;
+      b.max_step = sh[w][k].max_step > b.max_step ? sh[w][k].max_step : b.max_step;
+      b.clipped += sh[w][k].clipped;
+      b.floored += sh[w][k].floored;
+      b.flags |= sh[w][k].flags;
+    }
+    if (w == 0) {
+      unsigned int af = 0;
+      for (int k = 0; k < NW; ++k) af |= sh_avg[k];
+      b.pad = af;  // the average's flags ride in worker 0's partial
+    }
+    ws_partials(a.ws[w])[blockIdx.x] = b;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&hdr0->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int w = 0; w < a.g && w < KG; ++w) {
+    const Partial* parts = ws_partials(a.ws[w]);
+    Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+      const Partial* q = parts + i;
+      double qmg = __ldcg(&q->min_gap), qms = __ldcg(&q->max_step);
+      b.min_gap = qmg < b.min_gap ? qmg : b.min_gap;
+      b.max_step = qms > b.max_step ? qms : b.max_step;
+      b.clipped += __ldcg(&q->clipped);
+      b.floored += __ldcg(&q->floored);
+      b.flags |= __ldcg(&q->flags);
+      b.pad |= __ldcg(&q->pad);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double omg = __shfl_xor_sync(0xffffffffu, b.min_gap, o);
+      double oms = __shfl_xor_sync(0xffffffffu, b.max_step, o);
+      b.min_gap = omg < b.min_gap ? omg : b.min_gap;
+      b.max_step = oms > b.max_step ? oms : b.max_step;
+      b.clipped += __shfl_xor_sync(0xffffffffu, b.clipped, o);
+      b.floored += __shfl_xor_sync(0xffffffffu, b.floored, o);
+      b.flags |= __shfl_xor_sync(0xffffffffu, b.flags, o);
+      b.pad |= __shfl_xor_sync(0xffffffffu, b.pad, o);
+    }
+    __syncthreads();
+    if (lane == 0) sh[0][wid] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Partial r = sh[0][0];
+      for (int k = 1; k < NW; ++k) {
+        r.min_gap = sh[0][k].min_gap < r.min_gap ? sh[0][k].min_gap : r.min_gap;
+        r.max_step = sh[0][k].max_step > r.max_step ? sh[0][k].max_step : r.max_step;
+        r.clipped += sh[0][k].clipped;
+        r.floored += sh[0][k].floored;
+        r.flags |= sh[0][k].flags;
+        r.pad |= sh[0][k].pad;
+      }
+      co2_diag_t d;
+      d.min_gap = r.min_gap;
+      d.max_outer_step = r.max_step;
+      d.n_clipped = (int64_t)r.clipped;
+      d.n_floored = (int64_t)r.floored;
+      d.flags = r.flags;
+      d.pad = 0;
+      ws_header(a.ws[w])->diag = d;
+      if (a.host_diag[w]) *a.host_diag[w] = d;
+      if (w == 0 && a.avg_diag) {
+        co2_diag_t ad{INFINITY, 0.0, 0, 0, r.pad, 0};
+        *a.avg_diag = ad;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    hdr0->ticket = 0;  // self-reset for the next launch
+    __threadfence_system();
+  }
+}
+
+template <class M, int KG>
+co2_status_t launch_local_round(const LocalRoundArgs& a, bool vec, cudaStream_t s) {
+  constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+  if (vec) {
+    auto k = local_round_kernel<M, KG, V, kThreads>;
+    k<<<grid_for(k, a.n / V > 0 ? a.n / V : 1, kThreads), kThreads, 0, s>>>(a);
+  } else {
+    auto k = local_round_kernel<M, KG, 1, kThreads>;
+    k<<<grid_for(k, a.n > 0 ? a.n : 1, kThreads), kThreads, 0, s>>>(a);
+  }
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+template <class M>
+co2_status_t launch_local_round_g(const LocalRoundArgs& a, bool vec, cudaStream_t s) {
+  if (a.g <= 2) return launch_local_round<M, 2>(a, vec, s);
+  if (a.g <= 4) return launch_local_round<M, 4>(a, vec, s);
+  return launch_local_round<M, 8>(a, vec, s);
+}
+}  // namespace
+
+co2_status_t local_round_impl(co2_mode_t mode, int g, int64_t n, const void* const* x_t0,
+                              const void* const* p0, const void* const* p1, void* const* m,
+                              void* const* anchor, void* const* params, void* const* gap,
+                              const void* const* cur, void* const* ws,
+                              co2_diag_t* const* host_diag, co2_diag_t* avg_diag,
+                              const void* xbar, void* avg_out, const co2_hyper_t* h,
+                              cudaStream_t s) {
+  if (g < 1 || g > kMaxLocalRound)
+    return fail(CO2_ERR_VALIDATION, "local round: 1..%d workers", kMaxLocalRound);
+  LocalRoundArgs a{};
+  bool vec = aligned16(xbar) && aligned16(avg_out);
+  for (int w = 0; w < g; ++w) {
+    a.x_t0[w] = x_t0[w];
+    a.p0[w] = p0[w];
+    a.p1[w] = p1[w];
+    a.m[w] = m[w];
+    a.anchor[w] = anchor[w];
+    a.params[w] = params[w];
+    a.gap[w] = gap[w];
+    a.cur[w] = cur[w];
+    a.ws[w] = ws[w];
+    a.host_diag[w] = host_diag ? host_diag[w] : nullptr;
+    vec = vec && aligned16(x_t0[w]) && aligned16(p0[w]) && aligned16(p1[w]) && aligned16(m[w]) &&
+          aligned16(anchor[w]) && aligned16(params[w]) && aligned16(gap[w]) && aligned16(cur[w]);
+  }
+  a.avg_diag = avg_diag;
+  a.xbar = xbar;
+  a.avg_out = avg_out;
+  a.g = g;
+  a.n = n;
+  a.alpha = h->alpha;
+  a.beta = h->beta;
+  a.phi = h->phi;
+  a.eps = h->epsilon;
+  a.tau = h->tau;
+  a.penalty = h->penalty ? 1 : 0;
+  a.clip = h->clip ? 1 : 0;
+  switch (mode) {
+    case CO2_MODE_F64: return launch_local_round_g<ModeF64>(a, vec, s);
+    case CO2_MODE_F32: return launch_local_round_g<ModeF32>(a, vec, s);
+    case CO2_MODE_BF16_MIXED: return launch_local_round_g<ModeBF16>(a, vec, s);
+  }
+  return fail(CO2_ERR_VALIDATION, "local round: unknown mode %d", (int)mode);
+}
+}  // namespace co2
+
 // ====================================================== divergence metric
 // Simulation::step's round diagnostic (proj/src/outer_algorithms.cpp:
 // 503-508): xbar = average_params() (fixed worker order, one division) and

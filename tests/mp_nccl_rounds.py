@@ -92,12 +92,13 @@ def main():
         if rank == 0:
             consumed = orr.pending  # the average the oracle consumes this round
             ends = [tr[2] for tr in traces]
+            bf = mode == O.MODE_BF16_MIXED
+            u = 2.0 ** -8 if bf else 2.0 ** -23
             if t >= 1 and not exact:
-                bf = mode == O.MODE_BF16_MIXED
-                u = 2.0 ** -8 if bf else 2.0 ** -23
-                xmax = np.max(np.stack([np.abs(O.to_f64(e)) for e in ends]), axis=0)
-                delta = world * u * xmax
+                # the consumed average reduces the PREVIOUS round's x_{t,tau}
+                delta = world * u * prev_xmax
                 prev_m = [mm.copy() for mm in orr.m]
+            prev_xmax = np.max(np.stack([np.abs(O.to_f64(e)) for e in ends]), axis=0)
             ref = orr.round(ends, traces, np.zeros(n, np.float32))
             for i in range(world):
                 if exact:

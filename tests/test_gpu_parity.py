@@ -409,6 +409,19 @@ def test_cpp_round_driver_binary():
     assert "ROUNDS OK" in r.stdout
 
 
+def test_cpp_co2sim_round_facade_replays_fixture():
+    """The reference-shaped round API (include/co2sim_b200.hpp: co2sim::
+    co2_round over WorkerState / OuterState / InnerTrace / CollectiveEngine /
+    Clock, outer_algorithms.hpp:77-81) replays proj/fixtures/co2_dim1.json at
+    tolerance 0, plus the engine audit and the ghost branch."""
+    exe = os.path.join(ROOT, "build", "co2sim_round_test")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", ROOT, "co2sim_round_test"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "co2sim round facade: all passed" in r.stdout
+
+
 def test_cpp_facade_binary():
     exe = os.path.join(ROOT, "build", "facade_test")
     if not os.path.exists(exe):
