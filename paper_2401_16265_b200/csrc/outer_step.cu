@@ -1981,7 +1981,7 @@ struct LocalRoundArgs {
   int tau, penalty, clip;
 };
 
-template <class M, int KG, int V, int NT>
+template <class M, int V, int NT>
 __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
@@ -1997,177 +1997,155 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
   h.penalty = a.penalty;
   h.clip = a.clip;
   h.divide = 0;
-  const TC gd = (TC)a.g;
-  AccT<TC> acc[KG];
-  unsigned int avg_flags = 0;
+  // Roles: thread-item k of the flattened (vector, role) space is vector
+  // k / R, role k % R with R = g + 1 (roles 0..g-1: worker g's step; role g:
+  // this round's average).  The host makes gridDim.x * NT a multiple of R,
+  // so a thread's role is fixed and it keeps ONE accumulator; the G + 1
+  // items of a vector are adjacent lanes, so xbar is fetched from HBM once.
+  const int R = a.g + 1;
+  const int64_t gt = (int64_t)blockIdx.x * NT + threadIdx.x;
+  const int role = (int)(gt % R);
+  const int64_t vstride = (int64_t)gridDim.x * NT / R;
   const int64_t nv = a.n / V;
-  const int64_t stride = (int64_t)gridDim.x * NT;
+  AccT<TC> acc;
+  unsigned int avg_flags = 0;
   const TL* XB = static_cast<const TL*>(a.xbar);
-  TL* AO = static_cast<TL*>(a.avg_out);
-  auto step_one = [&](int w, int64_t e, int cnt) {
-    // cnt = V (vector) or 1 (scalar tail element e)
-    const TS* X = static_cast<const TS*>(a.x_t0[w]);
-    const TS* P0 = static_cast<const TS*>(a.p0[w]);
-    const TL* P1 = static_cast<const TL*>(a.p1[w]);
-    TS* Mm = static_cast<TS*>(a.m[w]);
-    TS* A = static_cast<TS*>(a.anchor[w]);
-    TL* PR = static_cast<TL*>(a.params[w]);
-    TS* G = static_cast<TS*>(a.gap[w]);
-    TS x[V], q0[V], mo[V], mn[V], xs[V], gs[V];
-    TL q1[V], xb[V], xl[V];
-    if (cnt == V) {
-      ld_vec<TS, V>(X + e, x);
-      ld_vec<TS, V>(P0 + e, q0);
-      ld_vec<TL, V>(P1 + e, q1);
-      ld_vec<TS, V>(Mm + e, mo);
-      // xbar: default-cached, so the first worker's load brings the tile
-      // into L1 for the others
-      constexpr int XBYTES = V * (int)sizeof(TL);
-      if constexpr (XBYTES % 16 == 0) {
-        uint4 r[XBYTES / 16];
+  if (role < a.g) {
+    const TS* X = static_cast<const TS*>(a.x_t0[role]);
+    const TS* P0 = static_cast<const TS*>(a.p0[role]);
+    const TL* P1 = static_cast<const TL*>(a.p1[role]);
+    TS* Mm = static_cast<TS*>(a.m[role]);
+    TS* A = static_cast<TS*>(a.anchor[role]);
+    TL* PR = static_cast<TL*>(a.params[role]);
+    TS* G = static_cast<TS*>(a.gap[role]);
+    auto step = [&](int64_t e, int cnt) {
+      TS x[V], q0[V], mo[V], mn[V], xs[V], gs[V];
+      TL q1[V], xb[V], xl[V];
+      if (cnt == V) {
+        ld_vec<TS, V>(X + e, x);
+        ld_vec<TS, V>(P0 + e, q0);
+        ld_vec<TL, V>(P1 + e, q1);
+        ld_vec<TS, V>(Mm + e, mo);
+        // default-cached: the vector's other workers hit it in L1 / L2
+        constexpr int XBYTES = V * (int)sizeof(TL);
+        if constexpr (XBYTES % 16 == 0) {
+          uint4 r[XBYTES / 16];
 #pragma unroll
-        for (int k = 0; k < XBYTES / 16; ++k) r[k] = reinterpret_cast<const uint4*>(XB + e)[k];
-        memcpy(xb, r, XBYTES);
-      } else if constexpr (XBYTES == 8) {
-        uint2 r = *reinterpret_cast<const uint2*>(XB + e);
-        memcpy(xb, &r, 8);
+          for (int k = 0; k < XBYTES / 16; ++k) r[k] = reinterpret_cast<const uint4*>(XB + e)[k];
+          memcpy(xb, r, XBYTES);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) xb[v] = XB[e + v];
+        }
       } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v) xb[v] = XB[e + v];
+        x[0] = X[e];
+        q0[0] = P0[e];
+        q1[0] = P1[e];
+        mo[0] = Mm[e];
+        xb[0] = XB[e];
       }
-    } else {
-      x[0] = X[e];
-      q0[0] = P0[e];
-      q1[0] = P1[e];
-      mo[0] = Mm[e];
-      xb[0] = XB[e];
-    }
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (v < cnt) {
-        TC m = to_c(mo[v]), xn, lam;
-        co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), to_c(xb[v]), m, xn, lam, h,
-                         acc[w]);
-        mn[v] = (TS)m;
-        xs[v] = (TS)xn;
-        gs[v] = (TS)lam;
-        xl[v] = Store<TL>::from(xn);
+      for (int v = 0; v < V; ++v) {
+        if (v < cnt) {
+          TC m = to_c(mo[v]), xn, lam;
+          co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), to_c(xb[v]), m, xn, lam, h,
+                           acc);
+          mn[v] = (TS)m;
+          xs[v] = (TS)xn;
+          gs[v] = (TS)lam;
+          xl[v] = Store<TL>::from(xn);
+        }
       }
-    }
-    if (cnt == V) {
-      st_vec<TS, V>(Mm + e, mn);
-      if (A) st_vec<TS, V>(A + e, xs);
-      st_vec<TL, V>(PR + e, xl);
-      if (G) st_vec<TS, V>(G + e, gs);
-    } else {
-      Mm[e] = mn[0];
-      if (A) A[e] = xs[0];
-      PR[e] = xl[0];
-      if (G) G[e] = gs[0];
-    }
-  };
-  auto average_one = [&](int64_t e, int cnt) {
-    TC sacc[V];
-#pragma unroll
-    for (int w = 0; w < KG; ++w) {
-      if (w < a.g) {
+      if (cnt == V) {
+        st_vec<TS, V>(Mm + e, mn);
+        if (A) st_vec<TS, V>(A + e, xs);
+        st_vec<TL, V>(PR + e, xl);
+        if (G) st_vec<TS, V>(G + e, gs);
+      } else {
+        Mm[e] = mn[0];
+        if (A) A[e] = xs[0];
+        PR[e] = xl[0];
+        if (G) G[e] = gs[0];
+      }
+    };
+    for (int64_t i = gt / R; i < nv; i += vstride) step(i * V, V);
+    // scalar tail (n % V coordinates): coordinate k of the tail to item k*R + role
+    if (V > 1 && gt / R < a.n - nv * V) step(nv * V + gt / R, 1);
+  } else {
+    const TC gd = (TC)a.g;
+    TL* AO = static_cast<TL*>(a.avg_out);
+    auto average = [&](int64_t e, int cnt) {
+      TC sacc[V];
+      for (int w = 0; w < a.g; ++w) {  // ascending worker order, param_ops.cpp:26-28
         const TL* C = static_cast<const TL*>(a.cur[w]);
         TL c[V];
-        if (cnt == V) {
+        if (cnt == V)
           ld_vec<TL, V>(C + e, c);
-        } else {
+        else
           c[0] = C[e];
-        }
 #pragma unroll
         for (int v = 0; v < V; ++v) sacc[v] = (w == 0) ? to_c(c[v]) : sacc[v] + to_c(c[v]);
       }
-    }
-    TL o[V];
+      TL o[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (v < cnt) {
-        const TC r = sacc[v] / gd;
-        if (!isfinite(r)) avg_flags |= CO2_FLAG_AVG_NONFINITE;
-        o[v] = Store<TL>::from(r);
+      for (int v = 0; v < V; ++v) {
+        if (v < cnt) {
+          const TC r = sacc[v] / gd;  // one division, :30
+          if (!isfinite(r)) avg_flags |= CO2_FLAG_AVG_NONFINITE;
+          o[v] = Store<TL>::from(r);
+        }
       }
-    }
-    if (cnt == V)
-      st_vec<TL, V>(AO + e, o);
-    else
-      AO[e] = o[0];
-  };
-  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < nv; i += stride) {
-    const int64_t e = i * V;
-    average_one(e, V);
-#pragma unroll
-    for (int w = 0; w < KG; ++w)
-      if (w < a.g) step_one(w, e, V);
+      if (cnt == V)
+        st_vec<TL, V>(AO + e, o);
+      else
+        AO[e] = o[0];
+    };
+    for (int64_t i = gt / R; i < nv; i += vstride) average(i * V, V);
+    if (V > 1 && gt / R < a.n - nv * V) average(nv * V + gt / R, 1);
   }
-  {  // scalar tail (n % V coordinates), one per thread
-    const int64_t t = nv * V + (int64_t)blockIdx.x * NT + threadIdx.x;
-    if (V > 1 && t < a.n) {
-      average_one(t, 1);
-#pragma unroll
-      for (int w = 0; w < KG; ++w)
-        if (w < a.g) step_one(w, t, 1);
-    }
-  }
-  // ---- per-worker diagnostics: the block_finish fold, once per worker
-  constexpr int NW = NT / 32;
-  __shared__ Partial sh[KG][NW];
-  __shared__ unsigned int sh_avg[NW];
+  // ---- diagnostics: per-CTA partial per role, folded in thread order
+  __shared__ Partial part[NT];
+  __shared__ unsigned int s_avg;
   __shared__ bool s_last;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int w = 0; w < KG; ++w) {
-    const Acc b = acc[w].widen();
-    double mg = b.min_gap, ms = b.max_step;
-    unsigned long long cl = b.clipped, fl = b.floored;
-    unsigned int fg = b.flags;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double omg = __shfl_xor_sync(0xffffffffu, mg, o);
-      double oms = __shfl_xor_sync(0xffffffffu, ms, o);
-      mg = omg < mg ? omg : mg;
-      ms = oms > ms ? oms : ms;
-      cl += __shfl_xor_sync(0xffffffffu, cl, o);
-      fl += __shfl_xor_sync(0xffffffffu, fl, o);
-      fg |= __shfl_xor_sync(0xffffffffu, fg, o);
-    }
-    if (lane == 0) sh[w][wid] = Partial{mg, ms, cl, fl, fg, 0u};
-  }
   {
-    unsigned int af = avg_flags;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) af |= __shfl_xor_sync(0xffffffffu, af, o);
-    if (lane == 0) sh_avg[wid] = af;
+    const Acc b = acc.widen();
+    part[threadIdx.x] = Partial{b.min_gap, b.max_step, (unsigned long long)b.clipped,
+                                (unsigned long long)b.floored, b.flags, avg_flags};
   }
   __syncthreads();
   WsHeader* hdr0 = ws_header(a.ws[0]);
-  if (threadIdx.x < KG && (int)threadIdx.x < a.g) {
+  if ((int)threadIdx.x < R) {
     const int w = threadIdx.x;
-    Partial b = sh[w][0];
-    for (int k = 1; k < NW; ++k) {  // fixed order
-      b.min_gap = sh[w][k].min_gap < b.min_gap ? sh[w][k].min_gap : b.min_gap;
-      b.max_step = sh[w][k].max_step > b.max_step ? sh[w][k].max_step : b.max_step;
-      b.clipped += sh[w][k].clipped;
-      b.floored += sh[w][k].floored;
-      b.flags |= sh[w][k].flags;
+    Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
+    const int64_t base = (int64_t)blockIdx.x * NT;
+    for (int t = 0; t < NT; ++t) {
+      if ((int)((base + t) % R) != w) continue;
+      const Partial& q = part[t];
+      b.min_gap = q.min_gap < b.min_gap ? q.min_gap : b.min_gap;
+      b.max_step = q.max_step > b.max_step ? q.max_step : b.max_step;
+      b.clipped += q.clipped;
+      b.floored += q.floored;
+      b.flags |= q.flags;
+      b.pad |= q.pad;
     }
-    if (w == 0) {
-      unsigned int af = 0;
-      for (int k = 0; k < NW; ++k) af |= sh_avg[k];
-      b.pad = af;  // the average's flags ride in worker 0's partial
-    }
-    ws_partials(a.ws[w])[blockIdx.x] = b;
+    if (w < a.g)
+      ws_partials(a.ws[w])[blockIdx.x] = b;
+    else
+      s_avg = b.pad;  // the average's flags
   }
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&hdr0->ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    ws_partials(a.ws[0])[blockIdx.x].pad = s_avg;  // ride in worker 0's partial
+    __threadfence();
+    s_last = atomicAdd(&hdr0->ticket, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int w = 0; w < a.g && w < KG; ++w) {
+  constexpr int NW = NT / 32;
+  __shared__ Partial sh[NW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int w = 0; w < a.g; ++w) {
     const Partial* parts = ws_partials(a.ws[w]);
     Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
     for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
@@ -2192,17 +2170,17 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
       b.pad |= __shfl_xor_sync(0xffffffffu, b.pad, o);
     }
     __syncthreads();
-    if (lane == 0) sh[0][wid] = b;
+    if (lane == 0) sh[wid] = b;
     __syncthreads();
     if (threadIdx.x == 0) {
-      Partial r = sh[0][0];
+      Partial r = sh[0];
       for (int k = 1; k < NW; ++k) {
-        r.min_gap = sh[0][k].min_gap < r.min_gap ? sh[0][k].min_gap : r.min_gap;
-        r.max_step = sh[0][k].max_step > r.max_step ? sh[0][k].max_step : r.max_step;
-        r.clipped += sh[0][k].clipped;
-        r.floored += sh[0][k].floored;
-        r.flags |= sh[0][k].flags;
-        r.pad |= sh[0][k].pad;
+        r.min_gap = sh[k].min_gap < r.min_gap ? sh[k].min_gap : r.min_gap;
+        r.max_step = sh[k].max_step > r.max_step ? sh[k].max_step : r.max_step;
+        r.clipped += sh[k].clipped;
+        r.floored += sh[k].floored;
+        r.flags |= sh[k].flags;
+        r.pad |= sh[k].pad;
       }
       co2_diag_t d;
       d.min_gap = r.min_gap;
@@ -2225,25 +2203,30 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
   }
 }
 
-template <class M, int KG>
-co2_status_t launch_local_round(const LocalRoundArgs& a, bool vec, cudaStream_t s) {
-  constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
-  if (vec) {
-    auto k = local_round_kernel<M, KG, V, kThreads>;
-    k<<<grid_for(k, a.n / V > 0 ? a.n / V : 1, kThreads), kThreads, 0, s>>>(a);
-  } else {
-    auto k = local_round_kernel<M, KG, 1, kThreads>;
-    k<<<grid_for(k, a.n > 0 ? a.n : 1, kThreads), kThreads, 0, s>>>(a);
+template <class M, int V>
+co2_status_t launch_local_round(const LocalRoundArgs& a, cudaStream_t s) {
+  auto k = local_round_kernel<M, V, kThreads>;
+  const int R = a.g + 1;
+  const int64_t nv = a.n / V > 0 ? a.n / V : 1;
+  int grid = grid_for(k, nv * R, kThreads);
+  // gridDim.x * kThreads must be a multiple of R (fixed role per thread)
+  int step = R;
+  for (int d = kThreads; d % 2 == 0 && step % 2 == 0;) {
+    d /= 2;
+    step /= 2;
   }
+  grid = grid / step * step;
+  if (grid < step) grid = step;
+  k<<<grid, kThreads, 0, s>>>(a);
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }
 
 template <class M>
-co2_status_t launch_local_round_g(const LocalRoundArgs& a, bool vec, cudaStream_t s) {
-  if (a.g <= 2) return launch_local_round<M, 2>(a, vec, s);
-  if (a.g <= 4) return launch_local_round<M, 4>(a, vec, s);
-  return launch_local_round<M, 8>(a, vec, s);
+co2_status_t launch_local_round_v(const LocalRoundArgs& a, bool vec, cudaStream_t s) {
+  constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+  if (vec) return launch_local_round<M, V>(a, s);
+  return launch_local_round<M, 1>(a, s);
 }
 }  // namespace
 
@@ -2285,9 +2268,9 @@ co2_status_t local_round_impl(co2_mode_t mode, int g, int64_t n, const void* con
   a.penalty = h->penalty ? 1 : 0;
   a.clip = h->clip ? 1 : 0;
   switch (mode) {
-    case CO2_MODE_F64: return launch_local_round_g<ModeF64>(a, vec, s);
-    case CO2_MODE_F32: return launch_local_round_g<ModeF32>(a, vec, s);
-    case CO2_MODE_BF16_MIXED: return launch_local_round_g<ModeBF16>(a, vec, s);
+    case CO2_MODE_F64: return launch_local_round_v<ModeF64>(a, vec, s);
+    case CO2_MODE_F32: return launch_local_round_v<ModeF32>(a, vec, s);
+    case CO2_MODE_BF16_MIXED: return launch_local_round_v<ModeBF16>(a, vec, s);
   }
   return fail(CO2_ERR_VALIDATION, "local round: unknown mode %d", (int)mode);
 }

@@ -89,7 +89,11 @@ def test_acceptance_criterion8_invariant_matrix(alpha, beta, phi, het, batch, sc
     stand-ins: heterogeneity scales worker i's gradients by (1 + het * i),
     the batch regime is the number of draws summed per step (repeat), and two
     gradient scales cover the unclipped and the clip-saturated regimes.
-    4 workers, tau 3, 40 rounds, F64."""
+    4 workers, tau 3, 40 rounds, F64.  The reference's quadratic keeps
+    |x| = O(1), where the rounding of x' = x - alpha*c is inside its 1e-15
+    slack; the synthetic random walk drifts to |x| >> 1, so the bound adds
+    that rounding explicitly: 2^-52 * max|x'| (one rounding of x' plus one
+    of |x' - x|, each at most half an ulp of |x'|)."""
     G, tau, rounds, n = 4, 3, 40, 8191
     hyper = co2.Co2Hyper(alpha=alpha, beta=beta, phi=phi, epsilon=1e-12)
     eng = co2.CollectiveEngine(G, transport="local")
@@ -110,7 +114,10 @@ def test_acceptance_criterion8_invariant_matrix(alpha, beta, phi, het, batch, sc
             continue
         checked += 1
         assert np.isfinite(r.min_gap) and r.min_gap >= 1.0, (t, r.min_gap)
-        assert r.max_outer_step <= bound, (t, r.max_outer_step, bound)
+        xmax = max(float(w.params.abs().max()) for w in ws)
+        assert r.max_outer_step <= bound + 2.0 ** -52 * xmax, (t, r.max_outer_step, bound, xmax)
+        if xmax <= 1.0:  # the reference's O(1) regime: its bound as written
+            assert r.max_outer_step <= bound, (t, r.max_outer_step, bound)
         clipped_rounds += r.n_clipped > 0
     assert checked == rounds - 1
     if scale == 50.0:  # the saturated regime really exercises the clip bound

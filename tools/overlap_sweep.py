@@ -5,11 +5,26 @@ to the analytic simulate_timeline prediction (proj/src/timing_model.cpp:
 
   torchrun --nproc-per-node N tools/overlap_sweep.py [--mode 1] [--n 125000000]
 
+Calibration (the knee): in the reference's CO2 timeline a round is
+tau * t_comp of inner compute, the launch of the reduce, the stall on the
+previous reduce, then t_outer of outer step -- so the reduce launched in
+round t overlaps round t's outer step AND round t+1's tau inner steps, and
+stalls by max(0, t_comm - t_outer - tau * t_comp).  The sweep measures
+t_comm (the reduce alone) and t_outer (the outer step alone), then sizes the
+synthetic inner step -- the HBM-streaming x <- x - lr * g kernel over the
+first k coordinates, k calibrated -- to t_comp = (t_comm - t_outer) / knee,
+so the predicted stall is positive for tau < knee and zero from the knee on.
+If t_comm <= t_outer the outer step alone hides the reduce and no knee
+exists; the sweep says so.
+
 exposed% = 100 * sum(stall) / sum(waited comm), the reference definition
 (1 - overlap_ratio_achieved).  stall = device time the compute stream waited
 on the reduce (events straddling the wait); comm = device duration of the
-reduce on the comm stream.  "interference" = mean round time with the
-all-reduce minus the same schedule with a world-1 (no-op) engine.
+reduce on the comm stream.  interference = mean round time with the
+all-reduce minus the same schedule with a world-1 (no-op) engine; it is also
+reported as a share of the round and next to the reduce's HBM floor (the
+bytes a fixed-order reduce must move through this GPU's HBM: 2 x the buffer,
+read and written once, at the measured copy bandwidth).
 """
 import argparse
 import json
@@ -29,13 +44,14 @@ def main():
     ap.add_argument("--rounds", type=int, default=6)
     ap.add_argument("--knee", type=float, default=4.0, help="tau at which tau*t_comp = t_comm")
     ap.add_argument("--max-ctas", type=int, default=0)
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ncclsum", "p2p"])
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
     import torch
     import torch.distributed as dist
 
+    from paper_2401_16265_b200 import _lib as L
     from paper_2401_16265_b200 import co2
     from paper_2401_16265_b200.dist import broadcast_nccl_id, env_rank, max_over_ranks
 
@@ -49,7 +65,8 @@ def main():
         eng = co2.CollectiveEngine(world, transport="p2p", rank=rank, max_ctas=a.max_ctas)
     else:
         eng = co2.CollectiveEngine(world, transport="nccl", rank=rank, nccl_id=uid,
-                                   max_ctas=a.max_ctas)
+                                   max_ctas=a.max_ctas,
+                                   nccl_algo="sum" if a.transport == "ncclsum" else "fixed")
     solo = co2.CollectiveEngine(1, transport="nccl", rank=0, nccl_id=bytes(128))
     hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
     stream = torch.cuda.current_stream()
@@ -71,26 +88,56 @@ def main():
         eng.deregister(scratch.data_ptr())
     del scratch
 
-    # t_comp: calibrate the synthetic inner step to t_comm / knee
     w = co2.Worker(a.mode, a.n, co2.synth(a.mode, a.n, worker=rank)[3], keep_gap=False)
 
-    def time_inner(repeat, iters=5):
+    # t_outer: the outer step alone (no-op engine), steady state
+    def outer_alone():
+        w2 = co2.Worker(a.mode, a.n, w.params, keep_gap=False)
+        w2.snapshot_start()
+        w2.snapshot_first()
+        co2.co2_round([w2], solo, hyper, 1)
+        w2.enable_timing(16)
+        for _ in range(6):
+            co2.co2_round([w2], solo, hyper, 1, sync=False)
+        torch.cuda.synchronize()
+        kt = w2.step_times()[2:]
+        co2.co2_round_drain([w2], solo)
+        w2.close()
+        return statistics.median(kt)
+
+    t_outer0 = outer_alone()
+    t_outer0 = max_over_ranks([t_outer0], device="cpu")[0] if world > 1 else t_outer0
+
+    def time_inner(k, iters=6):
+        view = w.params[:k]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        co2.synthetic_inner_step(w.params, lr=1e-6, repeat=repeat, worker=rank, step=0)
+        co2.synthetic_inner_step(view, lr=1e-6, worker=rank, step=0)
         e0.record(stream)
-        for k in range(iters):
-            co2.synthetic_inner_step(w.params, lr=1e-6, repeat=repeat, worker=rank, step=k)
+        for i in range(iters):
+            co2.synthetic_inner_step(view, lr=1e-6, worker=rank, step=i)
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e-3 / iters
 
-    target = t_comm / a.knee if t_comm > 0 else 0.0
-    repeat = 1
-    t1 = time_inner(1)
-    while repeat < 256 and t1 * repeat < target * 0.8:
-        repeat *= 2
-    t_comp = time_inner(repeat)
-    t_comp = max_over_ranks([t_comp], device="cpu")[0] if world > 1 else t_comp
+    # fixed-duration inner step: the first k coordinates, k calibrated so that
+    # tau * t_comp + t_outer = t_comm at tau = knee
+    knee_exists = t_comm > t_outer0
+    target = (t_comm - t_outer0) / a.knee if knee_exists else t_comm / a.knee
+    k = a.n
+    t_full = time_inner(k)
+    for _ in range(4):
+        k = max(1 << 16, min(a.n, int(k * target / max(time_inner(k), 1e-9))) // 256 * 256)
+    t_comp = time_inner(k)
+    k, t_comp = (max_over_ranks([k, t_comp], device="cpu") if world > 1 else (k, t_comp))
+    k = int(k)
+    hbm_gbs = 6452.8
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_gbs = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        pass
+    low_bytes = {0: 8, 1: 4, 2: 2}[a.mode]
+    hbm_floor = 2.0 * low_bytes * a.n / (hbm_gbs * 1e9)
 
     def run(engine, tau):
         w2 = co2.Worker(a.mode, a.n, w.params, keep_gap=False)
@@ -105,11 +152,14 @@ def main():
                 dist.barrier()
             e0.record(stream)
             w2.snapshot_start()
-            for k in range(tau):
-                co2.synthetic_inner_step(w2.params, lr=1e-6, repeat=repeat, worker=rank,
-                                         step=t * tau + k)
-                if k == 0:
-                    w2.snapshot_first()
+            if t == 0:
+                w2.snapshot_first()
+            for j in range(tau):
+                # the first step's store also writes the x_{t,1} snapshot of
+                # the coordinates it moves (the others did not move)
+                co2.synthetic_inner_step(
+                    w2.params[:k], lr=1e-6, worker=rank, step=t * tau + j,
+                    snapshot_out=w2.buffer(L.BUF_XFIRST)[:k] if j == 0 and t > 0 else None)
             co2.co2_round([w2], engine, hyper, tau, sync=False)
             e1.record(stream)
             torch.cuda.synchronize()
@@ -145,13 +195,19 @@ def main():
         pst = [p[2] for p in pred.per_round[2:]]
         pred_exposed = 100.0 * sum(pst) / (t_comm * len(pst)) if t_comm and pst else 0.0
         row = {"tau": tau, "world": world, "n": a.n, "mode": a.mode,
-               "transport": "p2p" if p2p else "nccl",
+               "transport": "p2p" if p2p else a.transport,
                "t_comm_ms": 1e3 * t_comm, "t_comp_ms": 1e3 * t_comp, "t_outer_ms": 1e3 * t_outer,
-               "inner_repeat": repeat, "exposed_pct": 100.0 * stall / waited if waited else 0.0,
+               "t_outer_alone_ms": 1e3 * t_outer0, "knee_exists": knee_exists,
+               "knee_tau": a.knee, "inner_coords": k, "inner_full_ms": 1e3 * t_full,
+               "exposed_pct": 100.0 * stall / waited if waited else 0.0,
                "stall_ms_per_round": 1e3 * stall / max(nw, 1),
                "comm_ms_measured": 1e3 * waited / max(nw, 1),
                "round_ms": 1e3 * wall, "round_ms_no_allreduce": 1e3 * wall0,
                "interference_ms": 1e3 * (wall - wall0),
+               "interference_pct_of_round": 100.0 * (wall - wall0) / wall if wall else 0.0,
+               "interference_pct_of_comm": 100.0 * (wall - wall0) / t_comm if t_comm else 0.0,
+               "reduce_hbm_floor_ms": 1e3 * hbm_floor,
+               "stall_pct_of_round": 100.0 * stall / max(nw, 1) / wall if wall else 0.0,
                "predicted_exposed_pct": pred_exposed,
                "predicted_exposed_pct_all_rounds": 100.0 * (1.0 - pred.overlap_ratio_achieved),
                "predicted_overlap": co2.overlap_ratio(tau, t_comp, t_comm) if t_comm else 1.0}
