@@ -677,11 +677,299 @@ int fused_variant() {
   return v;
 }
 
+// ------------------------------------------- bulk-copy (TMA 1D) fused step
+// The same per-element body as fused_step_kernel, with the five input
+// streams moved by the TMA engine instead of per-thread LDGs:
+//   * one producer lane per CTA claims TILE-element tiles from a global
+//     counter (dynamic: a co-running reduce kernel slows some SMs, the
+//     counter keeps every SM busy to the end) and issues five
+//     cp.async.bulk global->shared copies per tile into a STAGES-deep ring,
+//     completing on the stage's `full` mbarrier (expect_tx);
+//   * NCW consumer warps wait on `full`, read 16 B per lane per stream from
+//     shared memory (conflict-free: lane-contiguous), compute, store the
+//     outputs with 128-bit evict-first STGs, and release the stage on its
+//     `empty` mbarrier (one arrive per warp).
+// Bytes in flight sit in shared memory (STAGES x 16-20 KB per CTA), so the
+// kernel needs few registers and threads per SM: a reduce kernel on the comm
+// stream co-resides without displacing step CTAs (the register-file limit of
+// the LDG kernel at 4 x 256 x 64 registers).  Diagnostics are min / max /
+// counts / OR, independent of which CTA processed which tile, so dynamic
+// scheduling keeps them deterministic.  Aliasing as in fused_step_kernel
+// (anchor over prev_x0, params over xbar) is safe: a tile's outputs are
+// written after its inputs landed in shared memory.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBAR_WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Lane-contiguous shared-memory vector read (16 / 8 B per lane).
+template <typename T, int N>
+__device__ __forceinline__ void ld_smem(const T* p, T (&out)[N]) {
+  constexpr int BYTES = N * (int)sizeof(T);
+  static_assert(BYTES == 16 || BYTES == 8, "smem vector");
+  if constexpr (BYTES == 16) {
+    const uint4 r = *reinterpret_cast<const uint4*>(p);
+    memcpy(out, &r, 16);
+  } else {
+    const uint2 r = *reinterpret_cast<const uint2*>(p);
+    memcpy(out, &r, 8);
+  }
+}
+
+template <class M, int TILE>
+struct BulkStage {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  static constexpr int kS = TILE * (int)sizeof(TS);
+  static constexpr int kL = TILE * (int)sizeof(TL);
+  static constexpr int kBytes = 3 * kS + 2 * kL;  // x_t0, p0, m | p1, xbar
+};
+
+// mbarriers full[STAGES], empty[STAGES] and the tile index per stage, padded
+// so every stage buffer stays 128-byte aligned.
+__host__ __device__ constexpr size_t bulk_hdr_bytes(int stages) { return ((size_t)stages * 24 + 127) / 128 * 128; }
+
+template <class M, int TILE, int STAGES, int NCW>
+constexpr size_t bulk_smem_bytes() {
+  return (size_t)STAGES * BulkStage<M, TILE>::kBytes + bulk_hdr_bytes(STAGES);
+}
+
+template <class M, int TILE, int STAGES, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) bulk_step_kernel(const StepArgs a) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  using SG = BulkStage<M, TILE>;
+  constexpr int NT = (NCW + 1) * 32;
+  constexpr int VE = 16 / (int)sizeof(TS);  // elements per lane per access
+  constexpr int GROUPS = TILE / (NCW * 32 * VE);
+  static_assert(TILE % (NCW * 32 * VE) == 0, "tile must split evenly over the consumer lanes");
+  constexpr bool LQ = !std::is_same<TS, TL>::value;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + STAGES;
+  long long* tile_of = reinterpret_cast<long long*>(empty + STAGES);
+  unsigned char* ring = smem + bulk_hdr_bytes(STAGES);
+
+  Hyp<TC> h;
+  h.tau = (TC)a.tau;
+  h.eps = (TC)a.eps;
+  h.beta = (TC)a.beta;
+  h.phi = (TC)a.phi;
+  h.alpha = (TC)a.alpha;
+  h.divisor = (TC)a.divisor;
+  h.penalty = a.penalty;
+  h.clip = a.clip;
+  h.divide = a.divisor > 1;
+  Hyp<TC> hg = h;
+  hg.divide = 0;
+
+  const TS* __restrict__ X = static_cast<const TS*>(a.x_t0);
+  const TS* __restrict__ P0 = static_cast<const TS*>(a.p0);
+  const TL* __restrict__ P1 = static_cast<const TL*>(a.p1);
+  const TL* XB = static_cast<const TL*>(a.xbar);
+  TS* Mm = static_cast<TS*>(a.m);
+  TS* A = static_cast<TS*>(a.anchor);
+  TL* PR = static_cast<TL*>(a.params);
+  TS* G = static_cast<TS*>(a.gap);
+  TL* XO = static_cast<TL*>(a.xbar_out);
+  WsHeader* hdr = ws_header(a.ws);
+  const long long ntiles = a.n / TILE;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  AccT<TC> acc;
+  if (warp == NCW) {
+    if (lane == 0) {  // producer
+      const uint64_t pol = evict_first_policy();
+      for (int it = 0;; ++it) {
+        const int s = it % STAGES;
+        const unsigned ph = (unsigned)(it / STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        const long long t = (long long)atomicAdd(&hdr->tile_next, 1u);
+        if (t >= ntiles) {
+          tile_of[s] = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        tile_of[s] = t;
+        unsigned char* st = ring + (size_t)s * SG::kBytes;
+        const int64_t e = t * (int64_t)TILE;
+        mbar_arrive_expect_tx(&full[s], SG::kBytes);
+        bulk_g2s(st, X + e, SG::kS, &full[s], pol);
+        bulk_g2s(st + SG::kS, P0 + e, SG::kS, &full[s], pol);
+        bulk_g2s(st + 2 * SG::kS, Mm + e, SG::kS, &full[s], pol);
+        bulk_g2s(st + 3 * SG::kS, P1 + e, SG::kL, &full[s], pol);
+        bulk_g2s(st + 3 * SG::kS + SG::kL, XB + e, SG::kL, &full[s], pol);
+      }
+    }
+  } else {  // consumers
+    for (int it = 0;; ++it) {
+      const int s = it % STAGES;
+      const unsigned ph = (unsigned)(it / STAGES) & 1u;
+      mbar_wait(&full[s], ph);
+      const long long t = tile_of[s];
+      if (t < 0) break;
+      const unsigned char* st = ring + (size_t)s * SG::kBytes;
+      const TS* sx = reinterpret_cast<const TS*>(st);
+      const TS* sp0 = reinterpret_cast<const TS*>(st + SG::kS);
+      const TS* sm = reinterpret_cast<const TS*>(st + 2 * SG::kS);
+      const TL* sp1 = reinterpret_cast<const TL*>(st + 3 * SG::kS);
+      const TL* sxb = reinterpret_cast<const TL*>(st + 3 * SG::kS + SG::kL);
+#pragma unroll
+      for (int g = 0; g < GROUPS; ++g) {
+        const int o = (g * NCW * 32 + warp * 32 + lane) * VE;
+        TS x[VE], q0[VE], mo[VE];
+        TL q1[VE], xb[VE];
+        ld_smem<TS, VE>(sx + o, x);
+        ld_smem<TS, VE>(sp0 + o, q0);
+        ld_smem<TS, VE>(sm + o, mo);
+        ld_smem<TL, VE>(sp1 + o, q1);
+        ld_smem<TL, VE>(sxb + o, xb);
+        TS mn[VE], xs[VE], gs[VE];
+        TL xl[VE];
+#pragma unroll
+        for (int v = 0; v < VE; ++v) {
+          TC m = to_c(mo[v]), xn, lam;
+          TC xbv = to_c(xb[v]);
+          if (h.divide) xbv = xbv / h.divisor;  // average(): sum / G, param_ops.cpp:30
+          co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), xbv, m, xn, lam, hg, acc);
+          mn[v] = (TS)m;
+          xs[v] = (TS)xn;
+          gs[v] = (TS)lam;
+          xl[v] = Store<TL>::from(xn);
+        }
+        const int64_t e = t * (int64_t)TILE + o;
+        st_vec<TS, VE>(Mm + e, mn);
+        if (A) st_vec<TS, VE>(A + e, xs);
+        if (PR) st_vec<TL, VE>(PR + e, xl);
+        if (G) st_vec<TS, VE>(G + e, gs);
+        if (XO) st_vec<TL, VE>(XO + e, xb);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  // Tail (n % TILE coordinates): the last CTA, straight from global memory.
+  if (blockIdx.x == gridDim.x - 1) {
+    for (int64_t j = ntiles * (int64_t)TILE + threadIdx.x; j < a.n; j += NT) {
+      TC m = to_c(Mm[j]), xn, lam;
+      TC xbv = to_c(XB[j]);
+      if (h.divide) xbv = xbv / h.divisor;
+      co2_elem<TC, LQ>(to_c(X[j]), to_c(P0[j]), to_c(P1[j]), xbv, m, xn, lam, hg, acc);
+      if (XO) XO[j] = XB[j];
+      Mm[j] = (TS)m;
+      if (A) A[j] = (TS)xn;
+      if (PR) PR[j] = Store<TL>::from(xn);
+      if (G) G[j] = (TS)lam;
+    }
+  }
+  if (block_finish<NT>(acc.widen(), a.ws) && threadIdx.x == 0) {
+    // Every producer has fetched its terminating index: reset the tile
+    // counter for the next launch on this workspace (like the ticket).
+    hdr->tile_next = 0u;
+    __threadfence();
+  }
+}
+
+template <class M, int TILE, int STAGES, int NCW>
+co2_status_t launch_bulk(const StepArgs& a, cudaStream_t s) {
+  auto k = bulk_step_kernel<M, TILE, STAGES, NCW>;
+  constexpr size_t smem = bulk_smem_bytes<M, TILE, STAGES, NCW>();
+  constexpr int NT = (NCW + 1) * 32;
+  static const int per_sm = [&] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, NT, smem);
+    return v < 1 ? 1 : v;
+  }();
+  int64_t grid = (int64_t)per_sm * sm_count();
+  const int64_t tiles = a.n / TILE;
+  if (grid > tiles) grid = tiles < 1 ? 1 : tiles;
+  k<<<(int)grid, NT, smem, s>>>(a);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+// Bulk-copy variants (co2_set_fused_variant >= 10): (TILE, STAGES, consumer
+// warps) per mode.  Stage bytes: TILE x 16 (bf16-mixed), x 20 (fp32), x 40 (fp64).
+template <class M>
+co2_status_t launch_bulk_variant(int v, const StepArgs& a, cudaStream_t s) {
+  if constexpr (std::is_same<M, ModeBF16>::value) {
+    switch (v) {
+      case 11: return launch_bulk<M, 1024, 4, 4>(a, s);   // 64 KB: 3 CTA/SM
+      case 12: return launch_bulk<M, 2048, 3, 8>(a, s);   // 96 KB: 2 CTA/SM
+      case 13: return launch_bulk<M, 4096, 3, 8>(a, s);   // 192 KB: 1 CTA/SM
+      case 14: return launch_bulk<M, 1024, 6, 8>(a, s);   // 96 KB: 2 CTA/SM
+      default: return launch_bulk<M, 2048, 4, 4>(a, s);   // 128 KB: 1 CTA/SM
+    }
+  } else if constexpr (std::is_same<M, ModeF32>::value) {
+    switch (v) {
+      case 11: return launch_bulk<M, 1024, 4, 4>(a, s);   // 80 KB: 2 CTA/SM
+      case 12: return launch_bulk<M, 2048, 4, 8>(a, s);   // 160 KB: 1 CTA/SM
+      case 13: return launch_bulk<M, 1024, 8, 8>(a, s);   // 160 KB
+      case 14: return launch_bulk<M, 512, 6, 4>(a, s);    // 60 KB: 3 CTA/SM
+      default: return launch_bulk<M, 1024, 5, 4>(a, s);   // 100 KB: 2 CTA/SM
+    }
+  } else {
+    switch (v) {
+      case 11: return launch_bulk<M, 256, 6, 2>(a, s);    // 60 KB: 3 CTA/SM
+      case 12: return launch_bulk<M, 1024, 4, 8>(a, s);   // 160 KB: 1 CTA/SM
+      default: return launch_bulk<M, 512, 5, 4>(a, s);    // 100 KB: 2 CTA/SM
+    }
+  }
+}
+
 template <class M>
 co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
   bool vec_ok = aligned16(a.x_t0) && aligned16(a.p0) && aligned16(a.p1) && aligned16(a.xbar) &&
                 aligned16(a.m) && aligned16(a.anchor) && aligned16(a.params) && aligned16(a.gap) &&
                 aligned16(a.xbar_out);
+  if (vec_ok && fused_variant() >= 10) {
+    return launch_bulk_variant<M>(fused_variant(), a, s);
+  }
   if (!vec_ok) {
     launch_variant<M, 1, 4>(a, s);
   } else if constexpr (std::is_same<M, ModeBF16>::value) {
@@ -1854,63 +2142,123 @@ struct BaseArgs {
   void* ws;
 };
 
+// One coordinate of the baseline updates, IEEE ops in the reference's order.
 template <class M, int OP>
+__device__ __forceinline__ void base_elem(typename M::TC xb, typename M::TC x, typename M::TS& m,
+                                          typename M::TL& pr, typename M::TS& an,
+                                          typename M::TC af, typename M::TC bf,
+                                          AccT<typename M::TC>& acc) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  if (OP == B_SLOWMO) {  // outer_algorithms.cpp:229-233
+    TC delta = x - xb;
+    TC bm = bf * to_c(m);
+    TC mn = bm + delta;
+    TC am = af * mn;
+    TC xn = x - am;
+    if (!isfinite(mn)) acc.flags |= CO2_FLAG_SLOWMO_M;
+    if (!isfinite(xn)) acc.flags |= CO2_FLAG_SLOWMO_X;
+    m = (TS)mn;
+    pr = Store<TL>::from(xn);
+    an = (TS)xn;
+    TC st = fabs(xn - x);
+    acc.max_step = st > acc.max_step ? st : acc.max_step;
+  } else if (OP == B_LOCAL) {  // outer_algorithms.cpp:252-255
+    TC st = fabs(xb - x);
+    acc.max_step = st > acc.max_step ? st : acc.max_step;
+    pr = Store<TL>::from(xb);
+    an = (TS)xb;
+  } else {  // B_OVERLAP, outer_algorithms.cpp:278-279 (an = the anchor, read only)
+    TC p = to_c(pr);
+    TC d = to_c(an) - xb;
+    TC pn = p - d;
+    if (!isfinite(pn)) acc.flags |= CO2_FLAG_OVERLAP;
+    TL stored = Store<TL>::from(pn);
+    pr = stored;
+    TC st = fabs(to_c(stored) - p);
+    acc.max_step = st > acc.max_step ? st : acc.max_step;
+  }
+}
+
+// V-element vectors per thread (128-bit state streams; V = 1 is the
+// unaligned path), grid-stride over grid_for()'s oversubscribed grid, the
+// n % V tail in scalar form.  Streams per op (bf16-mixed bytes / param):
+// SlowMo reads x, xbar, m and writes m, params, anchor (22 B); Local-SGD
+// reads x, xbar and writes params, anchor (12 B; 10 B without the anchor);
+// Overlap reads params, anchor, xbar and writes params (10 B).
+template <class M, int OP, int V>
 __global__ void __launch_bounds__(kThreads) baseline_kernel(const BaseArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
   using TC = typename M::TC;
   const TC af = (TC)a.alpha, bf = (TC)a.beta, gd = (TC)a.divisor;
+  const bool div = a.divisor > 1;
   AccT<TC> acc;
   const TS* X = static_cast<const TS*>(a.x);
   const TL* XB = static_cast<const TL*>(a.xb);
   TS* Mm = static_cast<TS*>(a.m);
   TL* PR = static_cast<TL*>(a.params);
   TS* A = static_cast<TS*>(a.anchor);
-  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < a.n;
-       j += (int64_t)gridDim.x * kThreads) {
-    TC xb = to_c(XB[j]);
-    if (a.divisor > 1) xb = xb / gd;  // average(): one division, param_ops.cpp:30
-    if (OP == B_SLOWMO) {             // outer_algorithms.cpp:229-233
-      TC x = to_c(X[j]);
-      TC delta = x - xb;
-      TC bm = bf * to_c(Mm[j]);
-      TC mn = bm + delta;
-      TC am = af * mn;
-      TC xn = x - am;
-      if (!isfinite(mn)) acc.flags |= CO2_FLAG_SLOWMO_M;
-      if (!isfinite(xn)) acc.flags |= CO2_FLAG_SLOWMO_X;
-      Mm[j] = (TS)mn;
-      PR[j] = Store<TL>::from(xn);
-      if (A) A[j] = (TS)xn;
-      TC st = fabs(xn - x);
-      acc.max_step = st > acc.max_step ? st : acc.max_step;
-    } else if (OP == B_LOCAL) {  // outer_algorithms.cpp:252-255
-      TC st = fabs(xb - to_c(X[j]));
-      acc.max_step = st > acc.max_step ? st : acc.max_step;
-      PR[j] = Store<TL>::from(xb);
-      if (A) A[j] = (TS)xb;
-    } else {  // B_OVERLAP, outer_algorithms.cpp:278-279
-      TC p = to_c(PR[j]);
-      TC d = to_c(A[j]) - xb;
-      TC pn = p - d;
-      if (!isfinite(pn)) acc.flags |= CO2_FLAG_OVERLAP;
-      TL stored = Store<TL>::from(pn);
-      PR[j] = stored;
-      TC st = fabs(to_c(stored) - p);
-      acc.max_step = st > acc.max_step ? st : acc.max_step;
+  const int64_t nv = a.n / V;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nv; i += stride) {
+    const int64_t e = i * V;
+    TL xb[V], pr[V];
+    TS x[V], m[V], an[V];
+    ld_vec<TL, V>(XB + e, xb);
+    if (OP != B_OVERLAP) ld_vec<TS, V>(X + e, x);
+    if (OP == B_SLOWMO) ld_vec<TS, V>(Mm + e, m);
+    if (OP == B_OVERLAP) {
+      ld_vec<TL, V>(PR + e, pr);
+      ld_vec<TS, V>(A + e, an);
     }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      TC xbv = to_c(xb[v]);
+      if (div) xbv = xbv / gd;  // average(): one division, param_ops.cpp:30
+      base_elem<M, OP>(xbv, OP == B_OVERLAP ? (TC)0 : to_c(x[v]), m[v], pr[v], an[v], af, bf,
+                       acc);
+    }
+    if (OP == B_SLOWMO) st_vec<TS, V>(Mm + e, m);
+    st_vec<TL, V>(PR + e, pr);
+    if (OP != B_OVERLAP && A) st_vec<TS, V>(A + e, an);
+  }
+  for (int64_t j = nv * V + (int64_t)blockIdx.x * kThreads + threadIdx.x; V > 1 && j < a.n;
+       j += stride) {
+    TC xbv = to_c(XB[j]);
+    if (div) xbv = xbv / gd;
+    TS m = OP == B_SLOWMO ? Mm[j] : (TS)0;
+    TS an = OP == B_OVERLAP ? A[j] : (TS)0;
+    TL pr = OP == B_OVERLAP ? PR[j] : TL{};
+    base_elem<M, OP>(xbv, OP == B_OVERLAP ? (TC)0 : to_c(X[j]), m, pr, an, af, bf, acc);
+    if (OP == B_SLOWMO) Mm[j] = m;
+    PR[j] = pr;
+    if (OP != B_OVERLAP && A) A[j] = an;
   }
   block_finish<kThreads>(acc.widen(), a.ws);
 }
 
+template <class M, int OP>
+void launch_baseline_mode(const BaseArgs& a, cudaStream_t s) {
+  constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+  const bool vec = aligned16(a.x) && aligned16(a.xb) && aligned16(a.m) && aligned16(a.params) &&
+                   aligned16(a.anchor);
+  if (vec) {
+    auto k = baseline_kernel<M, OP, V>;
+    k<<<grid_for(k, a.n / V, kThreads), kThreads, 0, s>>>(a);
+  } else {
+    auto k = baseline_kernel<M, OP, 1>;
+    k<<<grid_for(k, a.n, kThreads), kThreads, 0, s>>>(a);
+  }
+}
+
 template <int OP>
 co2_status_t launch_baseline(co2_mode_t mode, const BaseArgs& a, cudaStream_t s) {
-  int grid = simple_grid(a.n, kThreads);
-  if (grid > kMaxBlocks) grid = kMaxBlocks;
   switch (mode) {
-    case CO2_MODE_F64: baseline_kernel<ModeF64, OP><<<grid, kThreads, 0, s>>>(a); break;
-    case CO2_MODE_F32: baseline_kernel<ModeF32, OP><<<grid, kThreads, 0, s>>>(a); break;
-    case CO2_MODE_BF16_MIXED: baseline_kernel<ModeBF16, OP><<<grid, kThreads, 0, s>>>(a); break;
+    case CO2_MODE_F64: launch_baseline_mode<ModeF64, OP>(a, s); break;
+    case CO2_MODE_F32: launch_baseline_mode<ModeF32, OP>(a, s); break;
+    case CO2_MODE_BF16_MIXED: launch_baseline_mode<ModeBF16, OP>(a, s); break;
     default: return fail(CO2_ERR_VALIDATION, "baseline step: unknown mode %d", (int)mode);
   }
   CO2_CUDA(cudaGetLastError());

@@ -583,3 +583,56 @@ def test_fused_step_property_vs_oracle(mode):
             ref.diag.min_gap, ref.diag.max_outer_step, ref.diag.n_clipped, ref.diag.n_floored)
 
     check()
+
+
+BULK_VARIANTS = [10, 11, 12, 13, 14]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("variant", BULK_VARIANTS)
+@pytest.mark.parametrize("n", [1, 4095, 8192, 1000003])
+def test_bulk_copy_step_bitwise(mode, variant, n):
+    """The TMA bulk-copy step (co2_set_fused_variant >= 10: cp.async.bulk into
+    a shared-memory ring, dynamic tile claiming) gives the oracle's bits, with
+    the in-place aliasing of the round driver, a worker-sum divisor and the
+    gap output, and back-to-back launches on one workspace (tile counter
+    self-reset)."""
+    G = 2
+    try:
+        co2.check(L.lib().co2_set_fused_variant(variant))
+        ws = co2.Workspace()
+        for penalty, clip in COMBOS[:2]:
+            x, p0, p1, _, m = co2.synth(mode, n)
+            ox, op0, op1, _, om = O.synth(mode, n)
+            s = O.synth(mode, n, worker=0)[3]
+            e = O.synth(mode, n, worker=1)[3]
+            if mode == O.MODE_BF16_MIXED:
+                s = O.f32_to_bf16_bits(O.bf16_bits_to_f32(s) + O.bf16_bits_to_f32(e))
+            else:
+                s = s + e
+            ref = O.outer_step(mode, ox, op0, op1, s, om, ohyper(4, penalty, clip), divisor=G)
+            xe = to_dev(s)
+            gap = torch.empty_like(x)
+            d = co2.outer_step(mode, x, p0, p1, xe, m, hyper(4, penalty, clip), 4, divisor=G,
+                               anchor_out=p0, params_out=xe, gap_out=gap, workspace=ws)
+            assert same(to_np(m), ref.m) and same(to_np(p0), ref.anchor)
+            assert same(to_np(xe), ref.params) and same(to_np(gap), ref.gap)
+            assert (d.min_gap, d.max_outer_step, d.n_clipped, d.n_floored, d.flags) == (
+                ref.diag.min_gap, ref.diag.max_outer_step, ref.diag.n_clipped,
+                ref.diag.n_floored, 0)
+    finally:
+        co2.check(L.lib().co2_set_fused_variant(0))
+
+
+@pytest.mark.parametrize("variant", [10, 12])
+def test_bulk_copy_step_flags(variant):
+    """Non-finite inputs raise the same flags through the bulk-copy kernel."""
+    mode, n = co2.MODE_F32, 50000
+    try:
+        co2.check(L.lib().co2_set_fused_variant(variant))
+        x, p0, p1, xe, m = co2.synth(mode, n)
+        x[31337] = float("nan")
+        with pytest.raises(co2.NumericError, match="staleness_gap"):
+            co2.outer_step(mode, x, p0, p1, xe, m, hyper(), 4)
+    finally:
+        co2.check(L.lib().co2_set_fused_variant(0))

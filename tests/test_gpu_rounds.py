@@ -477,3 +477,37 @@ def test_rounds_global_clip_mode(mode):
             assert to_np(w.buffer(L.BUF_MOMENTUM)).tobytes() == to_np(m).tobytes(), (t, i)
             assert to_np(w.buffer(L.BUF_ANCHOR)).tobytes() == to_np(anchor).tobytes(), (t, i)
             assert to_np(w.params).tobytes() == to_np(params).tobytes(), (t, i)
+
+
+@pytest.mark.parametrize("mode", [co2.MODE_F64, co2.MODE_F32, co2.MODE_BF16_MIXED])
+@pytest.mark.parametrize("n,off", [(7, 0), (1_000_003, 0), (65_537, 1)])
+def test_baseline_steps_vector_tail_unaligned(mode, n, off):
+    """The vectorised baseline kernels: the V-element path with its scalar
+    n % V tail (off = 0) and the scalar path for buffers that are not 16-byte
+    aligned (off = 1), all bitwise the oracle, with the anchor output."""
+    x, p0, p1, xe, m = (t[off:] for t in co2.synth(mode, n + off))
+    ox, op0, op1, oxe, om = (a[off:] for a in O.synth(mode, n + off))
+    ws = co2.Workspace()
+    st = torch.cuda.current_stream().cuda_stream
+    mm = m.clone()
+    pbuf = torch.empty(n + off, dtype=xe.dtype, device="cuda")[off:]
+    abuf = torch.empty(n + off, dtype=x.dtype, device="cuda")[off:]
+    co2.check(co2.lib().co2_slowmo_step(mode, n, x.data_ptr(), xe.data_ptr(), 2, mm.data_ptr(),
+                                        pbuf.data_ptr(), abuf.data_ptr(), 0.8, 0.6, ws.ptr, st))
+    d = ws.fetch()
+    rm, rp, rd, code, _ = O.slowmo_step(mode, ox, oxe, om, 0.8, 0.6, divisor=2)
+    assert code == 0 and to_np(mm).tobytes() == rm.tobytes()
+    assert to_np(pbuf).tobytes() == rp.tobytes() and d.max_outer_step == rd.max_outer_step
+    if mode != co2.MODE_BF16_MIXED:
+        assert to_np(abuf).tobytes() == rp.tobytes()
+    co2.check(co2.lib().co2_local_sgd_step(mode, n, x.data_ptr(), xe.data_ptr(), 2,
+                                           pbuf.data_ptr(), abuf.data_ptr(), ws.ptr, st))
+    d = ws.fetch()
+    rp, rd, code = O.local_sgd_step(mode, ox, oxe, divisor=2)
+    assert to_np(pbuf).tobytes() == rp.tobytes() and d.max_outer_step == rd.max_outer_step
+    params = p1.clone()
+    co2.check(co2.lib().co2_overlap_correction(mode, n, params.data_ptr(), x.data_ptr(),
+                                               xe.data_ptr(), 2, ws.ptr, st))
+    d = ws.fetch()
+    rp, rd, code, _ = O.overlap_correction(mode, op1, ox, oxe, divisor=2)
+    assert to_np(params).tobytes() == rp.tobytes() and d.max_outer_step == rd.max_outer_step
