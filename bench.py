@@ -48,6 +48,11 @@ CONFIGS = {
                        "tau=4 (BASELINE.json configs[0], the reference's CPU fixture scale)",
            "mode": 1, "n": 1 << 20, "tau": 4, "bytes_per_param": 32, "local_workers": 4,
            "storage": "fp32"},
+    "c3f64": {"workload": "C3 in the reference's own precision: 1.3B-param fp64 params and state "
+                          "(the F64 mode, bitwise the reference's fp64 outer step), one CO2 worker "
+                          "per B200, tau=12 (secondary line; the headline C3 is bf16-mixed)",
+              "mode": 0, "n": 1_300_000_000, "tau": 12, "bytes_per_param": 64,
+              "storage": "fp64 everywhere", "e2e_default": False},
     "c4shard": {"workload": "C4 shard on one GPU: 7B/8 = 875M-param bf16-mixed shard, "
                             "worker-local step",
                 "mode": 2, "n": 875_000_000, "tau": 12, "bytes_per_param": 26,
@@ -596,7 +601,7 @@ def main():
 
     # --- e2e through the host-buffer entry (pinned H2D + kernel + D2H timed)
     e2e = None
-    if not args.no_e2e and not sharded and not gclip:  # the host entry is the reference clip
+    if not args.no_e2e and cfg.get("e2e_default", True) and not sharded and not gclip:  # the host entry is the reference clip
         e2e = run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist)
         e2e["numa_bound_cores"] = numa_cores  # None: not bound (CO2_BENCH_NUMA=0 / no NVML)
 

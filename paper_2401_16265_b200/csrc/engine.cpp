@@ -432,14 +432,21 @@ static co2_status_t nccl_fixed_rs(co2_aar* e, ncclComm_t comm, int which, co2_dt
   CO2_TRY(stage_reserve(e, which, es * (size_t)slice * (size_t)G + 16));
   char* stg = static_cast<char*>(e->stage[which]);
   const char* s8 = static_cast<const char*>(src);
-  CO2_NCCL(ncclGroupStart());
-  for (int p = 0; p < G; ++p) {
-    if (p == r) continue;
-    if (len(p) > 0) CO2_NCCL(ncclSend(s8 + es * lo(p), (size_t)len(p), nccl_dtype(dt), p, comm, st));
-    if (mine > 0)
-      CO2_NCCL(ncclRecv(stg + es * (size_t)slice * p, (size_t)mine, nccl_dtype(dt), p, comm, st));
+  if (n == slice * G) {
+    // Equal slices: NCCL's all-to-all collective (one kernel over every
+    // peer) moves the same bytes as the grouped send / recv below.
+    CO2_NCCL(ncclAlltoAll(s8, stg, (size_t)slice, nccl_dtype(dt), comm, st));
+  } else {
+    CO2_NCCL(ncclGroupStart());
+    for (int p = 0; p < G; ++p) {
+      if (p == r) continue;
+      if (len(p) > 0)
+        CO2_NCCL(ncclSend(s8 + es * lo(p), (size_t)len(p), nccl_dtype(dt), p, comm, st));
+      if (mine > 0)
+        CO2_NCCL(ncclRecv(stg + es * (size_t)slice * p, (size_t)mine, nccl_dtype(dt), p, comm, st));
+    }
+    CO2_NCCL(ncclGroupEnd());
   }
-  CO2_NCCL(ncclGroupEnd());
   const void* parts[kMaxNcclRanks];
   for (int p = 0; p < G; ++p)
     parts[p] = p == r ? static_cast<const void*>(s8 + es * lo(r))
@@ -455,6 +462,10 @@ static co2_status_t nccl_fixed_ag(co2_aar* e, ncclComm_t comm, co2_dtype_t dt, v
   auto lo = [&](int p) { return std::min<int64_t>((int64_t)p * slice, n); };
   auto len = [&](int p) { return std::max<int64_t>(0, std::min<int64_t>(slice, n - lo(p))); };
   char* b8 = static_cast<char*>(buf);
+  if (n == slice * G) {  // equal slices: the in-place all-gather collective
+    CO2_NCCL(ncclAllGather(b8 + es * lo(r), b8, (size_t)slice, nccl_dtype(dt), comm, st));
+    return CO2_OK;
+  }
   CO2_NCCL(ncclGroupStart());
   for (int p = 0; p < G; ++p) {
     if (p == r) continue;

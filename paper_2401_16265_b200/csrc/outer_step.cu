@@ -240,6 +240,68 @@ __device__ bool block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr
   return true;
 }
 
+__device__ __forceinline__ void partial_merge(Partial& b, const Partial& q) {
+  b.min_gap = q.min_gap < b.min_gap ? q.min_gap : b.min_gap;
+  b.max_step = q.max_step > b.max_step ? q.max_step : b.max_step;
+  b.clipped += q.clipped;
+  b.floored += q.floored;
+  b.flags |= q.flags;
+  b.pad |= q.pad;
+}
+
+__device__ __forceinline__ Partial warp_fold(Partial b) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Partial q;
+    q.min_gap = __shfl_xor_sync(0xffffffffu, b.min_gap, o);
+    q.max_step = __shfl_xor_sync(0xffffffffu, b.max_step, o);
+    q.clipped = __shfl_xor_sync(0xffffffffu, b.clipped, o);
+    q.floored = __shfl_xor_sync(0xffffffffu, b.floored, o);
+    q.flags = __shfl_xor_sync(0xffffffffu, b.flags, o);
+    q.pad = __shfl_xor_sync(0xffffffffu, b.pad, o);
+    partial_merge(b, q);
+  }
+  return b;
+}
+
+// Fold one Partial per thread warp -> smem -> fixed warp order; the result
+// is valid in thread 0.  Every thread must call it.
+template <int NT>
+__device__ Partial block_fold(const Partial& mine) {
+  constexpr int NW = NT / 32;
+  __shared__ Partial sh[NW];
+  const Partial b = warp_fold(mine);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();  // sh may still be read by a previous call's thread 0
+  if (lane == 0) sh[wid] = b;
+  __syncthreads();
+  Partial r = sh[0];
+  if (threadIdx.x == 0)
+    for (int w = 1; w < NW; ++w) partial_merge(r, sh[w]);
+  return r;
+}
+
+// This CTA's diagnostics (valid in thread 0).
+template <int NT>
+__device__ Partial block_partial(const Acc& a) {
+  return block_fold<NT>(Partial{a.min_gap, a.max_step, (unsigned long long)a.clipped,
+                                (unsigned long long)a.floored, a.flags, 0u});
+}
+
+// Fold count partials written by other CTAs in fixed order: thread-strided,
+// then block_fold.  Valid in thread 0; all threads call.
+template <int NT>
+__device__ Partial fold_partials(const Partial* parts, int count) {
+  Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
+  for (int i = threadIdx.x; i < count; i += NT) {
+    const Partial* q = parts + i;
+    Partial v{__ldcg(&q->min_gap), __ldcg(&q->max_step), __ldcg(&q->clipped),
+              __ldcg(&q->floored), __ldcg(&q->flags), __ldcg(&q->pad)};
+    partial_merge(b, v);
+  }
+  return block_fold<NT>(b);
+}
+
 // ---------------------------------------------------------- fused element
 template <typename TC>
 struct Hyp {
@@ -2345,16 +2407,21 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
   h.penalty = a.penalty;
   h.clip = a.clip;
   h.divide = 0;
-  // Roles: thread-item k of the flattened (vector, role) space is vector
-  // k / R, role k % R with R = g + 1 (roles 0..g-1: worker g's step; role g:
-  // this round's average).  The host makes gridDim.x * NT a multiple of R,
-  // so a thread's role is fixed and it keeps ONE accumulator; the G + 1
-  // items of a vector are adjacent lanes, so xbar is fetched from HBM once.
+  // Roles are CTA-uniform: CTA b has role b % R (R = g + 1; roles 0..g-1:
+  // worker role's fused step, role g: this round's average) and chunk b / R,
+  // and the host makes gridDim.x a multiple of R.  Every warp therefore runs
+  // one code path over one worker's contiguous vectors (no divergence, fully
+  // coalesced), and the average's G loads per vector are issued together.
+  // xbar is read by the G step roles of the same chunk, adjacent CTAs, so
+  // its repeat reads hit L2.
   const int R = a.g + 1;
-  const int64_t gt = (int64_t)blockIdx.x * NT + threadIdx.x;
-  const int role = (int)(gt % R);
-  const int64_t vstride = (int64_t)gridDim.x * NT / R;
+  const int role = (int)(blockIdx.x % R);
+  const int chunk = (int)(blockIdx.x / R);
+  const int nchunks = (int)(gridDim.x / R);
+  const int64_t vstride = (int64_t)nchunks * NT;
+  const int64_t v0 = (int64_t)chunk * NT + threadIdx.x;
   const int64_t nv = a.n / V;
+  const int64_t tail = a.n - nv * V;  // n % V coordinates, one per thread of chunk 0
   AccT<TC> acc;
   unsigned int avg_flags = 0;
   const TL* XB = static_cast<const TL*>(a.xbar);
@@ -2374,7 +2441,7 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
         ld_vec<TS, V>(P0 + e, q0);
         ld_vec<TL, V>(P1 + e, q1);
         ld_vec<TS, V>(Mm + e, mo);
-        // default-cached: the vector's other workers hit it in L1 / L2
+        // default-cached: the other workers' CTAs of this chunk hit it in L2
         constexpr int XBYTES = V * (int)sizeof(TL);
         if constexpr (XBYTES % 16 == 0) {
           uint4 r[XBYTES / 16];
@@ -2416,23 +2483,32 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
         if (G) G[e] = gs[0];
       }
     };
-    for (int64_t i = gt / R; i < nv; i += vstride) step(i * V, V);
-    // scalar tail (n % V coordinates): coordinate k of the tail to item k*R + role
-    if (V > 1 && gt / R < a.n - nv * V) step(nv * V + gt / R, 1);
+    for (int64_t i = v0; i < nv; i += vstride) step(i * V, V);
+    if (V > 1 && chunk == 0 && (int64_t)threadIdx.x < tail) step(nv * V + threadIdx.x, 1);
   } else {
     const TC gd = (TC)a.g;
     TL* AO = static_cast<TL*>(a.avg_out);
     auto average = [&](int64_t e, int cnt) {
-      TC sacc[V];
-      for (int w = 0; w < a.g; ++w) {  // ascending worker order, param_ops.cpp:26-28
-        const TL* C = static_cast<const TL*>(a.cur[w]);
-        TL c[V];
-        if (cnt == V)
-          ld_vec<TL, V>(C + e, c);
-        else
-          c[0] = C[e];
+      TL c[kMaxLocalRound][V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) sacc[v] = (w == 0) ? to_c(c[v]) : sacc[v] + to_c(c[v]);
+      for (int w = 0; w < kMaxLocalRound; ++w) {  // all loads in flight together
+        if (w < a.g) {
+          const TL* C = static_cast<const TL*>(a.cur[w]);
+          if (cnt == V)
+            ld_vec<TL, V>(C + e, c[w]);
+          else
+            c[w][0] = C[e];
+        }
+      }
+      TC sacc[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) sacc[v] = to_c(c[0][v]);
+#pragma unroll
+      for (int w = 1; w < kMaxLocalRound; ++w) {  // ascending worker order, param_ops.cpp:26-28
+        if (w < a.g) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) sacc[v] = sacc[v] + to_c(c[w][v]);
+        }
       }
       TL o[V];
 #pragma unroll
@@ -2448,99 +2524,43 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
       else
         AO[e] = o[0];
     };
-    for (int64_t i = gt / R; i < nv; i += vstride) average(i * V, V);
-    if (V > 1 && gt / R < a.n - nv * V) average(nv * V + gt / R, 1);
+    for (int64_t i = v0; i < nv; i += vstride) average(i * V, V);
+    if (V > 1 && chunk == 0 && (int64_t)threadIdx.x < tail) average(nv * V + threadIdx.x, 1);
   }
-  // ---- diagnostics: per-CTA partial per role, folded in thread order
-  __shared__ Partial part[NT];
-  __shared__ unsigned int s_avg;
-  __shared__ bool s_last;
-  {
-    const Acc b = acc.widen();
-    part[threadIdx.x] = Partial{b.min_gap, b.max_step, (unsigned long long)b.clipped,
-                                (unsigned long long)b.floored, b.flags, avg_flags};
-  }
-  __syncthreads();
+  // ---- diagnostics: this CTA's partial into its role's slot (the average's
+  // flags into worker 0's partial array after the nchunks step partials),
+  // then the last CTA folds each role's partials in fixed chunk order.
+  Acc b0 = acc.widen();
+  b0.flags |= avg_flags;
+  const Partial mine = block_partial<NT>(b0);
   WsHeader* hdr0 = ws_header(a.ws[0]);
-  if ((int)threadIdx.x < R) {
-    const int w = threadIdx.x;
-    Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
-    const int64_t base = (int64_t)blockIdx.x * NT;
-    for (int t = 0; t < NT; ++t) {
-      if ((int)((base + t) % R) != w) continue;
-      const Partial& q = part[t];
-      b.min_gap = q.min_gap < b.min_gap ? q.min_gap : b.min_gap;
-      b.max_step = q.max_step > b.max_step ? q.max_step : b.max_step;
-      b.clipped += q.clipped;
-      b.floored += q.floored;
-      b.flags |= q.flags;
-      b.pad |= q.pad;
-    }
-    if (w < a.g)
-      ws_partials(a.ws[w])[blockIdx.x] = b;
-    else
-      s_avg = b.pad;  // the average's flags
-  }
-  __syncthreads();
+  __shared__ bool s_last;
   if (threadIdx.x == 0) {
-    ws_partials(a.ws[0])[blockIdx.x].pad = s_avg;  // ride in worker 0's partial
+    Partial* dst = role < a.g ? ws_partials(a.ws[role]) + chunk
+                              : ws_partials(a.ws[0]) + nchunks + chunk;
+    *dst = mine;
     __threadfence();
     s_last = atomicAdd(&hdr0->ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  constexpr int NW = NT / 32;
-  __shared__ Partial sh[NW];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int w = 0; w < a.g; ++w) {
-    const Partial* parts = ws_partials(a.ws[w]);
-    Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
-      const Partial* q = parts + i;
-      double qmg = __ldcg(&q->min_gap), qms = __ldcg(&q->max_step);
-      b.min_gap = qmg < b.min_gap ? qmg : b.min_gap;
-      b.max_step = qms > b.max_step ? qms : b.max_step;
-      b.clipped += __ldcg(&q->clipped);
-      b.floored += __ldcg(&q->floored);
-      b.flags |= __ldcg(&q->flags);
-      b.pad |= __ldcg(&q->pad);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double omg = __shfl_xor_sync(0xffffffffu, b.min_gap, o);
-      double oms = __shfl_xor_sync(0xffffffffu, b.max_step, o);
-      b.min_gap = omg < b.min_gap ? omg : b.min_gap;
-      b.max_step = oms > b.max_step ? oms : b.max_step;
-      b.clipped += __shfl_xor_sync(0xffffffffu, b.clipped, o);
-      b.floored += __shfl_xor_sync(0xffffffffu, b.floored, o);
-      b.flags |= __shfl_xor_sync(0xffffffffu, b.flags, o);
-      b.pad |= __shfl_xor_sync(0xffffffffu, b.pad, o);
-    }
-    __syncthreads();
-    if (lane == 0) sh[wid] = b;
-    __syncthreads();
+  for (int w = 0; w <= a.g; ++w) {
+    const Partial* parts = w < a.g ? ws_partials(a.ws[w]) : ws_partials(a.ws[0]) + nchunks;
+    const Partial r = fold_partials<NT>(parts, nchunks);
     if (threadIdx.x == 0) {
-      Partial r = sh[0];
-      for (int k = 1; k < NW; ++k) {
-        r.min_gap = sh[k].min_gap < r.min_gap ? sh[k].min_gap : r.min_gap;
-        r.max_step = sh[k].max_step > r.max_step ? sh[k].max_step : r.max_step;
-        r.clipped += sh[k].clipped;
-        r.floored += sh[k].floored;
-        r.flags |= sh[k].flags;
-        r.pad |= sh[k].pad;
-      }
       co2_diag_t d;
-      d.min_gap = r.min_gap;
-      d.max_outer_step = r.max_step;
-      d.n_clipped = (int64_t)r.clipped;
-      d.n_floored = (int64_t)r.floored;
-      d.flags = r.flags;
-      d.pad = 0;
-      ws_header(a.ws[w])->diag = d;
-      if (a.host_diag[w]) *a.host_diag[w] = d;
-      if (w == 0 && a.avg_diag) {
-        co2_diag_t ad{INFINITY, 0.0, 0, 0, r.pad, 0};
+      if (w < a.g) {
+        d.min_gap = r.min_gap;
+        d.max_outer_step = r.max_step;
+        d.n_clipped = (int64_t)r.clipped;
+        d.n_floored = (int64_t)r.floored;
+        d.flags = r.flags;
+        d.pad = 0;
+        ws_header(a.ws[w])->diag = d;
+        if (a.host_diag[w]) *a.host_diag[w] = d;
+      } else if (a.avg_diag) {
+        co2_diag_t ad{INFINITY, 0.0, 0, 0, r.flags, 0};
         *a.avg_diag = ad;
       }
     }
@@ -2556,16 +2576,12 @@ co2_status_t launch_local_round(const LocalRoundArgs& a, cudaStream_t s) {
   auto k = local_round_kernel<M, V, kThreads>;
   const int R = a.g + 1;
   const int64_t nv = a.n / V > 0 ? a.n / V : 1;
-  int grid = grid_for(k, nv * R, kThreads);
-  // gridDim.x * kThreads must be a multiple of R (fixed role per thread)
-  int step = R;
-  for (int d = kThreads; d % 2 == 0 && step % 2 == 0;) {
-    d /= 2;
-    step /= 2;
-  }
-  grid = grid / step * step;
-  if (grid < step) grid = step;
-  k<<<grid, kThreads, 0, s>>>(a);
+  // chunks per role: the step grid for one worker's vectors, and at most
+  // kMaxBlocks / 2 so the average's partials fit after worker 0's.
+  int chunks = grid_for(k, nv, kThreads);
+  if (chunks > kMaxBlocks / 2) chunks = kMaxBlocks / 2;
+  if ((int64_t)chunks * R > kMaxBlocks) chunks = kMaxBlocks / R;
+  k<<<chunks * R, kThreads, 0, s>>>(a);
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }

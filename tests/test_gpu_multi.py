@@ -24,16 +24,21 @@ def _port():
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("transport,world", [("nccl", 2), ("nccl", 4), ("p2p", 2), ("p2p", 4),
-                                             ("p2pfused", 2), ("p2pfused", 4)])
-def test_multi_rank_rounds_bitwise(mode, transport, world):
+@pytest.mark.parametrize("transport,world,n", [("nccl", 2, 1 << 20), ("nccl", 4, 1 << 20),
+                                               ("nccl", 4, 1_000_003), ("p2p", 2, 1 << 20),
+                                               ("p2p", 4, 1 << 20), ("p2pfused", 2, 1 << 20),
+                                               ("p2pfused", 4, 1 << 20)])
+def test_multi_rank_rounds_bitwise(mode, transport, world, n):
     """Worker-local co2_round across ranks, bitwise against the oracle --
     params, momentum and the consumed average -- for every fixed-order
     transport (NCCL's default slice-exchange algorithm, P2P, fused P2P): the
-    reference's average() (param_ops.cpp:16-33) at any G."""
+    reference's average() (param_ops.cpp:16-33) at any G.  NCCL: n = 2^20
+    splits into equal slices (ncclAlltoAll + in-place ncclAllGather), the
+    ragged n into short last slices (grouped ncclSend / ncclRecv)."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT=transport)
+    env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT=transport,
+               CO2_TEST_N=str(n))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),

@@ -41,7 +41,7 @@ def main():
     ap.add_argument("--mode", type=int, default=1)
     ap.add_argument("--n", type=int, default=125_000_000)
     ap.add_argument("--taus", default="1,2,3,4,6,8,12,16,24,32")
-    ap.add_argument("--rounds", type=int, default=6)
+    ap.add_argument("--rounds", type=int, default=8)
     ap.add_argument("--knee", type=float, default=4.0, help="tau at which tau*t_comp = t_comm")
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ncclsum", "p2p"])
@@ -145,12 +145,15 @@ def main():
             engine.register_worker(w2)
         w2.enable_timing(4 * a.rounds)
         n_ev0 = len(engine.events())
-        walls = []
+        # Rounds run back to back with no host synchronisation: a device-wide
+        # synchronize between rounds would drain the comm stream and hide the
+        # one-step-stale reduce's stall.  Round walls are compute-stream events.
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.rounds + 1)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         for t in range(a.rounds):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            if world > 1:
-                dist.barrier()
-            e0.record(stream)
+            evs[t].record(stream)
             w2.snapshot_start()
             if t == 0:
                 w2.snapshot_first()
@@ -161,11 +164,10 @@ def main():
                     w2.params[:k], lr=1e-6, worker=rank, step=t * tau + j,
                     snapshot_out=w2.buffer(L.BUF_XFIRST)[:k] if j == 0 and t > 0 else None)
             co2.co2_round([w2], engine, hyper, tau, sync=False)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            walls.append(e0.elapsed_time(e1) * 1e-3)
+        evs[a.rounds].record(stream)
         co2.co2_round_drain([w2], engine)
         torch.cuda.synchronize()
+        walls = [evs[t].elapsed_time(evs[t + 1]) * 1e-3 for t in range(a.rounds)]
         kt = w2.step_times()
         ev = engine.events()[n_ev0:]
         launches = {e["handle_id"]: e["t_sim"] for e in ev if e["event"] == "launch"}
