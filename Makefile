@@ -20,7 +20,7 @@ all: $(LIB) oracle
 build:
 	mkdir -p build
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh include/co2_b200.h | build
+build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/bulk.cuh $(CSRC)/p2p_sync.cuh include/co2_b200.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 build/%.o: $(CSRC)/%.cpp $(CSRC)/common.cuh include/co2_b200.h | build

@@ -26,6 +26,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include "bulk.cuh"
 #include "common.cuh"
 #include "p2p_sync.cuh"
 
@@ -171,6 +172,166 @@ __global__ void __launch_bounds__(NT) p2p_average_kernel(const P2PArgs a) {
   }
 }
 
+// Bulk-copy variant of p2p_average_kernel (CO2_P2P_BULK=1): the same slice
+// ownership, barriers and arithmetic, with the G remote loads of each tile
+// issued by ONE lane as cp.async.bulk copies (TMA over NVLink) into a
+// STAGES-deep shared-memory ring, so the bytes in flight sit in shared
+// memory instead of registers.  NCW consumer warps sum the G copies of each
+// 16-byte vector in ascending rank order, divide once, and store the result
+// into every rank with 128-bit STGs.  A CTA is (NCW + 1) warps, so the reduce
+// displaces far fewer registers of the co-running fused step (which fills
+// the register file at 4 x 256 threads x 64 registers per SM) than the
+// register-staged kernel's 256 threads x ~84 registers.
+template <typename TL, typename TC, int TILE, int STAGES, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32) p2p_bulk_average_kernel(const P2PArgs a) {
+  constexpr int NT = (NCW + 1) * 32;
+  constexpr int V = 16 / (int)sizeof(TL);
+  constexpr int CH = TILE * (int)sizeof(TL);  // bytes per rank per tile
+  static_assert(TILE % (NCW * 32 * V) == 0, "tile must split over the consumer lanes");
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + STAGES;
+  unsigned char* ring = smem + 128;
+  static_assert(STAGES * 16 <= 128, "barrier header");
+  Signals* mine = a.sig[a.rank];
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int p = 0; p < a.world; ++p) st_release_sys(&a.sig[p]->ready[a.rank], a.epoch);
+    bool ok = true;
+    for (int p = 0; p < a.world && ok; ++p) ok = spin_until(&mine->ready[p], a.epoch, mine);
+    if (!ok) mine->error = 1;
+    s_ok = ok;
+  }
+  __syncthreads();
+  const int G = a.world;
+  const int64_t lo = (int64_t)a.rank * a.shard;
+  int64_t hi = lo + a.shard;
+  if (hi > a.n) hi = a.n;
+  const int64_t len = hi > lo ? hi - lo : 0;
+  const int64_t ntiles = len / TILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TC g = (TC)G;
+  if (s_ok) {
+    if (warp == NCW) {
+      if (lane == 0) {  // producer
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((unsigned)(it / STAGES) & 1u) ^ 1u);
+          unsigned char* st = ring + (size_t)s * CH * G;
+          const int64_t e = lo + t * TILE;
+          mbar_arrive_expect_tx(&full[s], (unsigned)(CH * G));
+          for (int p = 0; p < G; ++p)
+            bulk_g2s_nohint(st + (size_t)p * CH, static_cast<const TL*>(a.bufs[p]) + e, CH,
+                            &full[s]);
+        }
+      }
+    } else {  // consumers
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (unsigned)(it / STAGES) & 1u);
+        const unsigned char* st = ring + (size_t)s * CH * G;
+        const int64_t e0 = lo + t * TILE;
+#pragma unroll
+        for (int q = 0; q < TILE / (NCW * 32 * V); ++q) {
+          const int o = (q * NCW * 32 + warp * 32 + lane) * V;
+          TC acc[V];
+          {
+            const uint4 r = *reinterpret_cast<const uint4*>(st + (size_t)o * sizeof(TL));
+            const TL* v0 = reinterpret_cast<const TL*>(&r);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              if constexpr (sizeof(TL) == 2) acc[k] = ld_c(reinterpret_cast<const bf16raw*>(v0 + k));
+              else acc[k] = (TC)v0[k];
+            }
+          }
+          for (int p = 1; p < G; ++p) {
+            const uint4 r =
+                *reinterpret_cast<const uint4*>(st + (size_t)p * CH + (size_t)o * sizeof(TL));
+            const TL* vp = reinterpret_cast<const TL*>(&r);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              TC x;
+              if constexpr (sizeof(TL) == 2) x = ld_c(reinterpret_cast<const bf16raw*>(vp + k));
+              else x = (TC)vp[k];
+              acc[k] = acc[k] + x;  // ascending worker order, param_ops.cpp:26-28
+            }
+          }
+          uint4 out;
+          TL* ov = reinterpret_cast<TL*>(&out);
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            TC r = acc[k] / g;  // one division, param_ops.cpp:30
+            if constexpr (sizeof(TL) == 2) {
+              __nv_bfloat16 h = __float2bfloat16_rn((float)r);
+              reinterpret_cast<uint16_t*>(ov)[k] = __bfloat16_as_ushort(h);
+            } else {
+              ov[k] = (TL)r;
+            }
+          }
+          for (int p = 0; p < G; ++p)
+            __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.bufs[p]) + e0 + o), out);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    }
+    // remainder of the slice (len % TILE, vectors then scalars): CTA 0
+    if (blockIdx.x == 0) {
+      for (int64_t j = lo + ntiles * TILE + threadIdx.x; j < hi; j += NT) {
+        TC acc;
+        if constexpr (sizeof(TL) == 2)
+          acc = ld_c(static_cast<const bf16raw*>(a.bufs[0]) + j);
+        else
+          acc = (TC)__ldcg(static_cast<const TL*>(a.bufs[0]) + j);
+        for (int p = 1; p < G; ++p) {
+          TC x;
+          if constexpr (sizeof(TL) == 2)
+            x = ld_c(static_cast<const bf16raw*>(a.bufs[p]) + j);
+          else
+            x = (TC)__ldcg(static_cast<const TL*>(a.bufs[p]) + j);
+          acc = acc + x;
+        }
+        TC r = acc / g;
+        for (int p = 0; p < G; ++p) {
+          if constexpr (sizeof(TL) == 2) {
+            __nv_bfloat16 h = __float2bfloat16_rn((float)r);
+            static_cast<bf16raw*>(a.bufs[p])[j].b = __bfloat16_as_ushort(h);
+          } else {
+            static_cast<TL*>(a.bufs[p])[j] = (TL)r;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
+    if (!spin_until(&mine->done, a.done_target, mine)) mine->error = 2;
+  }
+}
+
+template <typename TL, typename TC, int TILE, int STAGES, int NCW>
+void launch_p2p_bulk(const P2PArgs& a, int ctas, cudaStream_t s) {
+  auto k = p2p_bulk_average_kernel<TL, TC, TILE, STAGES, NCW>;
+  // ring sized for the world: G chunks of TILE per stage
+  const size_t smem = 128 + (size_t)STAGES * TILE * sizeof(TL) * a.world;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(128 + (size_t)STAGES * TILE * sizeof(TL) * kMaxRanks));
+    attr = true;
+  }
+  k<<<ctas, (NCW + 1) * 32, smem, s>>>(a);
+}
+
 // Slice reduce for the sharded (ghost-consistent) layout: rank r averages
 // slice r of `nb` logical buffers (x_{t,tau} and x_{t,1}) over all ranks in
 // ascending rank order into local slice outputs -- a deterministic
@@ -289,6 +450,17 @@ int p2p_threads() {
   return v;
 }
 
+// Bulk-copy all-reduce kernel (CO2_P2P_BULK = consumer warps per CTA, 2 or
+// 4; 0 / unset = the register-staged kernel).
+int p2p_bulk() {
+  static const int v = [] {
+    const char* e = getenv("CO2_P2P_BULK");
+    const int x = e ? atoi(e) : 0;
+    return x <= 0 ? 0 : (x >= 4 ? 4 : 2);
+  }();
+  return v;
+}
+
 // Threads per CTA of the sharded slice reduce (CO2_P2P_SLICE_THREADS = 256
 // | 512, default 512).  At equal total threads 256 and 512 measure the same
 // (profiles/r01/bench/c4_slice_threads.txt); the slice reduce is NVLink-bound.
@@ -379,6 +551,26 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
   a.done_target = *done_total;
   // R = rank capacity of the instantiation, U = vectors in flight per thread
   // (fewer ranks -> more vectors, keeping ~R*U*16 B of loads per thread).
+  if (p2p_bulk() > 0) {
+    // 4 KB per rank per tile, 4 stages; consumer warps from CO2_P2P_BULK
+    const int ncw = p2p_bulk();
+    switch (dt) {
+      case CO2_DTYPE_F64:
+        if (ncw >= 4) launch_p2p_bulk<double, double, 512, 4, 4>(a, ctas, s);
+        else launch_p2p_bulk<double, double, 512, 4, 2>(a, ctas, s);
+        break;
+      case CO2_DTYPE_F32:
+        if (ncw >= 4) launch_p2p_bulk<float, float, 1024, 4, 4>(a, ctas, s);
+        else launch_p2p_bulk<float, float, 1024, 4, 2>(a, ctas, s);
+        break;
+      default:
+        if (ncw >= 4) launch_p2p_bulk<bf16raw, float, 2048, 4, 4>(a, ctas, s);
+        else launch_p2p_bulk<bf16raw, float, 2048, 4, 2>(a, ctas, s);
+        break;
+    }
+    CO2_CUDA(cudaGetLastError());
+    return CO2_OK;
+  }
   const int cap = rank_cap(world);
   const int nt = p2p_threads();
 #define CO2_P2P_NT(TL, TC, V, R, U)                                                      \

@@ -27,7 +27,8 @@ def _port():
 @pytest.mark.parametrize("transport,world,n", [("nccl", 2, 1 << 20), ("nccl", 4, 1 << 20),
                                                ("nccl", 4, 1_000_003), ("p2p", 2, 1 << 20),
                                                ("p2p", 4, 1 << 20), ("p2pfused", 2, 1 << 20),
-                                               ("p2pfused", 4, 1 << 20)])
+                                               ("p2pfused", 4, 1 << 20), ("p2pbulk", 2, 1 << 20),
+                                               ("p2pbulk", 4, 1_000_003)])
 def test_multi_rank_rounds_bitwise(mode, transport, world, n):
     """Worker-local co2_round across ranks, bitwise against the oracle --
     params, momentum and the consumed average -- for every fixed-order
@@ -39,6 +40,8 @@ def test_multi_rank_rounds_bitwise(mode, transport, world, n):
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ, CO2_TEST_MODE=str(mode), CO2_TEST_TRANSPORT=transport,
                CO2_TEST_N=str(n))
+    if transport == "p2pbulk":  # the TMA bulk-copy all-reduce kernel
+        env.update(CO2_P2P_BULK="2", CO2_TEST_TRANSPORT="p2p")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
