@@ -1015,6 +1015,7 @@ co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
       case 2: launch_variant<M, 4, 1>(a, s); break;
       case 3: launch_variant<M, 8, 1>(a, s); break;
       case 4: launch_variant<M, 8, 1, 4>(a, s); break;
+      case 5: launch_variant<M, 4, 2, 4>(a, s); break;
       default: launch_variant<M, 4, 1, 4>(a, s); break;
     }
   } else {
@@ -1023,6 +1024,7 @@ co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
       case 2: launch_variant<M, 2, 1>(a, s); break;
       case 3: launch_variant<M, 4, 1>(a, s); break;
       case 4: launch_variant<M, 2, 2, 3>(a, s); break;
+      case 5: launch_variant<M, 2, 1, 3>(a, s); break;
       default: launch_variant<M, 2, 1, 4>(a, s); break;
     }
   }

@@ -10,3 +10,5 @@ timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
 for b in 2 4; do for c in 32 64 148; do
 CO2_P2P_BULK=$b timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port $((29670+b*3+rep)) bench.py --gpus 2 --steps 20 --warmup 5 --no-e2e --no-cpu --max-ctas $c > $O/bench_c3_n2_bulk${b}_c${c}_r$rep.json 2> $O/bench_c3_n2_bulk${b}_c${c}_r$rep.err
 done; done; done
+timeout 400 python tools/tune_fused.py --mode 1 --n 125000000 --variants 0,3,4,5 --waves 4,8,32 --reps 3 --iters 60 > $O/tune_c2_f32.jsonl 2> $O/tune_c2_f32.err
+timeout 600 python tools/tune_fused.py --mode 0 --n 1300000000 --variants 0,5 --reps 3 --iters 20 > $O/tune_c3_f64.jsonl 2> $O/tune_c3_f64.err

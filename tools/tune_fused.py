@@ -24,9 +24,11 @@ NAMES = {
         10: "bulk 2048x4 st, 4 cw", 11: "bulk 1024x4, 4 cw", 12: "bulk 2048x3, 8 cw",
         13: "bulk 4096x3, 8 cw", 14: "bulk 1024x6, 8 cw"},
     1: {0: "(4,1) 4 CTA/SM", 1: "(4,2)", 2: "(4,1)", 3: "(8,1)", 4: "(8,1) 4 CTA/SM",
+        5: "(4,2) 4 CTA/SM",
         10: "bulk 1024x5, 4 cw", 11: "bulk 1024x4, 4 cw", 12: "bulk 2048x4, 8 cw",
         13: "bulk 1024x8, 8 cw", 14: "bulk 512x6, 4 cw"},
     0: {0: "(2,1) 4 CTA/SM", 1: "(2,2)", 2: "(2,1)", 3: "(4,1)", 4: "(2,2) 3 CTA/SM",
+        5: "(2,1) 3 CTA/SM",
         10: "bulk 512x5, 4 cw", 11: "bulk 256x6, 2 cw", 12: "bulk 1024x4, 8 cw"},
 }
 
