@@ -2493,45 +2493,42 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
     if (V > 1 && chunk == 0 && (int64_t)threadIdx.x < tail) average(nv * V + threadIdx.x, 1);
   }
   // ---- diagnostics: this CTA's partial into its role's slot (the average's
-  // flags into worker 0's partial array after the nchunks step partials),
-  // then the last CTA folds each role's partials in fixed chunk order.
+  // flags into worker 0's partial array after the nchunks step partials);
+  // the last CTA OF EACH ROLE (a ticket per role: worker w's workspace
+  // ticket, the average's ticket2 in worker 0's) folds that role's partials
+  // in fixed chunk order, so the G + 1 folds run in parallel.
   Acc b0 = acc.widen();
   b0.flags |= avg_flags;
   const Partial mine = block_partial<NT>(b0);
-  WsHeader* hdr0 = ws_header(a.ws[0]);
+  Partial* parts = role < a.g ? ws_partials(a.ws[role]) : ws_partials(a.ws[0]) + nchunks;
+  unsigned int* ticket =
+      role < a.g ? &ws_header(a.ws[role])->ticket : &ws_header(a.ws[0])->ticket2;
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
-    Partial* dst = role < a.g ? ws_partials(a.ws[role]) + chunk
-                              : ws_partials(a.ws[0]) + nchunks + chunk;
-    *dst = mine;
+    parts[chunk] = mine;
     __threadfence();
-    s_last = atomicAdd(&hdr0->ticket, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(ticket, 1u) == (unsigned)nchunks - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int w = 0; w <= a.g; ++w) {
-    const Partial* parts = w < a.g ? ws_partials(a.ws[w]) : ws_partials(a.ws[0]) + nchunks;
-    const Partial r = fold_partials<NT>(parts, nchunks);
-    if (threadIdx.x == 0) {
-      co2_diag_t d;
-      if (w < a.g) {
-        d.min_gap = r.min_gap;
-        d.max_outer_step = r.max_step;
-        d.n_clipped = (int64_t)r.clipped;
-        d.n_floored = (int64_t)r.floored;
-        d.flags = r.flags;
-        d.pad = 0;
-        ws_header(a.ws[w])->diag = d;
-        if (a.host_diag[w]) *a.host_diag[w] = d;
-      } else if (a.avg_diag) {
-        co2_diag_t ad{INFINITY, 0.0, 0, 0, r.flags, 0};
-        *a.avg_diag = ad;
-      }
-    }
-  }
+  const Partial r = fold_partials<NT>(parts, nchunks);
   if (threadIdx.x == 0) {
-    hdr0->ticket = 0;  // self-reset for the next launch
+    if (role < a.g) {
+      co2_diag_t d;
+      d.min_gap = r.min_gap;
+      d.max_outer_step = r.max_step;
+      d.n_clipped = (int64_t)r.clipped;
+      d.n_floored = (int64_t)r.floored;
+      d.flags = r.flags;
+      d.pad = 0;
+      ws_header(a.ws[role])->diag = d;
+      if (a.host_diag[role]) *a.host_diag[role] = d;
+    } else if (a.avg_diag) {
+      co2_diag_t ad{INFINITY, 0.0, 0, 0, r.flags, 0};
+      *a.avg_diag = ad;
+    }
+    *ticket = 0;  // self-reset for the next launch
     __threadfence_system();
   }
 }
