@@ -148,8 +148,29 @@ struct AccT {
   }
 };
 
+// Order-preserving 64-bit key of a double (monotone in the value for every
+// non-NaN double) and its inverse.
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
 // Returns true in every thread of the last block to arrive (after it wrote
 // the folded diagnostics), false elsewhere.
+//
+// Each block folds its threads (warp shuffles, then warps in fixed order)
+// and merges the block result into the workspace header with atomics: min
+// Lambda and max |x' - x_t0| as atomicMax over order-preserving keys, the
+// counts as 64-bit adds, the flags as OR.  Min, max, integer sums and OR are
+// exact and order-independent, so the result is bitwise deterministic for
+// any grid and any block completion order (per-thread and per-block values
+// are never NaN: a NaN never wins the `<` / `>` folds that produce them).
+// The last block (atomic ticket) publishes the diagnostics and resets the
+// accumulators: an O(1) tail instead of a fold over every block's partial.
 template <int NT>
 __device__ bool block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr) {
   // Warp level.
@@ -173,7 +194,6 @@ __device__ bool block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr
   if (lane == 0) sh[wid] = Partial{mg, ms, cl, fl, fg, 0u};
   __syncthreads();
   WsHeader* hdr = ws_header(ws);
-  Partial* parts = ws_partials(ws);
   if (threadIdx.x == 0) {
     Partial b = sh[0];
     for (int w = 1; w < NW; ++w) {  // fixed order
@@ -183,7 +203,13 @@ __device__ bool block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr
       b.floored += sh[w].floored;
       b.flags |= sh[w].flags;
     }
-    parts[blockIdx.x] = b;
+    // min as a max of inverted keys (0 = empty = +inf), max as a max of keys
+    // (0 = empty; the initial max_step +0.0 has a larger key than any "empty")
+    atomicMax(&hdr->acc_min_key, ~dkey(b.min_gap));
+    atomicMax(&hdr->acc_max_key, dkey(b.max_step));
+    if (b.clipped) atomicAdd(&hdr->acc_clipped, b.clipped);
+    if (b.floored) atomicAdd(&hdr->acc_floored, b.floored);
+    if (b.flags) atomicOr(&hdr->acc_flags, b.flags);
     if (px)
       __threadfence_system();  // this CTA's peer stores before the ticket
     else
@@ -193,51 +219,26 @@ __device__ bool block_finish(const Acc& a, void* ws, const P2PExit* px = nullptr
   }
   __syncthreads();
   if (!s_last) return false;
-  // Last block: fold all partials in fixed index order (thread-strided, then
-  // a fixed warp tree and fixed warp order), deterministic for a given grid.
-  __threadfence();
-  Partial b{INFINITY, 0.0, 0ull, 0ull, 0u, 0u};
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
-    const Partial* q = parts + i;
-    double qmg = __ldcg(&q->min_gap), qms = __ldcg(&q->max_step);
-    b.min_gap = qmg < b.min_gap ? qmg : b.min_gap;
-    b.max_step = qms > b.max_step ? qms : b.max_step;
-    b.clipped += __ldcg(&q->clipped);
-    b.floored += __ldcg(&q->floored);
-    b.flags |= __ldcg(&q->flags);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double omg = __shfl_xor_sync(0xffffffffu, b.min_gap, o);
-    double oms = __shfl_xor_sync(0xffffffffu, b.max_step, o);
-    b.min_gap = omg < b.min_gap ? omg : b.min_gap;
-    b.max_step = oms > b.max_step ? oms : b.max_step;
-    b.clipped += __shfl_xor_sync(0xffffffffu, b.clipped, o);
-    b.floored += __shfl_xor_sync(0xffffffffu, b.floored, o);
-    b.flags |= __shfl_xor_sync(0xffffffffu, b.flags, o);
-  }
-  __syncthreads();
-  if (lane == 0) sh[wid] = b;
-  __syncthreads();
   if (threadIdx.x == 0) {
-    Partial r = sh[0];
-    for (int w = 1; w < NW; ++w) {
-      r.min_gap = sh[w].min_gap < r.min_gap ? sh[w].min_gap : r.min_gap;
-      r.max_step = sh[w].max_step > r.max_step ? sh[w].max_step : r.max_step;
-      r.clipped += sh[w].clipped;
-      r.floored += sh[w].floored;
-      r.flags |= sh[w].flags;
-    }
-    hdr->diag.min_gap = r.min_gap;
-    hdr->diag.max_outer_step = r.max_step;
-    hdr->diag.n_clipped = (int64_t)r.clipped;
-    hdr->diag.n_floored = (int64_t)r.floored;
-    hdr->diag.flags = r.flags;
+    __threadfence();
+    volatile WsHeader* vh = hdr;
+    const unsigned long long kmin = vh->acc_min_key, kmax = vh->acc_max_key;
+    hdr->diag.min_gap = kmin ? dkey_inv(~kmin) : (double)INFINITY;
+    hdr->diag.max_outer_step = kmax ? dkey_inv(kmax) : 0.0;
+    hdr->diag.n_clipped = (int64_t)vh->acc_clipped;
+    hdr->diag.n_floored = (int64_t)vh->acc_floored;
+    hdr->diag.flags = vh->acc_flags;
     hdr->diag.pad = 0;
-    hdr->ticket = 0;  // self-reset for the next launch on this workspace
+    hdr->acc_min_key = 0ull;  // self-reset for the next launch on this workspace
+    hdr->acc_max_key = 0ull;
+    hdr->acc_clipped = 0ull;
+    hdr->acc_floored = 0ull;
+    hdr->acc_flags = 0u;
+    hdr->ticket = 0;
     __threadfence();
     if (px) p2p_exit_barrier(*px);
   }
+  __syncthreads();
   return true;
 }
 
