@@ -343,12 +343,15 @@ def run_local_workers(args, cfg) -> int:
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    host = []
     with ClockSampler(torch, torch.cuda.current_device()) as clk:
         for e0, e1 in ev:
             flush_w.zero_()  # evict the previous round's lines from L2 ...
             flush_r.max()    # ... and leave only clean lines behind
             e0.record(stream)
+            h0 = time.perf_counter()
             co2.co2_round(ws, eng, hyper, tau, sync=False)
+            host.append(time.perf_counter() - h0)
             e1.record(stream)
         torch.cuda.synchronize()
     t = sum(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3
@@ -386,6 +389,7 @@ def run_local_workers(args, cfg) -> int:
                      "bytes_per_param": bytes_round / (g * n)},
         "e2e": None, "cpu_baseline": None,
         "gpu_launches": args.steps, "clocks": clk.summary(),
+        "host_us_per_round": 1e6 * statistics.median(host),
         "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step},
     }
     print(json.dumps(line), flush=True)

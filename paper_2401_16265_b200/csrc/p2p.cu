@@ -52,9 +52,15 @@ struct P2PArgs {
   uint32_t done_target;       // cumulative exit-barrier count after this launch
 };
 
-// TL storage, TC compute, V elements per 16-byte vector.
+// TL storage, TC compute, V elements per 16-byte vector.  bf16 / fp32
+// instantiations are capped at 64 registers per thread (min blocks 1024/NT):
+// the co-running fused step fills the register file at 4 x 256 threads x 64
+// registers per SM, so a reduce CTA of NT x 64 registers takes exactly NT/256
+// step CTAs' worth of registers instead of rounding up to one more (the
+// uncapped 256-thread bf16 kernel used 72-84 registers, i.e. two step CTAs).
 template <typename TL, typename TC, int V, int R, int U, int NT>
-__global__ void __launch_bounds__(NT) p2p_average_kernel(const P2PArgs a) {
+__global__ void __launch_bounds__(NT, sizeof(TL) <= 4 ? 1024 / NT : 1)
+    p2p_average_kernel(const P2PArgs a) {
   Signals* mine = a.sig[a.rank];
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
