@@ -339,8 +339,8 @@ def run_local_workers(args, cfg) -> int:
     flush_w, flush_r = flush[:256 << 20], flush[256 << 20:].view(torch.int32)
     for _ in range(max(args.warmup, 3)):
         co2.co2_round(ws, eng, hyper, tau, sync=False)
-    ws[0].enable_timing(args.steps + 8)
     torch.cuda.synchronize()
+    h_first = eng.handle_count()  # one reduce handle per round
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     host = []
@@ -355,7 +355,10 @@ def run_local_workers(args, cfg) -> int:
             e1.record(stream)
         torch.cuda.synchronize()
     t = sum(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3
-    kt = ws[0].step_times()
+    # The round's own launch / done events bracket exactly local_round_kernel
+    # (no per-worker timing events: each event record costs the stream
+    # ~2.5 us, which would be charged to the round).
+    kt = [eng.info(h)["comm"] for h in range(h_first, h_first + args.steps)]
     k_mean = statistics.mean(kt) if kt else None
     r = co2.L.RoundResult()
     arr = (co2.C.c_void_p * g)(*[w.handle.value for w in ws])

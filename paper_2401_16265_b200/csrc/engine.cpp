@@ -46,6 +46,12 @@ struct Handle {
   cudaEvent_t start = nullptr, done = nullptr, wait_begin = nullptr, wait_end = nullptr;
   bool consumed = false, polled = false, last_poll = false, completion_logged = false;
   bool waited = false;
+  // Stream-ordered consume (single-launch LOCAL round): the reduce completed
+  // on the consumer's own stream, so the wait cannot stall and records no
+  // events; its end is the start event of handle `wait_alias` (recorded at
+  // the same stream position).  -1: an ordinary wait (wait_begin/wait_end).
+  int64_t wait_alias = -1;
+  cudaStream_t done_stream = nullptr;  // the stream `done` was recorded on
   int contributions = 0;
   co2_diag_t* diag = nullptr;  // LOCAL: pinned copy of the average's flags (pool slot)
   uint32_t* p2p_error = nullptr;  // P2P: pinned copy of the signal area's error word (pool slot)
@@ -222,11 +228,13 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
   e->rank = rank;
   e->world = world;
   e->workers = world;
-  // 96 (G = 2) / 64 (G >= 4) CTAs of 256 threads measured best while the
-  // reduce shares HBM and SMs with the 32-wave fused outer step (bench.py
-  // --max-ctas sweeps, profiles/r01/bench/{ctas,p2p_threads}_sweep.txt):
-  // fewer starve the reduce, more steal SM slots from the step.
-  e->ctas = ctas > 0 ? ctas : (world <= 2 ? 96 : 64);
+  // 96 CTAs of 256 threads while the reduce shares HBM and SMs with the
+  // 32-wave fused outer step (bench.py --max-ctas sweeps): fewer starve the
+  // reduce, more steal SM slots from the step.  With the 64-register reduce
+  // kernel, C3 N=4 at 64 CTAs leaves 27 % of the reduce exposed (5.68e11
+  // params/s) against 2.3 % at 96 (7.10e11); N=2 is best at 96 too
+  // (profiles/r02/tune/c3_p2p_ctas_r6/).
+  e->ctas = ctas > 0 ? ctas : 96;
   // The sharded slice reduce runs beside a step that touches 1/world of the
   // parameters, so it wants the whole chip: 0 = the launcher's per-world
   // default (C4 N=4: 592 CTAs 49.0 ms/round vs 64 CTAs 61.7,
@@ -510,7 +518,16 @@ static co2_status_t cache_handle(co2_aar* e, Handle& h) {
   h.c_start = ms_between(e->epoch, h.start);
   h.c_done = ms_between(e->epoch, h.done);
   h.c_comm = ms_between(h.start, h.done);
-  if (h.waited) {
+  if (h.waited && h.wait_alias >= 0) {
+    const Handle& a = e->handles[(size_t)h.wait_alias];  // newer: events still live
+    if (a.cached) {
+      h.c_wait_end = a.c_start;
+    } else {
+      CO2_CUDA(cudaEventSynchronize(a.start));
+      h.c_wait_end = ms_between(e->epoch, a.start);
+    }
+    h.c_stall = 0.0;
+  } else if (h.waited) {
     CO2_CUDA(cudaEventSynchronize(h.wait_end));
     h.c_stall = ms_between(h.wait_begin, h.wait_end);
     h.c_wait_end = ms_between(e->epoch, h.wait_end);
@@ -526,7 +543,12 @@ static co2_status_t cache_handle(co2_aar* e, Handle& h) {
 static co2_status_t cache_handle_if_ready(co2_aar* e, Handle& h) {
   if (h.cached) return CO2_OK;
   if (cudaEventQuery(h.done) != cudaSuccess) return CO2_OK;
-  if (h.waited && cudaEventQuery(h.wait_end) != cudaSuccess) return CO2_OK;
+  if (h.waited && h.wait_alias >= 0) {
+    const Handle& a = e->handles[(size_t)h.wait_alias];
+    if (!a.cached && cudaEventQuery(a.start) != cudaSuccess) return CO2_OK;
+  } else if (h.waited && cudaEventQuery(h.wait_end) != cudaSuccess) {
+    return CO2_OK;
+  }
   return cache_handle(e, h);
 }
 
@@ -631,6 +653,7 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
   }
   CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
+  h.done_stream = e->comm_stream;
   e->handles.push_back(h);
   e->live += 1;
   *handle_out = e->handles.size() - 1;
@@ -669,6 +692,7 @@ static co2_status_t launch_slice(co2_aar* e, co2_dtype_t dt, const void* src0, c
   CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
                            cudaMemcpyDeviceToHost, e->comm_stream));
   CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
+  h.done_stream = e->comm_stream;
   e->handles.push_back(h);
   e->live += 1;
   *handle_out = e->handles.size() - 1;
@@ -812,7 +836,10 @@ extern "C" co2_status_t co2_aar_events(co2_aar_t* e, co2_event_t* out, int64_t c
     push(0, i, ms * 1e-3, 0.0);
     CO2_CUDA(cudaEventElapsedTime(&ms, e->epoch, h.done));
     push(1, i, ms * 1e-3, 0.0);
-    if (h.waited) {
+    if (h.waited && h.wait_alias >= 0) {
+      CO2_TRY(cache_handle(e, h));
+      push(2, i, h.c_wait_end, 0.0);
+    } else if (h.waited) {
       CO2_CUDA(cudaEventSynchronize(h.wait_end));
       float st = 0.f, te = 0.f;
       CO2_CUDA(cudaEventElapsedTime(&st, h.wait_begin, h.wait_end));
@@ -1110,7 +1137,23 @@ static co2_status_t local_round_fused(co2_worker_t* const* ws, int32_t g, co2_aa
   const uint64_t prev = w0->pending;
   int32_t done = 0;
   CO2_TRY(co2_aar_poll(e, prev, &done));  // :155-157
-  CO2_TRY(co2_aar_wait(e, prev, stream));
+  // wait (collective.cpp:88-105).  A reduce that completed on this stream
+  // (the previous single-launch round) is ordered before this round by the
+  // stream itself: consume it without a cross-stream wait or its two timing
+  // events (each event record costs the stream ~2.5 us, measured beside a
+  // ~37 us C1 round; profiles/r02/c1/), stall 0, its wait time the start
+  // event of the handle launched below.  Otherwise (round 1: the reduce ran
+  // on the comm stream) the ordinary wait.
+  Handle& ph = e->handles[prev];
+  const bool ordered = ph.done_stream == st && !ph.consumed;
+  if (ordered) {
+    ph.consumed = true;
+    ph.waited = true;
+    ph.wait_alias = (int64_t)e->handles.size();  // the handle new_handle adds next
+    e->live -= 1;
+  } else {
+    CO2_TRY(co2_aar_wait(e, prev, stream));
+  }
   const int t = w0->t;
   void* xbar = w0->avg[(t - 1) % 2];
   void* avg_out = w0->avg[t % 2];
@@ -1147,6 +1190,7 @@ static co2_status_t local_round_fused(co2_worker_t* const* ws, int32_t g, co2_aa
     w0->tev_recorded += 1;
   }
   CO2_CUDA(cudaEventRecord(h.done, st));
+  h.done_stream = st;
   e->handles.push_back(h);
   e->live += 1;
   const uint64_t launched = e->handles.size() - 1;

@@ -336,17 +336,17 @@ __device__ __forceinline__ TC start_of_inner(TC q0) {
 template <typename TC, bool LQ = false>
 __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& xn, TC& lam,
                                          const Hyp<TC>& h, AccT<TC>& acc) {
-  if (h.divide) xb = xb / h.divisor;  // average(): sum / G, param_ops.cpp:30
+  if (h.divide) xb = div_rn(xb, h.divisor);  // average(): sum / G, param_ops.cpp:30
   TC n0 = fabs(x - q0);
   TC av = fabs(h.tau * (q1 - start_of_inner<TC, LQ>(q0)));
   bool floored = av < h.eps;
   TC d = floored ? h.eps : av;
-  lam = n0 / d + (TC)1;
+  lam = div_rn(n0, d) + (TC)1;
   TC dl = q0 - xb;
   TC mn;
   if (h.penalty) {
     TC bm = h.beta * m;
-    TC q = dl / lam;
+    TC q = div_rn(dl, lam);
     mn = bm + q;
   } else {
     TC bm = h.beta * m;
@@ -437,7 +437,7 @@ __device__ __forceinline__ void aar_vector(const StepArgs& a, int64_t e) {
   uint4 out;
   const TC g = (TC)a.exit.world;
 #pragma unroll
-  for (int k = 0; k < VA; ++k) reinterpret_cast<TL*>(&out)[k] = Store<TL>::from(acc[k] / g);
+  for (int k = 0; k < VA; ++k) reinterpret_cast<TL*>(&out)[k] = Store<TL>::from(div_rn(acc[k], (TC)g));
 #pragma unroll
   for (int p = 0; p < R; ++p)
     if (p < a.exit.world) __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.aar_bufs[p]) + e), out);
@@ -449,7 +449,7 @@ template <typename TC>
 __device__ __forceinline__ TC ghost_avg(TC v, int g) {
   TC s = v;
   for (int i = 1; i < g; ++i) s = s + v;
-  return s / (TC)g;
+  return div_rn(s, (TC)g);
 }
 
 template <class M, int V, int U, int NT, int MINB, bool GHOST = false, bool P2POUT = false,
@@ -531,11 +531,11 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
         for (int v = 0; v < V; ++v) {
           TC m = to_c(mo[u][v]), xn, lam;
           TC xbv = to_c(xb[u][v]);
-          if (h.divide) xbv = xbv / h.divisor;  // average(): sum / G, param_ops.cpp:30
+          if (h.divide) xbv = div_rn(xbv, h.divisor);  // average(): sum / G, param_ops.cpp:30
           if constexpr (GHOST) {
             TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(x[u][v]), a.ghost_g);
             TC p1v = to_c(q1[u][v]);
-            if (a.p1_div > 1) p1v = p1v / p1d;
+            if (a.p1_div > 1) p1v = div_rn(p1v, p1d);
             b0[v] = (TS)xv;
             co2_elem<TC, LQ>(xv, to_c(q0[u][v]), p1v, xbv, m, xn, lam, hg, acc);
           } else {
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
            j += NT) {
         TC s0 = to_c(static_cast<const TL*>(a.aar_bufs[0])[j]);
         for (int p = 1; p < a.exit.world; ++p) s0 = s0 + to_c(static_cast<const TL*>(a.aar_bufs[p])[j]);
-        const TL r = Store<TL>::from(s0 / (TC)a.exit.world);
+        const TL r = Store<TL>::from(div_rn(s0, (TC)a.exit.world));
         for (int p = 0; p < a.exit.world; ++p) static_cast<TL*>(a.aar_bufs[p])[j] = r;
       }
     }
@@ -599,11 +599,11 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
   if (V > 1 && t < a.n) {
     TC m = to_c(Mm[t]), xn, lam;
     TC xbv = to_c(XB[t]);
-    if (h.divide) xbv = xbv / h.divisor;
+    if (h.divide) xbv = div_rn(xbv, h.divisor);
     if constexpr (GHOST) {
       TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(X[t]), a.ghost_g);
       TC p1v = to_c(P1[t]);
-      if (a.p1_div > 1) p1v = p1v / p1d;
+      if (a.p1_div > 1) p1v = div_rn(p1v, p1d);
       const TC q0 = to_c(P0[t]);  // read before bar0_out (may alias prev_x0) is written
       if (B0) B0[t] = (TS)xv;
       co2_elem<TC, LQ>(xv, q0, p1v, xbv, m, xn, lam, hg, acc);
@@ -900,7 +900,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) bulk_step_kernel(const Step
         for (int v = 0; v < VE; ++v) {
           TC m = to_c(mo[v]), xn, lam;
           TC xbv = to_c(xb[v]);
-          if (h.divide) xbv = xbv / h.divisor;  // average(): sum / G, param_ops.cpp:30
+          if (h.divide) xbv = div_rn(xbv, h.divisor);  // average(): sum / G, param_ops.cpp:30
           co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), xbv, m, xn, lam, hg, acc);
           mn[v] = (TS)m;
           xs[v] = (TS)xn;
@@ -923,7 +923,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) bulk_step_kernel(const Step
     for (int64_t j = ntiles * (int64_t)TILE + threadIdx.x; j < a.n; j += NT) {
       TC m = to_c(Mm[j]), xn, lam;
       TC xbv = to_c(XB[j]);
-      if (h.divide) xbv = xbv / h.divisor;
+      if (h.divide) xbv = div_rn(xbv, h.divisor);
       co2_elem<TC, LQ>(to_c(X[j]), to_c(P0[j]), to_c(P1[j]), xbv, m, xn, lam, hg, acc);
       if (XO) XO[j] = XB[j];
       Mm[j] = (TS)m;
@@ -1070,7 +1070,7 @@ __global__ void __launch_bounds__(kThreads) op_kernel(const OpArgs a) {
       TC av = fabs(tau * (q1 - q0));
       bool fl = av < eps;
       TC d = fl ? eps : av;
-      TC lam = n0 / d + (TC)1;
+      TC lam = div_rn(n0, d) + (TC)1;
       if (!isfinite(lam)) acc.flags |= CO2_FLAG_GAP_NONFINITE;
       acc.floored += fl;
       double dl = (double)lam;
@@ -1083,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads) op_kernel(const OpArgs a) {
       if (a.i0) {
         if (g < (TC)1) acc.flags |= CO2_FLAG_GAP_BELOW_ONE;
         TC bm = beta * mp;
-        TC q = dl / g;
+        TC q = div_rn(dl, g);
         m = bm + q;
       } else {
         TC bm = beta * mp;
@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(kThreads)
        j += (int64_t)gridDim.x * kThreads) {
     TC s = to_c(c.p[0][j]);
     for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
-    TC r = s / gd;
+    TC r = div_rn(s, gd);
     if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
     out[j] = Store<T>::from(r);
   }
@@ -1174,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads)
     T o[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) {
-      const TC r = s[q] / gd;
+      const TC r = div_rn(s[q], gd);
       if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
       o[q] = Store<T>::from(r);
     }
@@ -1184,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int64_t j = nv * V + threadIdx.x; j < n; j += kThreads) {
       TC s = to_c(c.p[0][j]);
       for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
-      const TC r = s / gd;
+      const TC r = div_rn(s, gd);
       if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
       out[j] = Store<T>::from(r);
     }
@@ -1372,10 +1372,10 @@ __device__ __forceinline__ TC gc_momentum(TC x, TC q0, TC q1, TC xb, TC m, TC& l
   TC av = fabs(h.tau * (q1 - start_of_inner<TC, LQ>(q0)));
   bool floored = av < h.eps;
   TC d = floored ? h.eps : av;
-  lam = n0 / d + (TC)1;
+  lam = div_rn(n0, d) + (TC)1;
   TC dl = q0 - xb;
   TC bm = h.beta * m;
-  TC mn = h.penalty ? bm + dl / lam : bm + dl;
+  TC mn = h.penalty ? bm + div_rn(dl, lam) : bm + dl;
   unsigned int f = 0;
   if (!isfinite(lam)) f |= CO2_FLAG_GAP_NONFINITE;
   if (h.penalty && lam < (TC)1) f |= CO2_FLAG_GAP_BELOW_ONE;
@@ -1459,7 +1459,7 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int6
       for (int v = 0; v < V; ++v) {
         TC lam;
         TC xbv = to_c(xb[v]);
-        if (h.divide) xbv = xbv / h.divisor;
+        if (h.divide) xbv = div_rn(xbv, h.divisor);
         const TC m = gc_momentum<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), xbv, to_c(mo[v]),
                                          lam, h, acc);
         mn[v] = (TS)m;
@@ -1475,7 +1475,7 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int6
       for (int64_t e = nvE; e < a.n; ++e) {
         TC lam;
         TC xbv = to_c(XB[e]);
-        if (h.divide) xbv = xbv / h.divisor;
+        if (h.divide) xbv = div_rn(xbv, h.divisor);
         if (XO) XO[e] = XB[e];
         const TC m =
             gc_momentum<TC, LQ>(to_c(X[e]), to_c(P0[e]), to_c(P1[e]), xbv, to_c(Mm[e]), lam, h,
@@ -2069,7 +2069,7 @@ __global__ void scale_div_kernel(T* b, int64_t n, int g) {
   const TC gd = (TC)g;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x)
-    b[j] = Store<T>::from(to_c(b[j]) / gd);
+    b[j] = Store<T>::from(div_rn(to_c(b[j]), gd));
 }
 }  // namespace
 
@@ -2244,7 +2244,7 @@ __global__ void __launch_bounds__(kThreads) baseline_kernel(const BaseArgs a) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       TC xbv = to_c(xb[v]);
-      if (div) xbv = xbv / gd;  // average(): one division, param_ops.cpp:30
+      if (div) xbv = div_rn(xbv, gd);  // average(): one division, param_ops.cpp:30
       base_elem<M, OP>(xbv, OP == B_OVERLAP ? (TC)0 : to_c(x[v]), m[v], pr[v], an[v], af, bf,
                        acc);
     }
@@ -2255,7 +2255,7 @@ __global__ void __launch_bounds__(kThreads) baseline_kernel(const BaseArgs a) {
   for (int64_t j = nv * V + (int64_t)blockIdx.x * kThreads + threadIdx.x; V > 1 && j < a.n;
        j += stride) {
     TC xbv = to_c(XB[j]);
-    if (div) xbv = xbv / gd;
+    if (div) xbv = div_rn(xbv, gd);
     TS m = OP == B_SLOWMO ? Mm[j] : (TS)0;
     TS an = OP == B_OVERLAP ? A[j] : (TS)0;
     TL pr = OP == B_OVERLAP ? PR[j] : TL{};
@@ -2480,7 +2480,7 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         if (v < cnt) {
-          const TC r = sacc[v] / gd;  // one division, :30
+          const TC r = div_rn(sacc[v], gd);  // one division, :30
           if (!isfinite(r)) avg_flags |= CO2_FLAG_AVG_NONFINITE;
           o[v] = Store<TL>::from(r);
         }
@@ -2629,7 +2629,7 @@ __global__ void __launch_bounds__(kThreads)
          j += (int64_t)gridDim.x * kThreads) {
       TC s = to_c(c.p[0][j]);
       for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
-      const TC xb = s / gd;
+      const TC xb = div_rn(s, gd);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (w0 + k < g) {
