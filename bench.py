@@ -314,52 +314,84 @@ def run_local_workers(args, cfg) -> int:
     """C1: G simulated workers on one GPU through the LOCAL engine.  Every
     co2_round (t >= 1) is ONE kernel (local_round_kernel): this round's
     fixed-order average of the G contributions plus the G fused outer steps
-    on the previous average.  The working set (~120 MB) is about the L2
-    size, so L2 is flushed (a 256 MB write, then a 256 MB read, leaving only
-    clean lines) before every timed round and only the round itself is
-    inside the CUDA events."""
+    on the previous average.
+
+    One round's working set (142 MB) is about the L2 size (126 MB), so the
+    timed rounds rotate over S = 4 independent simulated jobs (each G
+    workers + its own LOCAL engine): consecutive rounds touch disjoint
+    buffers, and a job's inputs were last touched S - 1 rounds (426 MB of
+    traffic) earlier, so they stream from HBM -- the "inputs larger than L2"
+    rule without a flush between rounds.  K rounds run back to back between
+    one pair of CUDA events (whole-job throughput).  Two side passes, outside
+    that region: the kernel duration on CUDA events around each launch (the
+    roofline), and the older protocol (L2 flushed before every round, events
+    around each round) for comparison."""
     import torch
 
     from paper_2401_16265_b200 import co2
     mode, n, tau, g = cfg["mode"], cfg["n"], cfg["tau"], cfg["local_workers"]
     hyper = co2.Co2Hyper(**HYPER)
-    eng = co2.CollectiveEngine(g, transport="local")
-    ws = [co2.Worker(mode, n, co2.synth_params(mode, n, worker=i), keep_gap=False)
-          for i in range(g)]
-    for w in ws:
-        w.snapshot_start()
-        w.snapshot_first()
-    co2.co2_round(ws, eng, hyper, tau)  # round 0
+    S = 4
+    jobs = []
+    for _ in range(S):
+        eng = co2.CollectiveEngine(g, transport="local")
+        ws = [co2.Worker(mode, n, co2.synth_params(mode, n, worker=i), keep_gap=False)
+              for i in range(g)]
+        for w in ws:
+            w.snapshot_start()
+            w.snapshot_first()
+        co2.co2_round(ws, eng, hyper, tau)  # round 0
+        jobs.append((eng, ws))
     stream = torch.cuda.current_stream()
-    # L2 flush: write 256 MB (> the 126 MB L2), then read another 256 MB so
-    # the L2 holds CLEAN lines when the timed round starts (a write-only
-    # flush leaves ~126 MB of dirty lines whose write-back the round's first
-    # misses would pay for -- a cost of the flush, not of the round).
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    flush_w, flush_r = flush[:256 << 20], flush[256 << 20:].view(torch.int32)
     for _ in range(max(args.warmup, 3)):
-        co2.co2_round(ws, eng, hyper, tau, sync=False)
+        for eng, ws in jobs:
+            co2.co2_round(ws, eng, hyper, tau, sync=False)
     torch.cuda.synchronize()
-    h_first = eng.handle_count()  # one reduce handle per round
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     host = []
+    hc0 = [eng.handle_count() for eng, _ in jobs]  # one reduce handle per round
     with ClockSampler(torch, torch.cuda.current_device()) as clk:
-        for e0, e1 in ev:
-            flush_w.zero_()  # evict the previous round's lines from L2 ...
-            flush_r.max()    # ... and leave only clean lines behind
-            e0.record(stream)
+        e0.record(stream)
+        for k in range(args.steps):
+            eng, ws = jobs[k % S]
             h0 = time.perf_counter()
             co2.co2_round(ws, eng, hyper, tau, sync=False)
             host.append(time.perf_counter() - h0)
-            e1.record(stream)
+        e1.record(stream)
         torch.cuda.synchronize()
-    t = sum(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3
-    # The round's own launch / done events bracket exactly local_round_kernel
-    # (no per-worker timing events: each event record costs the stream
-    # ~2.5 us, which would be charged to the round).
-    kt = [eng.info(h)["comm"] for h in range(h_first, h_first + args.steps)]
+    t = e0.elapsed_time(e1) * 1e-3
+    hspan = list(zip(hc0, [eng.handle_count() for eng, _ in jobs]))
+    # Side pass 1: the kernel's duration on CUDA events around each launch
+    # (the worker's step-timing events, on the launching stream; they add a
+    # timing record before and after every kernel, so this pass is not the
+    # throughput pass above).
+    for eng, ws in jobs:
+        ws[0].enable_timing(args.steps + 8)
+    for k in range(args.steps):
+        eng, ws = jobs[k % S]
+        co2.co2_round(ws, eng, hyper, tau, sync=False)
+    torch.cuda.synchronize()
+    kt = [x for eng, ws in jobs for x in ws[0].step_times()]
     k_mean = statistics.mean(kt) if kt else None
+    # in-kernel span (CTA 0's start to the last CTA's end, %globaltimer) of
+    # the throughput pass's rounds, from the engines' kernel-timed handles
+    span = [eng.info(h)["comm"] for (eng, _), (a0, a1) in zip(jobs, hspan)
+            for h in range(a0, a1)]
+    # Side pass 2: the round-1 protocol -- L2 flushed (256 MB write, then a
+    # 256 MB read, leaving clean lines) before every round, events around it.
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush_w, flush_r = flush[:256 << 20], flush[256 << 20:].view(torch.int32)
+    eng, ws = jobs[0]
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(min(args.steps, 20))]
+    for f0, f1 in fev:
+        flush_w.zero_()
+        flush_r.max()
+        f0.record(stream)
+        co2.co2_round(ws, eng, hyper, tau, sync=False)
+        f1.record(stream)
+    torch.cuda.synchronize()
+    flushed_us = statistics.median(f0.elapsed_time(f1) * 1e3 for f0, f1 in fev)
     r = co2.L.RoundResult()
     arr = (co2.C.c_void_p * g)(*[w.handle.value for w in ws])
     co2.check(co2.lib().co2_round_finish(arr, g, stream.cuda_stream, co2.C.byref(r)))
@@ -380,25 +412,31 @@ def run_local_workers(args, cfg) -> int:
         "data": "synthetic (counter-SplitMix64 uniforms, SURVEY.md 8d)",
         "config": {"workload": cfg["workload"], "n_params_per_worker": n, "workers": g,
                    "tau": tau, "hyper": HYPER,
-                   "l2": "L2 flushed before every timed round (256 MB write, then a 256 MB "
-                         "read so no dirty lines remain); the flush is outside the per-round "
-                         "CUDA events",
+                   "l2": f"inputs larger than L2: rounds rotate over {S} independent simulated "
+                         f"jobs, so each round's inputs were last touched {S - 1} rounds "
+                         f"({(S - 1) * bytes_round / 1e6:.0f} MB of traffic) earlier; no flush",
+                   "timing": "K rounds back to back between one pair of CUDA events",
                    "step": f"co2_round over {g} simulated workers: ONE kernel = fixed-order "
                            f"average of x_t,tau + {g} fused outer steps on the stale average"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": None,
                      "algorithmic_bytes": bytes_round, "peak_kind": peak_kind,
                      "kernel": "local_round_kernel", "kernel_ms": k_mean * 1e3 if k_mean else None,
+                     "kernel_timing": "CUDA events around each launch on the launching stream "
+                                      "(separate pass)",
                      "bytes_per_param": bytes_round / (g * n)},
+        "kernel_span_us": 1e6 * statistics.median(span) if span else None,
+        "l2_flushed_round_us": flushed_us,
         "e2e": None, "cpu_baseline": None,
         "gpu_launches": args.steps, "clocks": clk.summary(),
         "host_us_per_round": 1e6 * statistics.median(host),
         "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step},
     }
     print(json.dumps(line), flush=True)
-    for w in ws:
-        w.close()
-    eng.close()
+    for eng, ws in jobs:
+        for w in ws:
+            w.close()
+        eng.close()
     return 0
 
 

@@ -44,6 +44,19 @@ enum { T_NCCL = 0, T_LOCAL = 1, T_P2P = 2 };
 
 struct Handle {
   cudaEvent_t start = nullptr, done = nullptr, wait_begin = nullptr, wait_end = nullptr;
+  // Kernel-timed handle (single-launch LOCAL round): the kernel writes its
+  // own start / end %globaltimer and the average's diagnostics into the
+  // engine's DEVICE slot of the handle, fetched into the pinned slot (`ts`,
+  // `diag`) only when the handle is cached; completion is the non-timing
+  // event `fin`.  A timing event record costs the stream ~2.5 us and the
+  // mapped host writes + system fence at a kernel's end ~2.3 us
+  // (profiles/r02/c1/), against a ~31 us C1 round kernel; a non-timing
+  // record costs nothing measurable.
+  cudaEvent_t fin = nullptr;
+  bool ktimed = false;
+  uint64_t* ts = nullptr;
+  uint64_t* ts_dev = nullptr;
+  co2_diag_t* diag_dev = nullptr;
   bool consumed = false, polled = false, last_poll = false, completion_logged = false;
   bool waited = false;
   // Stream-ordered consume (single-launch LOCAL round): the reduce completed
@@ -57,7 +70,7 @@ struct Handle {
   uint32_t* p2p_error = nullptr;  // P2P: pinned copy of the signal area's error word (pool slot)
   // After kRing newer launches a handle's events are recycled; its device
   // times and status are cached first (the reference keeps every record).
-  bool cached = false;
+  bool cached = false, cached_wait = false;
   double c_start = 0, c_done = 0, c_wait_end = 0, c_stall = 0, c_comm = 0;
   uint32_t c_flags = 0, c_err = 0;
 };
@@ -123,8 +136,19 @@ struct co2_aar {
   co2_diag_t* pin_diag = nullptr;
   co2_diag_t* pin_diag_dev = nullptr;  // device mapping of pin_diag
   uint32_t* pin_err = nullptr;
+  uint64_t* pin_ts = nullptr;      // kernel-timed handles: [start, end] globaltimer ns
+  uint64_t* dev_ts = nullptr;      // ... written by the kernel here (device ring)
+  co2_diag_t* dev_diag = nullptr;  // ... and the average's diagnostics
+  cudaStream_t aux_stream = nullptr;  // fetches of the device slots
+  uint64_t epoch_ns = 0;           // %globaltimer read right after the epoch event
   cudaEvent_t fence = nullptr;
 };
+
+__global__ void co2_globaltimer_kernel(uint64_t* out) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
 
 static co2_status_t engine_common_init(co2_aar* e) {
   int lo = 0, hi = 0;
@@ -138,6 +162,16 @@ static co2_status_t engine_common_init(co2_aar* e) {
   CO2_CUDA(cudaStreamCreateWithPriority(&e->comm_stream, cudaStreamNonBlocking, prio));
   CO2_CUDA(cudaEventCreate(&e->epoch));
   CO2_CUDA(cudaEventRecord(e->epoch, e->comm_stream));
+  {  // the epoch on the %globaltimer clock, for kernel-timed handles
+    uint64_t* d = nullptr;
+    CO2_CUDA(cudaMalloc(&d, sizeof(uint64_t)));
+    co2_globaltimer_kernel<<<1, 1, 0, e->comm_stream>>>(d);
+    cudaError_t ce = cudaMemcpyAsync(&e->epoch_ns, d, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                     e->comm_stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->comm_stream);
+    cudaFree(d);
+    if (ce != cudaSuccess) return cuda_fail(ce, "epoch globaltimer");
+  }
   CO2_CUDA(cudaMalloc(&e->ws, co2_workspace_bytes()));
   CO2_CUDA(cudaMemsetAsync(e->ws, 0, co2_workspace_bytes(), e->comm_stream));
   return CO2_OK;
@@ -372,11 +406,15 @@ extern "C" co2_status_t co2_aar_destroy(co2_aar_t* e) {
   if (!e) return CO2_OK;
   cudaDeviceSynchronize();  // kernels on any stream may use the peer mappings
   for (Handle& h : e->handles) {
-    for (cudaEvent_t ev : {h.start, h.done, h.wait_begin, h.wait_end})
+    for (cudaEvent_t ev : {h.start, h.done, h.wait_begin, h.wait_end, h.fin})
       if (ev) cudaEventDestroy(ev);
   }
   if (e->pin_diag) cudaFreeHost(e->pin_diag);
   if (e->pin_err) cudaFreeHost(e->pin_err);
+  if (e->pin_ts) cudaFreeHost(e->pin_ts);
+  if (e->dev_ts) cudaFree(e->dev_ts);
+  if (e->dev_diag) cudaFree(e->dev_diag);
+  if (e->aux_stream) cudaStreamDestroy(e->aux_stream);
   if (e->fence) cudaEventDestroy(e->fence);
   if (e->comm2) ncclCommDestroy(e->comm2);
   if (e->comm) ncclCommDestroy(e->comm);
@@ -510,27 +548,50 @@ static double ms_between(cudaEvent_t a, cudaEvent_t b) {
   return ms * 1e-3;
 }
 
-// Cache a finished handle's device times and status, then free its events
-// for reuse (handles older than kRing launches; at most two are ever live).
-static co2_status_t cache_handle(co2_aar* e, Handle& h) {
+// The event a handle completes on (poll / wait / synchronize).
+static cudaEvent_t sync_event(const Handle& h) { return h.ktimed ? h.fin : h.done; }
+
+// Kernel-timed handle: wait for it, then copy its device slots (times, the
+// average's diagnostics) into its pinned slots.
+static co2_status_t fetch_slots(co2_aar* e, const Handle& h) {
+  CO2_CUDA(cudaEventSynchronize(h.fin));
+  CO2_CUDA(cudaMemcpyAsync(h.ts, h.ts_dev, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                           e->aux_stream));
+  CO2_CUDA(cudaMemcpyAsync(h.diag, h.diag_dev, sizeof(co2_diag_t), cudaMemcpyDeviceToHost,
+                           e->aux_stream));
+  CO2_CUDA(cudaStreamSynchronize(e->aux_stream));
+  return CO2_OK;
+}
+
+// Launch time (s since the epoch) of a completed handle.
+static co2_status_t start_time(co2_aar* e, const Handle& h, double* t) {
+  if (h.cached) {
+    *t = h.c_start;
+  } else if (h.ktimed) {
+    CO2_TRY(fetch_slots(e, h));
+    *t = (double)(int64_t)(h.ts[0] - e->epoch_ns) * 1e-9;
+  } else {
+    CO2_CUDA(cudaEventSynchronize(h.start));
+    *t = ms_between(e->epoch, h.start);
+  }
+  return CO2_OK;
+}
+
+// Cache a finished handle's device times and status (blocking) ...
+static co2_status_t cache_done(co2_aar* e, Handle& h) {
   if (h.cached) return CO2_OK;
-  CO2_CUDA(cudaEventSynchronize(h.done));
-  h.c_start = ms_between(e->epoch, h.start);
-  h.c_done = ms_between(e->epoch, h.done);
-  h.c_comm = ms_between(h.start, h.done);
-  if (h.waited && h.wait_alias >= 0) {
-    const Handle& a = e->handles[(size_t)h.wait_alias];  // newer: events still live
-    if (a.cached) {
-      h.c_wait_end = a.c_start;
-    } else {
-      CO2_CUDA(cudaEventSynchronize(a.start));
-      h.c_wait_end = ms_between(e->epoch, a.start);
-    }
-    h.c_stall = 0.0;
-  } else if (h.waited) {
-    CO2_CUDA(cudaEventSynchronize(h.wait_end));
-    h.c_stall = ms_between(h.wait_begin, h.wait_end);
-    h.c_wait_end = ms_between(e->epoch, h.wait_end);
+  if (h.ktimed)
+    CO2_TRY(fetch_slots(e, h));
+  else
+    CO2_CUDA(cudaEventSynchronize(h.done));
+  if (h.ktimed) {
+    h.c_start = (double)(int64_t)(h.ts[0] - e->epoch_ns) * 1e-9;
+    h.c_done = (double)(int64_t)(h.ts[1] - e->epoch_ns) * 1e-9;
+    h.c_comm = (double)(int64_t)(h.ts[1] - h.ts[0]) * 1e-9;
+  } else {
+    h.c_start = ms_between(e->epoch, h.start);
+    h.c_done = ms_between(e->epoch, h.done);
+    h.c_comm = ms_between(h.start, h.done);
   }
   h.c_flags = h.diag ? h.diag->flags : 0;
   h.c_err = h.p2p_error ? *h.p2p_error : 0;
@@ -538,18 +599,40 @@ static co2_status_t cache_handle(co2_aar* e, Handle& h) {
   return CO2_OK;
 }
 
-// Non-blocking variant for info(): caches only when every event the cache
-// reads has already completed.
+// ... and, once it has been waited, its wait times (blocking).
+static co2_status_t cache_wait(co2_aar* e, Handle& h) {
+  if (!h.waited || h.cached_wait) return CO2_OK;
+  if (h.wait_alias >= 0) {  // stream-ordered consume: ends where handle wait_alias starts
+    CO2_TRY(start_time(e, e->handles[(size_t)h.wait_alias], &h.c_wait_end));
+    h.c_stall = 0.0;
+  } else {
+    CO2_CUDA(cudaEventSynchronize(h.wait_end));
+    h.c_stall = ms_between(h.wait_begin, h.wait_end);
+    h.c_wait_end = ms_between(e->epoch, h.wait_end);
+  }
+  h.cached_wait = true;
+  return CO2_OK;
+}
+
+// Both; handles older than kRing launches are cached this way before their
+// events are recycled (at most two are ever live).
+static co2_status_t cache_handle(co2_aar* e, Handle& h) {
+  CO2_TRY(cache_done(e, h));
+  return cache_wait(e, h);
+}
+
+// Non-blocking variant for info(): caches only what has already completed.
 static co2_status_t cache_handle_if_ready(co2_aar* e, Handle& h) {
-  if (h.cached) return CO2_OK;
-  if (cudaEventQuery(h.done) != cudaSuccess) return CO2_OK;
-  if (h.waited && h.wait_alias >= 0) {
+  if (!h.cached && cudaEventQuery(sync_event(h)) != cudaSuccess) return CO2_OK;
+  CO2_TRY(cache_done(e, h));
+  if (!h.waited || h.cached_wait) return CO2_OK;
+  if (h.wait_alias >= 0) {
     const Handle& a = e->handles[(size_t)h.wait_alias];
-    if (!a.cached && cudaEventQuery(a.start) != cudaSuccess) return CO2_OK;
-  } else if (h.waited && cudaEventQuery(h.wait_end) != cudaSuccess) {
+    if (!a.cached && cudaEventQuery(a.ktimed ? a.fin : a.start) != cudaSuccess) return CO2_OK;
+  } else if (cudaEventQuery(h.wait_end) != cudaSuccess) {
     return CO2_OK;
   }
-  return cache_handle(e, h);
+  return cache_wait(e, h);
 }
 
 // A new handle: events (recycled from the handle kRing launches back) and
@@ -560,6 +643,10 @@ static co2_status_t new_handle(co2_aar* e, Handle* h) {
     CO2_CUDA(cudaMallocHost(&e->pin_diag, kRing * sizeof(co2_diag_t)));
     CO2_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->pin_diag_dev), e->pin_diag, 0));
     CO2_CUDA(cudaMallocHost(&e->pin_err, kRing * sizeof(uint32_t)));
+    CO2_CUDA(cudaMallocHost(&e->pin_ts, 2 * kRing * sizeof(uint64_t)));
+    CO2_CUDA(cudaMalloc(&e->dev_ts, 2 * kRing * sizeof(uint64_t)));
+    CO2_CUDA(cudaMalloc(&e->dev_diag, kRing * sizeof(co2_diag_t)));
+    CO2_CUDA(cudaStreamCreateWithFlags(&e->aux_stream, cudaStreamNonBlocking));
     CO2_CUDA(cudaEventCreateWithFlags(&e->fence, cudaEventDisableTiming));
   }
   if (id >= kRing) {
@@ -570,7 +657,11 @@ static co2_status_t new_handle(co2_aar* e, Handle* h) {
     h->done = old.done;
     h->wait_begin = old.wait_begin;
     h->wait_end = old.wait_end;
-    old.start = old.done = old.wait_begin = old.wait_end = nullptr;
+    h->fin = old.fin;
+    old.start = old.done = old.wait_begin = old.wait_end = old.fin = nullptr;
+    old.ts = nullptr;
+    old.ts_dev = nullptr;
+    old.diag_dev = nullptr;
     old.diag = nullptr;
     old.p2p_error = nullptr;
   } else {
@@ -578,9 +669,14 @@ static co2_status_t new_handle(co2_aar* e, Handle* h) {
     CO2_CUDA(cudaEventCreateWithFlags(&h->done, cudaEventDefault));
     CO2_CUDA(cudaEventCreateWithFlags(&h->wait_begin, cudaEventDefault));
     CO2_CUDA(cudaEventCreateWithFlags(&h->wait_end, cudaEventDefault));
+    CO2_CUDA(cudaEventCreateWithFlags(&h->fin, cudaEventDisableTiming));
   }
   h->diag = &e->pin_diag[id % kRing];
   h->p2p_error = &e->pin_err[id % kRing];
+  h->ts = &e->pin_ts[2 * (id % kRing)];
+  h->ts[0] = h->ts[1] = 0;
+  h->ts_dev = e->dev_ts + 2 * (id % kRing);
+  h->diag_dev = e->dev_diag + id % kRing;
   h->diag->flags = 0;
   *h->p2p_error = 0;
   return CO2_OK;
@@ -709,7 +805,7 @@ extern "C" co2_status_t co2_aar_poll(co2_aar_t* e, uint64_t handle, int32_t* don
   Handle* h = nullptr;
   CO2_TRY(record_for(e, handle, &h));
   if (h->consumed) return fail(CO2_ERR_VALIDATION, "is_completed: handle already consumed");
-  cudaError_t q = cudaEventQuery(h->done);
+  cudaError_t q = cudaEventQuery(sync_event(*h));
   if (q != cudaSuccess && q != cudaErrorNotReady) return cuda_fail(q, "cudaEventQuery");
   bool d = q == cudaSuccess;
   h->polled = true;
@@ -726,7 +822,7 @@ extern "C" co2_status_t co2_aar_wait(co2_aar_t* e, uint64_t handle, void* consum
   CO2_TRY(record_for(e, handle, &h));
   if (h->consumed) return fail(CO2_ERR_VALIDATION, "wait: handle already consumed");
   CO2_CUDA(cudaEventRecord(h->wait_begin, S(consumer)));
-  CO2_CUDA(cudaStreamWaitEvent(S(consumer), h->done, 0));
+  CO2_CUDA(cudaStreamWaitEvent(S(consumer), sync_event(*h), 0));
   CO2_CUDA(cudaEventRecord(h->wait_end, S(consumer)));
   h->consumed = true;
   h->waited = true;
@@ -741,7 +837,7 @@ extern "C" co2_status_t co2_aar_order_after(co2_aar_t* e, uint64_t handle, void*
   Handle* h = nullptr;
   CO2_TRY(record_for(e, handle, &h));
   if (h->consumed) return fail(CO2_ERR_VALIDATION, "order_after: handle already consumed");
-  CO2_CUDA(cudaStreamWaitEvent(S(stream), h->done, 0));
+  CO2_CUDA(cudaStreamWaitEvent(S(stream), sync_event(*h), 0));
   return CO2_OK;
 }
 
@@ -776,13 +872,13 @@ extern "C" co2_status_t co2_aar_info(co2_aar_t* e, uint64_t handle, co2_handle_i
   const double nan = std::numeric_limits<double>::quiet_NaN();
   co2_handle_info_t r{handle, nan, nan, nan, nan, 0, h->consumed ? 1 : 0, h->contributions,
                       h->polled ? 1 : 0, h->last_poll ? 1 : 0, 0};
-  if (!h->cached && cudaEventQuery(h->done) == cudaSuccess) CO2_TRY(cache_handle_if_ready(e, *h));
+  CO2_TRY(cache_handle_if_ready(e, *h));
   if (h->cached) {
     r.launch_time = h->c_start;
     r.completion_time = h->c_done;
     r.comm = h->c_comm;
     r.completed = 1;
-    if (h->waited) r.stall = h->c_stall;
+    if (h->cached_wait) r.stall = h->c_stall;
   }
   // log_completion (collective.cpp:66-71): a successful poll or the wait
   r.completion_logged = (h->completion_logged || h->consumed) ? 1 : 0;
@@ -824,28 +920,10 @@ extern "C" co2_status_t co2_aar_events(co2_aar_t* e, co2_event_t* out, int64_t c
   };
   for (uint64_t i = 0; i < e->handles.size(); ++i) {
     Handle& h = e->handles[i];
-    if (h.cached) {  // events recycled: the cached device times
-      push(0, i, h.c_start, 0.0);
-      push(1, i, h.c_done, 0.0);
-      if (h.waited) push(2, i, h.c_wait_end, h.c_stall);
-      continue;
-    }
-    CO2_CUDA(cudaEventSynchronize(h.done));
-    float ms = 0.f;
-    CO2_CUDA(cudaEventElapsedTime(&ms, e->epoch, h.start));
-    push(0, i, ms * 1e-3, 0.0);
-    CO2_CUDA(cudaEventElapsedTime(&ms, e->epoch, h.done));
-    push(1, i, ms * 1e-3, 0.0);
-    if (h.waited && h.wait_alias >= 0) {
-      CO2_TRY(cache_handle(e, h));
-      push(2, i, h.c_wait_end, 0.0);
-    } else if (h.waited) {
-      CO2_CUDA(cudaEventSynchronize(h.wait_end));
-      float st = 0.f, te = 0.f;
-      CO2_CUDA(cudaEventElapsedTime(&st, h.wait_begin, h.wait_end));
-      CO2_CUDA(cudaEventElapsedTime(&te, e->epoch, h.wait_end));
-      push(2, i, te * 1e-3, st * 1e-3);
-    }
+    CO2_TRY(cache_handle(e, h));  // blocks until the handle (and its wait) completed
+    push(0, i, h.c_start, 0.0);
+    push(1, i, h.c_done, 0.0);
+    if (h.waited) push(2, i, h.c_wait_end, h.c_stall);
   }
   *count = k;
   return CO2_OK;
@@ -874,7 +952,9 @@ struct co2_worker {
   bool keep_avg = false;
   void* ws = nullptr;
   co2_diag_t* host_diag = nullptr;  // pinned
-  co2_diag_t* host_diag_dev = nullptr;  // its device mapping (kernels write it directly)
+  // the last round's diagnostics are only in the workspace header (the
+  // single-launch LOCAL round): co2_round_finish fetches them first
+  bool diag_on_device = false;
   // fused P2P schedule: pinned copy of the engine's signal error word, read
   // back after every fused round (a timed-out barrier means the consumed
   // average is incomplete); checked by co2_round_finish and the next round
@@ -942,7 +1022,6 @@ extern "C" co2_status_t co2_worker_create(co2_worker_t** out, co2_mode_t mode, i
   }
   cudaStream_t st = S(stream);
   CO2_CUDA(cudaMallocHost(&w->host_diag, sizeof(co2_diag_t)));
-  CO2_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&w->host_diag_dev), w->host_diag, 0));
   CO2_CUDA(cudaMemsetAsync(w->ws, 0, co2_workspace_bytes(), st));
   // OuterState init, outer_algorithms.cpp:416-418: momentum zeros, gap ones.
   CO2_CUDA(cudaMemsetAsync(w->m, 0, sb ? sb : 1, st));
@@ -1063,6 +1142,11 @@ extern "C" co2_status_t co2_round_finish(co2_worker_t* const* ws, int32_t g, voi
   if (!ws || !res || g < 1) return fail(CO2_ERR_VALIDATION, "co2_round_finish: bad arguments");
   for (int i = 0; i < g; ++i)
     if (!ws[i]) return fail(CO2_ERR_VALIDATION, "co2_round_finish: null worker");
+  for (int i = 0; i < g; ++i)
+    if (ws[i]->diag_on_device) {
+      CO2_TRY(co2_diag_fetch_async(ws[i]->ws, ws[i]->host_diag, stream));
+      ws[i]->diag_on_device = false;
+    }
   CO2_CUDA(cudaStreamSynchronize(S(stream)));
   co2_round_result_t r = *res;
   r.min_gap = INFINITY;
@@ -1140,9 +1224,9 @@ static co2_status_t local_round_fused(co2_worker_t* const* ws, int32_t g, co2_aa
   // wait (collective.cpp:88-105).  A reduce that completed on this stream
   // (the previous single-launch round) is ordered before this round by the
   // stream itself: consume it without a cross-stream wait or its two timing
-  // events (each event record costs the stream ~2.5 us, measured beside a
-  // ~37 us C1 round; profiles/r02/c1/), stall 0, its wait time the start
-  // event of the handle launched below.  Otherwise (round 1: the reduce ran
+  // events (each timing event record costs the stream ~2.5 us, measured
+  // beside a ~35 us C1 round; profiles/r02/c1/), stall 0, its wait time the
+  // start of the handle launched below.  Otherwise (round 1: the reduce ran
   // on the comm stream) the ordinary wait.
   Handle& ph = e->handles[prev];
   const bool ordered = ph.done_stream == st && !ph.consumed;
@@ -1161,7 +1245,6 @@ static co2_status_t local_round_fused(co2_worker_t* const* ws, int32_t g, co2_aa
       *cur[kMaxLocalRound];
   void *m[kMaxLocalRound], *an[kMaxLocalRound], *pr[kMaxLocalRound], *gp[kMaxLocalRound],
       *wsp[kMaxLocalRound];
-  co2_diag_t* hd[kMaxLocalRound];
   for (int i = 0; i < g; ++i) {
     co2_worker* w = ws[i];
     x0[i] = w->anchor;
@@ -1173,23 +1256,27 @@ static co2_status_t local_round_fused(co2_worker_t* const* ws, int32_t g, co2_aa
     pr[i] = w->params[1 - w->cur];
     gp[i] = w->gap;
     wsp[i] = w->ws;
-    hd[i] = w->host_diag_dev;
   }
   Handle h;
   CO2_TRY(new_handle(e, &h));
   h.contributions = g;
   const size_t slot = e->handles.size() % kRing;
-  CO2_CUDA(cudaEventRecord(h.start, st));
+  // Kernel-timed: the kernel stamps its own start / end into the handle's
+  // pinned slot and completion is a non-timing event, so the round adds no
+  // timing event to the stream (the worker's optional step timing still does).
+  h.ktimed = true;
   const int64_t cap = (int64_t)w0->tev.size() / 2;
   const int64_t tslot = cap ? w0->tev_recorded % cap : 0;
   if (cap) CO2_CUDA(cudaEventRecord(w0->tev[2 * tslot], st));
-  CO2_TRY(local_round_impl(w0->mode, g, w0->n, x0, p0, p1, m, an, pr, gp, cur, wsp, hd,
-                           e->pin_diag_dev + slot, xbar, avg_out, hyper, st));
+  CO2_TRY(local_round_impl(w0->mode, g, w0->n, x0, p0, p1, m, an, pr, gp, cur, wsp, nullptr,
+                           e->dev_diag + slot, xbar, avg_out, hyper,
+                           reinterpret_cast<unsigned long long*>(e->dev_ts + 2 * slot), st));
+  for (int i = 0; i < g; ++i) ws[i]->diag_on_device = true;  // co2_round_finish fetches
   if (cap) {
     CO2_CUDA(cudaEventRecord(w0->tev[2 * tslot + 1], st));
     w0->tev_recorded += 1;
   }
-  CO2_CUDA(cudaEventRecord(h.done, st));
+  CO2_CUDA(cudaEventRecord(h.fin, st));
   h.done_stream = st;
   e->handles.push_back(h);
   e->live += 1;

@@ -2326,17 +2326,34 @@ namespace {
 //     the fixed-order average of every worker's params into avg_out
 //     (param_ops.cpp:16-33: ascending worker order, one division);
 //   * every worker's fused outer step consuming the previous round's
-//     average xbar (:186-202), in worker order per tile, so xbar is read from
-//     HBM once per tile and from L1 for the other workers.
+//     average xbar (:186-202).
 // The two halves touch disjoint buffers (the average reads params[cur] and
 // writes avg[t%2]; the steps read avg[(t-1)%2] and write params[1-cur],
 // m and the anchor), so one grid is exactly the two-kernel schedule.  Per
 // element every op is the fused step's / average_kernel's, so results and
 // per-worker diagnostics are bitwise those of the separate launches.
-// Diagnostics: per worker, warp -> smem -> per-CTA partials in that worker's
-// workspace; the last CTA (ticket in worker 0's workspace) folds each in
-// fixed order and also writes it straight into the worker's pinned host
-// diag (device-mapped), so no per-worker D2H copy is issued.
+//
+// Work split: G + 1 roles (worker w's step, then the average) of
+// tiles_per_role tiles each, NT threads x TV vectors per tile, numbered
+// role-major.  A persistent grid (one wave) claims tiles from a counter in
+// worker 0's workspace, the next claim issued while the current tile runs,
+// so CTAs stay busy to the end whatever the per-role cost (a step tile moves
+// 28 B/param, an average tile 20) and whatever the HBM unevenness.  The C1
+// working set (1M params x 4 workers, 142 MB) is a single short wave: the
+// earlier oversubscribed grid (5 waves of CTAs that each did 1-2 vectors per
+// thread, then a fold) ran at 0.58 of copy.  xbar (one buffer, read by every
+// worker role) is read with default caching and stays in L2 between roles;
+// every other stream is evict-first.
+// Diagnostics: a CTA folds its accumulators (warp shuffles, warps in fixed
+// order) whenever its claimed role changes and merges them into that role's
+// order-independent atomic accumulators (block_finish's keys / counts / OR;
+// the average's flags in worker 0's acc_flags2), so the result does not
+// depend on which CTA ran which tile.  The last CTA (ticket) publishes every
+// role into the worker's workspace header (and the average's flags and this
+// launch's %globaltimer start / end into the engine's device slot of the
+// handle) and resets them.  Nothing is written to mapped host memory: those
+// PCIe writes and the system fence they need cost ~2.3 us at the kernel's
+// end (profiles/r02/c1/), and the engine fetches the slots only on demand.
 struct LocalRoundArgs {
   const void* x_t0[kMaxLocalRound];
   const void* p0[kMaxLocalRound];
@@ -2347,22 +2364,47 @@ struct LocalRoundArgs {
   void* gap[kMaxLocalRound];
   const void* cur[kMaxLocalRound];  // x_{t,tau}: this round's contributions
   void* ws[kMaxLocalRound];
-  co2_diag_t* host_diag[kMaxLocalRound];  // device-mapped pinned (nullable)
-  co2_diag_t* avg_diag;                   // device-mapped pinned (nullable)
+  co2_diag_t* host_diag[kMaxLocalRound];  // extra copy of each worker's diag (nullable)
+  co2_diag_t* avg_diag;                   // the average's diag slot (nullable)
   const void* xbar;                       // the average consumed this round
   void* avg_out;                          // this round's average
   int g;
   int64_t n;
   double alpha, beta, phi, eps;
   int tau, penalty, clip;
+  int tiles_per_role;
+  int tv;        // vectors per thread per tile
+  int prefetch;  // L2 bulk prefetch of the tile after next (CO2_LOCAL_ROUND_PF=1 enables)
+  // [start, end] %globaltimer of this launch (nullable): the engine's
+  // kernel-timed handle's device slot
+  unsigned long long* ts;
 };
 
-template <class M, int V, int NT>
-__global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a) {
+// Merge this CTA's accumulators for one role into the role's atomic
+// accumulators.  Every thread calls (block-uniform role).
+template <int NT>
+__device__ __forceinline__ void role_merge(const Acc& a, WsHeader* hdr, bool avg) {
+  const Partial b = block_partial<NT>(a);  // valid in thread 0
+  if (threadIdx.x == 0) {
+    if (avg) {
+      if (b.flags) atomicOr(&hdr->acc_flags2, b.flags);
+    } else {
+      atomicMax(&hdr->acc_min_key, ~dkey(b.min_gap));
+      atomicMax(&hdr->acc_max_key, dkey(b.max_step));
+      if (b.clipped) atomicAdd(&hdr->acc_clipped, b.clipped);
+      if (b.floored) atomicAdd(&hdr->acc_floored, b.floored);
+      if (b.flags) atomicOr(&hdr->acc_flags, b.flags);
+    }
+  }
+}
+
+template <class M, int V, int U, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) local_round_kernel(const LocalRoundArgs a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
   using TC = typename M::TC;
   constexpr bool LQ = !std::is_same<TS, TL>::value;
+  const int TV = a.tv;  // vectors per thread per tile (a multiple of U)
   Hyp<TC> h;
   h.tau = (TC)a.tau;
   h.eps = (TC)a.eps;
@@ -2373,180 +2415,308 @@ __global__ void __launch_bounds__(NT) local_round_kernel(const LocalRoundArgs a)
   h.penalty = a.penalty;
   h.clip = a.clip;
   h.divide = 0;
-  // Roles are CTA-uniform: CTA b has role b % R (R = g + 1; roles 0..g-1:
-  // worker role's fused step, role g: this round's average) and chunk b / R,
-  // and the host makes gridDim.x a multiple of R.  Every warp therefore runs
-  // one code path over one worker's contiguous vectors (no divergence, fully
-  // coalesced), and the average's G loads per vector are issued together.
-  // xbar is read by the G step roles of the same chunk, adjacent CTAs, so
-  // its repeat reads hit L2.
-  const int R = a.g + 1;
-  const int role = (int)(blockIdx.x % R);
-  const int chunk = (int)(blockIdx.x / R);
-  const int nchunks = (int)(gridDim.x / R);
-  const int64_t vstride = (int64_t)nchunks * NT;
-  const int64_t v0 = (int64_t)chunk * NT + threadIdx.x;
+  const int G = a.g;
+  const int tpr = a.tiles_per_role;
+  const int ntiles = tpr * (G + 1);
   const int64_t nv = a.n / V;
-  const int64_t tail = a.n - nv * V;  // n % V coordinates, one per thread of chunk 0
-  AccT<TC> acc;
-  unsigned int avg_flags = 0;
+  const int64_t tail = a.n - nv * V;  // n % V coordinates, by the last tile of each role
   const TL* XB = static_cast<const TL*>(a.xbar);
-  if (role < a.g) {
-    const TS* X = static_cast<const TS*>(a.x_t0[role]);
-    const TS* P0 = static_cast<const TS*>(a.p0[role]);
-    const TL* P1 = static_cast<const TL*>(a.p1[role]);
-    TS* Mm = static_cast<TS*>(a.m[role]);
-    TS* A = static_cast<TS*>(a.anchor[role]);
-    TL* PR = static_cast<TL*>(a.params[role]);
-    TS* G = static_cast<TS*>(a.gap[role]);
-    auto step = [&](int64_t e, int cnt) {
-      TS x[V], q0[V], mo[V], mn[V], xs[V], gs[V];
-      TL q1[V], xb[V], xl[V];
-      if (cnt == V) {
-        ld_vec<TS, V>(X + e, x);
-        ld_vec<TS, V>(P0 + e, q0);
-        ld_vec<TL, V>(P1 + e, q1);
-        ld_vec<TS, V>(Mm + e, mo);
-        // default-cached: the other workers' CTAs of this chunk hit it in L2
-        constexpr int XBYTES = V * (int)sizeof(TL);
-        if constexpr (XBYTES % 16 == 0) {
-          uint4 r[XBYTES / 16];
-#pragma unroll
-          for (int k = 0; k < XBYTES / 16; ++k) r[k] = reinterpret_cast<const uint4*>(XB + e)[k];
-          memcpy(xb, r, XBYTES);
-        } else {
-#pragma unroll
-          for (int v = 0; v < V; ++v) xb[v] = XB[e + v];
-        }
-      } else {
-        x[0] = X[e];
-        q0[0] = P0[e];
-        q1[0] = P1[e];
-        mo[0] = Mm[e];
-        xb[0] = XB[e];
-      }
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        if (v < cnt) {
-          TC m = to_c(mo[v]), xn, lam;
-          co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), to_c(xb[v]), m, xn, lam, h,
-                           acc);
-          mn[v] = (TS)m;
-          xs[v] = (TS)xn;
-          gs[v] = (TS)lam;
-          xl[v] = Store<TL>::from(xn);
-        }
-      }
-      if (cnt == V) {
-        st_vec<TS, V>(Mm + e, mn);
-        if (A) st_vec<TS, V>(A + e, xs);
-        st_vec<TL, V>(PR + e, xl);
-        if (G) st_vec<TS, V>(G + e, gs);
-      } else {
-        Mm[e] = mn[0];
-        if (A) A[e] = xs[0];
-        PR[e] = xl[0];
-        if (G) G[e] = gs[0];
-      }
+  WsHeader* h0 = ws_header(a.ws[0]);
+  if (a.ts && blockIdx.x == 0 && threadIdx.x == 0) h0->t_start = (unsigned long long)global_ns();
+
+  // Tile pipeline (thread 0): while tile i runs, the claim of tile i + 2 is
+  // in flight, and at the end of tile i the streams of tile i + 2 are
+  // prefetched into L2 with bulk prefetches, so tile i + 1's loads were
+  // issued to HBM a whole tile earlier and hit L2.  The kernel is short
+  // (~1 MB per SM) and latency-bound without it: 768 threads x 80 B in
+  // flight per SM cover only ~1 us of HBM latency.
+  const int64_t per_tile = (int64_t)NT * TV;
+  auto prefetch = [&](int t) {  // thread 0 only
+    if (t >= ntiles) return;
+    const int r = t / tpr;
+    const int64_t v0 = (int64_t)(t - r * tpr) * per_tile;
+    int64_t cnt = nv - v0 < per_tile ? nv - v0 : per_tile;
+    if (cnt <= 0) return;
+    auto pf = [&](const void* base, int esz) {
+      const unsigned bytes = (unsigned)((cnt * V * esz) & ~(int64_t)15);
+      if (bytes) bulk_prefetch_l2(static_cast<const char*>(base) + v0 * V * esz, bytes);
     };
-    for (int64_t i = v0; i < nv; i += vstride) step(i * V, V);
-    if (V > 1 && chunk == 0 && (int64_t)threadIdx.x < tail) step(nv * V + threadIdx.x, 1);
-  } else {
-    const TC gd = (TC)a.g;
-    TL* AO = static_cast<TL*>(a.avg_out);
-    auto average = [&](int64_t e, int cnt) {
-      TL c[kMaxLocalRound][V];
+    if (r < G) {
+      pf(a.x_t0[r], sizeof(TS));
+      pf(a.p0[r], sizeof(TS));
+      pf(a.p1[r], sizeof(TL));
+      pf(a.m[r], sizeof(TS));
+      pf(a.xbar, sizeof(TL));
+    } else {
+      for (int w = 0; w < G; ++w) pf(a.cur[w], sizeof(TL));
+    }
+  };
+  // The first two tiles of CTA b are static (b and grid + b): the launch
+  // does not open with 2 x grid atomics on one counter (serialised in L2,
+  // microseconds at this kernel's scale); later claims are spread in time.
+  const int nstatic = 2 * (int)gridDim.x;
+  __shared__ int s_next[2];
+  int ahead = (int)gridDim.x + (int)blockIdx.x;  // thread 0: the tile after the next one
+  if (threadIdx.x == 0 && V * (int)sizeof(TL) % 16 == 0 && a.prefetch) prefetch(ahead);
+  int tile = (int)blockIdx.x;
+  int slot = 0;
+  int role_cur = -1;
+  AccT<TC> acc;
+
+  while (tile < ntiles) {
+    int claim = 0;
+    if (threadIdx.x == 0 && ahead < ntiles)  // used after the tile
+      claim = nstatic + (int)atomicAdd(&h0->tile_next, 1u);
+    else
+      claim = ntiles;
+    const int role = tile / tpr;
+    const int k = tile - role * tpr;
+    if (role != role_cur) {
+      if (role_cur >= 0) {
+        role_merge<NT>(acc.widen(), ws_header(a.ws[role_cur < G ? role_cur : 0]), role_cur == G);
+        acc = AccT<TC>();
+      }
+      role_cur = role;
+    }
+    const int64_t vbase = (int64_t)k * per_tile + threadIdx.x;
+    const bool last_tile = k == tpr - 1;
+    if (role < G) {
+      const TS* X = static_cast<const TS*>(a.x_t0[role]);
+      const TS* P0 = static_cast<const TS*>(a.p0[role]);
+      const TL* P1 = static_cast<const TL*>(a.p1[role]);
+      TS* Mm = static_cast<TS*>(a.m[role]);
+      TS* A = static_cast<TS*>(a.anchor[role]);
+      TL* PR = static_cast<TL*>(a.params[role]);
+      TS* Gp = static_cast<TS*>(a.gap[role]);
+      auto elem = [&](TS x, TS q0, TL q1, TL xb, TS& mo, TS& xs, TL& xl, TS& gs) {
+        TC m = to_c(mo), xn, lam;
+        co2_elem<TC, LQ>(to_c(x), to_c(q0), to_c(q1), to_c(xb), m, xn, lam, h, acc);
+        mo = (TS)m;
+        xs = (TS)xn;
+        gs = (TS)lam;
+        xl = Store<TL>::from(xn);
+      };
+#pragma unroll 1
+      for (int j = 0; j < TV; j += U) {
+        TS x[U][V], q0[U][V], mo[U][V];
+        TL q1[U][V], xb[U][V];
 #pragma unroll
-      for (int w = 0; w < kMaxLocalRound; ++w) {  // all loads in flight together
-        if (w < a.g) {
-          const TL* C = static_cast<const TL*>(a.cur[w]);
-          if (cnt == V)
-            ld_vec<TL, V>(C + e, c[w]);
-          else
-            c[w][0] = C[e];
+        for (int u = 0; u < U; ++u) {  // every load of the U vectors in flight together
+          const int64_t v = vbase + (int64_t)(j + u) * NT;
+          if (v < nv) {
+            const int64_t e = v * V;
+            ld_vec<TS, V>(X + e, x[u]);
+            ld_vec<TS, V>(P0 + e, q0[u]);
+            ld_vec<TL, V>(P1 + e, q1[u]);
+            ld_vec<TS, V>(Mm + e, mo[u]);
+            constexpr int XBYTES = V * (int)sizeof(TL);
+            if constexpr (XBYTES % 16 == 0) {  // default-cached: the other roles hit it in L2
+              uint4 r[XBYTES / 16];
+#pragma unroll
+              for (int q = 0; q < XBYTES / 16; ++q) r[q] = reinterpret_cast<const uint4*>(XB + e)[q];
+              memcpy(xb[u], r, XBYTES);
+            } else {
+#pragma unroll
+              for (int q = 0; q < V; ++q) xb[u][q] = XB[e + q];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t v = vbase + (int64_t)(j + u) * NT;
+          if (v < nv) {
+            const int64_t e = v * V;
+            TS xs[V], gs[V];
+            TL xl[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) elem(x[u][q], q0[u][q], q1[u][q], xb[u][q], mo[u][q], xs[q], xl[q], gs[q]);
+            st_vec<TS, V>(Mm + e, mo[u]);
+            if (A) st_vec<TS, V>(A + e, xs);
+            st_vec<TL, V>(PR + e, xl);
+            if (Gp) st_vec<TS, V>(Gp + e, gs);
+          }
         }
       }
-      TC sacc[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) sacc[v] = to_c(c[0][v]);
-#pragma unroll
-      for (int w = 1; w < kMaxLocalRound; ++w) {  // ascending worker order, param_ops.cpp:26-28
-        if (w < a.g) {
-#pragma unroll
-          for (int v = 0; v < V; ++v) sacc[v] = sacc[v] + to_c(c[w][v]);
-        }
+      if (V > 1 && last_tile && (int64_t)threadIdx.x < tail) {
+        const int64_t e = nv * V + threadIdx.x;
+        TS mo = Mm[e], xs, gs;
+        TL xl;
+        elem(X[e], P0[e], P1[e], XB[e], mo, xs, xl, gs);
+        Mm[e] = mo;
+        if (A) A[e] = xs;
+        PR[e] = xl;
+        if (Gp) Gp[e] = gs;
       }
-      TL o[V];
+    } else {
+      const TC gd = (TC)G;
+      TL* AO = static_cast<TL*>(a.avg_out);
+      auto average = [&](int64_t e, int cnt) {
+        // contributions in groups of 4 (all loads of a group in flight
+        // together), summed in ascending worker order, param_ops.cpp:26-28
+        TC s[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        if (v < cnt) {
-          const TC r = div_rn(sacc[v], gd);  // one division, :30
-          if (!isfinite(r)) avg_flags |= CO2_FLAG_AVG_NONFINITE;
-          o[v] = Store<TL>::from(r);
+        for (int w0 = 0; w0 < kMaxLocalRound; w0 += 4) {
+          if (w0 < G) {
+            TL c[4][V];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              if (w0 + w < G) {
+                const TL* C = static_cast<const TL*>(a.cur[w0 + w]);
+                if (cnt == V)
+                  ld_vec<TL, V>(C + e, c[w]);
+                else
+                  c[w][0] = C[e];
+              }
+            }
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              if (w0 + w < G) {
+#pragma unroll
+                for (int q = 0; q < V; ++q)
+                  s[q] = (w0 + w == 0) ? to_c(c[w][q]) : s[q] + to_c(c[w][q]);
+              }
+            }
+          }
         }
+        TL o[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          if (q < cnt) {
+            const TC r = div_rn(s[q], gd);  // one division, :30
+            if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
+            o[q] = Store<TL>::from(r);
+          }
+        }
+        if (cnt == V)
+          st_vec<TL, V>(AO + e, o);
+        else
+          AO[e] = o[0];
+      };
+#pragma unroll 1
+      for (int j = 0; j < TV; ++j) {
+        const int64_t v = vbase + (int64_t)j * NT;
+        if (v < nv) average(v * V, V);
       }
-      if (cnt == V)
-        st_vec<TL, V>(AO + e, o);
-      else
-        AO[e] = o[0];
-    };
-    for (int64_t i = v0; i < nv; i += vstride) average(i * V, V);
-    if (V > 1 && chunk == 0 && (int64_t)threadIdx.x < tail) average(nv * V + threadIdx.x, 1);
+      if (V > 1 && last_tile && (int64_t)threadIdx.x < tail) average(nv * V + threadIdx.x, 1);
+    }
+    if (threadIdx.x == 0) {
+      s_next[slot ^ 1] = ahead;
+      if (V * (int)sizeof(TL) % 16 == 0 && a.prefetch) prefetch(claim);
+      ahead = claim;
+    }
+    __syncthreads();  // s_next[slot ^ 1] is visible
+    tile = s_next[slot ^ 1];
+    slot ^= 1;
   }
-  // ---- diagnostics: this CTA's partial into its role's slot (the average's
-  // flags into worker 0's partial array after the nchunks step partials);
-  // the last CTA OF EACH ROLE (a ticket per role: worker w's workspace
-  // ticket, the average's ticket2 in worker 0's) folds that role's partials
-  // in fixed chunk order, so the G + 1 folds run in parallel.
-  Acc b0 = acc.widen();
-  b0.flags |= avg_flags;
-  const Partial mine = block_partial<NT>(b0);
-  Partial* parts = role < a.g ? ws_partials(a.ws[role]) : ws_partials(a.ws[0]) + nchunks;
-  unsigned int* ticket =
-      role < a.g ? &ws_header(a.ws[role])->ticket : &ws_header(a.ws[0])->ticket2;
+  if (role_cur >= 0)
+    role_merge<NT>(acc.widen(), ws_header(a.ws[role_cur < G ? role_cur : 0]), role_cur == G);
+
+  // Last CTA: publish and reset every role (thread r publishes role r).
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
-    parts[chunk] = mine;
     __threadfence();
-    s_last = atomicAdd(ticket, 1u) == (unsigned)nchunks - 1;
+    s_last = atomicAdd(&h0->ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const Partial r = fold_partials<NT>(parts, nchunks);
-  if (threadIdx.x == 0) {
-    if (role < a.g) {
-      co2_diag_t d;
-      d.min_gap = r.min_gap;
-      d.max_outer_step = r.max_step;
-      d.n_clipped = (int64_t)r.clipped;
-      d.n_floored = (int64_t)r.floored;
-      d.flags = r.flags;
-      d.pad = 0;
-      ws_header(a.ws[role])->diag = d;
-      if (a.host_diag[role]) *a.host_diag[role] = d;
-    } else if (a.avg_diag) {
-      co2_diag_t ad{INFINITY, 0.0, 0, 0, r.flags, 0};
+  const int r = (int)threadIdx.x;
+  if (r < G) {
+    volatile WsHeader* vh = ws_header(a.ws[r]);
+    const unsigned long long kmin = vh->acc_min_key, kmax = vh->acc_max_key;
+    co2_diag_t d;
+    d.min_gap = kmin ? dkey_inv(~kmin) : (double)INFINITY;
+    d.max_outer_step = kmax ? dkey_inv(kmax) : 0.0;
+    d.n_clipped = (int64_t)vh->acc_clipped;
+    d.n_floored = (int64_t)vh->acc_floored;
+    d.flags = vh->acc_flags;
+    d.pad = 0;
+    WsHeader* hr = ws_header(a.ws[r]);
+    hr->diag = d;
+    hr->acc_min_key = 0ull;
+    hr->acc_max_key = 0ull;
+    hr->acc_clipped = 0ull;
+    hr->acc_floored = 0ull;
+    hr->acc_flags = 0u;
+    if (a.host_diag[r]) *a.host_diag[r] = d;
+  } else if (r == G) {
+    volatile WsHeader* vh = h0;
+    const unsigned int f = vh->acc_flags2;
+    h0->acc_flags2 = 0u;
+    if (a.avg_diag) {
+      co2_diag_t ad{INFINITY, 0.0, 0, 0, f, 0};
       *a.avg_diag = ad;
     }
-    *ticket = 0;  // self-reset for the next launch
-    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    h0->tile_next = 0u;  // self-reset for the next launch
+    h0->ticket = 0u;
+    if (a.ts) {
+      a.ts[0] = *static_cast<volatile unsigned long long*>(&h0->t_start);
+      a.ts[1] = (unsigned long long)global_ns();
+    }
   }
 }
 
-template <class M, int V>
-co2_status_t launch_local_round(const LocalRoundArgs& a, cudaStream_t s) {
-  auto k = local_round_kernel<M, V, kThreads>;
-  const int R = a.g + 1;
-  const int64_t nv = a.n / V > 0 ? a.n / V : 1;
-  // chunks per role: the step grid for one worker's vectors, and at most
-  // kMaxBlocks / 2 so the average's partials fit after worker 0's.
-  int chunks = grid_for(k, nv, kThreads);
-  if (chunks > kMaxBlocks / 2) chunks = kMaxBlocks / 2;
-  if ((int64_t)chunks * R > kMaxBlocks) chunks = kMaxBlocks / R;
-  k<<<chunks * R, kThreads, 0, s>>>(a);
+template <class M, int V, int U, int MINB>
+co2_status_t launch_local_round_k(LocalRoundArgs a, cudaStream_t s) {
+  auto k = local_round_kernel<M, V, U, kThreads, MINB>;
+  const int TV = a.tv;
+  const int64_t nv = a.n / V;
+  const int64_t per_tile = (int64_t)kThreads * TV;
+  int64_t tpr = (nv + per_tile - 1) / per_tile;
+  if (tpr < 1) tpr = 1;  // the scalar tail (and n = 0) still gets a tile per role
+  const int64_t ntiles = tpr * (a.g + 1);
+  if (ntiles > (int64_t)INT32_MAX / 2)
+    return fail(CO2_ERR_VALIDATION, "local round: %lld params per worker is too many",
+                (long long)a.n);
+  a.tiles_per_role = (int)tpr;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)per_sm * sm_count();  // persistent: one wave
+  if (grid > ntiles) grid = ntiles;
+  k<<<(int)grid, kThreads, 0, s>>>(a);
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
+}
+
+// Vectors in flight per thread (CO2_LOCAL_ROUND_U = 1 | 2, default 1): U = 2
+// needs the register budget of 2 CTAs/SM, U = 1 fits 3 (fp32).
+int local_round_u() {
+  static const int v = [] {
+    const char* e = getenv("CO2_LOCAL_ROUND_U");
+    return (e && atoi(e) == 2) ? 2 : 1;
+  }();
+  return v;
+}
+
+int local_round_pf() {
+  static const int v = [] {
+    const char* e = getenv("CO2_LOCAL_ROUND_PF");
+    return (e && atoi(e) == 1) ? 1 : 0;
+  }();
+  return v;
+}
+
+// Vectors per thread per tile (CO2_LOCAL_ROUND_TV, even, 2..32, default 4).
+int local_round_tv() {
+  static const int v = [] {
+    const char* e = getenv("CO2_LOCAL_ROUND_TV");
+    const int x = e ? atoi(e) : 4;
+    return x < 2 ? 2 : (x > 32 ? 32 : x & ~1);
+  }();
+  return v;
+}
+
+template <class M, int V>
+co2_status_t launch_local_round(LocalRoundArgs a, cudaStream_t s) {
+  a.prefetch = local_round_pf();
+  a.tv = local_round_tv();
+  if (local_round_u() == 1)
+    return launch_local_round_k<M, V, 1, std::is_same<M, ModeF32>::value ? 3 : 2>(a, s);
+  return launch_local_round_k<M, V, 2, 2>(a, s);
 }
 
 template <class M>
@@ -2563,7 +2733,7 @@ co2_status_t local_round_impl(co2_mode_t mode, int g, int64_t n, const void* con
                               const void* const* cur, void* const* ws,
                               co2_diag_t* const* host_diag, co2_diag_t* avg_diag,
                               const void* xbar, void* avg_out, const co2_hyper_t* h,
-                              cudaStream_t s) {
+                              unsigned long long* ts, cudaStream_t s) {
   if (g < 1 || g > kMaxLocalRound)
     return fail(CO2_ERR_VALIDATION, "local round: 1..%d workers", kMaxLocalRound);
   LocalRoundArgs a{};
@@ -2583,6 +2753,7 @@ co2_status_t local_round_impl(co2_mode_t mode, int g, int64_t n, const void* con
           aligned16(anchor[w]) && aligned16(params[w]) && aligned16(gap[w]) && aligned16(cur[w]);
   }
   a.avg_diag = avg_diag;
+  a.ts = ts;
   a.xbar = xbar;
   a.avg_out = avg_out;
   a.g = g;

@@ -1,0 +1,5 @@
+# 1-GPU call: LOCAL round with device-side diag/time slots -- tests, C1 bench
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/r17; mkdir -p $O
+(timeout 1200 python -m pytest tests/test_gpu_rounds.py tests/test_gpu_acceptance.py tests/test_gpu_parity.py tests/test_gpu_large.py -m gpu -q -x 2>&1; echo rc=$?) > $O/pytest.log 2>&1
+for r in 1 2; do timeout 300 python bench.py --config c1 --no-cpu --steps 40 > $O/bench_c1_r$r.json 2> $O/bench_c1_r$r.err; done
