@@ -70,22 +70,26 @@ def peaks():
         return 6650.0, "fallback"
 
 
-# ncu --set full capture of this bench's fused kernel (committed under
-# profiles/; the capture ran `bench.py --steps 3 --warmup 1 --no-e2e --no-cpu`
-# on the default C3 workload).
-NCU_CAPTURE = os.path.join("profiles", "r01", "final", "fused_step_bf16_c3_raw.csv")
+# ncu --set full captures of each config's dominant kernel (committed under
+# profiles/r02/ncu/; each ran the same bench.py config, see its README).
+NCU_CAPTURES = {
+    "c3": os.path.join("profiles", "r02", "ncu", "c3_fused_step_raw.csv"),
+    "c2": os.path.join("profiles", "r02", "ncu", "c2_fused_step_raw.csv"),
+    "c1": os.path.join("profiles", "r02", "ncu", "c1_local_round_raw.csv"),
+}
 # NVLink denominator: B200_PROFILING.md's measured peer copy, GB/s per direction
 NVLINK_PEER_GBS = 770.0
 
 
-def ncu_traffic(cfg):
+def ncu_traffic(cfg, n_gpus: int = 1):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
-    committed capture, for the workload it was taken on (else None)."""
-    if cfg.get("sharded") or cfg["n"] != 1_300_000_000 or cfg["mode"] != 2:
-        return None
+    committed capture of this config's kernel (one GPU), else None."""
+    path = NCU_CAPTURES.get(cfg.get("name", ""))
+    if path is None or n_gpus != 1:
+        return None, None
     try:
         import csv
-        with open(os.path.join(ROOT, NCU_CAPTURE)) as f:
+        with open(os.path.join(ROOT, path)) as f:
             rows = list(csv.reader(f))
         hdr, units, vals = rows[0], rows[1], rows[2]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -93,9 +97,9 @@ def ncu_traffic(cfg):
         for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = hdr.index(name)
             tot += float(vals[i]) * scale[units[i]]
-        return tot
+        return tot, path
     except Exception:
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -419,7 +423,10 @@ def run_local_workers(args, cfg) -> int:
                    "step": f"co2_round over {g} simulated workers: ONE kernel = fixed-order "
                            f"average of x_t,tau + {g} fused outer steps on the stale average"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "frac": achieved / peak if achieved else None,
+                     "traffic": ncu_traffic(cfg)[0], "traffic_source": ncu_traffic(cfg)[1],
+                     "traffic_note": "ncu replays the kernel on cold caches: the round's "
+                                     "writes mostly stay dirty in L2 and reach DRAM later",
                      "algorithmic_bytes": bytes_round, "peak_kind": peak_kind,
                      "kernel": "local_round_kernel", "kernel_ms": k_mean * 1e3 if k_mean else None,
                      "kernel_timing": "CUDA events around each launch on the launching stream "
@@ -468,7 +475,9 @@ def main():
                          "contract; worker-local split schedule only)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    cfg["name"] = args.config
     if args.nparams > 0:
+        cfg["name"] = None  # no committed capture of that size
         cfg["n"] = args.nparams
         cfg["workload"] += f" [n overridden to {args.nparams}]"
 
@@ -701,9 +710,9 @@ def main():
                        if sharded else "co2_round: AAR launch + stale wait + fused outer step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None,
-                         "traffic": None if gclip else ncu_traffic(cfg),
+                         "traffic": None if gclip else ncu_traffic(cfg, world)[0],
                          "traffic_unit": "bytes per launch",
-                         "traffic_source": NCU_CAPTURE if ncu_traffic(cfg) and not gclip else None,
+                         "traffic_source": None if gclip else ncu_traffic(cfg, world)[1],
                          "algorithmic_bytes": bpp * per_rank, "peak_kind": peak_kind,
                          "kernel": ("gclip_pass1 + gclip_pass2 (global-norm clip extension)"
                                     if gclip else

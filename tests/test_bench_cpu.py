@@ -52,8 +52,12 @@ def test_roofline_denominators():
     peak, kind = bench.peaks()
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
         assert kind == "measured" and peak > 1000
-    # the committed ncu capture gives the traffic of the default C3 launch
-    t = bench.ncu_traffic(bench.CONFIGS["c3"])
-    assert t is not None and abs(t / 1.3e9 - 26.0) < 0.5
-    assert bench.ncu_traffic(bench.CONFIGS["c2"]) is None
+    # the committed ncu captures give the DRAM traffic of the default C3 and
+    # C2 launches (26 / 32 algorithmic B/param); none for other sizes or N > 1
+    t, src = bench.ncu_traffic(dict(bench.CONFIGS["c3"], name="c3"))
+    assert t is not None and abs(t / 1.3e9 - 26.0) < 0.5 and src.endswith(".csv")
+    t, _ = bench.ncu_traffic(dict(bench.CONFIGS["c2"], name="c2"))
+    assert t is not None and abs(t / 125e6 - 32.0) < 1.0
+    assert bench.ncu_traffic(dict(bench.CONFIGS["c3"], name="c3"), 2) == (None, None)
+    assert bench.ncu_traffic(dict(bench.CONFIGS["c3"], name=None)) == (None, None)
     assert bench.NVLINK_PEER_GBS == 770.0
