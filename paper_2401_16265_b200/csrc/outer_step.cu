@@ -452,9 +452,10 @@ __device__ __forceinline__ TC ghost_avg(TC v, int g) {
   return div_rn(s, (TC)g);
 }
 
-template <class M, int V, int U, int NT, int MINB, bool GHOST = false, bool P2POUT = false,
-          int AAR = 0>
-__global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) {
+// The fused step's body, shared by the launch-bounded kernel and the
+// register-capped variant below.
+template <class M, int V, int U, int NT, bool GHOST, bool P2POUT, int AAR>
+__device__ __forceinline__ void fused_step_body(const StepArgs& a) {
   using TS = typename M::TS;
   using TL = typename M::TL;
   using TC = typename M::TC;
@@ -626,6 +627,21 @@ __global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) 
     block_finish<NT>(acc.widen(), a.ws);
 }
 
+template <class M, int V, int U, int NT, int MINB, bool GHOST = false, bool P2POUT = false,
+          int AAR = 0>
+__global__ void __launch_bounds__(NT, MINB) fused_step_kernel(const StepArgs a) {
+  fused_step_body<M, V, U, NT, GHOST, P2POUT, AAR>(a);
+}
+
+// Register-capped worker-local step (co2_set_fused_variant 6 / 7): with at
+// most REGS registers, four 256-thread CTAs leave 65536 - 1024 * REGS
+// registers of the SM free, so a reduce CTA on the comm stream can be
+// resident beside them instead of displacing one (the multi-GPU rounds).
+template <class M, int V, int U, int REGS>
+__global__ void __maxnreg__(REGS) fused_step_kernel_r(const StepArgs a) {
+  fused_step_body<M, V, U, 256, false, false, 0>(a);
+}
+
 constexpr int kThreads = 256;
 
 // Grid waves for the grid-stride kernels, in units of the resident CTAs of an
@@ -690,6 +706,13 @@ int grid_for(K kernel, int64_t work_items, int threads) {
 template <class M, int V, int U, int MINB = 1>
 void launch_variant(const StepArgs& a, cudaStream_t s) {
   auto k = fused_step_kernel<M, V, U, kThreads, MINB>;
+  int grid = grid_for(k, (a.n / V + U - 1) / U, kThreads);
+  k<<<grid, kThreads, 0, s>>>(a);
+}
+
+template <class M, int V, int U, int REGS>
+void launch_variant_r(const StepArgs& a, cudaStream_t s) {
+  auto k = fused_step_kernel_r<M, V, U, REGS>;
   int grid = grid_for(k, (a.n / V + U - 1) / U, kThreads);
   k<<<grid, kThreads, 0, s>>>(a);
 }
@@ -1008,6 +1031,8 @@ co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
       case 3: launch_variant<M, 4, 1>(a, s); break;
       case 4: launch_variant<M, 8, 1>(a, s); break;
       case 5: launch_variant<M, 4, 2, 3>(a, s); break;
+      case 6: launch_variant_r<M, 8, 1, 56>(a, s); break;
+      case 7: launch_variant_r<M, 4, 1, 56>(a, s); break;
       default: launch_variant<M, 8, 1, 4>(a, s); break;
     }
   } else if constexpr (std::is_same<M, ModeF32>::value) {
@@ -1017,6 +1042,8 @@ co2_status_t launch_fused(const StepArgs& a, cudaStream_t s) {
       case 3: launch_variant<M, 8, 1>(a, s); break;
       case 4: launch_variant<M, 8, 1, 4>(a, s); break;
       case 5: launch_variant<M, 4, 2, 4>(a, s); break;
+      case 6: launch_variant_r<M, 4, 1, 56>(a, s); break;
+      case 7: launch_variant_r<M, 4, 1, 48>(a, s); break;
       default: launch_variant<M, 4, 1, 4>(a, s); break;
     }
   } else {

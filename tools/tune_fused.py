@@ -21,10 +21,11 @@ sys.path.insert(0, ROOT)
 BPP = {0: 64, 1: 32, 2: 26}
 NAMES = {
     2: {0: "(8,1) 4 CTA/SM", 1: "(8,2)", 2: "(4,4)", 3: "(4,1)", 4: "(8,1)", 5: "(4,2) 3 CTA/SM",
+        6: "(8,1) <= 56 regs", 7: "(4,1) <= 56 regs",
         10: "bulk 2048x4 st, 4 cw", 11: "bulk 1024x4, 4 cw", 12: "bulk 2048x3, 8 cw",
         13: "bulk 4096x3, 8 cw", 14: "bulk 1024x6, 8 cw"},
     1: {0: "(4,1) 4 CTA/SM", 1: "(4,2)", 2: "(4,1)", 3: "(8,1)", 4: "(8,1) 4 CTA/SM",
-        5: "(4,2) 4 CTA/SM",
+        5: "(4,2) 4 CTA/SM", 6: "(4,1) <= 56 regs", 7: "(4,1) <= 48 regs",
         10: "bulk 1024x5, 4 cw", 11: "bulk 1024x4, 4 cw", 12: "bulk 2048x4, 8 cw",
         13: "bulk 1024x8, 8 cw", 14: "bulk 512x6, 4 cw"},
     0: {0: "(2,1) 4 CTA/SM", 1: "(2,2)", 2: "(2,1)", 3: "(4,1)", 4: "(2,2) 3 CTA/SM",
