@@ -251,6 +251,49 @@ def test_engine_semantics():
     assert eng.reduce_time() > 0.0
 
 
+def test_single_launch_round_handles():
+    """Kernel-timed handles of the single-launch LOCAL round: the kernel
+    stamps its own start / end, completion is a non-timing event, and the
+    previous round's reduce is consumed in stream order (stall 0, its wait
+    at the next launch).  300 rounds also recycle the 256-slot handle ring
+    (the device slots are fetched before their events are reused)."""
+    g, n, rounds = 3, 4099, 300
+    hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    eng = co2.CollectiveEngine(g, transport="local")
+    ws = [co2.Worker(co2.MODE_F32, n, co2.synth_params(co2.MODE_F32, n, worker=i))
+          for i in range(g)]
+    for w in ws:
+        w.snapshot_start()
+        w.snapshot_first()
+    for _ in range(rounds):
+        co2.co2_round(ws, eng, hyper, 2, sync=False)
+    r = co2.L.RoundResult()
+    arr = (co2.C.c_void_p * g)(*[w.handle.value for w in ws])
+    co2.check(co2.lib().co2_round_finish(arr, g, torch.cuda.current_stream().cuda_stream,
+                                         co2.C.byref(r)))
+    assert r.min_gap >= 1.0 and 0.0 <= r.max_outer_step <= 5e-3 * (1 + 1e-6)
+    assert eng.handle_count() == rounds
+    ev = eng.events()
+    by = {}
+    for e in ev:
+        by.setdefault(e["handle_id"], {})[e["event"]] = e
+    for h in range(1, rounds - 1):  # launched by a single-launch round, consumed in order
+        i = eng.info(h)
+        assert i["completed"] and i["consumed"] and i["comm"] > 0.0
+        assert 0.0 <= i["launch_time"] <= i["completion_time"]
+        assert i["stall"] == 0.0
+        assert by[h]["wait"]["stall"] == 0.0
+        assert by[h]["wait"]["t_sim"] == by[h + 1]["launch"]["t_sim"]  # stream order
+        assert by[h]["complete"]["t_sim"] <= by[h + 1]["launch"]["t_sim"] + 1e-5
+    last = eng.info(rounds - 1)
+    assert not last["consumed"] and last["completed"] and np.isnan(last["stall"])
+    assert "wait" not in by[rounds - 1]
+    assert eng.total_stall() >= 0.0 and eng.reduce_time() > 0.0
+    co2.co2_round_drain(ws, eng)
+    torch.cuda.synchronize()
+    assert eng.info(rounds - 1)["consumed"]
+
+
 def test_round_rejects_bad_hyper_and_counts():
     eng = co2.CollectiveEngine(2, transport="local")
     ws = [co2.Worker(co2.MODE_F32, 16) for _ in range(2)]
