@@ -2402,6 +2402,7 @@ struct LocalRoundArgs {
   int tiles_per_role;
   int tv;        // vectors per thread per tile
   int prefetch;  // L2 bulk prefetch of the tile after next (CO2_LOCAL_ROUND_PF=1 enables)
+  int pdl_early;  // signal dependents at entry rather than after the tiles
   // [start, end] %globaltimer of this launch (nullable): the engine's
   // kernel-timed handle's device slot
   unsigned long long* ts;
@@ -2449,6 +2450,12 @@ __global__ void __launch_bounds__(NT, MINB) local_round_kernel(const LocalRoundA
   const int64_t tail = a.n - nv * V;  // n % V coordinates, by the last tile of each role
   const TL* XB = static_cast<const TL*>(a.xbar);
   WsHeader* h0 = ws_header(a.ws[0]);
+  // Programmatic dependent launch: with the launch attribute this grid is
+  // scheduled while the previous kernel on the stream finishes; nothing
+  // above touched memory it writes, and this waits for its completion and
+  // memory flush (a no-op without the attribute).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.ts && blockIdx.x == 0 && threadIdx.x == 0) h0->t_start = (unsigned long long)global_ns();
 
   // Tile pipeline (thread 0): while tile i runs, the claim of tile i + 2 is
@@ -2637,6 +2644,10 @@ __global__ void __launch_bounds__(NT, MINB) local_round_kernel(const LocalRoundA
   }
   if (role_cur >= 0)
     role_merge<NT>(acc.widen(), ws_header(a.ws[role_cur < G ? role_cur : 0]), role_cur == G);
+  // This CTA's tiles are done: the next kernel on the stream (launched with
+  // programmatic serialization) may start scheduling; it still waits for
+  // this grid's completion before touching memory.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Last CTA: publish and reset every role (thread r publishes role r).
   __shared__ bool s_last;
@@ -2686,6 +2697,19 @@ __global__ void __launch_bounds__(NT, MINB) local_round_kernel(const LocalRoundA
   }
 }
 
+// Programmatic dependent launch of the round kernel (CO2_LOCAL_ROUND_PDL:
+// 0 off, 1 (default) dependents signalled after this CTA's tiles, 2 at
+// entry): back-to-back rounds overlap one kernel's launch with the previous
+// one's tail.  C1, 4 rotating jobs: 36.1-36.8 -> 33.7-34.6 us per round
+// (profiles/r02/c1/r24, r25; 1 and 2 measure the same).
+int local_round_pdl() {
+  static const int v = [] {
+    const char* e = getenv("CO2_LOCAL_ROUND_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <class M, int V, int U, int MINB>
 co2_status_t launch_local_round_k(LocalRoundArgs a, cudaStream_t s) {
   auto k = local_round_kernel<M, V, U, kThreads, MINB>;
@@ -2704,7 +2728,22 @@ co2_status_t launch_local_round_k(LocalRoundArgs a, cudaStream_t s) {
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * sm_count();  // persistent: one wave
   if (grid > ntiles) grid = ntiles;
-  k<<<(int)grid, kThreads, 0, s>>>(a);
+  a.pdl_early = local_round_pdl() == 2;
+  if (local_round_pdl()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CO2_CUDA(cudaLaunchKernelEx(&cfg, k, a));
+  } else {
+    k<<<(int)grid, kThreads, 0, s>>>(a);
+  }
   CO2_CUDA(cudaGetLastError());
   return CO2_OK;
 }
