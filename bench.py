@@ -661,11 +661,12 @@ def main():
             step_hbm = {"bytes_per_param": bpp_step, "achieved": hbm_gbs, "peak": peak,
                         "unit": "GB/s", "frac": hbm_gbs / peak}
 
-    # --- e2e through the host-buffer entry (pinned H2D + kernel + D2H timed)
-    e2e = None
+    # --- e2e through the host-facing entries (pinned H2D + round + D2H timed)
+    e2e = e2e_full = None
     if not args.no_e2e and cfg.get("e2e_default", True) and not sharded and not gclip:  # the host entry is the reference clip
-        e2e = run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist)
+        e2e = run_e2e_round(co2, torch, w, eng, mode, n, tau, hyper, args, world, rank, dist)
         e2e["numa_bound_cores"] = numa_cores  # None: not bound (CO2_BENCH_NUMA=0 / no NVML)
+        e2e_full = run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist)
 
     # --- CPU baseline (rank 0, N=1 only): single-core reference restatement
     cpu = None
@@ -722,7 +723,7 @@ def main():
                          "kernel_ms": k_max * 1e3,
                          "bytes_per_param": bpp},
             "link": link, "step_hbm": step_hbm,
-            "e2e": e2e, "cpu_baseline": cpu, "comm": comm,
+            "e2e": e2e, "e2e_full_state": e2e_full, "cpu_baseline": cpu, "comm": comm,
             # our kernels per step per rank: the fused step (two passes for the
             # global-norm clip), plus our P2P reduce kernel when it runs as its
             # own launch (NCCL's kernels are not ours)
@@ -741,9 +742,65 @@ def main():
     return 0
 
 
+def run_e2e_round(co2, torch, w, eng, mode, n, tau, hyper, args, world, rank, dist):
+    """The metric through co2_round_host, the drop-in for the reference's
+    co2_round with the inner loop on the host: every step uploads this
+    step's inputs -- the inner loop's trace x_{t,1} and x_{t,tau} -- from
+    pinned host memory, runs the round on the device-resident outer state
+    (reduce launch, stale wait, fused step) and reads its result -- the next
+    inner loop's start x_{t+1,0} -- back to pinned host memory."""
+    lo = co2.LOW_TORCH[mode]
+    h_first = co2.synth_params(mode, n, worker=rank).cpu().pin_memory()
+    h_end = co2.synth_params(mode, n, worker=rank + 64).cpu().pin_memory()
+    h_next = torch.empty(n, dtype=lo, pin_memory=True)
+    torch.cuda.synchronize()
+    times = []
+    for i in range(args.e2e_steps + 1):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        co2.co2_round_host([w], eng, hyper, tau, [h_end], [h_next], x_first=[h_first],
+                           sync=False)
+        torch.cuda.current_stream().synchronize()  # the result is on the host
+        dt = time.perf_counter() - t0
+        if i > 0:
+            times.append(dt)
+    # the same copies with no round: two uploads, then the download (the
+    # round's data dependence orders them the same way)
+    d = [torch.empty(n, dtype=lo, device="cuda") for _ in range(2)]
+    copy_times = []
+    for i in range(4):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d[0].copy_(h_first, non_blocking=True)
+        d[1].copy_(h_end, non_blocking=True)
+        h_next.copy_(d[1], non_blocking=True)
+        torch.cuda.synchronize()
+        if i > 0:
+            copy_times.append(time.perf_counter() - t0)
+    del d
+    torch.cuda.empty_cache()
+    t = torch.tensor([statistics.mean(times), statistics.mean(copy_times)], dtype=torch.float64,
+                     device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_e2e, t_copy = t.tolist()
+    lb = 8 if mode == 0 else (4 if mode == 1 else 2)
+    return {"value": world * n / t_e2e, "unit": "params/s",
+            "h2d_bytes_per_step": 2 * n * lb, "d2h_bytes_per_step": n * lb,
+            "ms_per_step": 1e3 * t_e2e,
+            "pcie_copy_only_ms": 1e3 * t_copy, "pcie_frac": t_copy / t_e2e,
+            "api": "co2_round_host (the reference's co2_round with the inner loop on the host: "
+                   "x_{t,1}, x_{t,tau} uploaded, x_{t+1,0} downloaded, outer state resident)"}
+
+
 def run_e2e(co2, torch, mode, n, tau, hyper, args, world, rank, dist):
-    """Same metric through co2_outer_step_host: every step copies this step's
-    inputs host->device from pinned memory and reads the results back."""
+    """The outer step alone through co2_outer_step_host, with the WHOLE
+    outer state host-resident: every step copies x_t0, p0, p1, xbar and m
+    host->device from pinned memory and reads m, the anchor and the params
+    back (reported as e2e_full_state)."""
     st = co2.STATE_TORCH[mode]
     lo = co2.LOW_TORCH[mode]
     x, p0, p1, xe, m = co2.synth(mode, n, worker=rank)

@@ -459,6 +459,24 @@ co2_status_t co2_round(co2_worker_t* const* workers, int32_t g, co2_aar_t* engin
                        co2_round_result_t* result);
 co2_status_t co2_round_finish(co2_worker_t* const* workers, int32_t g, void* stream,
                               co2_round_result_t* result);
+/* co2_round with the inner loop on the HOST (the reference's own setting:
+ * proj/include/co2sim/outer_algorithms.hpp:77-81 takes WorkerState /
+ * InnerTrace in host memory, proj/include/co2sim/inner_loop.hpp:18-24).
+ * The outer state (x_{t,0} anchor, the previous snapshots, momentum, the
+ * reduce buffers) stays resident on the device; per round only the inner
+ * loop's trace crosses PCIe: each worker's x_{t,1} (`x_first_host[i]`,
+ * nullable: then the device snapshot is kept) and x_{t,tau}
+ * (`x_end_host[i]`) are uploaded into the worker's buffers, the round runs
+ * (reduce launch, stale wait, fused step), and the params the next inner
+ * loop starts from (x_{t+1,0}; x_{0,tau} after round 0) are downloaded into
+ * `x_next_host[i]`.  Host buffers hold n low-dtype values each and should be
+ * pinned.  The worker's x_{0,0} anchor must be on the device before round 0
+ * (co2_worker_create's init + co2_worker_snapshot_start).  Asynchronous on
+ * `stream` unless `sync` != 0 (then as co2_round, after the download). */
+co2_status_t co2_round_host(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,
+                            const co2_hyper_t* hyper, const void* const* x_first_host,
+                            const void* const* x_end_host, void* const* x_next_host,
+                            void* stream, int32_t sync, co2_round_result_t* result);
 /* End of a run: consume (wait on, without applying) the reduce the last
  * round launched, releasing its slot in the engine's two-handle window. */
 co2_status_t co2_round_drain(co2_worker_t* const* workers, int32_t g, co2_aar_t* engine,

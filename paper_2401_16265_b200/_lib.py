@@ -156,6 +156,8 @@ SIGNATURES = {
     "co2_worker_snapshot_first": (ST, [P, P]),
     "co2_round": (ST, [C.POINTER(P), I32, P, C.POINTER(Hyper), P, I32, C.POINTER(RoundResult)]),
     "co2_round_finish": (ST, [C.POINTER(P), I32, P, C.POINTER(RoundResult)]),
+    "co2_round_host": (ST, [C.POINTER(P), I32, P, C.POINTER(Hyper), C.POINTER(P), C.POINTER(P),
+                            C.POINTER(P), P, I32, C.POINTER(RoundResult)]),
     "co2_round_drain": (ST, [C.POINTER(P), I32, P, P]),
     "co2_slowmo_step": (ST, [I32, I64, P, P, I32, P, P, P, D, D, P, P]),
     "co2_local_sgd_step": (ST, [I32, I64, P, P, I32, P, P, P, P]),

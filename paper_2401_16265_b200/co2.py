@@ -732,6 +732,28 @@ def overlap_local_sgd_round(workers: list[Worker], engine: CollectiveEngine, *,
     return r
 
 
+def co2_round_host(workers: list[Worker], engine: CollectiveEngine, hyper: Co2Hyper, tau: int,
+                   x_end: list, x_next: list, *, x_first: list | None = None, stream=None,
+                   sync: bool = True) -> L.RoundResult:
+    """co2_round with the inner loop on the host (include/co2_b200.h
+    co2_round_host): uploads each worker's x_{t,1} (optional) and x_{t,tau}
+    from host tensors, runs the round on the device-resident outer state,
+    downloads the next inner loop's start x_{t+1,0} into `x_next`."""
+    g = len(workers)
+    arr = (C.c_void_p * g)(*[w.handle.value for w in workers])
+
+    def ptrs(ts):
+        return (C.c_void_p * g)(*[t.data_ptr() for t in ts]) if ts is not None else None
+    for t in list(x_end) + list(x_next) + list(x_first or []):
+        if t.is_cuda or not t.is_contiguous() or t.numel() != workers[0].n:
+            raise ValueError("co2_round_host: contiguous host tensors of n values expected")
+    h = hyper.c(tau)
+    r = L.RoundResult()
+    check(lib().co2_round_host(arr, g, engine.handle, C.byref(h), ptrs(x_first), ptrs(x_end),
+                               ptrs(x_next), _stream(stream), int(sync), C.byref(r)))
+    return r
+
+
 def co2_round_drain(workers: list[Worker], engine: CollectiveEngine, *, stream=None) -> None:
     """Consume the reduce launched by the last round (end of a run)."""
     arr = (C.c_void_p * len(workers))(*[w.handle.value for w in workers])

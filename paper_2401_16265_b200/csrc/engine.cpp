@@ -1175,6 +1175,39 @@ extern "C" co2_status_t co2_round_finish(co2_worker_t* const* ws, int32_t g, voi
   return CO2_OK;
 }
 
+extern "C" co2_status_t co2_round_host(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
+                                       const co2_hyper_t* hyper,
+                                       const void* const* x_first_host,
+                                       const void* const* x_end_host, void* const* x_next_host,
+                                       void* stream, int32_t sync, co2_round_result_t* res) {
+  if (!ws || g < 1 || !x_end_host || !x_next_host)
+    return fail(CO2_ERR_VALIDATION, "co2_round_host: bad arguments");
+  cudaStream_t st = S(stream);
+  for (int i = 0; i < g; ++i) {
+    co2_worker* w = ws[i];
+    if (!w || !x_end_host[i] || !x_next_host[i])
+      return fail(CO2_ERR_VALIDATION, "co2_round_host: null worker or host buffer");
+    const size_t lb = low_bytes(w->mode) * (size_t)w->n;
+    if (!lb) continue;
+    if (x_first_host && x_first_host[i])  // InnerTrace::x_first (inner_loop.cpp:96-98)
+      CO2_CUDA(cudaMemcpyAsync(w->xfirst, x_first_host[i], lb, cudaMemcpyHostToDevice, st));
+    // InnerTrace::x_end: the params the round reduces and steps from (:110)
+    CO2_CUDA(cudaMemcpyAsync(w->params[w->cur], x_end_host[i], lb, cudaMemcpyHostToDevice, st));
+  }
+  co2_round_result_t r{};
+  const co2_status_t s0 = co2_round(ws, g, e, hyper, stream, sync, &r);
+  if (res) *res = r;
+  if (s0 != CO2_OK && s0 != CO2_ERR_NUMERIC) return s0;
+  for (int i = 0; i < g; ++i) {  // the next inner loop's start
+    co2_worker* w = ws[i];
+    const size_t lb = low_bytes(w->mode) * (size_t)w->n;
+    if (lb)
+      CO2_CUDA(cudaMemcpyAsync(x_next_host[i], w->params[w->cur], lb, cudaMemcpyDeviceToHost, st));
+  }
+  if (sync) CO2_CUDA(cudaStreamSynchronize(st));
+  return s0;
+}
+
 extern "C" co2_status_t co2_round_drain(co2_worker_t* const* ws, int32_t g, co2_aar_t* e,
                                         void* stream) {
   if (!ws || g < 1 || !e) return fail(CO2_ERR_VALIDATION, "co2_round_drain: bad arguments");

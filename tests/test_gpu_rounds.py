@@ -294,6 +294,41 @@ def test_single_launch_round_handles():
     assert eng.info(rounds - 1)["consumed"]
 
 
+@pytest.mark.parametrize("mode", [co2.MODE_F32, co2.MODE_BF16_MIXED])
+def test_round_host_matches_device_round(mode):
+    """co2_round_host (inner loop on the host, outer state resident) equals
+    uploading the same traces by hand and calling co2_round, bitwise, and
+    hands back the next inner loop's start."""
+    g, n, tau, rounds = 2, 10007, 3, 5
+    hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    lo = co2.LOW_TORCH[mode]
+    ea, eb = co2.CollectiveEngine(g, transport="local"), co2.CollectiveEngine(g, transport="local")
+    wa = [co2.Worker(mode, n, co2.synth_params(mode, n, worker=i)) for i in range(g)]
+    wb = [co2.Worker(mode, n, co2.synth_params(mode, n, worker=i)) for i in range(g)]
+    for w in wa + wb:
+        w.snapshot_start()
+    gen = torch.Generator().manual_seed(5)
+    for t in range(rounds):
+        first = [(torch.rand(n, generator=gen) * 0.02 - 0.01).to(lo).pin_memory()
+                 for _ in range(g)]
+        end = [(torch.rand(n, generator=gen) * 0.02 - 0.01).to(lo).pin_memory()
+               for _ in range(g)]
+        for i, w in enumerate(wa):
+            if t % 2 == 0:  # odd rounds: x_first omitted, the device snapshot stays
+                w.buffer(L.BUF_XFIRST).copy_(first[i])
+            w.params.copy_(end[i])
+        co2.co2_round(wa, ea, hyper, tau)
+        nxt = [torch.empty(n, dtype=lo).pin_memory() for _ in range(g)]
+        rb = co2.co2_round_host(wb, eb, hyper, tau, end, nxt,
+                                x_first=first if t % 2 == 0 else None, sync=True)
+        for i in range(g):
+            assert to_np(wa[i].params).tobytes() == to_np(nxt[i]).tobytes(), (t, i)
+            assert to_np(wa[i].buffer(L.BUF_MOMENTUM)).tobytes() == \
+                to_np(wb[i].buffer(L.BUF_MOMENTUM)).tobytes(), (t, i)
+        if t >= 1:
+            assert rb.outer_applied == 1 and rb.min_gap >= 1.0
+
+
 def test_round_rejects_bad_hyper_and_counts():
     eng = co2.CollectiveEngine(2, transport="local")
     ws = [co2.Worker(co2.MODE_F32, 16) for _ in range(2)]
