@@ -1831,6 +1831,17 @@ extern "C" co2_status_t co2_sharded_drain(co2_sharded_t* s, co2_aar_t* e, void* 
   return CO2_OK;
 }
 
+// All-gather of the sharded P2P round (CO2_SHARD_AG = ce | fused): "fused"
+// stores the x_{t+1,0} slice into every rank's params from the step kernel
+// itself; "ce" lets the step write locally and the copy engines push it.
+static bool shard_allgather_ce() {
+  static const bool ce = [] {
+    const char* v = getenv("CO2_SHARD_AG");
+    return v && strcmp(v, "ce") == 0;
+  }();
+  return ce;
+}
+
 extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
                                           const co2_hyper_t* hyper, void* stream, int32_t sync,
                                           co2_round_result_t* res) {
@@ -1904,10 +1915,26 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
     std::vector<void*> outs(s->world);
     for (int p = 0; p < s->world; ++p) outs[p] = static_cast<char*>(pb->ptrs[p]) + lb * s->offset;
     e->shard_epoch += 1;
-    CO2_TRY(outer_step_ghost_p2p_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, xsum,
-                                      ghost_copies, s->m, s->anchor, s->prev_x0, outs.data(),
-                                      e->peer_signals.data(), s->world, s->rank, e->shard_epoch,
-                                      s->gap, hyper, s->ws, st));
+    if (shard_allgather_ce()) {
+      // The step writes the x_{t+1,0} slice locally (the slice averages are
+      // averages: divisors 1); the copy engines push it into every peer's
+      // params; the exit barrier runs after the copies on this stream.
+      CO2_TRY(outer_step_ghost_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, 1, xsum, 1,
+                                    ghost_copies, s->m, s->anchor, s->prev_x0, out_params, s->gap,
+                                    hyper, s->ws, st));
+      if (cap) CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));  // the step kernel alone
+      for (int p = 0; p < s->world; ++p)
+        if (p != s->rank && s->length > 0)
+          CO2_CUDA(cudaMemcpyAsync(outs[p], out_params, lb * (size_t)s->length,
+                                   cudaMemcpyDeviceToDevice, st));
+      CO2_TRY(p2p_barrier_launch(e->peer_signals.data(), s->world, s->rank, e->shard_epoch, st));
+    } else {
+      CO2_TRY(outer_step_ghost_p2p_impl(s->mode, s->length, s->anchor, s->prev_x0, p1, xsum,
+                                        ghost_copies, s->m, s->anchor, s->prev_x0, outs.data(),
+                                        e->peer_signals.data(), s->world, s->rank,
+                                        e->shard_epoch, s->gap, hyper, s->ws, st));
+      if (cap) CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));
+    }
   } else {
     CO2_TRY(outer_step_ghost_impl(s->mode, s->length, s->anchor, s->prev_x0, p1,
                                   reduce_divisor(e), xsum, reduce_divisor(e), ghost_copies,
@@ -1915,7 +1942,7 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
                                   st));
   }
   if (cap) {
-    CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));
+    if (!s->p2p) CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));
     s->tev_recorded += 1;
   }
   CO2_TRY(co2_diag_fetch_async(s->ws, s->host_diag, stream));

@@ -605,6 +605,28 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
   return CO2_OK;
 }
 
+namespace {
+// One thread: the sharded step's exit barrier on its own, after an
+// all-gather the copy engines did (cudaMemcpyAsync into the peers' params,
+// ordered before this kernel on the stream).
+__global__ void p2p_barrier_kernel(const P2PExit x) { p2p_exit_barrier(x); }
+}  // namespace
+
+co2_status_t p2p_barrier_launch(void* const* sigs, int world, int rank, uint32_t epoch,
+                                cudaStream_t s) {
+  if (world < 1 || world > kMaxRanks)
+    return fail(CO2_ERR_VALIDATION, "p2p: world must lie in [1, %d]", kMaxRanks);
+  P2PExit x{};
+  for (int p = 0; p < world; ++p) x.sig[p] = static_cast<Signals*>(sigs[p]);
+  x.world = world;
+  x.rank = rank;
+  x.epoch = epoch;
+  x.counter = 0;  // done2, as the fused sharded step's exit barrier
+  p2p_barrier_kernel<<<1, 1, 0, s>>>(x);
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
 size_t p2p_signal_bytes() { return sizeof(Signals); }
 size_t p2p_signal_timeout_offset() { return offsetof(Signals, timeout_ms); }
 size_t p2p_signal_error_offset() { return offsetof(Signals, error); }
