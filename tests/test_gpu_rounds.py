@@ -202,6 +202,49 @@ def test_c1_simulated_workers_bitwise(mode):
             assert r.max_outer_step <= np.float32(5e-3) * (1 + 1e-6)
 
 
+@pytest.mark.parametrize("mode", [co2.MODE_F32, co2.MODE_BF16_MIXED])
+@pytest.mark.parametrize("g", [1, 3, 8])
+@pytest.mark.parametrize("n", [1, 7, 1029, 263171])
+def test_local_round_kernel_shapes_bitwise(mode, g, n):
+    """The single-launch LOCAL round (persistent grid, role-major tiles, the
+    scalar tail in each role's last tile, atomic per-role diagnostics) at
+    ragged sizes and 1..8 workers: params, momentum and the round's
+    min_gap / max_outer_step bitwise against the oracle, three rounds."""
+    tau = 3
+    hyper = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12)
+    oh = O.hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=1e-12, tau=tau)
+    eng = co2.CollectiveEngine(g, transport="local")
+    ws = [co2.Worker(mode, n, co2.synth(mode, n, worker=w)[3]) for w in range(g)]
+    orr = OracleRoundLP(mode, g, oh)
+    m0 = np.zeros(n, np.float32)
+    for t in range(4):
+        traces = []
+        for i, w in enumerate(ws):
+            w.snapshot_start()
+            for k in range(tau):
+                co2.synthetic_inner_step(w.params, lr=1e-3, scale=1.0, worker=i,
+                                         step=t * tau + k)
+                if k == 0:
+                    w.snapshot_first()
+            traces.append((to_np(w.buffer(L.BUF_ANCHOR)), to_np(w.buffer(L.BUF_XFIRST)),
+                           to_np(w.params)))
+        params_before = [tr[2] for tr in traces]
+        r = co2.co2_round(ws, eng, hyper, tau)
+        if t >= 1:  # the oracle's per-worker diagnostics, folded as RoundResult does
+            diags = [O.outer_step(mode, traces[i][0], orr.p0[i], orr.p1[i], orr.pending,
+                                  orr.m[i], oh).diag for i in range(g)]
+        ref = orr.round(params_before, traces, m0)
+        for i, w in enumerate(ws):
+            assert to_np(w.params).tobytes() == ref[i].tobytes(), (t, i)
+            if t >= 1:
+                assert to_np(w.buffer(L.BUF_MOMENTUM)).tobytes() == orr.m[i].tobytes(), (t, i)
+        if t >= 1:
+            assert r.min_gap == min(d.min_gap for d in diags)
+            assert r.max_outer_step == max(d.max_outer_step for d in diags)
+            assert r.n_clipped == sum(d.n_clipped for d in diags)
+            assert r.n_floored == sum(d.n_floored for d in diags)
+
+
 def test_engine_semantics():
     """CollectiveEngine contract (proj/tests/test_collective.cpp:43-207)."""
     eng = co2.CollectiveEngine(2, transport="local")
