@@ -726,11 +726,13 @@ def main():
             "e2e": e2e, "e2e_full_state": e2e_full, "cpu_baseline": cpu, "comm": comm,
             # our kernels per step per rank: the fused step (two passes for the
             # global-norm clip), plus our P2P reduce kernel when it runs as its
-            # own launch (NCCL's kernels are not ours)
+            # own launch, or the ascending-rank sum kernel of the fixed-order
+            # NCCL all-reduce (NCCL's own kernels are not ours)
             "gpu_launches": world * args.steps * (
                 (2 if gclip else 1) +
                 (1 if world > 1 and transport == "p2p" and
-                 (sharded or args.schedule == "split") else 0)),
+                 (sharded or args.schedule == "split") else 0) +
+                (1 if world > 1 and transport == "nccl" and not sharded else 0)),
             "clocks": clk.summary(),
             "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step,
                      "n_clipped": r.n_clipped, "n_floored": r.n_floored},
