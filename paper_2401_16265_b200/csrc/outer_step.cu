@@ -336,7 +336,7 @@ __device__ __forceinline__ TC start_of_inner(TC q0) {
 template <typename TC, bool LQ = false>
 __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& xn, TC& lam,
                                          const Hyp<TC>& h, AccT<TC>& acc) {
-  if (h.divide) xb = div_rn(xb, h.divisor);  // average(): sum / G, param_ops.cpp:30
+  if (h.divide) xb = div_rn_nz(xb, h.divisor);  // average(): sum / G, param_ops.cpp:30
   TC n0 = fabs(x - q0);
   TC av = fabs(h.tau * (q1 - start_of_inner<TC, LQ>(q0)));
   bool floored = av < h.eps;
@@ -346,7 +346,7 @@ __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& x
   TC mn;
   if (h.penalty) {
     TC bm = h.beta * m;
-    TC q = div_rn(dl, lam);
+    TC q = div_rn_nz(dl, lam);  // lam >= 1, +inf or NaN
     mn = bm + q;
   } else {
     TC bm = h.beta * m;
@@ -370,9 +370,11 @@ __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& x
   acc.flags |= f;
   acc.floored += floored;
   acc.clipped += clipped;
-  acc.min_gap = lam < acc.min_gap ? lam : acc.min_gap;
+  // fmin / fmax: a NaN operand never wins, as in the `<` / `>` folds of the
+  // block and role merges; lam >= 1 and |x' - x| >= +0 have no signed zeros.
+  acc.min_gap = fmin(lam, acc.min_gap);
   TC st = fabs(xn - x);
-  acc.max_step = st > acc.max_step ? st : acc.max_step;
+  acc.max_step = fmax(st, acc.max_step);
 }
 
 struct StepArgs {
@@ -437,7 +439,7 @@ __device__ __forceinline__ void aar_vector(const StepArgs& a, int64_t e) {
   uint4 out;
   const TC g = (TC)a.exit.world;
 #pragma unroll
-  for (int k = 0; k < VA; ++k) reinterpret_cast<TL*>(&out)[k] = Store<TL>::from(div_rn(acc[k], (TC)g));
+  for (int k = 0; k < VA; ++k) reinterpret_cast<TL*>(&out)[k] = Store<TL>::from(div_rn_nz(acc[k], (TC)g));
 #pragma unroll
   for (int p = 0; p < R; ++p)
     if (p < a.exit.world) __stcg(reinterpret_cast<uint4*>(static_cast<TL*>(a.aar_bufs[p]) + e), out);
@@ -449,7 +451,7 @@ template <typename TC>
 __device__ __forceinline__ TC ghost_avg(TC v, int g) {
   TC s = v;
   for (int i = 1; i < g; ++i) s = s + v;
-  return div_rn(s, (TC)g);
+  return div_rn_nz(s, (TC)g);
 }
 
 // The fused step's body, shared by the launch-bounded kernel and the
@@ -532,11 +534,11 @@ __device__ __forceinline__ void fused_step_body(const StepArgs& a) {
         for (int v = 0; v < V; ++v) {
           TC m = to_c(mo[u][v]), xn, lam;
           TC xbv = to_c(xb[u][v]);
-          if (h.divide) xbv = div_rn(xbv, h.divisor);  // average(): sum / G, param_ops.cpp:30
+          if (h.divide) xbv = div_rn_nz(xbv, h.divisor);  // average(): sum / G, param_ops.cpp:30
           if constexpr (GHOST) {
             TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(x[u][v]), a.ghost_g);
             TC p1v = to_c(q1[u][v]);
-            if (a.p1_div > 1) p1v = div_rn(p1v, p1d);
+            if (a.p1_div > 1) p1v = div_rn_nz(p1v, p1d);
             b0[v] = (TS)xv;
             co2_elem<TC, LQ>(xv, to_c(q0[u][v]), p1v, xbv, m, xn, lam, hg, acc);
           } else {
@@ -590,7 +592,7 @@ __device__ __forceinline__ void fused_step_body(const StepArgs& a) {
            j += NT) {
         TC s0 = to_c(static_cast<const TL*>(a.aar_bufs[0])[j]);
         for (int p = 1; p < a.exit.world; ++p) s0 = s0 + to_c(static_cast<const TL*>(a.aar_bufs[p])[j]);
-        const TL r = Store<TL>::from(div_rn(s0, (TC)a.exit.world));
+        const TL r = Store<TL>::from(div_rn_nz(s0, (TC)a.exit.world));
         for (int p = 0; p < a.exit.world; ++p) static_cast<TL*>(a.aar_bufs[p])[j] = r;
       }
     }
@@ -600,11 +602,11 @@ __device__ __forceinline__ void fused_step_body(const StepArgs& a) {
   if (V > 1 && t < a.n) {
     TC m = to_c(Mm[t]), xn, lam;
     TC xbv = to_c(XB[t]);
-    if (h.divide) xbv = div_rn(xbv, h.divisor);
+    if (h.divide) xbv = div_rn_nz(xbv, h.divisor);
     if constexpr (GHOST) {
       TC xv = a.x_from_xbar ? xbv : ghost_avg<TC>(to_c(X[t]), a.ghost_g);
       TC p1v = to_c(P1[t]);
-      if (a.p1_div > 1) p1v = div_rn(p1v, p1d);
+      if (a.p1_div > 1) p1v = div_rn_nz(p1v, p1d);
       const TC q0 = to_c(P0[t]);  // read before bar0_out (may alias prev_x0) is written
       if (B0) B0[t] = (TS)xv;
       co2_elem<TC, LQ>(xv, q0, p1v, xbv, m, xn, lam, hg, acc);
@@ -923,7 +925,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) bulk_step_kernel(const Step
         for (int v = 0; v < VE; ++v) {
           TC m = to_c(mo[v]), xn, lam;
           TC xbv = to_c(xb[v]);
-          if (h.divide) xbv = div_rn(xbv, h.divisor);  // average(): sum / G, param_ops.cpp:30
+          if (h.divide) xbv = div_rn_nz(xbv, h.divisor);  // average(): sum / G, param_ops.cpp:30
           co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), xbv, m, xn, lam, hg, acc);
           mn[v] = (TS)m;
           xs[v] = (TS)xn;
@@ -946,7 +948,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) bulk_step_kernel(const Step
     for (int64_t j = ntiles * (int64_t)TILE + threadIdx.x; j < a.n; j += NT) {
       TC m = to_c(Mm[j]), xn, lam;
       TC xbv = to_c(XB[j]);
-      if (h.divide) xbv = div_rn(xbv, h.divisor);
+      if (h.divide) xbv = div_rn_nz(xbv, h.divisor);
       co2_elem<TC, LQ>(to_c(X[j]), to_c(P0[j]), to_c(P1[j]), xbv, m, xn, lam, hg, acc);
       if (XO) XO[j] = XB[j];
       Mm[j] = (TS)m;
@@ -1110,7 +1112,7 @@ __global__ void __launch_bounds__(kThreads) op_kernel(const OpArgs a) {
       if (a.i0) {
         if (g < (TC)1) acc.flags |= CO2_FLAG_GAP_BELOW_ONE;
         TC bm = beta * mp;
-        TC q = div_rn(dl, g);
+        TC q = div_rn(dl, g);  // gap: an arbitrary input array
         m = bm + q;
       } else {
         TC bm = beta * mp;
@@ -1162,7 +1164,7 @@ __global__ void __launch_bounds__(kThreads)
        j += (int64_t)gridDim.x * kThreads) {
     TC s = to_c(c.p[0][j]);
     for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
-    TC r = div_rn(s, gd);
+    TC r = div_rn_nz(s, gd);
     if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
     out[j] = Store<T>::from(r);
   }
@@ -1201,7 +1203,7 @@ __global__ void __launch_bounds__(kThreads)
     T o[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) {
-      const TC r = div_rn(s[q], gd);
+      const TC r = div_rn_nz(s[q], gd);
       if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
       o[q] = Store<T>::from(r);
     }
@@ -1211,7 +1213,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int64_t j = nv * V + threadIdx.x; j < n; j += kThreads) {
       TC s = to_c(c.p[0][j]);
       for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
-      const TC r = div_rn(s, gd);
+      const TC r = div_rn_nz(s, gd);
       if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
       out[j] = Store<T>::from(r);
     }
@@ -1402,7 +1404,7 @@ __device__ __forceinline__ TC gc_momentum(TC x, TC q0, TC q1, TC xb, TC m, TC& l
   lam = div_rn(n0, d) + (TC)1;
   TC dl = q0 - xb;
   TC bm = h.beta * m;
-  TC mn = h.penalty ? bm + div_rn(dl, lam) : bm + dl;
+  TC mn = h.penalty ? bm + div_rn_nz(dl, lam) : bm + dl;
   unsigned int f = 0;
   if (!isfinite(lam)) f |= CO2_FLAG_GAP_NONFINITE;
   if (h.penalty && lam < (TC)1) f |= CO2_FLAG_GAP_BELOW_ONE;
@@ -1486,7 +1488,7 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int6
       for (int v = 0; v < V; ++v) {
         TC lam;
         TC xbv = to_c(xb[v]);
-        if (h.divide) xbv = div_rn(xbv, h.divisor);
+        if (h.divide) xbv = div_rn_nz(xbv, h.divisor);
         const TC m = gc_momentum<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), xbv, to_c(mo[v]),
                                          lam, h, acc);
         mn[v] = (TS)m;
@@ -1502,7 +1504,7 @@ __global__ void __launch_bounds__(kGcThreads) gclip_pass1(const StepArgs a, int6
       for (int64_t e = nvE; e < a.n; ++e) {
         TC lam;
         TC xbv = to_c(XB[e]);
-        if (h.divide) xbv = div_rn(xbv, h.divisor);
+        if (h.divide) xbv = div_rn_nz(xbv, h.divisor);
         if (XO) XO[e] = XB[e];
         const TC m =
             gc_momentum<TC, LQ>(to_c(X[e]), to_c(P0[e]), to_c(P1[e]), xbv, to_c(Mm[e]), lam, h,
@@ -2096,7 +2098,7 @@ __global__ void scale_div_kernel(T* b, int64_t n, int g) {
   const TC gd = (TC)g;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x)
-    b[j] = Store<T>::from(div_rn(to_c(b[j]), gd));
+    b[j] = Store<T>::from(div_rn_nz(to_c(b[j]), gd));
 }
 }  // namespace
 
@@ -2271,7 +2273,7 @@ __global__ void __launch_bounds__(kThreads) baseline_kernel(const BaseArgs a) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       TC xbv = to_c(xb[v]);
-      if (div) xbv = div_rn(xbv, gd);  // average(): one division, param_ops.cpp:30
+      if (div) xbv = div_rn_nz(xbv, gd);  // average(): one division, param_ops.cpp:30
       base_elem<M, OP>(xbv, OP == B_OVERLAP ? (TC)0 : to_c(x[v]), m[v], pr[v], an[v], af, bf,
                        acc);
     }
@@ -2282,7 +2284,7 @@ __global__ void __launch_bounds__(kThreads) baseline_kernel(const BaseArgs a) {
   for (int64_t j = nv * V + (int64_t)blockIdx.x * kThreads + threadIdx.x; V > 1 && j < a.n;
        j += stride) {
     TC xbv = to_c(XB[j]);
-    if (div) xbv = div_rn(xbv, gd);
+    if (div) xbv = div_rn_nz(xbv, gd);
     TS m = OP == B_SLOWMO ? Mm[j] : (TS)0;
     TS an = OP == B_OVERLAP ? A[j] : (TS)0;
     TL pr = OP == B_OVERLAP ? PR[j] : TL{};
@@ -2616,7 +2618,7 @@ __global__ void __launch_bounds__(NT, MINB) local_round_kernel(const LocalRoundA
 #pragma unroll
         for (int q = 0; q < V; ++q) {
           if (q < cnt) {
-            const TC r = div_rn(s[q], gd);  // one division, :30
+            const TC r = div_rn_nz(s[q], gd);  // one division, :30
             if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
             o[q] = Store<TL>::from(r);
           }
@@ -2866,7 +2868,7 @@ __global__ void __launch_bounds__(kThreads)
          j += (int64_t)gridDim.x * kThreads) {
       TC s = to_c(c.p[0][j]);
       for (int i = 1; i < g; ++i) s += to_c(c.p[i][j]);
-      const TC xb = div_rn(s, gd);
+      const TC xb = div_rn_nz(s, gd);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (w0 + k < g) {

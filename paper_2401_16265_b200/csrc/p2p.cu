@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(NT, sizeof(TL) <= 4 ? 1024 / NT : 1)
       TL* o = reinterpret_cast<TL*>(&out);
 #pragma unroll
       for (int k = 0; k < V; ++k) {
-        TC r = div_rn(acc[k], (TC)g);  // one division, param_ops.cpp:30
+        TC r = div_rn_nz(acc[k], (TC)g);  // one division, param_ops.cpp:30
         if constexpr (sizeof(TL) == 2) {
           __nv_bfloat16 h = __float2bfloat16_rn((float)r);
           reinterpret_cast<uint16_t*>(o)[k] = __bfloat16_as_ushort(h);
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(NT, sizeof(TL) <= 4 ? 1024 / NT : 1)
             x = (TC)__ldcg(static_cast<const TL*>(a.bufs[p]) + j);
           acc = acc + x;
         }
-        TC r = div_rn(acc, (TC)g);
+        TC r = div_rn_nz(acc, (TC)g);
         for (int p = 0; p < a.world; ++p) {
           if constexpr (sizeof(TL) == 2) {
             __nv_bfloat16 h = __float2bfloat16_rn((float)r);
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) p2p_bulk_average_kernel(const 
           TL* ov = reinterpret_cast<TL*>(&out);
 #pragma unroll
           for (int k = 0; k < V; ++k) {
-            TC r = div_rn(acc[k], (TC)g);  // one division, param_ops.cpp:30
+            TC r = div_rn_nz(acc[k], (TC)g);  // one division, param_ops.cpp:30
             if constexpr (sizeof(TL) == 2) {
               __nv_bfloat16 h = __float2bfloat16_rn((float)r);
               reinterpret_cast<uint16_t*>(ov)[k] = __bfloat16_as_ushort(h);
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) p2p_bulk_average_kernel(const 
             x = (TC)__ldcg(static_cast<const TL*>(a.bufs[p]) + j);
           acc = acc + x;
         }
-        TC r = div_rn(acc, (TC)g);
+        TC r = div_rn_nz(acc, (TC)g);
         for (int p = 0; p < G; ++p) {
           if constexpr (sizeof(TL) == 2) {
             __nv_bfloat16 h = __float2bfloat16_rn((float)r);
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(NT) p2p_slice_average_kernel(const SliceArgs a
               acc[k] = acc[k] + to_c(reinterpret_cast<const TL*>(&raw[u][p]), k);
         uint4 out;
 #pragma unroll
-        for (int k = 0; k < V; ++k) store(reinterpret_cast<TL*>(&out), k, div_rn(acc[k], (TC)g));
+        for (int k = 0; k < V; ++k) store(reinterpret_cast<TL*>(&out), k, div_rn_nz(acc[k], (TC)g));
         *reinterpret_cast<uint4*>(static_cast<TL*>(a.dst[b]) + iv * V) = out;
       }
     }
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(NT) p2p_slice_average_kernel(const SliceArgs a
         TC acc = to_c(static_cast<const TL*>(a.src[b][0]) + a.lo + j, 0);
         for (int p = 1; p < a.world; ++p)
           acc = acc + to_c(static_cast<const TL*>(a.src[b][p]) + a.lo + j, 0);
-        store(static_cast<TL*>(a.dst[b]) + j, 0, div_rn(acc, (TC)g));
+        store(static_cast<TL*>(a.dst[b]) + j, 0, div_rn_nz(acc, (TC)g));
       }
     }
   }

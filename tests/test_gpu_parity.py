@@ -227,6 +227,49 @@ def test_fused_special_values_bitwise(mode, seed, penalty, clip):
 
 
 @pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("eps", [1e-12, 1e-40, 1e-46, 1e-310])
+def test_gap_zero_dividend_edges(mode, eps):
+    """The divisions' zero-dividend path (div_rn, div_rn_nz): n0 = 0
+    against a denominator at the epsilon floor -- normal, subnormal or
+    rounded to zero in the compute type (0/0: NaN, the staleness_gap error)
+    -- or +inf (p1 = inf: 0/inf = 0, gap 1); delta = 0 against the gap.
+    Same bits and the same status as the oracle."""
+    n = 4 * 257
+    st_dt = np.float64 if mode == co2.MODE_F64 else np.float32
+    rng = np.random.default_rng(11)
+    p0 = rng.uniform(-0.02, 0.02, n).astype(st_dt)
+    x = p0.copy()                                    # n0 = 0 everywhere
+    p1 = p0.astype(np.float64).copy()
+    p1[1::4] = np.inf                                # av = inf
+    p1[2::4] += 1e-3                                 # ordinary denominators
+    xb = p0.astype(np.float64).copy()                # delta = 0 ...
+    xb[3::4] -= 1e-3                                 # ... except here
+    m = rng.uniform(-1e-2, 1e-2, n).astype(st_dt)
+    if mode == co2.MODE_BF16_MIXED:
+        p1, xb = O.f32_to_bf16_bits(p1.astype(np.float32)), O.f32_to_bf16_bits(xb.astype(np.float32))
+        x = p0 = O.bf16_bits_to_f32(O.f32_to_bf16_bits(p0)).astype(np.float32)
+    else:
+        p1, xb = p1.astype(st_dt), xb.astype(st_dt)
+    oh = O.hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=eps, tau=4)
+    ref = O.outer_step(mode, x, p0, p1, xb, m, oh)
+    h = co2.Co2Hyper(alpha=1.0, beta=0.7, phi=5e-3, epsilon=eps)
+    dx, dp0, dp1, dxb, dm = (to_dev(a) for a in (x, p0, p1, xb, m))
+    anchor, params, gap = torch.empty_like(dx), torch.empty_like(dxb), torch.empty_like(dx)
+    if ref.status != 0:
+        with pytest.raises((co2.NumericError, co2.ValidationError)) as ei:
+            co2.outer_step(mode, dx, dp0, dp1, dxb, dm, h, 4, anchor_out=anchor,
+                           params_out=params, gap_out=gap)
+        assert str(ei.value) == ref.message
+        return
+    d = co2.outer_step(mode, dx, dp0, dp1, dxb, dm, h, 4, anchor_out=anchor, params_out=params,
+                       gap_out=gap)
+    assert same(to_np(dm), ref.m) and same(to_np(anchor), ref.anchor)
+    assert same(to_np(params), ref.params) and same(to_np(gap), ref.gap)
+    assert (d.min_gap, d.max_outer_step, d.n_clipped, d.n_floored) == (
+        ref.diag.min_gap, ref.diag.max_outer_step, ref.diag.n_clipped, ref.diag.n_floored)
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("where", ["momentum", "iterate"])
 def test_fused_overflow_status_matches_oracle(mode, where):
     """An overflow to inf inside the step raises the same error as the
@@ -555,7 +598,8 @@ def test_fused_step_property_vs_oracle(mode):
     @settings(max_examples=150, deadline=None, derandomize=True)
     @given(vals=st.lists(st.tuples(fin, fin, fin, fin, fin), min_size=1, max_size=40),
            alpha=st.floats(1e-3, 4.0), beta=st.floats(0.0, 0.999), phi=st.floats(1e-9, 1e3),
-           eps=st.sampled_from([1e-12, 1e-30, 1.0]), tau=st.integers(1, 64),
+           eps=st.sampled_from([1e-12, 1e-30, 1.0, 1e-40, 1e-46, 1e-310]),
+           tau=st.integers(1, 64),
            penalty=st.booleans(), clip=st.booleans())
     def check(vals, alpha, beta, phi, eps, tau, penalty, clip):
         st_dt = np.float64 if mode == co2.MODE_F64 else np.float32
