@@ -57,6 +57,31 @@ __global__ void step_mix(const uint4* __restrict__ a, const uint4* __restrict__ 
   }
 }
 
+// The same stream pulling its remote share with loads instead of pushing
+// it with stores (what a pull-based all-gather would do).
+__global__ void step_mix_pull(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                              const uint4* __restrict__ c, uint4* __restrict__ o,
+                              const uint4* const* __restrict__ remote, int peers, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    uint4 x = __ldcs(a + i), y = __ldcs(b + i), z = __ldcs(c + i);
+    uint4 r;
+    r.x = x.x ^ y.x ^ z.x;
+    r.y = x.y ^ y.y ^ z.y;
+    r.z = x.z ^ y.z ^ z.z;
+    r.w = x.w ^ y.w ^ z.w;
+    if ((i & 3) == 0)
+      for (int p = 0; p < peers; ++p) {
+        const uint4 q = __ldcg(remote[p] + (i >> 2));
+        r.x ^= q.x;
+        r.y ^= q.y;
+        r.z ^= q.z;
+        r.w ^= q.w;
+      }
+    __stcs(o + i, r);
+  }
+}
+
 struct Dev {
   int id;
   cudaStream_t s;
@@ -206,6 +231,12 @@ int main(int argc, char** argv) {
         step_mix<<<grid * 8, nt, 0, dv[g].s>>>((const uint4*)src[g], (const uint4*)c3[g],
                                               (const uint4*)dst[g], (uint4*)dst[g], rem_d[g],
                                               ng - 1, nmix);
+      },
+      (double)nmix * 16 * 4);
+  run("step_mix_pull", all, [&](int g) {
+        step_mix_pull<<<grid * 8, nt, 0, dv[g].s>>>((const uint4*)src[g], (const uint4*)c3[g],
+                                                   (const uint4*)dst[g], (uint4*)dst[g],
+                                                   (const uint4* const*)rem_d[g], ng - 1, nmix);
       },
       (double)nmix * 16 * 4);
   printf("{\"probe\": \"step_mix_note\", \"remote_bytes_per_gpu_out\": %.0f}\n",
