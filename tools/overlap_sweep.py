@@ -17,6 +17,13 @@ so the predicted stall is positive for tau < knee and zero from the knee on.
 If t_comm <= t_outer the outer step alone hides the reduce and no knee
 exists; the sweep says so.
 
+--inner selects the stand-in for the inner step: `hbm` (default) the
+HBM-streaming update above -- the worst case for sharing HBM with the
+reduce; `gemm` a bf16 tensor-core GEMM on resident operands (cuBLAS through
+torch.matmul, square m x m, m calibrated to t_comp) plus the x_{t,1}
+snapshot copy after the first step -- the compute-bound shape of a real
+model's inner step.
+
 exposed% = 100 * sum(stall) / sum(waited comm), the reference definition
 (1 - overlap_ratio_achieved).  stall = device time the compute stream waited
 on the reduce (events straddling the wait); comm = device duration of the
@@ -45,6 +52,7 @@ def main():
     ap.add_argument("--knee", type=float, default=4.0, help="tau at which tau*t_comp = t_comm")
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ncclsum", "p2p"])
+    ap.add_argument("--inner", default="hbm", choices=["hbm", "gemm"])
     ap.add_argument("--out", default="")
     a = ap.parse_args()
 
@@ -108,13 +116,34 @@ def main():
     t_outer0 = outer_alone()
     t_outer0 = max_over_ranks([t_outer0], device="cpu")[0] if world > 1 else t_outer0
 
+    gemm_ops = {}
+
+    def gemm_operands(m):
+        if m not in gemm_ops:
+            g = torch.Generator(device="cuda").manual_seed(rank)
+            gemm_ops.clear()
+            gemm_ops[m] = (torch.randn(m, m, device="cuda", dtype=torch.bfloat16, generator=g),
+                           torch.randn(m, m, device="cuda", dtype=torch.bfloat16, generator=g),
+                           torch.empty(m, m, device="cuda", dtype=torch.bfloat16))
+        return gemm_ops[m]
+
+    def inner_step(k, params, step, snapshot_out=None):
+        if a.inner == "hbm":
+            co2.synthetic_inner_step(params[:k], lr=1e-6, worker=rank, step=step,
+                                     snapshot_out=snapshot_out[:k] if snapshot_out is not None
+                                     else None)
+        else:  # k is the GEMM size m
+            x, y, out = gemm_operands(k)
+            torch.matmul(x, y, out=out)
+            if snapshot_out is not None:
+                snapshot_out.copy_(params)
+
     def time_inner(k, iters=6):
-        view = w.params[:k]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        co2.synthetic_inner_step(view, lr=1e-6, worker=rank, step=0)
+        inner_step(k, w.params, 0)
         e0.record(stream)
         for i in range(iters):
-            co2.synthetic_inner_step(view, lr=1e-6, worker=rank, step=i)
+            inner_step(k, w.params, i)
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e-3 / iters
@@ -123,10 +152,16 @@ def main():
     # tau * t_comp + t_outer = t_comm at tau = knee
     knee_exists = t_comm > t_outer0
     target = (t_comm - t_outer0) / a.knee if knee_exists else t_comm / a.knee
-    k = a.n
-    t_full = time_inner(k)
-    for _ in range(4):
-        k = max(1 << 16, min(a.n, int(k * target / max(time_inner(k), 1e-9))) // 256 * 256)
+    if a.inner == "hbm":
+        k = a.n
+        t_full = time_inner(k)
+        for _ in range(4):
+            k = max(1 << 16, min(a.n, int(k * target / max(time_inner(k), 1e-9))) // 256 * 256)
+    else:  # GEMM time ~ m^3
+        k = 4096
+        t_full = time_inner(k)
+        for _ in range(4):
+            k = max(256, int(k * (target / max(time_inner(k), 1e-9)) ** (1.0 / 3.0)) // 128 * 128)
     t_comp = time_inner(k)
     k, t_comp = (max_over_ranks([k, t_comp], device="cpu") if world > 1 else (k, t_comp))
     k = int(k)
@@ -159,10 +194,10 @@ def main():
                 w2.snapshot_first()
             for j in range(tau):
                 # the first step's store also writes the x_{t,1} snapshot of
-                # the coordinates it moves (the others did not move)
-                co2.synthetic_inner_step(
-                    w2.params[:k], lr=1e-6, worker=rank, step=t * tau + j,
-                    snapshot_out=w2.buffer(L.BUF_XFIRST)[:k] if j == 0 and t > 0 else None)
+                # the coordinates it moves (the others did not move); the
+                # GEMM stand-in copies the snapshot after its first step
+                inner_step(k, w2.params, t * tau + j,
+                           snapshot_out=w2.buffer(L.BUF_XFIRST) if j == 0 and t > 0 else None)
             co2.co2_round([w2], engine, hyper, tau, sync=False)
         evs[a.rounds].record(stream)
         co2.co2_round_drain([w2], engine)
@@ -197,7 +232,7 @@ def main():
         pst = [p[2] for p in pred.per_round[2:]]
         pred_exposed = 100.0 * sum(pst) / (t_comm * len(pst)) if t_comm and pst else 0.0
         row = {"tau": tau, "world": world, "n": a.n, "mode": a.mode,
-               "transport": "p2p" if p2p else a.transport,
+               "transport": "p2p" if p2p else a.transport, "inner": a.inner,
                "t_comm_ms": 1e3 * t_comm, "t_comp_ms": 1e3 * t_comp, "t_outer_ms": 1e3 * t_outer,
                "t_outer_alone_ms": 1e3 * t_outer0, "knee_exists": knee_exists,
                "knee_tau": a.knee, "inner_coords": k, "inner_full_ms": 1e3 * t_full,
