@@ -372,9 +372,14 @@ __device__ __forceinline__ void co2_elem(TC x, TC q0, TC q1, TC xb, TC& m, TC& x
   acc.clipped += clipped;
   // fmin / fmax: a NaN operand never wins, as in the `<` / `>` folds of the
   // block and role merges; lam >= 1 and |x' - x| >= +0 have no signed zeros.
-  acc.min_gap = fmin(lam, acc.min_gap);
   TC st = fabs(xn - x);
-  acc.max_step = fmax(st, acc.max_step);
+  if constexpr (std::is_same<TC, float>::value) {
+    acc.min_gap = fmin(lam, acc.min_gap);
+    acc.max_step = fmax(st, acc.max_step);
+  } else {  // fp64: the compare-select form keeps the F64 body within 64 registers
+    acc.min_gap = lam < acc.min_gap ? lam : acc.min_gap;
+    acc.max_step = st > acc.max_step ? st : acc.max_step;
+  }
 }
 
 struct StepArgs {
