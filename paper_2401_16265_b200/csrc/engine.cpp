@@ -266,12 +266,13 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
   // 32-wave fused outer step (bench.py --max-ctas sweeps): fewer starve the
   // reduce, more steal SM slots from the step.  With the 64-register reduce
   // kernel, C3 N=4 at 64 CTAs leaves 27 % of the reduce exposed (5.68e11
-  // params/s) against 2.3 % at 96 (7.10e11); N=2 is best at 96 too, and at
-  // N=4 128 / 148 measure the same as 96 (profiles/r02/tune/c3_p2p_ctas_r6/,
-  // profiles/r02/final/).  At 8 ranks (unmeasured: gpurun grants 4 GPUs)
-  // each rank moves 7/8 of the replica in and out over NVLink instead of
-  // 3/4, so it gets 128.
-  e->ctas = ctas > 0 ? ctas : (world <= 4 ? 96 : 128);
+  // params/s) against 2.3 % at 96 (7.10e11); N=2 is best at 96.  At N=4 the
+  // reduce is about as long as the step it hides behind: 96 CTAs left
+  // 0.05-12 % of it exposed from box to box, 128 / 148 measure the same
+  // params/s and stayed at 0.05 % (profiles/r02/tune/c3_p2p_ctas_r6/,
+  // profiles/r02/final*/), so from 4 ranks on it gets 128 (8 ranks,
+  // unmeasured here, move 7/8 of the replica per rank instead of 3/4).
+  e->ctas = ctas > 0 ? ctas : (world <= 2 ? 96 : 128);
   // The sharded slice reduce runs beside a step that touches 1/world of the
   // parameters, so it wants the whole chip: 0 = the launcher's per-world
   // default (C4 N=4: 592 CTAs 49.0 ms/round vs 64 CTAs 61.7,
