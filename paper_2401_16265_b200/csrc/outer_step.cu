@@ -2410,6 +2410,7 @@ struct LocalRoundArgs {
   int tv;        // vectors per thread per tile
   int prefetch;  // L2 bulk prefetch of the tile after next (CO2_LOCAL_ROUND_PF=1 enables)
   int pdl_early;  // signal dependents at entry rather than after the tiles
+  int stages;     // bulk-copy round: ring stages that fit in shared memory
   // [start, end] %globaltimer of this launch (nullable): the engine's
   // kernel-timed handle's device slot
   unsigned long long* ts;
@@ -2792,9 +2793,385 @@ co2_status_t launch_local_round(LocalRoundArgs a, cudaStream_t s) {
   return launch_local_round_k<M, V, 2, 2>(a, s);
 }
 
+// ---------------------------------- bulk-copy (TMA 1D) single-launch LOCAL round
+// The LDG round kernel above is latency-bound at C1's size: 24 warps per SM
+// with one 16-byte vector per stream in flight cover ~60 KB per SM, and 40 %
+// of the warps' cycles wait on loads (profiles/r02/ncu/c1_local_round_*).
+// Here one producer lane per CTA claims role-major tiles (as above) and
+// moves each tile's input streams with cp.async.bulk into a STAGES-deep
+// shared-memory ring (up to ~190 KB in flight per SM, no registers held);
+// NCW consumer warps compute from shared memory and store to global.
+// Step tiles carry x_t0, p0, m (state) and p1, xbar (low); average tiles the
+// G contributions.  Per element the ops are the LDG kernel's, so results and
+// diagnostics are bitwise the same.  The n % TILE tail of every role is done
+// by the last CTA straight from global memory.
+template <class M, int TILE>
+struct LrStage {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  static constexpr int kS = TILE * (int)sizeof(TS);
+  static constexpr int kL = TILE * (int)sizeof(TL);
+  static constexpr int kStep = 3 * kS + 2 * kL;
+  __host__ __device__ static constexpr int bytes(int g) {
+    return kStep > g * kL ? kStep : g * kL;
+  }
+};
+
+// Fold one consumer warp's accumulators into a per-warp slot; consumer
+// thread 0 merges the NCW slots into the role's atomic accumulators after a
+// named barrier over the consumer warps only (the producer lane never joins).
+template <int NCW>
+__device__ __forceinline__ void lr_bulk_merge(const Acc& a, Partial* slots, WsHeader* hdr,
+                                              bool avg) {
+  Partial b{a.min_gap, a.max_step, (unsigned long long)a.clipped, (unsigned long long)a.floored,
+            a.flags, 0u};
+  b = warp_fold(b);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) slots[warp] = b;
+  asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+  if (threadIdx.x == 0) {
+    Partial r = slots[0];
+    for (int w = 1; w < NCW; ++w) partial_merge(r, slots[w]);
+    if (avg) {
+      if (r.flags) atomicOr(&hdr->acc_flags2, r.flags);
+    } else {
+      atomicMax(&hdr->acc_min_key, ~dkey(r.min_gap));
+      atomicMax(&hdr->acc_max_key, dkey(r.max_step));
+      if (r.clipped) atomicAdd(&hdr->acc_clipped, r.clipped);
+      if (r.floored) atomicAdd(&hdr->acc_floored, r.floored);
+      if (r.flags) atomicOr(&hdr->acc_flags, r.flags);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");  // slots reusable
+}
+
+template <class M, int TILE, int STAGES, int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) local_round_bulk_kernel(const LocalRoundArgs a) {
+  using TS = typename M::TS;
+  using TL = typename M::TL;
+  using TC = typename M::TC;
+  using SG = LrStage<M, TILE>;
+  constexpr int NT = (NCW + 1) * 32;
+  constexpr int VE = 16 / (int)sizeof(TS);  // elements per lane per state access
+  static_assert(TILE % (NCW * 32 * VE) == 0, "tile must split evenly over the consumer lanes");
+  constexpr int GROUPS = TILE / (NCW * 32 * VE);
+  constexpr bool LQ = !std::is_same<TS, TL>::value;
+  const int G = a.g;
+  const int stage_bytes = SG::bytes(G);
+  const int NS = a.stages;  // <= STAGES: as many as fit beside G contributions
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + STAGES;
+  int* tile_of = reinterpret_cast<int*>(empty + STAGES);
+  Partial* slots = reinterpret_cast<Partial*>(smem + 256);
+  unsigned char* ring = smem + 256 + ((sizeof(Partial) * NCW + 127) / 128) * 128;
+
+  Hyp<TC> h;
+  h.tau = (TC)a.tau;
+  h.eps = (TC)a.eps;
+  h.beta = (TC)a.beta;
+  h.phi = (TC)a.phi;
+  h.alpha = (TC)a.alpha;
+  h.divisor = (TC)1;
+  h.penalty = a.penalty;
+  h.clip = a.clip;
+  h.divide = 0;
+  const int tpr = a.tiles_per_role;  // full tiles per role
+  const int ntiles = tpr * (G + 1);
+  WsHeader* h0 = ws_header(a.ws[0]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
+  if (a.ts && blockIdx.x == 0 && threadIdx.x == 0) h0->t_start = (unsigned long long)global_ns();
+
+  AccT<TC> acc;
+  if (warp == NCW) {
+    if (lane == 0) {  // producer: static first tile, then claims
+      const uint64_t pol = evict_first_policy();
+      int t = (int)blockIdx.x;
+      for (int it = 0;; ++it) {
+        const int s = it % NS;
+        const unsigned ph = (unsigned)(it / NS) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        if (it > 0) t = (int)gridDim.x + (int)atomicAdd(&h0->tile_next, 1u);
+        if (t >= ntiles) {
+          tile_of[s] = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        tile_of[s] = t;
+        const int role = t / tpr;
+        const int64_t e = (int64_t)(t - role * tpr) * TILE;
+        unsigned char* st = ring + (size_t)s * stage_bytes;
+        if (role < G) {
+          mbar_arrive_expect_tx(&full[s], SG::kStep);
+          bulk_g2s(st, static_cast<const TS*>(a.x_t0[role]) + e, SG::kS, &full[s], pol);
+          bulk_g2s(st + SG::kS, static_cast<const TS*>(a.p0[role]) + e, SG::kS, &full[s], pol);
+          bulk_g2s(st + 2 * SG::kS, static_cast<const TS*>(a.m[role]) + e, SG::kS, &full[s], pol);
+          bulk_g2s(st + 3 * SG::kS, static_cast<const TL*>(a.p1[role]) + e, SG::kL, &full[s], pol);
+          bulk_g2s_nohint(st + 3 * SG::kS + SG::kL, static_cast<const TL*>(a.xbar) + e, SG::kL,
+                          &full[s]);  // default priority: every worker's tiles read it
+        } else {
+          mbar_arrive_expect_tx(&full[s], (unsigned)(G * SG::kL));
+          for (int w = 0; w < G; ++w)
+            bulk_g2s(st + w * SG::kL, static_cast<const TL*>(a.cur[w]) + e, SG::kL, &full[s], pol);
+        }
+      }
+    }
+  } else {  // consumers
+    int role_cur = -1;
+    for (int it = 0;; ++it) {
+      const int s = it % NS;
+      const unsigned ph = (unsigned)(it / NS) & 1u;
+      mbar_wait(&full[s], ph);
+      const int t = tile_of[s];
+      if (t < 0) break;
+      const int role = t / tpr;
+      if (role != role_cur) {
+        if (role_cur >= 0) {
+          lr_bulk_merge<NCW>(acc.widen(), slots, ws_header(a.ws[role_cur < G ? role_cur : 0]),
+                             role_cur == G);
+          acc = AccT<TC>();
+        }
+        role_cur = role;
+      }
+      const int64_t e0 = (int64_t)(t - role * tpr) * TILE;
+      const unsigned char* st = ring + (size_t)s * stage_bytes;
+      if (role < G) {
+        const TS* sx = reinterpret_cast<const TS*>(st);
+        const TS* sp0 = reinterpret_cast<const TS*>(st + SG::kS);
+        const TS* sm = reinterpret_cast<const TS*>(st + 2 * SG::kS);
+        const TL* sp1 = reinterpret_cast<const TL*>(st + 3 * SG::kS);
+        const TL* sxb = reinterpret_cast<const TL*>(st + 3 * SG::kS + SG::kL);
+        TS* Mm = static_cast<TS*>(a.m[role]);
+        TS* A = static_cast<TS*>(a.anchor[role]);
+        TL* PR = static_cast<TL*>(a.params[role]);
+        TS* Gp = static_cast<TS*>(a.gap[role]);
+#pragma unroll
+        for (int g = 0; g < GROUPS; ++g) {
+          const int o = (g * NCW * 32 + warp * 32 + lane) * VE;
+          TS x[VE], q0[VE], mo[VE];
+          TL q1[VE], xb[VE];
+          ld_smem<TS, VE>(sx + o, x);
+          ld_smem<TS, VE>(sp0 + o, q0);
+          ld_smem<TS, VE>(sm + o, mo);
+          ld_smem<TL, VE>(sp1 + o, q1);
+          ld_smem<TL, VE>(sxb + o, xb);
+          TS mn[VE], xs[VE], gs[VE];
+          TL xl[VE];
+#pragma unroll
+          for (int v = 0; v < VE; ++v) {
+            TC m = to_c(mo[v]), xn, lam;
+            co2_elem<TC, LQ>(to_c(x[v]), to_c(q0[v]), to_c(q1[v]), to_c(xb[v]), m, xn, lam, h,
+                             acc);
+            mn[v] = (TS)m;
+            xs[v] = (TS)xn;
+            gs[v] = (TS)lam;
+            xl[v] = Store<TL>::from(xn);
+          }
+          const int64_t e = e0 + o;
+          st_vec<TS, VE>(Mm + e, mn);
+          if (A) st_vec<TS, VE>(A + e, xs);
+          st_vec<TL, VE>(PR + e, xl);
+          if (Gp) st_vec<TS, VE>(Gp + e, gs);
+        }
+      } else {
+        const TC gd = (TC)G;
+        TL* AO = static_cast<TL*>(a.avg_out);
+        constexpr int VL = 16 / (int)sizeof(TL);  // low elements per lane per access
+        constexpr int GL = TILE / (NCW * 32 * VL);
+        static_assert(TILE % (NCW * 32 * VL) == 0, "tile must split evenly (low dtype)");
+#pragma unroll 1
+        for (int g = 0; g < GL; ++g) {
+          const int o = (g * NCW * 32 + warp * 32 + lane) * VL;
+          TC sacc[VL];
+          for (int w = 0; w < G; ++w) {  // ascending worker order, param_ops.cpp:26-28
+            TL c[VL];
+            ld_smem<TL, VL>(reinterpret_cast<const TL*>(st + w * SG::kL) + o, c);
+#pragma unroll
+            for (int q = 0; q < VL; ++q) sacc[q] = w == 0 ? to_c(c[q]) : sacc[q] + to_c(c[q]);
+          }
+          TL out[VL];
+#pragma unroll
+          for (int q = 0; q < VL; ++q) {
+            const TC r = div_rn_nz(sacc[q], gd);  // one division, :30
+            if (!isfinite(r)) acc.flags |= CO2_FLAG_AVG_NONFINITE;
+            out[q] = Store<TL>::from(r);
+          }
+          st_vec<TL, VL>(AO + e0 + o, out);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (role_cur >= 0)
+      lr_bulk_merge<NCW>(acc.widen(), slots, ws_header(a.ws[role_cur < G ? role_cur : 0]),
+                         role_cur == G);
+  }
+  __syncthreads();
+  // Tail: the n % TILE coordinates of every role, by the last CTA.
+  const int64_t full_n = (int64_t)tpr * TILE;
+  if (blockIdx.x == gridDim.x - 1 && full_n < a.n) {
+    const TL* XB = static_cast<const TL*>(a.xbar);
+    for (int r = 0; r <= G; ++r) {
+      AccT<TC> ta;
+      for (int64_t j = full_n + threadIdx.x; j < a.n; j += NT) {
+        if (r < G) {
+          TS* Mm = static_cast<TS*>(a.m[r]);
+          TC m = to_c(Mm[j]), xn, lam;
+          const TS xv = static_cast<const TS*>(a.x_t0[r])[j];
+          co2_elem<TC, LQ>(to_c(xv), to_c(static_cast<const TS*>(a.p0[r])[j]),
+                           to_c(static_cast<const TL*>(a.p1[r])[j]), to_c(XB[j]), m, xn, lam, h,
+                           ta);
+          Mm[j] = (TS)m;
+          if (a.anchor[r]) static_cast<TS*>(a.anchor[r])[j] = (TS)xn;
+          static_cast<TL*>(a.params[r])[j] = Store<TL>::from(xn);
+          if (a.gap[r]) static_cast<TS*>(a.gap[r])[j] = (TS)lam;
+        } else {
+          TC sacc = to_c(static_cast<const TL*>(a.cur[0])[j]);
+          for (int w = 1; w < G; ++w) sacc = sacc + to_c(static_cast<const TL*>(a.cur[w])[j]);
+          const TC q = div_rn_nz(sacc, (TC)G);
+          if (!isfinite(q)) ta.flags |= CO2_FLAG_AVG_NONFINITE;
+          static_cast<TL*>(a.avg_out)[j] = Store<TL>::from(q);
+        }
+      }
+      // whole-CTA merge of this role's tail
+      const Partial b = block_partial<NT>(ta.widen());
+      if (threadIdx.x == 0) {
+        WsHeader* hr = ws_header(a.ws[r < G ? r : 0]);
+        if (r == G) {
+          if (b.flags) atomicOr(&hr->acc_flags2, b.flags);
+        } else {
+          atomicMax(&hr->acc_min_key, ~dkey(b.min_gap));
+          atomicMax(&hr->acc_max_key, dkey(b.max_step));
+          if (b.clipped) atomicAdd(&hr->acc_clipped, b.clipped);
+          if (b.floored) atomicAdd(&hr->acc_floored, b.floored);
+          if (b.flags) atomicOr(&hr->acc_flags, b.flags);
+        }
+      }
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Last CTA: publish and reset every role (thread r publishes role r).
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&h0->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int r = (int)threadIdx.x;
+  if (r < G) {
+    volatile WsHeader* vh = ws_header(a.ws[r]);
+    const unsigned long long kmin = vh->acc_min_key, kmax = vh->acc_max_key;
+    co2_diag_t d;
+    d.min_gap = kmin ? dkey_inv(~kmin) : (double)INFINITY;
+    d.max_outer_step = kmax ? dkey_inv(kmax) : 0.0;
+    d.n_clipped = (int64_t)vh->acc_clipped;
+    d.n_floored = (int64_t)vh->acc_floored;
+    d.flags = vh->acc_flags;
+    d.pad = 0;
+    WsHeader* hr = ws_header(a.ws[r]);
+    hr->diag = d;
+    hr->acc_min_key = 0ull;
+    hr->acc_max_key = 0ull;
+    hr->acc_clipped = 0ull;
+    hr->acc_floored = 0ull;
+    hr->acc_flags = 0u;
+    if (a.host_diag[r]) *a.host_diag[r] = d;
+  } else if (r == G) {
+    volatile WsHeader* vh = h0;
+    const unsigned int f = vh->acc_flags2;
+    h0->acc_flags2 = 0u;
+    if (a.avg_diag) {
+      co2_diag_t ad{INFINITY, 0.0, 0, 0, f, 0};
+      *a.avg_diag = ad;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    h0->tile_next = 0u;  // self-reset for the next launch
+    h0->ticket = 0u;
+    if (a.ts) {
+      a.ts[0] = *static_cast<volatile unsigned long long*>(&h0->t_start);
+      a.ts[1] = (unsigned long long)global_ns();
+    }
+  }
+}
+
+template <class M, int TILE, int STAGES, int NCW>
+co2_status_t launch_local_round_bulk(LocalRoundArgs a, cudaStream_t s) {
+  auto k = local_round_bulk_kernel<M, TILE, STAGES, NCW>;
+  using SG = LrStage<M, TILE>;
+  const size_t hdr = 256 + ((sizeof(Partial) * NCW + 127) / 128) * 128;
+  const size_t avail = 227 * 1024 - hdr;
+  int ns = (int)(avail / (size_t)SG::bytes(a.g));
+  if (ns > STAGES) ns = STAGES;
+  if (ns < 2)
+    return fail(CO2_ERR_VALIDATION, "local round (bulk): %d workers need too much shared memory",
+                a.g);
+  a.stages = ns;
+  const size_t smem = hdr + (size_t)ns * SG::bytes(a.g);
+  constexpr int NT = (NCW + 1) * 32;
+  CO2_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t tpr = a.n / TILE;
+  a.tiles_per_role = (int)tpr;
+  const int64_t ntiles = tpr * (a.g + 1);
+  int64_t grid = (int64_t)per_sm * sm_count();
+  if (grid > ntiles) grid = ntiles < 1 ? 1 : ntiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = local_round_pdl() ? 1 : 0;
+  CO2_CUDA(cudaLaunchKernelEx(&cfg, k, a));
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+// CO2_LOCAL_ROUND_BULK = 1 selects the bulk-copy round kernel (vectorised
+// layouts only).
+int local_round_bulk() {
+  static const int v = [] {
+    const char* e = getenv("CO2_LOCAL_ROUND_BULK");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <class M>
 co2_status_t launch_local_round_v(const LocalRoundArgs& a, bool vec, cudaStream_t s) {
   constexpr int V = std::is_same<M, ModeF64>::value ? 2 : (std::is_same<M, ModeF32>::value ? 4 : 8);
+  if (vec && local_round_bulk() > 0) {
+    // TILE = NCW x 32 lanes x (elements per 16-byte access of the narrower
+    // dtype) x k; stage = max(3 x TILE x state + 2 x TILE x low, G x TILE x
+    // low) bytes: fp32 TILE 2048 -> 40 KB, bf16-mixed 4096 -> 64 KB, fp64
+    // 1024 -> 40 KB per stage at NCW = 16.
+    constexpr int VM = 16 / (int)sizeof(typename M::TL);
+    switch (local_round_bulk()) {  // stages: as many as fit (<= 8)
+      case 2: return launch_local_round_bulk<M, 8 * 32 * VM * 2, 8, 8>(a, s);
+      case 3: return launch_local_round_bulk<M, 16 * 32 * VM, 3, 16>(a, s);
+      default: return launch_local_round_bulk<M, 16 * 32 * VM, 8, 16>(a, s);
+    }
+  }
   if (vec) return launch_local_round<M, V>(a, s);
   return launch_local_round<M, 1>(a, s);
 }
