@@ -354,6 +354,16 @@ co2_status_t co2_aar_p2p_detach(co2_aar_t* engine, const void* local);
  * bitwise those of the two-kernel schedule; the reduce then overlaps the
  * outer step's HBM stream instead of the inner loop. */
 co2_status_t co2_aar_set_fused(co2_aar_t* engine, int32_t on);
+/* P2P: adaptive reduce occupancy (no reference counterpart; a runtime
+ * policy of this transport).  When on, the all-reduce's CTA count follows
+ * the measured slack of the consumed reduces between 16 and the SM count:
+ * more CTAs after a reduce stalled its consumer, fewer while reduces finish
+ * with more than half their duration to spare (fewer SMs taken from the
+ * overlapped compute).  Results are unaffected.  Also the environment
+ * variable CO2_P2P_ADAPT (1: on).
+ * co2_aar_ctas reports the current count. */
+co2_status_t co2_aar_set_adaptive(co2_aar_t* engine, int32_t on);
+int32_t co2_aar_ctas(const co2_aar_t* engine);
 co2_status_t co2_aar_destroy(co2_aar_t* engine);
 int32_t co2_aar_world(const co2_aar_t* engine);
 /* launch_all_reduce (collective.cpp:31-58).  NCCL: bufs[0] is reduced in

@@ -133,6 +133,8 @@ SIGNATURES = {
     "co2_aar_p2p_attach": (ST, [P, P, C.POINTER(C.c_uint8)]),
     "co2_aar_p2p_detach": (ST, [P, P]),
     "co2_aar_set_fused": (ST, [P, I32]),
+    "co2_aar_set_adaptive": (ST, [P, I32]),
+    "co2_aar_ctas": (I32, [P]),
     "co2_aar_set_nccl_algo": (ST, [P, I32]),
     "co2_aar_order_after": (ST, [P, U64, P]),
     "co2_aar_destroy": (ST, [P]),

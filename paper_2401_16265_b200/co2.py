@@ -501,6 +501,13 @@ class CollectiveEngine:
         """P2P: fuse the one-step-stale all-reduce into the outer-step kernel."""
         check(lib().co2_aar_set_fused(self.handle, int(on)))
 
+    def set_adaptive(self, on: bool = True) -> None:
+        """P2P: let the all-reduce's CTA count follow the measured slack."""
+        check(lib().co2_aar_set_adaptive(self.handle, int(on)))
+
+    def ctas(self) -> int:
+        return int(lib().co2_aar_ctas(self.handle))
+
     def register_worker(self, worker: "Worker") -> None:
         """P2P: register both ping-pong params buffers of a worker."""
         for which in (L.BUF_PARAMS, L.BUF_PARAMS_ALT):

@@ -118,6 +118,13 @@ struct co2_aar {
   int slice_ctas = 0;  // sharded slice reduce; 0 = one CTA per SM
   uint32_t p2p_epoch = 0;      // ready flags of every P2P reduce launch (average and slice)
   uint32_t p2p_done = 0;       // cumulative exit-barrier target of the average kernel
+  // Adaptive reduce occupancy (co2_aar_set_adaptive / CO2_P2P_ADAPT=1): the
+  // P2P all-reduce's CTA count follows the measured slack of the consumed
+  // reduces, between ctas_min and ctas_max; adapt_next = first handle not
+  // yet used for a decision.
+  bool adaptive = false;
+  int ctas_min = 16, ctas_max = 148;
+  size_t adapt_next = 0;
   bool fused = false;        // worker-local rounds use the fused all-reduce + step kernel
   uint32_t fused_epoch = 0;  // exit barrier (done3) of the fused all-reduce + step
   uint32_t shard_epoch = 0;  // exit barrier (done2) of the sharded P2P step: per engine,
@@ -273,6 +280,10 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
   // profiles/r02/final*/), so from 4 ranks on it gets 128 (8 ranks,
   // unmeasured here, move 7/8 of the replica per rank instead of 3/4).
   e->ctas = ctas > 0 ? ctas : (world <= 2 ? 96 : 128);
+  {
+    const char* ad = getenv("CO2_P2P_ADAPT");
+    e->adaptive = ad && atoi(ad) == 1;
+  }
   // The sharded slice reduce runs beside a step that touches 1/world of the
   // parameters, so it wants the whole chip: 0 = the launcher's per-world
   // default (C4 N=4: 592 CTAs 49.0 ms/round vs 64 CTAs 61.7,
@@ -301,6 +312,16 @@ extern "C" co2_status_t co2_aar_create_p2p(co2_aar_t** out, int32_t rank, int32_
 }
 
 extern "C" void* co2_aar_signal_buffer(co2_aar_t* e) { return e ? e->signals : nullptr; }
+
+extern "C" co2_status_t co2_aar_set_adaptive(co2_aar_t* e, int32_t on) {
+  if (!e || e->transport != T_P2P)
+    return fail(CO2_ERR_VALIDATION, "set_adaptive: not a P2P engine");
+  e->adaptive = on != 0;
+  e->adapt_next = e->handles.size();
+  return CO2_OK;
+}
+
+extern "C" int32_t co2_aar_ctas(const co2_aar_t* e) { return e ? e->ctas : 0; }
 
 extern "C" co2_status_t co2_aar_set_fused(co2_aar_t* e, int32_t on) {
   if (!e || e->transport != T_P2P)
@@ -688,6 +709,35 @@ static co2_status_t new_handle(co2_aar* e, Handle* h) {
 
 // kind 0: all-reduce (NCCL in place / LOCAL average); kind 1: reduce-scatter
 // (sum) of the full buffer bufs[0] (n = world * shard) into out (one shard).
+// Adaptive reduce occupancy.  From the newest consumed reduce whose device
+// times are known (never blocking): it stalled the consumer (> 1 % of its
+// duration) -> more CTAs; it finished with slack to spare before the consumer
+// reached its wait (> half its duration) -> fewer, so the reduce takes fewer
+// SMs from the compute it overlaps.  The CTA count does not change results
+// (every element's fixed-order sum is the same) and ranks may differ (the
+// exit barrier counts ranks, not CTAs).  It never blocks, so when the host
+// enqueues rounds far ahead of the GPU it decides rarely; measured no gain
+// on the bench or the tau sweep (profiles/r02/tune/adaptive/), hence opt-in.
+static co2_status_t adapt_ctas(co2_aar* e) {
+  for (size_t i = e->handles.size(); i-- > e->adapt_next;) {
+    Handle& h = e->handles[i];
+    if (!h.waited) continue;
+    CO2_TRY(cache_handle_if_ready(e, h));
+    if (!h.cached || !h.cached_wait) continue;
+    e->adapt_next = i + 1;
+    const double comm = h.c_comm, stall = h.c_stall;
+    const double slack = (h.c_wait_end - stall) - h.c_done;  // wait begin - completion
+    int c = e->ctas;
+    if (stall > 0.01 * comm)
+      c = c + c / 4 + 4;
+    else if (slack > 0.5 * comm)
+      c = c - c / 8 - 1;
+    e->ctas = c < e->ctas_min ? e->ctas_min : (c > e->ctas_max ? e->ctas_max : c);
+    break;
+  }
+  return CO2_OK;
+}
+
 static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const void* const* bufs,
                                 void* out, int64_t n, void* producer, uint64_t* handle_out) {
   // launch_all_reduce, collective.cpp:31-58
@@ -726,6 +776,7 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     if (e->world > 1 && (int)e->peer_signals.size() != e->world)
       return fail(CO2_ERR_VALIDATION, "launch_all_reduce: P2P signals not attached");
     if (e->world > 1 && n > 0) {
+      if (e->adaptive) CO2_TRY(adapt_ctas(e));
       e->p2p_epoch += 1;
       CO2_TRY(p2p_average_launch(dt, pb->ptrs.data(), e->peer_signals.data(), e->world, e->rank,
                                  n, e->p2p_epoch, &e->p2p_done, e->ctas, e->comm_stream));

@@ -58,6 +58,20 @@ struct P2PArgs {
 // registers per SM, so a reduce CTA of NT x 64 registers takes exactly NT/256
 // step CTAs' worth of registers instead of rounding up to one more (the
 // uncapped 256-thread bf16 kernel used 72-84 registers, i.e. two step CTAs).
+// Exit of the fixed-order all-reduce, by thread 0 of every CTA: each CTA
+// fences its peer stores at system scope and takes a ticket; the rank's last
+// CTA alone tells every rank it is done and waits until all ranks told it
+// (kernel completion then implies every slice reached every rank).  One
+// signal per rank per launch, so ranks may launch different grids.
+__device__ __forceinline__ void p2p_rank_exit(const P2PArgs& a, Signals* mine) {
+  __threadfence_system();
+  if (atomicAdd(&mine->ticket_local, 1u) != gridDim.x - 1) return;
+  mine->ticket_local = 0u;  // self-reset: the next launch starts after this grid
+  __threadfence_system();
+  for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
+  if (!spin_until(&mine->done, a.done_target, mine)) mine->error = 2;
+}
+
 template <typename TL, typename TC, int V, int R, int U, int NT>
 __global__ void __launch_bounds__(NT, sizeof(TL) <= 4 ? 1024 / NT : 1)
     p2p_average_kernel(const P2PArgs a) {
@@ -171,11 +185,7 @@ __global__ void __launch_bounds__(NT, sizeof(TL) <= 4 ? 1024 / NT : 1)
   // Exit barrier: our slice is in every peer's buffer before any rank's
   // consumer may read the result.
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
-    if (!spin_until(&mine->done, a.done_target, mine)) mine->error = 2;
-  }
+  if (threadIdx.x == 0) p2p_rank_exit(a, mine);
 }
 
 // Bulk-copy variant of p2p_average_kernel (CO2_P2P_BULK=1): the same slice
@@ -317,11 +327,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32) p2p_bulk_average_kernel(const 
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int p = 0; p < a.world; ++p) red_release_sys_add(&a.sig[p]->done, 1u);
-    if (!spin_until(&mine->done, a.done_target, mine)) mine->error = 2;
-  }
+  if (threadIdx.x == 0) p2p_rank_exit(a, mine);
 }
 
 template <typename TL, typename TC, int TILE, int STAGES, int NCW>
@@ -552,8 +558,8 @@ co2_status_t p2p_average_launch(co2_dtype_t dt, void* const* bufs, void* const* 
   per = (per + V - 1) / V * V;
   a.shard = per;
   if (ctas < 1) ctas = 1;
-  if (ctas > sm_count()) ctas = sm_count();  // all CTAs co-resident (they spin)
-  *done_total += (uint32_t)world * (uint32_t)ctas;  // wraps; compared wrap-safe
+  if (ctas > sm_count()) ctas = sm_count();  // every CTA spins at the entry barrier
+  *done_total += (uint32_t)world;  // one exit signal per rank per launch; wraps, compared wrap-safe
   a.done_target = *done_total;
   // R = rank capacity of the instantiation, U = vectors in flight per thread
   // (fewer ranks -> more vectors, keeping ~R*U*16 B of loads per thread).

@@ -17,6 +17,8 @@ constexpr int kMaxRanks = 8;
 //   ready2[r] / done3: entry / exit of the fused all-reduce + outer step
 //   timeout_ms  the spin budget of this rank's barriers (0 = 10 s); set by
 //               the host from CO2_P2P_TIMEOUT_MS when the engine is created
+//   ticket_local  used by this rank only: counts its CTAs finishing an
+//               all-reduce so the last one alone signals the peers
 struct Signals {
   uint32_t ready[kMaxRanks];
   uint32_t done;
@@ -25,7 +27,8 @@ struct Signals {
   uint32_t ready2[kMaxRanks];
   uint32_t done3;
   uint32_t timeout_ms;
-  uint32_t pad[43];
+  uint32_t ticket_local;  // this rank's CTAs finishing an all-reduce (local, self-reset)
+  uint32_t pad[42];
 };
 static_assert(sizeof(Signals) == 256, "signal area layout");
 

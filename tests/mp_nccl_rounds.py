@@ -57,7 +57,10 @@ def main():
     n, tau, rounds = int(os.environ.get("CO2_TEST_N", 1 << 20)), 4, 4
     transport = os.environ.get("CO2_TEST_TRANSPORT", "nccl")
     if transport in ("p2p", "p2pfused"):
-        eng = co2.CollectiveEngine(world, transport="p2p", rank=rank)
+        # CO2_TEST_RANK_CTAS: a different reduce grid on every rank (the exit
+        # barrier counts ranks, not CTAs)
+        ctas = 8 + 24 * rank if os.environ.get("CO2_TEST_RANK_CTAS") else 0
+        eng = co2.CollectiveEngine(world, transport="p2p", rank=rank, max_ctas=ctas)
         if transport == "p2pfused":
             eng.set_fused(True)
     else:

@@ -28,7 +28,8 @@ def _port():
                                                ("nccl", 4, 1_000_003), ("p2p", 2, 1 << 20),
                                                ("p2p", 4, 1 << 20), ("p2pfused", 2, 1 << 20),
                                                ("p2pfused", 4, 1 << 20), ("p2pbulk", 2, 1 << 20),
-                                               ("p2pbulk", 4, 1_000_003)])
+                                               ("p2pbulk", 4, 1_000_003), ("p2pgrids", 2, 1 << 20),
+                                               ("p2pgrids", 4, 1_000_003)])
 def test_multi_rank_rounds_bitwise(mode, transport, world, n):
     """Worker-local co2_round across ranks, bitwise against the oracle --
     params, momentum and the consumed average -- for every fixed-order
@@ -42,6 +43,8 @@ def test_multi_rank_rounds_bitwise(mode, transport, world, n):
                CO2_TEST_N=str(n))
     if transport == "p2pbulk":  # the TMA bulk-copy all-reduce kernel
         env.update(CO2_P2P_BULK="2", CO2_TEST_TRANSPORT="p2p")
+    if transport == "p2pgrids":  # a different reduce grid per rank, adaptive occupancy on
+        env.update(CO2_TEST_RANK_CTAS="1", CO2_P2P_ADAPT="1", CO2_TEST_TRANSPORT="p2p")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
