@@ -596,15 +596,25 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host_round = []
     with ClockSampler(torch, torch.cuda.current_device()) as clk:
         e0.record(stream)
         for _ in range(args.steps):
+            h0 = time.perf_counter()
             one_round()
+            host_round.append(time.perf_counter() - h0)
         e1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     elapsed = e0.elapsed_time(e1) * 1e-3
+    # per-rank diagnostics: device time and the host's enqueue time per round
+    per_rank = [elapsed, statistics.median(host_round), max(host_round)]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank)
+    else:
+        gathered = [per_rank]
     kt = w.step_times()
     r = co2.L.RoundResult()
     if sharded:
@@ -728,6 +738,9 @@ def main():
             # global-norm clip), plus our P2P reduce kernel when it runs as its
             # own launch, or the ascending-rank sum kernel of the fixed-order
             # NCCL all-reduce (NCCL's own kernels are not ours)
+            "ranks": {"elapsed_ms_per_step": [1e3 * g[0] / args.steps for g in gathered],
+                      "host_enqueue_ms_per_round_median": [1e3 * g[1] for g in gathered],
+                      "host_enqueue_ms_per_round_max": [1e3 * g[2] for g in gathered]},
             "gpu_launches": world * args.steps * (
                 (2 if gclip else 1) +
                 (1 if world > 1 and transport == "p2p" and

@@ -151,6 +151,33 @@ struct co2_aar {
   cudaEvent_t fence = nullptr;
 };
 
+// Comm-stream readbacks (the P2P barrier error word, a reduce's diagnostics)
+// as a one-thread kernel storing into device-mapped pinned memory, not a
+// cudaMemcpyAsync: a D2H copy on the comm stream waits for the reduce in
+// the copy engine's queue, and the compute stream's own D2H copies queued
+// behind it then wait for the reduce too -- a stall the wait events never
+// see (C3 N=4: 0.6-1.7 ms per round on some ranks, profiles/r02/tune/ce_hol/).
+__global__ void co2_copy_words_kernel(const uint32_t* src, uint32_t* dst, int nwords) {
+  for (int i = 0; i < nwords; ++i) dst[i] = *reinterpret_cast<const volatile uint32_t*>(src + i);
+}
+
+static co2_status_t copy_words_to_host(const void* src_dev, void* dst_host, size_t bytes,
+                                       cudaStream_t st) {
+  void* dst_dev = nullptr;
+  CO2_CUDA(cudaHostGetDevicePointer(&dst_dev, dst_host, 0));
+  co2_copy_words_kernel<<<1, 1, 0, st>>>(static_cast<const uint32_t*>(src_dev),
+                                         static_cast<uint32_t*>(dst_dev), (int)(bytes / 4));
+  CO2_CUDA(cudaGetLastError());
+  return CO2_OK;
+}
+
+// A workspace's diagnostics into a pinned host slot (engine-internal: the
+// slots are cudaMallocHost'd, so mapped), without the copy engine.
+static co2_status_t diag_to_host(const void* ws, co2_diag_t* host, void* stream) {
+  return copy_words_to_host(&ws_header(const_cast<void*>(ws))->diag, host, sizeof(co2_diag_t),
+                            S(stream));
+}
+
 __global__ void co2_globaltimer_kernel(uint64_t* out) {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -759,7 +786,8 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     const int64_t shard = n / e->world;
     if (e->world > 1 && shard > 0 && !e->nccl_sum) {
       CO2_TRY(nccl_fixed_rs(e, e->comm, 0, dt, bufs[0], n, shard, out, e->ws, e->comm_stream));
-      CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
+      CO2_TRY(copy_words_to_host(&ws_header(e->ws)->diag, h.diag, sizeof(co2_diag_t),
+                                 e->comm_stream));
     } else if (e->world > 1 && shard > 0)
       CO2_NCCL(ncclReduceScatter(bufs[0], out, (size_t)shard, nccl_dtype(dt), ncclSum, e->comm,
                                  e->comm_stream));
@@ -781,8 +809,8 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
       CO2_TRY(p2p_average_launch(dt, pb->ptrs.data(), e->peer_signals.data(), e->world, e->rank,
                                  n, e->p2p_epoch, &e->p2p_done, e->ctas, e->comm_stream));
       // the kernel records a timed-out barrier in the signal area's error word
-      CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
-                               cudaMemcpyDeviceToHost, e->comm_stream));
+      CO2_TRY(copy_words_to_host(static_cast<char*>(e->signals) + p2p_signal_error_offset(),
+                                 h.p2p_error, 4, e->comm_stream));
     }
   } else if (e->transport == T_NCCL) {
     if (out && out != bufs[0])
@@ -793,7 +821,8 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
       void* mine = static_cast<char*>(buf) +
                    dtype_bytes(dt) * (size_t)std::min<int64_t>((int64_t)e->rank * slice, n);
       CO2_TRY(nccl_fixed_rs(e, e->comm, 0, dt, buf, n, slice, mine, e->ws, e->comm_stream));
-      CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
+      CO2_TRY(copy_words_to_host(&ws_header(e->ws)->diag, h.diag, sizeof(co2_diag_t),
+                                 e->comm_stream));
       CO2_TRY(nccl_fixed_ag(e, e->comm, dt, buf, n, slice, e->comm_stream));
     } else if (e->world > 1 && n > 0) {
       CO2_NCCL(ncclAllReduce(bufs[0], const_cast<void*>(bufs[0]), (size_t)n, nccl_dtype(dt), ncclSum,
@@ -801,7 +830,8 @@ static co2_status_t launch_impl(co2_aar_t* e, int kind, co2_dtype_t dt, const vo
     }
   } else {
     CO2_TRY(co2_average(dt, e->workers, bufs, n, out, e->ws, e->comm_stream));
-    CO2_TRY(co2_diag_fetch_async(e->ws, h.diag, e->comm_stream));
+    CO2_TRY(copy_words_to_host(&ws_header(e->ws)->diag, h.diag, sizeof(co2_diag_t),
+                               e->comm_stream));
   }
   CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
   h.done_stream = e->comm_stream;
@@ -840,8 +870,8 @@ static co2_status_t launch_slice(co2_aar* e, co2_dtype_t dt, const void* src0, c
   CO2_TRY(p2p_slice_average_launch(dt, 2, b0->ptrs.data(), b1->ptrs.data(), dst0, dst1,
                                    e->peer_signals.data(), e->world, e->rank, lo, len,
                                    e->p2p_epoch, e->slice_ctas, e->comm_stream));
-  CO2_CUDA(cudaMemcpyAsync(h.p2p_error, static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
-                           cudaMemcpyDeviceToHost, e->comm_stream));
+  CO2_TRY(copy_words_to_host(static_cast<char*>(e->signals) + p2p_signal_error_offset(),
+                             h.p2p_error, 4, e->comm_stream));
   CO2_CUDA(cudaEventRecord(h.done, e->comm_stream));
   h.done_stream = e->comm_stream;
   e->handles.push_back(h);
@@ -1199,7 +1229,7 @@ extern "C" co2_status_t co2_round_finish(co2_worker_t* const* ws, int32_t g, voi
     if (!ws[i]) return fail(CO2_ERR_VALIDATION, "co2_round_finish: null worker");
   for (int i = 0; i < g; ++i)
     if (ws[i]->diag_on_device) {
-      CO2_TRY(co2_diag_fetch_async(ws[i]->ws, ws[i]->host_diag, stream));
+      CO2_TRY(diag_to_host(ws[i]->ws, ws[i]->host_diag, stream));
       ws[i]->diag_on_device = false;
     }
   CO2_CUDA(cudaStreamSynchronize(S(stream)));
@@ -1488,10 +1518,9 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
       CO2_CUDA(cudaEventRecord(w->tev[2 * slot + 1], st));
       w->tev_recorded += 1;
     }
-    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
-    CO2_CUDA(cudaMemcpyAsync(w->fused_err,
-                             static_cast<char*>(e->signals) + p2p_signal_error_offset(), 4,
-                             cudaMemcpyDeviceToHost, st));
+    CO2_TRY(diag_to_host(w->ws, w->host_diag, stream));
+    CO2_TRY(copy_words_to_host(static_cast<char*>(e->signals) + p2p_signal_error_offset(),
+                               w->fused_err, 4, st));
     std::swap(w->anchor, w->prev_x0);
     std::swap(w->prev_x1, w->xfirst);
     w->cur = 1 - w->cur;
@@ -1530,9 +1559,9 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
       if (!w0->tmp_state) CO2_TRY(walloc(&w0->tmp_state, sb));
       if (!w0->tmp_low) CO2_TRY(walloc(&w0->tmp_low, lb));
       CO2_TRY(co2_average(sdt, g, s0.data(), n, w0->tmp_state, w0->ws, stream));
-      CO2_TRY(co2_diag_fetch_async(w0->ws, w0->host_diag, stream));
+      CO2_TRY(diag_to_host(w0->ws, w0->host_diag, stream));
       CO2_TRY(co2_average(ldt, g, s1.data(), n, w0->tmp_low, w0->ws, stream));
-      CO2_TRY(co2_diag_fetch_async(w0->ws, ws[g - 1]->host_diag, stream));
+      CO2_TRY(diag_to_host(w0->ws, ws[g - 1]->host_diag, stream));
       for (int i = 0; i < g; ++i) {
         CO2_TRY(copy_dev(ws[i]->prev_x0, w0->tmp_state, sb, st));
         CO2_TRY(copy_dev(ws[i]->prev_x1, w0->tmp_low, lb, st));
@@ -1592,7 +1621,7 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
     void* out_params = w->params[1 - w->cur];
     CO2_TRY(step_launch(w, mode, n, w0->tmp_state, w->prev_x0, w->prev_x1, xbar, divisor, w->m,
                         w->prev_x0, out_params, w->gap, hyper, st));
-    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    CO2_TRY(diag_to_host(w->ws, w->host_diag, stream));
     // Rotation: anchor <- x_{t+1,0} (written over prev_x0), prev_x0 <- bar0,
     // prev_x1 <- bar1.
     void* old_anchor = w->anchor;
@@ -1628,7 +1657,7 @@ extern "C" co2_status_t co2_round(co2_worker_t* const* ws, int32_t g, co2_aar_t*
                           w->prev_x0, out_params, w->gap, hyper, st, keep));
       // the sum algorithm delivered the worker sum: keep the average
       if (keep && divisor > 1) CO2_TRY(scale_div_impl(ldt, keep, n, divisor, st));
-      CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+      CO2_TRY(diag_to_host(w->ws, w->host_diag, stream));
       std::swap(w->anchor, w->prev_x0);  // anchor <- x_{t+1,0}; prev_x0 <- x_{t,0}
       std::swap(w->prev_x1, w->xfirst);  // prev_x1 <- x_{t,1}
       w->cur = 1 - w->cur;
@@ -2000,7 +2029,7 @@ extern "C" co2_status_t co2_sharded_round(co2_sharded_t* s, co2_aar_t* e,
     if (!s->p2p) CO2_CUDA(cudaEventRecord(s->tev[2 * slot + 1], st));
     s->tev_recorded += 1;
   }
-  CO2_TRY(co2_diag_fetch_async(s->ws, s->host_diag, stream));
+  CO2_TRY(diag_to_host(s->ws, s->host_diag, stream));
   // x_{t+1,0} for every worker: in-place all-gather of the updated shards.
   if (!s->p2p) CO2_TRY(ag_inplace(e, ldt, s->params[1 - s->cur], s->shard, st));
   s->xbar = xsum;
@@ -2095,7 +2124,7 @@ extern "C" co2_status_t co2_slowmo_round(co2_worker_t* const* ws, int32_t g, co2
     // x_start = x_{t,0} (anchor); the new iterate is also the next anchor.
     CO2_TRY(slowmo_impl(w->mode, w->n, w->anchor, xbar, div, w->m, w->params[w->cur], w->anchor,
                         alpha, beta, w->ws, st));
-    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    CO2_TRY(diag_to_host(w->ws, w->host_diag, stream));
     w->xbar = const_cast<void*>(xbar);
     w->t += 1;
   }
@@ -2131,7 +2160,7 @@ extern "C" co2_status_t co2_local_sgd_round(co2_worker_t* const* ws, int32_t g, 
     co2_worker* w = ws[i];
     CO2_TRY(local_sgd_impl(w->mode, w->n, w->anchor, xbar, div, w->params[w->cur], w->anchor,
                            w->ws, st));
-    CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+    CO2_TRY(diag_to_host(w->ws, w->host_diag, stream));
     w->xbar = const_cast<void*>(xbar);
     w->t += 1;
   }
@@ -2163,7 +2192,7 @@ extern "C" co2_status_t co2_overlap_local_sgd_round(co2_worker_t* const* ws, int
       co2_worker* w = ws[i];
       CO2_TRY(overlap_correction_impl(mode, n, w->params[w->cur], w->anchor, xbar, div, w->ws,
                                       st));
-      CO2_TRY(co2_diag_fetch_async(w->ws, w->host_diag, stream));
+      CO2_TRY(diag_to_host(w->ws, w->host_diag, stream));
     }
     applied = true;
     return CO2_OK;
