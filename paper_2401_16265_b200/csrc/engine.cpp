@@ -607,10 +607,10 @@ static cudaEvent_t sync_event(const Handle& h) { return h.ktimed ? h.fin : h.don
 // average's diagnostics) into its pinned slots.
 static co2_status_t fetch_slots(co2_aar* e, const Handle& h) {
   CO2_CUDA(cudaEventSynchronize(h.fin));
-  CO2_CUDA(cudaMemcpyAsync(h.ts, h.ts_dev, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                           e->aux_stream));
-  CO2_CUDA(cudaMemcpyAsync(h.diag, h.diag_dev, sizeof(co2_diag_t), cudaMemcpyDeviceToHost,
-                           e->aux_stream));
+  // kernel copies, not cudaMemcpyAsync: a D2H copy could queue in the copy
+  // engine behind a caller's D2H that waits for a later round
+  CO2_TRY(copy_words_to_host(h.ts_dev, h.ts, 2 * sizeof(uint64_t), e->aux_stream));
+  CO2_TRY(copy_words_to_host(h.diag_dev, h.diag, sizeof(co2_diag_t), e->aux_stream));
   CO2_CUDA(cudaStreamSynchronize(e->aux_stream));
   return CO2_OK;
 }
