@@ -734,18 +734,21 @@ def main():
                          "bytes_per_param": bpp},
             "link": link, "step_hbm": step_hbm,
             "e2e": e2e, "e2e_full_state": e2e_full, "cpu_baseline": cpu, "comm": comm,
-            # our kernels per step per rank: the fused step (two passes for the
-            # global-norm clip), plus our P2P reduce kernel when it runs as its
-            # own launch, or the ascending-rank sum kernel of the fixed-order
-            # NCCL all-reduce (NCCL's own kernels are not ours)
             "ranks": {"elapsed_ms_per_step": [1e3 * g[0] / args.steps for g in gathered],
                       "host_enqueue_ms_per_round_median": [1e3 * g[1] for g in gathered],
                       "host_enqueue_ms_per_round_max": [1e3 * g[2] for g in gathered]},
+            # our kernels per step per rank: the fused step (two passes for the
+            # global-norm clip) and its diagnostics readback; the P2P reduce
+            # (or slice reduce) and its error-word readback when it runs as its
+            # own launch; the fixed-order NCCL all-reduce's ascending-rank sum
+            # kernel and its diagnostics readback (one more sum kernel for the
+            # sharded round's blocking x_{t,1} reduce-scatter).  NCCL's own
+            # kernels are not ours.
             "gpu_launches": world * args.steps * (
-                (2 if gclip else 1) +
-                (1 if world > 1 and transport == "p2p" and
+                (2 if gclip else 1) + 1 +
+                (2 if world > 1 and transport == "p2p" and
                  (sharded or args.schedule == "split") else 0) +
-                (1 if world > 1 and transport == "nccl" and not sharded else 0)),
+                ((3 if sharded else 2) if world > 1 and transport == "nccl" else 0)),
             "clocks": clk.summary(),
             "diag": {"min_gap": r.min_gap, "max_outer_step": r.max_outer_step,
                      "n_clipped": r.n_clipped, "n_floored": r.n_floored},
