@@ -47,10 +47,15 @@ round_example: tests/cpp/round_example.cpp include/co2_b200.h $(LIB)
 	    -o build/round_example -L$(CSRC)/.. -lco2b200 -L/usr/local/cuda/lib64 -lcudart \
 	    -Wl,-rpath,'$$ORIGIN/../paper_2401_16265_b200'
 
+round_host_example: tests/cpp/round_host_example.cpp include/co2_b200.h $(LIB)
+	g++ -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include tests/cpp/round_host_example.cpp \
+	    -o build/round_host_example -L$(CSRC)/.. -lco2b200 -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../paper_2401_16265_b200'
+
 nvlink_probe: tools/nvlink_probe.cu | build
 	$(NVCC) $(ARCH) -O3 -std=c++17 tools/nvlink_probe.cu -o build/nvlink_probe
 
 clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
-.PHONY: all oracle clean facade_test round_example co2sim_round_test nvlink_probe
+.PHONY: all oracle clean facade_test round_example round_host_example co2sim_round_test nvlink_probe

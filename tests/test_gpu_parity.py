@@ -452,6 +452,18 @@ def test_cpp_round_driver_binary():
     assert "ROUNDS OK" in r.stdout
 
 
+def test_cpp_round_host_binary():
+    """The CPU-inner-loop drop-in in C++ (tests/cpp/round_host_example.cpp):
+    co2_round_host with the inner loop in plain C++ on the host, bitwise
+    equal to uploading the same traces by hand and calling co2_round."""
+    exe = os.path.join(ROOT, "build", "round_host_example")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", ROOT, "round_host_example"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "HOST ROUNDS OK" in r.stdout
+
+
 def test_cpp_co2sim_round_facade_replays_fixture():
     """The reference-shaped round API (include/co2sim_b200.hpp: co2sim::
     co2_round over WorkerState / OuterState / InnerTrace / CollectiveEngine /
