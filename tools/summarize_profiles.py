@@ -1,8 +1,9 @@
 """Regenerate the headline table of profiles/<round>/README.md from the
 committed bench JSON lines (no GPU needed).
 
-  python tools/summarize_profiles.py [profiles/r01/final]
+  python tools/summarize_profiles.py [profiles/r02/final]
 """
+import argparse
 import glob
 import json
 import os
@@ -16,11 +17,16 @@ def fmt(v, f="{:.3g}"):
 
 
 def main():
-    d = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r01", "final")
+    ap = argparse.ArgumentParser(description="headline table from committed bench lines")
+    ap.add_argument("dir", nargs="?", default=os.path.join(ROOT, "profiles", "r02", "final"))
+    d = ap.parse_args().dir
     rows = []
     for path in sorted(glob.glob(os.path.join(d, "*.json"))):
         with open(path) as f:
-            line = json.loads(f.readline())
+            js = [ln for ln in f if ln.startswith("{")]
+        if not js:
+            continue
+        line = json.loads(js[-1])
         name = os.path.basename(path)
         if line.get("impl") == "reference":
             rows.append((name, "reference arm", line["value"], None, None, None, None))
