@@ -751,9 +751,11 @@ def co2_round_host(workers: list[Worker], engine: CollectiveEngine, hyper: Co2Hy
 
     def ptrs(ts):
         return (C.c_void_p * g)(*[t.data_ptr() for t in ts]) if ts is not None else None
+    lo = LOW_TORCH[workers[0].mode]
     for t in list(x_end) + list(x_next) + list(x_first or []):
-        if t.is_cuda or not t.is_contiguous() or t.numel() != workers[0].n:
-            raise ValueError("co2_round_host: contiguous host tensors of n values expected")
+        if t.is_cuda or not t.is_contiguous() or t.numel() != workers[0].n or t.dtype != lo:
+            raise ValueError(f"co2_round_host: contiguous host tensors of n {lo} values "
+                             "expected")
     h = hyper.c(tau)
     r = L.RoundResult()
     check(lib().co2_round_host(arr, g, engine.handle, C.byref(h), ptrs(x_first), ptrs(x_end),
